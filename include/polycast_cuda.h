@@ -1,0 +1,141 @@
+/* polycast_cuda.h — C-ABI of libpolycast_cuda.so, the B200 (sm_100a) batched
+ * point-in-polygon engine.
+ *
+ * This is the drop-in boundary of SURVEY.md §8(b).  The reference (polycast,
+ * header-only C++20) has no FFI: its hot path is the C++ call
+ *     classify_batch(const PointBatch&, const Polygon&, CrossingMode,
+ *                    size_t workers = 0, double boundary_tol = 1e-12)
+ *     (/root/reference/proj/include/polycast/batch.hpp:184-186)
+ * which runs contains() (geometry.hpp:281-300) -> count_crossings_c1/_c2 /
+ * robust_ray_crossings (geometry.hpp:182-273) per point.  The entry points
+ * below replace that call below the C++ types; include/polycast/*.hpp keeps
+ * the reference's public C++ API on top of them.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no exceptions cross this boundary.
+ *  - Status codes: PC_OK, PC_EINVAL, PC_ECUDA, PC_ENOMEM, PC_ENCCL; the message
+ *    of the last failure of a context is returned by pc_last_error().
+ *  - mode: 0 = C1, 1 = C2, 2 = Robust  (CrossingMode order, geometry.hpp:107).
+ *  - Verdict bytes: 0 Inside, 1 Outside, 2 Boundary, 3 Error (batch.hpp:60).
+ *  - stats[4] = {inside, outside, boundary, error} (BatchStats, batch.hpp:81-109).
+ *  - Points: interleaved x,y doubles (== reference Point2[], 16 B each).
+ *  - Polygons: SoA vertex arrays vx[], vy[] holding closed rings (first vertex
+ *    repeated at the end, as the reference Ring stores it, geometry.hpp:41-60);
+ *    ring r spans vertices [ring_off[r], ring_off[r+1]); ring 0 is the outer
+ *    ring, the rest are holes, combined by even-odd parity (geometry.hpp:281-300).
+ *  - Bit planes: bit (i % 32) of word i/32 belongs to point i.  inside_bits
+ *    marks Inside verdicts; aux_bits marks Error (C2) or Boundary (Robust).
+ *  - Host buffers are borrowed for the duration of a synchronous call (pinned
+ *    buffers make the copies faster but are not required).  Inputs are not
+ *    validated for finiteness (the C++ types do that, SURVEY §8 rule P9).
+ *  - Results are bit-identical to the reference CPU implementation for every
+ *    mode, input and device count (IEEE binary64, round-to-nearest, no FMA
+ *    contraction, the reference's expression order).
+ *  - A context serialises its own use; concurrent callers use separate contexts.
+ *  - There is no CPU fallback: with no usable GPU, pc_create fails.
+ */
+#ifndef POLYCAST_CUDA_H
+#define POLYCAST_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PC_OK 0
+#define PC_EINVAL 1
+#define PC_ECUDA 2
+#define PC_ENOMEM 3
+#define PC_ENCCL 4
+
+#define PC_MODE_C1 0
+#define PC_MODE_C2 1
+#define PC_MODE_ROBUST 2
+
+#define PC_INSIDE 0
+#define PC_OUTSIDE 1
+#define PC_BOUNDARY 2
+#define PC_ERROR 3
+
+typedef struct pc_ctx pc_ctx;
+
+/* Creates a context over GPUs 0..num_gpus-1 (num_gpus = 0: all visible).
+ * Replaces the reference's std::thread worker pool (batch.hpp:172-175,
+ * :212-229): points are sharded contiguously across the context's GPUs. */
+int pc_create(pc_ctx** out, int num_gpus);
+/* Creates a context over an explicit device list (e.g. one rank's LOCAL_RANK). */
+int pc_create_devices(pc_ctx** out, const int* device_ids, int n);
+void pc_destroy(pc_ctx* ctx);
+const char* pc_last_error(const pc_ctx* ctx);
+int pc_device_count(const pc_ctx* ctx);
+/* Library version string. */
+const char* pc_version(void);
+
+/* Batched classification of n points against one polygon; replaces
+ * classify_batch (batch.hpp:184-230) when bbox_prefilter = 1 and per-point
+ * contains() (geometry.hpp:281-300) when bbox_prefilter = 0.
+ * Every output pointer is optional (NULL = not wanted); inside_bits/aux_bits
+ * hold ceil(n/32) words, verdicts n bytes, stats 4 counters. */
+int pc_classify(pc_ctx* ctx, const double* pts_xy, uint64_t n, const double* vx, const double* vy,
+                const uint64_t* ring_off, uint32_t n_rings, int mode, double boundary_tol,
+                int bbox_prefilter, uint8_t* verdicts, uint32_t* inside_bits, uint32_t* aux_bits,
+                uint64_t stats[4]);
+
+/* Multi-polygon CSR batch: polygon p owns points
+ * [pt_off[p], pt_off[p+1]) and rings [poly_ring_off[p], poly_ring_off[p+1]);
+ * each polygon is classified with classify_batch semantics (bbox of its outer
+ * ring, closed interval).  Polygons are sharded across the context's GPUs. */
+int pc_classify_csr(pc_ctx* ctx, const double* pts_xy, const uint64_t* pt_off, uint64_t n_polys,
+                    const double* vx, const double* vy, const uint64_t* ring_off,
+                    const uint64_t* poly_ring_off, int mode, double boundary_tol,
+                    uint8_t* verdicts, uint32_t* inside_bits, uint32_t* aux_bits,
+                    uint64_t stats[4]);
+
+/* count_crossings_c1 (mode 0) / count_crossings_c2 (mode 1) of one closed
+ * ring of nv vertices for n points (geometry.hpp:182-229).  counts[i] is the
+ * crossing count; degenerate[i] = 1 where the reference throws DegenerateEdge
+ * (C2, horizontal edge on the ray; the count is then undefined). */
+int pc_count_crossings(pc_ctx* ctx, const double* pts_xy, uint64_t n, const double* vx,
+                       const double* vy, uint64_t nv, int mode, uint64_t* counts,
+                       uint8_t* degenerate);
+
+/* Device-pointer variants on the context's GPU `dev_index`, enqueued on
+ * `stream` (a cudaStream_t; NULL = the context's stream) and NOT synchronised.
+ * d_inside_bits / d_aux_bits (ceil(n/32) words) and d_stats (4 x u64) are
+ * required; d_verdicts is optional.  Used for kernel-only timing and by
+ * callers that keep their data resident in HBM. */
+int pc_classify_dev(pc_ctx* ctx, int dev_index, void* stream, const double* d_pts_xy, uint64_t n,
+                    const double* d_vx, const double* d_vy, const uint64_t* d_ring_off,
+                    uint32_t n_rings, uint64_t n_verts, int mode, double boundary_tol,
+                    int bbox_prefilter, uint8_t* d_verdicts, uint32_t* d_inside_bits,
+                    uint32_t* d_aux_bits, uint64_t* d_stats);
+
+int pc_classify_csr_dev(pc_ctx* ctx, int dev_index, void* stream, const double* d_pts_xy,
+                        const uint64_t* d_pt_off, uint64_t n_polys, uint64_t n_points,
+                        const double* d_vx, const double* d_vy, const uint64_t* d_ring_off,
+                        const uint64_t* d_poly_ring_off, int mode, double boundary_tol,
+                        uint8_t* d_verdicts, uint32_t* d_inside_bits, uint32_t* d_aux_bits,
+                        uint64_t* d_stats);
+
+/* Number of GPU kernels the last call on this context launched (all devices). */
+uint64_t pc_last_launch_count(const pc_ctx* ctx);
+
+/* Measurement hooks (bench.py).  With profiling on, every call records a pair
+ * of CUDA events around its main classify kernel, on the stream that kernel is
+ * launched on.  pc_profile_take() waits for the pairs recorded on device
+ * `dev_index` since the previous take, writes up to `cap` kernel durations
+ * (ms) to ms_out, clears them and returns how many there were. */
+int pc_set_profiling(pc_ctx* ctx, int on);
+int pc_profile_take(pc_ctx* ctx, int dev_index, double* ms_out, int cap);
+
+/* Runs an FP64 add/multiply throughput probe (no FMA: the instruction mix of
+ * the crossing test) on device `dev_index` for about `ms` milliseconds and
+ * returns the achieved rate in FP64 operations per second. */
+int pc_measure_fp64_rate(pc_ctx* ctx, int dev_index, double ms, double* flops_per_s);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* POLYCAST_CUDA_H */

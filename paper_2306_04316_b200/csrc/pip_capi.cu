@@ -1,0 +1,560 @@
+// C-ABI of libpolycast_cuda.so (include/polycast_cuda.h).
+//
+// Replaces the reference's batch engine (proj/include/polycast/batch.hpp:184-230):
+// the std::thread fork/join over contiguous point chunks becomes contiguous
+// point shards over the context's GPUs (one stream each), the per-point loop
+// becomes the sm_100a kernels of pip_kernels.cu, and per-point DegenerateEdge
+// / Boundary outcomes come back as bit planes + verdict bytes + BatchStats.
+#include "../../include/polycast_cuda.h"
+#include "pip_kernels.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        const size_t want = std::max<size_t>(bytes + bytes / 8, 256);
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+struct DevState {
+    int dev = 0;
+    cudaStream_t stream = nullptr;
+    DevBuf pts, vx, vy, ring_off, pt_off, poly_ring_off, filt, rec, bbox, bits, verdicts, stats, counts, degen;
+    unsigned long long* h_stats = nullptr; // pinned 4 x u64
+    // profiling: one event pair per main-kernel launch since the last take
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
+    size_t ev_used = 0;
+};
+
+} // namespace
+
+struct pc_ctx {
+    std::vector<DevState> devs;
+    std::string err;
+    std::mutex mu;
+    uint64_t launches = 0;
+    bool profiling = false;
+};
+
+namespace {
+
+struct Fail {
+    int code;
+};
+
+void check(pc_ctx* c, cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return;
+    c->err = std::string(what) + ": " + cudaGetErrorString(e);
+    cudaGetLastError(); // clear sticky-free errors
+    throw Fail{e == cudaErrorMemoryAllocation ? PC_ENOMEM : PC_ECUDA};
+}
+
+void invalid(pc_ctx* c, const char* msg) {
+    c->err = msg;
+    throw Fail{PC_EINVAL};
+}
+
+template <class Fn>
+int guarded(pc_ctx* c, Fn&& fn) {
+    if (!c) return PC_EINVAL;
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->launches = 0;
+    try {
+        fn();
+        c->err.clear();
+        return PC_OK;
+    } catch (const Fail& f) {
+        return f.code;
+    } catch (const std::exception& e) {
+        c->err = e.what();
+        return PC_ENOMEM;
+    }
+}
+
+void validate_rings(pc_ctx* c, const uint64_t* ring_off, uint64_t n_rings) {
+    if (n_rings < 1) invalid(c, "polygon needs at least one (outer) ring");
+    if (ring_off[0] != 0) invalid(c, "ring_off[0] must be 0");
+    for (uint64_t r = 0; r < n_rings; ++r)
+        if (ring_off[r + 1] <= ring_off[r]) invalid(c, "every ring needs at least one vertex (ring_off must increase)");
+}
+
+void mark_begin(pc_ctx* c, DevState& d, cudaStream_t st) {
+    if (!c->profiling) return;
+    if (d.ev_used == d.evs.size()) {
+        cudaEvent_t a, b;
+        check(c, cudaEventCreate(&a), "event");
+        check(c, cudaEventCreate(&b), "event");
+        d.evs.emplace_back(a, b);
+    }
+    check(c, cudaEventRecord(d.evs[d.ev_used].first, st), "event record");
+}
+
+void mark_end(pc_ctx* c, DevState& d, cudaStream_t st) {
+    if (!c->profiling) return;
+    check(c, cudaEventRecord(d.evs[d.ev_used].second, st), "event record");
+    ++d.ev_used;
+}
+
+// Enqueue the whole single-polygon pipeline for one device; inputs already on
+// the device.  prep (edge records, bbox, zeroed planes) -> classify -> finalize.
+void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts, uint64_t n, const double* d_vx,
+                    const double* d_vy, const uint64_t* d_ring_off, uint32_t n_rings, uint64_t n_verts, int mode,
+                    double tol, int prefilter, uint8_t* d_verdicts, uint32_t* d_inside, uint32_t* d_aux,
+                    unsigned long long* d_stats) {
+    const uint64_t n_edges = n_verts - n_rings;
+    if (n_edges > 0xffffffffull) invalid(c, "too many edges for one polygon (>= 2^32)");
+    const uint64_t nwords = (n + 31) / 32;
+    check(c, d.filt.ensure(std::max<uint64_t>(n_edges, 1) * sizeof(uint2)), "alloc edge keys");
+    check(c, d.rec.ensure(std::max<uint64_t>(n_edges, 1) * pcd::edge_rec_bytes()), "alloc edge records");
+    check(c, d.bbox.ensure(4 * sizeof(unsigned long long)), "alloc bbox");
+    pcd::PrepArgs pa{};
+    pa.mode = mode;
+    pa.vx = d_vx;
+    pa.vy = d_vy;
+    pa.ring_off = d_ring_off;
+    pa.n_rings = n_rings;
+    pa.n_verts = n_verts;
+    pa.filt = d.filt.as<uint2>();
+    pa.rec = d.rec.p;
+    pa.bbox_keys = d.bbox.as<unsigned long long>();
+    pa.stats = d_stats;
+    // inside and aux are zeroed separately (they need not be contiguous)
+    pa.zero_words = d_inside;
+    pa.n_zero_words = nwords;
+    check(c, pcd::launch_prep(pa, st, d.dev, &c->launches), "prep kernel");
+    check(c, cudaMemsetAsync(d_aux, 0, nwords * 4, st), "clear aux plane");
+    pcd::SingleArgs sa{};
+    sa.mode = mode;
+    sa.pts = d_pts;
+    sa.n = n;
+    sa.filt = d.filt.as<uint2>();
+    sa.rec = d.rec.p;
+    sa.n_edges = (uint32_t)n_edges;
+    sa.bbox_keys = d.bbox.as<unsigned long long>();
+    sa.prefilter = prefilter;
+    sa.tol = tol;
+    sa.tol2 = tol * tol;
+    sa.inside_bits = d_inside;
+    sa.aux_bits = d_aux;
+    mark_begin(c, d, st);
+    check(c, pcd::launch_single(sa, st, d.dev, &c->launches), "classify kernel");
+    mark_end(c, d, st);
+    check(c, pcd::launch_finalize(n, d_inside, d_aux, d_verdicts, mode, d_stats, st, d.dev, &c->launches),
+          "finalize kernel");
+}
+
+void enqueue_csr(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts, uint64_t n_points,
+                 const uint64_t* d_pt_off, uint64_t n_polys, const double* d_vx, const double* d_vy,
+                 const uint64_t* d_ring_off, const uint64_t* d_poly_ring_off, uint64_t pt_base, uint64_t ring_base,
+                 uint64_t vert_base, int mode, double tol, uint8_t* d_verdicts, uint32_t* d_inside, uint32_t* d_aux,
+                 unsigned long long* d_stats) {
+    const uint64_t nwords = (n_points + 31) / 32;
+    check(c, cudaMemsetAsync(d_inside, 0, nwords * 4, st), "clear inside plane");
+    check(c, cudaMemsetAsync(d_aux, 0, nwords * 4, st), "clear aux plane");
+    check(c, cudaMemsetAsync(d_stats, 0, 4 * sizeof(unsigned long long), st), "clear stats");
+    pcd::CsrArgs a{};
+    a.mode = mode;
+    a.pts = d_pts;
+    a.pt_off = d_pt_off;
+    a.n_polys = n_polys;
+    a.vx = d_vx;
+    a.vy = d_vy;
+    a.ring_off = d_ring_off;
+    a.poly_ring_off = d_poly_ring_off;
+    a.pt_base = pt_base;
+    a.ring_base = ring_base;
+    a.vert_base = vert_base;
+    a.tol = tol;
+    a.tol2 = tol * tol;
+    a.inside_bits = d_inside;
+    a.aux_bits = d_aux;
+    mark_begin(c, d, st);
+    check(c, pcd::launch_csr(a, st, d.dev, &c->launches), "csr kernel");
+    mark_end(c, d, st);
+    check(c, pcd::launch_finalize(n_points, d_inside, d_aux, d_verdicts, mode, d_stats, st, d.dev, &c->launches),
+          "finalize kernel");
+}
+
+void h2d(pc_ctx* c, DevBuf& b, const void* src, size_t bytes, cudaStream_t st, const char* what) {
+    check(c, b.ensure(std::max<size_t>(bytes, 16)), what);
+    if (bytes) check(c, cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, st), what);
+}
+
+// OR `nbits` bits from src (bit 0 = point `bit_off` of the destination) into dst.
+void merge_bits(uint32_t* dst, const uint32_t* src, uint64_t bit_off, uint64_t nbits) {
+    const uint64_t nw = (nbits + 31) / 32;
+    const uint32_t sh = (uint32_t)(bit_off & 31);
+    const uint64_t w0 = bit_off >> 5;
+    const uint64_t dst_words = (bit_off + nbits + 31) / 32;
+    for (uint64_t i = 0; i < nw; ++i) {
+        uint32_t v = src[i];
+        if (i == nw - 1 && (nbits & 31)) v &= (1u << (nbits & 31)) - 1u;
+        dst[w0 + i] |= v << sh;
+        if (sh && w0 + i + 1 < dst_words) dst[w0 + i + 1] |= v >> (32 - sh);
+    }
+}
+
+} // namespace
+
+extern "C" {
+
+const char* pc_version(void) { return "polycast-b200 0.1 (sm_100a)"; }
+
+int pc_create_devices(pc_ctx** out, const int* device_ids, int n) {
+    if (!out) return PC_EINVAL;
+    *out = nullptr;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        return PC_ECUDA;
+    }
+    if (n < 1) return PC_EINVAL;
+    auto* c = new pc_ctx();
+    for (int i = 0; i < n; ++i) {
+        if (device_ids[i] < 0 || device_ids[i] >= count) {
+            delete c;
+            return PC_EINVAL;
+        }
+        DevState d;
+        d.dev = device_ids[i];
+        if (cudaSetDevice(d.dev) != cudaSuccess || cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaMallocHost(&d.h_stats, 4 * sizeof(unsigned long long)) != cudaSuccess) {
+            cudaGetLastError();
+            delete c;
+            return PC_ECUDA;
+        }
+        c->devs.push_back(d);
+    }
+    *out = c;
+    return PC_OK;
+}
+
+int pc_create(pc_ctx** out, int num_gpus) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        if (out) *out = nullptr;
+        return PC_ECUDA;
+    }
+    if (num_gpus == 0) num_gpus = count;
+    if (num_gpus < 0 || num_gpus > count) return PC_EINVAL;
+    std::vector<int> ids(num_gpus);
+    for (int i = 0; i < num_gpus; ++i) ids[i] = i;
+    return pc_create_devices(out, ids.data(), num_gpus);
+}
+
+void pc_destroy(pc_ctx* c) {
+    if (!c) return;
+    for (auto& d : c->devs) {
+        cudaSetDevice(d.dev);
+        cudaStreamSynchronize(d.stream);
+        for (DevBuf* b : {&d.pts, &d.vx, &d.vy, &d.ring_off, &d.pt_off, &d.poly_ring_off, &d.filt, &d.rec, &d.bbox,
+                          &d.bits, &d.verdicts, &d.stats, &d.counts, &d.degen})
+            b->release();
+        if (d.h_stats) cudaFreeHost(d.h_stats);
+        for (auto& e : d.evs) {
+            cudaEventDestroy(e.first);
+            cudaEventDestroy(e.second);
+        }
+        cudaStreamDestroy(d.stream);
+    }
+    delete c;
+}
+
+const char* pc_last_error(const pc_ctx* c) { return c ? c->err.c_str() : "null context"; }
+int pc_device_count(const pc_ctx* c) { return c ? (int)c->devs.size() : 0; }
+uint64_t pc_last_launch_count(const pc_ctx* c) { return c ? c->launches : 0; }
+
+int pc_set_profiling(pc_ctx* c, int on) {
+    if (!c) return PC_EINVAL;
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->profiling = on != 0;
+    return PC_OK;
+}
+
+int pc_profile_take(pc_ctx* c, int dev_index, double* ms_out, int cap) {
+    if (!c || dev_index < 0 || dev_index >= (int)c->devs.size()) return -1;
+    std::lock_guard<std::mutex> lk(c->mu);
+    DevState& d = c->devs[dev_index];
+    cudaSetDevice(d.dev);
+    int k = 0;
+    for (size_t i = 0; i < d.ev_used; ++i) {
+        float ms = -1.0f;
+        if (cudaEventSynchronize(d.evs[i].second) != cudaSuccess ||
+            cudaEventElapsedTime(&ms, d.evs[i].first, d.evs[i].second) != cudaSuccess) {
+            cudaGetLastError();
+            ms = -1.0f;
+        }
+        if (k < cap && ms_out) ms_out[k] = ms;
+        ++k;
+    }
+    d.ev_used = 0;
+    return k;
+}
+
+int pc_measure_fp64_rate(pc_ctx* c, int dev_index, double ms, double* flops_per_s) {
+    return guarded(c, [&] {
+        if (dev_index < 0 || dev_index >= (int)c->devs.size() || !flops_per_s) invalid(c, "bad arguments");
+        DevState& d = c->devs[dev_index];
+        check(c, cudaSetDevice(d.dev), "cudaSetDevice");
+        DevBuf out;
+        check(c, out.ensure(64), "alloc");
+        cudaEvent_t e0, e1;
+        check(c, cudaEventCreate(&e0), "event");
+        check(c, cudaEventCreate(&e1), "event");
+        double flops = 0.0;
+        int iters = 1 << 14;
+        float el = 0.0f;
+        for (int pass = 0; pass < 4; ++pass) { // calibrate to ~ms, keep the last (warm) pass
+            check(c, cudaEventRecord(e0, d.stream), "event");
+            check(c, pcd::launch_fp64_probe(out.as<double>(), iters, d.dev, d.stream, &flops), "fp64 probe");
+            check(c, cudaEventRecord(e1, d.stream), "event");
+            check(c, cudaEventSynchronize(e1), "fp64 probe");
+            check(c, cudaEventElapsedTime(&el, e0, e1), "event");
+            if (pass < 3 && el > 0.0f) iters = std::max(1, (int)(iters * (ms / el)));
+        }
+        *flops_per_s = flops / (el * 1e-3);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        out.release();
+    });
+}
+
+int pc_classify(pc_ctx* c, const double* pts_xy, uint64_t n, const double* vx, const double* vy,
+                const uint64_t* ring_off, uint32_t n_rings, int mode, double tol, int prefilter, uint8_t* verdicts,
+                uint32_t* inside_bits, uint32_t* aux_bits, uint64_t stats[4]) {
+    return guarded(c, [&] {
+        if (mode < 0 || mode > 2) invalid(c, "mode must be 0 (C1), 1 (C2) or 2 (Robust)");
+        if (!ring_off || !vx || !vy) invalid(c, "null polygon arrays");
+        validate_rings(c, ring_off, n_rings);
+        if (n && !pts_xy) invalid(c, "null points");
+        uint64_t tot[4] = {0, 0, 0, 0};
+        if (n == 0) {
+            if (stats) std::memset(stats, 0, 4 * sizeof(uint64_t));
+            return;
+        }
+        const uint64_t n_verts = ring_off[n_rings];
+        // contiguous shards, 32-point aligned so every device owns whole words
+        const uint64_t ndev = std::min<uint64_t>(c->devs.size(), std::max<uint64_t>(1, n / 32));
+        uint64_t shard = (n + ndev - 1) / ndev;
+        shard = (shard + 31) & ~31ull;
+        struct Part {
+            uint64_t lo, hi;
+        };
+        std::vector<Part> parts;
+        for (uint64_t d = 0; d < ndev; ++d) {
+            const uint64_t lo = std::min(n, d * shard), hi = std::min(n, (d + 1) * shard);
+            if (hi > lo) parts.push_back({lo, hi});
+        }
+        for (size_t i = 0; i < parts.size(); ++i) {
+            DevState& d = c->devs[i];
+            const uint64_t m = parts[i].hi - parts[i].lo, nwords = (m + 31) / 32;
+            check(c, cudaSetDevice(d.dev), "cudaSetDevice");
+            cudaStream_t st = d.stream;
+            h2d(c, d.pts, pts_xy + 2 * parts[i].lo, m * 16, st, "upload points");
+            h2d(c, d.vx, vx, n_verts * 8, st, "upload vx");
+            h2d(c, d.vy, vy, n_verts * 8, st, "upload vy");
+            h2d(c, d.ring_off, ring_off, (n_rings + 1) * 8ull, st, "upload ring_off");
+            check(c, d.bits.ensure(2 * nwords * 4), "alloc bit planes");
+            check(c, d.stats.ensure(4 * 8), "alloc stats");
+            uint8_t* dv = nullptr;
+            if (verdicts) {
+                check(c, d.verdicts.ensure(m), "alloc verdicts");
+                dv = d.verdicts.as<uint8_t>();
+            }
+            uint32_t* din = d.bits.as<uint32_t>();
+            uint32_t* daux = din + nwords;
+            enqueue_single(c, d, st, d.pts.as<double>(), m, d.vx.as<double>(), d.vy.as<double>(),
+                           d.ring_off.as<uint64_t>(), n_rings, n_verts, mode, tol, prefilter, dv, din, daux,
+                           d.stats.as<unsigned long long>());
+            if (inside_bits)
+                check(c, cudaMemcpyAsync(inside_bits + parts[i].lo / 32, din, nwords * 4, cudaMemcpyDeviceToHost, st),
+                      "download inside plane");
+            if (aux_bits)
+                check(c, cudaMemcpyAsync(aux_bits + parts[i].lo / 32, daux, nwords * 4, cudaMemcpyDeviceToHost, st),
+                      "download aux plane");
+            if (verdicts)
+                check(c, cudaMemcpyAsync(verdicts + parts[i].lo, dv, m, cudaMemcpyDeviceToHost, st),
+                      "download verdicts");
+            check(c, cudaMemcpyAsync(d.h_stats, d.stats.p, 32, cudaMemcpyDeviceToHost, st), "download stats");
+        }
+        for (size_t i = 0; i < parts.size(); ++i) {
+            DevState& d = c->devs[i];
+            check(c, cudaSetDevice(d.dev), "cudaSetDevice");
+            check(c, cudaStreamSynchronize(d.stream), "classify");
+            for (int k = 0; k < 4; ++k) tot[k] += d.h_stats[k];
+        }
+        if (stats) std::memcpy(stats, tot, sizeof(tot));
+    });
+}
+
+int pc_classify_csr(pc_ctx* c, const double* pts_xy, const uint64_t* pt_off, uint64_t n_polys, const double* vx,
+                    const double* vy, const uint64_t* ring_off, const uint64_t* poly_ring_off, int mode, double tol,
+                    uint8_t* verdicts, uint32_t* inside_bits, uint32_t* aux_bits, uint64_t stats[4]) {
+    return guarded(c, [&] {
+        if (mode < 0 || mode > 2) invalid(c, "mode must be 0 (C1), 1 (C2) or 2 (Robust)");
+        if (!pt_off || !poly_ring_off) invalid(c, "null CSR offsets");
+        uint64_t tot[4] = {0, 0, 0, 0};
+        const uint64_t n_points = n_polys ? pt_off[n_polys] - pt_off[0] : 0;
+        if (n_points == 0) {
+            if (stats) std::memset(stats, 0, sizeof(tot));
+            return;
+        }
+        if (!pts_xy || !vx || !vy || !ring_off) invalid(c, "null arrays");
+        for (uint64_t p = 0; p < n_polys; ++p)
+            if (pt_off[p + 1] < pt_off[p] || poly_ring_off[p + 1] < poly_ring_off[p])
+                invalid(c, "CSR offsets must be non-decreasing");
+        const uint64_t P0 = pt_off[0];
+        const uint64_t nwords_all = (n_points + 31) / 32;
+        if (inside_bits) std::memset(inside_bits, 0, nwords_all * 4);
+        if (aux_bits) std::memset(aux_bits, 0, nwords_all * 4);
+        // shard polygons so each device gets ~n_points/ndev points
+        const uint64_t ndev = std::min<uint64_t>(c->devs.size(), n_polys);
+        std::vector<uint64_t> cut{0};
+        for (uint64_t d = 1; d < ndev; ++d) {
+            const uint64_t target = P0 + n_points * d / ndev;
+            uint64_t p = std::lower_bound(pt_off, pt_off + n_polys + 1, target) - pt_off;
+            p = std::max(p, cut.back());
+            cut.push_back(std::min(p, n_polys));
+        }
+        cut.push_back(n_polys);
+        std::vector<std::vector<uint32_t>> tmp_in(ndev), tmp_aux(ndev);
+        for (uint64_t i = 0; i < ndev; ++i) {
+            const uint64_t p0 = cut[i], p1 = cut[i + 1];
+            DevState& d = c->devs[i];
+            const uint64_t s = pt_off[p0], t = pt_off[p1], m = t - s, nwords = (m + 31) / 32;
+            if (p1 == p0) continue;
+            check(c, cudaSetDevice(d.dev), "cudaSetDevice");
+            cudaStream_t st = d.stream;
+            const uint64_t r0 = poly_ring_off[p0], r1 = poly_ring_off[p1];
+            const uint64_t v0 = r1 > r0 ? ring_off[r0] : 0, v1 = r1 > r0 ? ring_off[r1] : 0;
+            h2d(c, d.pts, pts_xy + 2 * (s - P0), m * 16, st, "upload points");
+            h2d(c, d.pt_off, pt_off + p0, (p1 - p0 + 1) * 8, st, "upload pt_off");
+            h2d(c, d.poly_ring_off, poly_ring_off + p0, (p1 - p0 + 1) * 8, st, "upload poly_ring_off");
+            h2d(c, d.ring_off, ring_off + r0, (r1 - r0 + 1) * 8, st, "upload ring_off");
+            h2d(c, d.vx, vx + v0, (v1 - v0) * 8, st, "upload vx");
+            h2d(c, d.vy, vy + v0, (v1 - v0) * 8, st, "upload vy");
+            check(c, d.bits.ensure(2 * nwords * 4), "alloc bit planes");
+            check(c, d.stats.ensure(32), "alloc stats");
+            uint8_t* dv = nullptr;
+            if (verdicts) {
+                check(c, d.verdicts.ensure(m), "alloc verdicts");
+                dv = d.verdicts.as<uint8_t>();
+            }
+            uint32_t* din = d.bits.as<uint32_t>();
+            uint32_t* daux = din + nwords;
+            enqueue_csr(c, d, st, d.pts.as<double>(), m, d.pt_off.as<uint64_t>(), p1 - p0, d.vx.as<double>(),
+                        d.vy.as<double>(), d.ring_off.as<uint64_t>(), d.poly_ring_off.as<uint64_t>(), s, r0, v0, mode,
+                        tol, dv, din, daux, d.stats.as<unsigned long long>());
+            tmp_in[i].resize(nwords);
+            tmp_aux[i].resize(nwords);
+            if (inside_bits)
+                check(c, cudaMemcpyAsync(tmp_in[i].data(), din, nwords * 4, cudaMemcpyDeviceToHost, st), "download");
+            if (aux_bits)
+                check(c, cudaMemcpyAsync(tmp_aux[i].data(), daux, nwords * 4, cudaMemcpyDeviceToHost, st), "download");
+            if (verdicts)
+                check(c, cudaMemcpyAsync(verdicts + (s - P0), dv, m, cudaMemcpyDeviceToHost, st), "download verdicts");
+            check(c, cudaMemcpyAsync(d.h_stats, d.stats.p, 32, cudaMemcpyDeviceToHost, st), "download stats");
+        }
+        for (uint64_t i = 0; i < ndev; ++i) {
+            if (cut[i + 1] == cut[i]) continue;
+            DevState& d = c->devs[i];
+            check(c, cudaSetDevice(d.dev), "cudaSetDevice");
+            check(c, cudaStreamSynchronize(d.stream), "classify_csr");
+            for (int k = 0; k < 4; ++k) tot[k] += d.h_stats[k];
+            const uint64_t s = pt_off[cut[i]] - P0, m = pt_off[cut[i + 1]] - pt_off[cut[i]];
+            if (inside_bits) merge_bits(inside_bits, tmp_in[i].data(), s, m);
+            if (aux_bits) merge_bits(aux_bits, tmp_aux[i].data(), s, m);
+        }
+        if (stats) std::memcpy(stats, tot, sizeof(tot));
+    });
+}
+
+int pc_count_crossings(pc_ctx* c, const double* pts_xy, uint64_t n, const double* vx, const double* vy, uint64_t nv,
+                       int mode, uint64_t* counts, uint8_t* degenerate) {
+    return guarded(c, [&] {
+        if (mode != 0 && mode != 1) invalid(c, "count_crossings: mode must be 0 (C1) or 1 (C2)");
+        if (n == 0) return;
+        if (!pts_xy || !counts || !degenerate || (nv && (!vx || !vy))) invalid(c, "null arrays");
+        DevState& d = c->devs[0];
+        check(c, cudaSetDevice(d.dev), "cudaSetDevice");
+        cudaStream_t st = d.stream;
+        h2d(c, d.pts, pts_xy, n * 16, st, "upload points");
+        h2d(c, d.vx, vx, nv * 8, st, "upload vx");
+        h2d(c, d.vy, vy, nv * 8, st, "upload vy");
+        check(c, d.counts.ensure(n * 8), "alloc counts");
+        check(c, d.degen.ensure(n), "alloc flags");
+        check(c, pcd::launch_count(d.pts.as<double>(), n, d.vx.as<double>(), d.vy.as<double>(), nv, mode,
+                                   d.counts.as<unsigned long long>(), d.degen.as<uint8_t>(), st, &c->launches),
+              "count kernel");
+        check(c, cudaMemcpyAsync(counts, d.counts.p, n * 8, cudaMemcpyDeviceToHost, st), "download counts");
+        check(c, cudaMemcpyAsync(degenerate, d.degen.p, n, cudaMemcpyDeviceToHost, st), "download flags");
+        check(c, cudaStreamSynchronize(st), "count_crossings");
+    });
+}
+
+int pc_classify_dev(pc_ctx* c, int dev_index, void* stream, const double* d_pts_xy, uint64_t n, const double* d_vx,
+                    const double* d_vy, const uint64_t* d_ring_off, uint32_t n_rings, uint64_t n_verts, int mode,
+                    double tol, int prefilter, uint8_t* d_verdicts, uint32_t* d_inside, uint32_t* d_aux,
+                    uint64_t* d_stats) {
+    return guarded(c, [&] {
+        if (dev_index < 0 || dev_index >= (int)c->devs.size()) invalid(c, "bad device index");
+        if (mode < 0 || mode > 2) invalid(c, "mode must be 0 (C1), 1 (C2) or 2 (Robust)");
+        if (n_rings < 1 || n_verts < n_rings) invalid(c, "bad ring layout");
+        if (!d_inside || !d_aux || !d_stats) invalid(c, "null output planes");
+        DevState& d = c->devs[dev_index];
+        check(c, cudaSetDevice(d.dev), "cudaSetDevice");
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d.stream;
+        if (n == 0) {
+            check(c, cudaMemsetAsync(d_stats, 0, 32, st), "clear stats");
+            return;
+        }
+        enqueue_single(c, d, st, d_pts_xy, n, d_vx, d_vy, d_ring_off, n_rings, n_verts, mode, tol, prefilter,
+                       d_verdicts, d_inside, d_aux, reinterpret_cast<unsigned long long*>(d_stats));
+    });
+}
+
+int pc_classify_csr_dev(pc_ctx* c, int dev_index, void* stream, const double* d_pts_xy, const uint64_t* d_pt_off,
+                        uint64_t n_polys, uint64_t n_points, const double* d_vx, const double* d_vy,
+                        const uint64_t* d_ring_off, const uint64_t* d_poly_ring_off, int mode, double tol,
+                        uint8_t* d_verdicts, uint32_t* d_inside, uint32_t* d_aux, uint64_t* d_stats) {
+    return guarded(c, [&] {
+        if (dev_index < 0 || dev_index >= (int)c->devs.size()) invalid(c, "bad device index");
+        if (mode < 0 || mode > 2) invalid(c, "mode must be 0 (C1), 1 (C2) or 2 (Robust)");
+        if (!d_inside || !d_aux || !d_stats) invalid(c, "null output planes");
+        DevState& d = c->devs[dev_index];
+        check(c, cudaSetDevice(d.dev), "cudaSetDevice");
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d.stream;
+        if (n_points == 0) {
+            check(c, cudaMemsetAsync(d_stats, 0, 32, st), "clear stats");
+            return;
+        }
+        enqueue_csr(c, d, st, d_pts_xy, n_points, d_pt_off, n_polys, d_vx, d_vy, d_ring_off, d_poly_ring_off, 0, 0, 0,
+                    mode, tol, d_verdicts, d_inside, d_aux, reinterpret_cast<unsigned long long*>(d_stats));
+    });
+}
+
+} // extern "C"

@@ -1,0 +1,153 @@
+// Device-side arithmetic of the point-in-polygon crossing tests.
+//
+// Every floating-point operation is an explicit round-to-nearest binary64
+// intrinsic (__dadd_rn/__dsub_rn/__dmul_rn/__ddiv_rn), so nvcc can neither
+// contract a multiply-add into a DFMA nor reassociate: each expression
+// evaluates exactly as the reference's C++ does on an x86-64 host
+// (SURVEY §8 rules P1, P2, P6, P7).
+#pragma once
+
+#include <cstdint>
+
+namespace pcd {
+
+enum Mode : int { kC1 = 0, kC2 = 1, kRobust = 2 };
+
+// Per-edge record staged in shared memory, mode-specific, precomputed once per
+// call by prep_edges_kernel from the raw vertices with the same RN operations
+// the reference performs per (point, edge):
+//   C1:     ax ay by nx ny   (n = (b.y-a.y, a.x-b.x), flipped so nx >= 0; geometry.hpp:191-196)
+//   C2:     ax ay by dx dy   (dx = b.x-a.x, dy = b.y-a.y; geometry.hpp:216-222)
+//   Robust: ax ay by abx aby len2 ylo yhi  (geometry.hpp:245-254)
+struct __align__(16) EdgeRec {
+    double d[8];
+};
+
+// Monotone 32-bit key of a double through its binary32 rounding.
+//   key(u) < key(v)  =>  u < v  (strictly),  and  u <= v  =>  key(u) <= key(v).
+// RN to binary32 is monotone non-decreasing; -0 is canonicalised to +0 so the
+// integer order equals the float order.  Values that share a key are "ties"
+// and always take the exact binary64 path, so the filter below never decides a
+// case the reference decides differently (proof in DESIGN.md §3).
+__device__ __forceinline__ int fkey(double v) {
+    const float f = __fadd_rn(__double2float_rn(v), 0.0f);
+    const int i = __float_as_int(f);
+    return i >= 0 ? i : (i ^ 0x7fffffff);
+}
+
+// Unsigned monotone 64-bit key of a double (for bbox atomics).
+__device__ __forceinline__ unsigned long long dkey(double v) {
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(__dadd_rn(v, 0.0)));
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double dkey_inv(unsigned long long k) {
+    const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+    return __longlong_as_double(static_cast<long long>(b));
+}
+
+// C1 exact test of one straddle candidate (geometry.hpp:189-200).
+__device__ __forceinline__ void exact_c1(double px, double py, const EdgeRec& r, int& cnt) {
+    const double ax = r.d[0], ay = r.d[1], by = r.d[2], nx = r.d[3], ny = r.d[4];
+    const double f_prev = __dsub_rn(ay, py);
+    const double f_next = __dsub_rn(by, py);
+    if (__dmul_rn(f_prev, f_next) <= 0.0) {
+        const double side = __dadd_rn(__dmul_rn(__dsub_rn(px, ax), nx), __dmul_rn(__dsub_rn(py, ay), ny));
+        if (side <= 0.0) ++cnt;
+    }
+}
+
+// C2 exact test (geometry.hpp:214-226); `err` marks the DegenerateEdge throw.
+__device__ __forceinline__ void exact_c2(double px, double py, const EdgeRec& r, int& cnt, bool& err) {
+    const double ax = r.d[0], ay = r.d[1], by = r.d[2], dx = r.d[3], dy = r.d[4];
+    const double f_prev = __dsub_rn(ay, py);
+    const double f_next = __dsub_rn(by, py);
+    if (__dmul_rn(f_prev, f_next) <= 0.0) {
+        if (dy == 0.0) {
+            err = true;
+        } else {
+            const double lambda = __ddiv_rn(__dsub_rn(py, ay), dy);
+            const double x = __dadd_rn(ax, __dmul_rn(lambda, dx));
+            if (x > px) ++cnt;
+        }
+    }
+}
+
+// Robust exact test (geometry.hpp:245-270); `bnd` marks on_boundary.
+__device__ __forceinline__ void exact_robust(double px, double py, double tol, double tol2,
+                                             const EdgeRec& r, int& cnt, bool& bnd) {
+    const double ax = r.d[0], ay = r.d[1], by = r.d[2], abx = r.d[3], aby = r.d[4], len2 = r.d[5],
+                 ylo = r.d[6], yhi = r.d[7];
+    if (__dadd_rn(py, tol) < ylo || __dsub_rn(py, tol) > yhi) return;
+    const double apx = __dsub_rn(px, ax);
+    const double apy = __dsub_rn(py, ay);
+    double t = __ddiv_rn(__dadd_rn(__dmul_rn(apx, abx), __dmul_rn(apy, aby)), len2);
+    t = (t < 0.0) ? 0.0 : ((1.0 < t) ? 1.0 : t); // std::clamp(t, 0.0, 1.0), NaN propagates
+    const double dx = __dsub_rn(apx, __dmul_rn(t, abx));
+    const double dyp = __dsub_rn(apy, __dmul_rn(t, aby));
+    if (__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dyp, dyp)) <= tol2) {
+        bnd = true;
+        return;
+    }
+    const bool upward = ay <= py && py < by;
+    const bool downward = by <= py && py < ay;
+    if (upward || downward) {
+        const double x = __dadd_rn(ax, __dmul_rn(__ddiv_rn(apy, aby), abx));
+        if (x > px) ++cnt;
+    }
+}
+
+// Literal per-edge step over raw vertices, for the CSR kernels and the count
+// kernel (which walk rings directly).  `f_prev` carries b.y - p.y to the next
+// edge exactly as the reference loop does.
+template <int MODE>
+__device__ __forceinline__ void raw_edge(double px, double py, double tol, double tol2, double ax,
+                                         double ay, double bx, double by, double& f_prev, int& cnt,
+                                         bool& aux) {
+    if (MODE == kRobust) {
+        const double ylo = by < ay ? by : ay;
+        const double yhi = ay < by ? by : ay;
+        if (__dadd_rn(py, tol) < ylo || __dsub_rn(py, tol) > yhi) return;
+        const double abx = __dsub_rn(bx, ax), aby = __dsub_rn(by, ay);
+        const double apx = __dsub_rn(px, ax), apy = __dsub_rn(py, ay);
+        const double len2 = __dadd_rn(__dmul_rn(abx, abx), __dmul_rn(aby, aby));
+        double t = __ddiv_rn(__dadd_rn(__dmul_rn(apx, abx), __dmul_rn(apy, aby)), len2);
+        t = (t < 0.0) ? 0.0 : ((1.0 < t) ? 1.0 : t);
+        const double dx = __dsub_rn(apx, __dmul_rn(t, abx));
+        const double dyp = __dsub_rn(apy, __dmul_rn(t, aby));
+        if (__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dyp, dyp)) <= tol2) {
+            aux = true;
+            return;
+        }
+        if ((ay <= py && py < by) || (by <= py && py < ay)) {
+            const double x = __dadd_rn(ax, __dmul_rn(__ddiv_rn(apy, aby), abx));
+            if (x > px) ++cnt;
+        }
+    } else {
+        const double f_next = __dsub_rn(by, py);
+        if (__dmul_rn(f_prev, f_next) <= 0.0) {
+            if (MODE == kC1) {
+                double nx = __dsub_rn(by, ay);
+                double ny = __dsub_rn(ax, bx);
+                if (nx < 0.0) {
+                    nx = -nx;
+                    ny = -ny;
+                }
+                const double side =
+                    __dadd_rn(__dmul_rn(__dsub_rn(px, ax), nx), __dmul_rn(__dsub_rn(py, ay), ny));
+                if (side <= 0.0) ++cnt;
+            } else {
+                const double dy = __dsub_rn(by, ay);
+                if (dy == 0.0) {
+                    aux = true;
+                } else {
+                    const double lambda = __ddiv_rn(__dsub_rn(py, ay), dy);
+                    const double x = __dadd_rn(ax, __dmul_rn(lambda, __dsub_rn(bx, ax)));
+                    if (x > px) ++cnt;
+                }
+            }
+        }
+        f_prev = f_next;
+    }
+}
+
+} // namespace pcd

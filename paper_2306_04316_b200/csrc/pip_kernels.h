@@ -1,0 +1,66 @@
+// Host-side launch interface of the sm_100a point-in-polygon kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace pcd {
+
+struct PrepArgs {
+    int mode;
+    const double* vx;
+    const double* vy;
+    const uint64_t* ring_off;
+    uint32_t n_rings;
+    uint64_t n_verts;
+    uint2* filt;                  // n_edges filter key pairs
+    void* rec;                    // n_edges EdgeRec (edge_rec_bytes() each)
+    unsigned long long* bbox_keys; // 4 monotone keys: min x, min y, ~max x, ~max y
+    uint32_t* zero_words;          // output bit planes to clear (inside ++ aux, contiguous)
+    uint64_t n_zero_words;
+    unsigned long long* stats;     // 4 counters to clear
+};
+
+struct SingleArgs {
+    int mode;
+    const double* pts;
+    uint64_t n;
+    const uint2* filt;
+    const void* rec;
+    uint32_t n_edges;
+    const unsigned long long* bbox_keys;
+    int prefilter;
+    double tol, tol2;
+    uint32_t* inside_bits;
+    uint32_t* aux_bits;
+};
+
+struct CsrArgs {
+    int mode;
+    const double* pts;
+    const uint64_t* pt_off;
+    uint64_t n_polys;
+    const double* vx;
+    const double* vy;
+    const uint64_t* ring_off;
+    const uint64_t* poly_ring_off;
+    uint64_t pt_base, ring_base, vert_base; // subtracted from pt_off / poly_ring_off / ring_off values
+    double tol, tol2;
+    uint32_t* inside_bits;
+    uint32_t* aux_bits;
+};
+
+size_t edge_rec_bytes();
+cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st, int dev, uint64_t* launches);
+cudaError_t launch_single(const SingleArgs& a, cudaStream_t st, int dev, uint64_t* launches);
+cudaError_t launch_csr(const CsrArgs& a, cudaStream_t st, int dev, uint64_t* launches);
+cudaError_t launch_finalize(uint64_t n, uint32_t* inside_bits, const uint32_t* aux_bits, uint8_t* verdicts,
+                            int mode, unsigned long long* stats, cudaStream_t st, int dev, uint64_t* launches);
+cudaError_t launch_count(const double* pts, uint64_t n, const double* vx, const double* vy, uint64_t nv, int mode,
+                         unsigned long long* counts, uint8_t* degenerate, cudaStream_t st, uint64_t* launches);
+
+cudaError_t launch_fp64_probe(double* out, int iters, int dev, cudaStream_t st, double* flops);
+
+} // namespace pcd

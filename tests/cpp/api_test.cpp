@@ -1,0 +1,218 @@
+// Drop-in C++ API test: the reference's own known-answer tests and properties
+// (proj/tests/unit/geometry_test.cpp, batch_test.cpp, acceptance.cpp checks
+// 3, 7, 8, 9), re-expressed against include/polycast/*.hpp, which evaluates
+// on the GPU through libpolycast_cuda.so.  Random cases are cross-checked
+// against the unmodified reference (oracle/_ref/libpolycast_ref.so, loaded
+// with dlopen) when it is present.  Exit code = number of failed checks.
+#include <dlfcn.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numbers>
+#include <random>
+#include <string>
+#include <vector>
+
+#include <polycast/polycast.hpp>
+
+using namespace polycast;
+
+static int g_checks = 0, g_fail = 0;
+#define CHECK(cond)                                                              \
+    do {                                                                         \
+        ++g_checks;                                                              \
+        if (!(cond)) {                                                           \
+            ++g_fail;                                                            \
+            std::fprintf(stderr, "FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond); \
+        }                                                                        \
+    } while (0)
+#define CHECK_THROWS(expr, Ex)                   \
+    do {                                         \
+        bool thrown_ = false;                    \
+        try {                                    \
+            (void)(expr);                        \
+        } catch (const Ex&) {                    \
+            thrown_ = true;                      \
+        }                                        \
+        CHECK(thrown_ && #expr " throws " #Ex);  \
+    } while (0)
+
+namespace {
+
+double uni(std::mt19937_64& g, double lo, double hi) { return lo + (double)(g() >> 11) * 0x1.0p-53 * (hi - lo); }
+
+Ring square() { return Ring({{0, 0}, {1, 0}, {1, 1}, {0, 1}, {0, 0}}); }
+
+Ring star(std::mt19937_64& g, std::size_t n, Point2 c, double r0, double r1) {
+    std::vector<Point2> v;
+    const double step = 2.0 * std::numbers::pi / (double)n;
+    for (std::size_t i = 0; i < n; ++i) {
+        const double th = step * ((double)i + uni(g, 0.05, 0.95));
+        const double r = uni(g, r0, r1);
+        v.emplace_back(c.x + r * std::cos(th), c.y + r * std::sin(th));
+    }
+    v.push_back(v.front());
+    return Ring(std::move(v));
+}
+
+Polygon random_polygon(std::mt19937_64& g, std::size_t n) {
+    const Point2 c(uni(g, -10, 10), uni(g, -10, 10));
+    const double R = uni(g, 0.5, 20.0);
+    if (g() % 2 == 0) return Polygon(star(g, n, c, R, R));
+    return Polygon(star(g, n, c, 0.35 * R, R));
+}
+
+// reference classify_batch through the oracle shim (optional)
+using RefClassify = int (*)(const double*, uint64_t, const double*, const double*, const uint64_t*, uint32_t, int,
+                            double, uint64_t, uint8_t*, uint64_t*);
+RefClassify g_ref = nullptr;
+
+void kats() {
+    const Ring sq = square();
+    const Polygon sqp(sq);
+    // geometry_test.cpp:34-50 — type validation
+    CHECK_THROWS(Point2(std::nan(""), 0.0), std::invalid_argument);
+    CHECK_THROWS(Point2(0.0, INFINITY), std::invalid_argument);
+    CHECK_THROWS(Ring({{0, 0}, {1, 0}, {0, 0}}), std::invalid_argument);
+    CHECK_THROWS(Ring({{0, 0}, {1, 0}, {1, 1}, {0, 1}}), std::invalid_argument);
+    CHECK_THROWS(Ring({{0, 0}, {1, 0}, {1, 0}, {0, 1}, {0, 0}}), std::invalid_argument);
+    // composed helpers (geometry_test.cpp:52-93)
+    CHECK((signed_offsets(sq, 0.5) == std::vector<double>{-0.5, -0.5, 0.5, 0.5, -0.5}));
+    CHECK((detect_sign_changes(std::vector<double>{0, 0, 1, 1, 0}) == std::vector<std::size_t>{0, 1, 3}));
+    CHECK(crossing_x({0, 0}, {2, 4}, 2.0) == 1.0);
+    CHECK_THROWS(crossing_x({3, 2}, {5, 2}, 2.0), DegenerateEdge);
+    CHECK(edge_normal({0, 1}, {0, 0}).nx == 1.0);
+    CHECK(edge_normal({0, 0}, {2, 4}).ny == -2.0);
+    CHECK(segment_distance({5, 0}, {0, 0}, {1, 0}) == 4.0);
+    // unit-square crossing counts (geometry_test.cpp:95-105) — on the GPU
+    CHECK(count_crossings_c1({0.5, 0.5}, sq) == 1);
+    CHECK(count_crossings_c1({-1.0, 0.5}, sq) == 2);
+    CHECK(count_crossings_c1({2.0, 0.5}, sq) == 0);
+    CHECK(count_crossings_c2({0.5, 0.5}, sq) == 1);
+    CHECK(count_crossings_c2({-1.0, 0.5}, sq) == 2);
+    CHECK_THROWS(count_crossings_c2({0.5, 0.0}, sq), DegenerateEdge);
+    // verdicts (geometry_test.cpp:107-121; acceptance check 3)
+    for (CrossingMode m : {CrossingMode::C1, CrossingMode::C2, CrossingMode::Robust}) {
+        CHECK(contains({0.5, 0.5}, sqp, m) == Classification::Inside);
+        CHECK(contains({5.0, 5.0}, sqp, m) == Classification::Outside);
+    }
+    CHECK(contains({1.0, 0.5}, sqp, CrossingMode::Robust) == Classification::Boundary);
+    CHECK_THROWS(contains({0.5, 0.0}, sqp, CrossingMode::C2), DegenerateEdge);
+    CHECK(contains({0.5, 0.0}, sqp, CrossingMode::Robust) == Classification::Boundary);
+    // holes (geometry_test.cpp:123-137)
+    const Polygon holed(square(), {Ring({{0.25, 0.25}, {0.75, 0.25}, {0.75, 0.75}, {0.25, 0.75}, {0.25, 0.25}})});
+    CHECK(contains({0.5, 0.5}, holed, CrossingMode::Robust) == Classification::Outside);
+    CHECK(contains({0.1, 0.5}, holed, CrossingMode::Robust) == Classification::Inside);
+    CHECK(contains({0.5, 0.5}, holed, CrossingMode::C1) == Classification::Outside);
+    // vertex on ray (geometry_test.cpp:145-160)
+    const Ring diamond({{0, 0}, {2, 2}, {4, 0}, {2, -2}, {0, 0}});
+    CHECK(count_crossings_c1({-3.0, 0.0}, diamond) == 4);
+    CHECK(contains({-3.0, 0.0}, Polygon(diamond), CrossingMode::C1) == Classification::Outside);
+    CHECK(contains({2.0, 0.0}, Polygon(diamond), CrossingMode::Robust) == Classification::Inside);
+    // prefilter changes C1 verdicts on degenerate rays
+    CHECK(contains({-1.0, 1.0}, sqp, CrossingMode::C1) == Classification::Inside);
+    {
+        PointBatch b;
+        b.points = {{-1.0, 1.0}};
+        CHECK(classify_batch(b, sqp, CrossingMode::C1).verdicts[0] == Verdict::Outside);
+    }
+    // batch probes (batch_test.cpp:65-85; acceptance check 9)
+    {
+        PointBatch b;
+        b.points = {{0.5, 0.5}, {1.5, 0.5}, {0.5, -0.5}, {-0.5, 0.5}};
+        const BatchResult r = classify_batch(b, sqp, CrossingMode::Robust);
+        CHECK((r.verdicts == std::vector<Verdict>{Verdict::Inside, Verdict::Outside, Verdict::Outside, Verdict::Outside}));
+        CHECK(r.stats.inside == 1 && r.stats.outside == 3 && r.stats.total() == 4);
+    }
+    {
+        PointBatch b;
+        b.points = {{0.5, 0.0}, {0.5, 0.5}, {-2.0, 0.5}};
+        const BatchResult r = classify_batch(b, sqp, CrossingMode::C2);
+        CHECK(r.verdicts[0] == Verdict::Error && r.verdicts[1] == Verdict::Inside && r.verdicts[2] == Verdict::Outside);
+        CHECK(r.stats.error == 1 && r.stats.total() == 3);
+    }
+    {
+        PointBatch b;
+        b.points = {{0.5, 0.0}, {-5.0, 0.0}, {0.5, 0.5}};
+        const BatchResult r = classify_batch(b, sqp, CrossingMode::C2, 2);
+        CHECK(r.verdicts[0] == Verdict::Error && r.verdicts[1] == Verdict::Outside && r.verdicts[2] == Verdict::Inside);
+    }
+    CHECK(classify_batch(PointBatch{}, sqp, CrossingMode::Robust).verdicts.empty());
+    CHECK(bbox_of(Polygon(Ring({{-2, 3}, {5, 3}, {5, 7}, {-2, 7}, {-2, 3}}))) == BBox(-2, 3, 5, 7));
+}
+
+void randomized() {
+    std::mt19937_64 g(42);
+    int compared = 0;
+    for (int trial = 0; trial < 30; ++trial) {
+        const Polygon poly = trial % 5 == 4 ? Polygon(star(g, 40, {0, 0}, 5, 9), {star(g, 12, {0, 0}, 1, 3)})
+                                            : random_polygon(g, 5 + g() % 300);
+        const BBox box = bbox_of(poly).inflated(0.3);
+        PointBatch b;
+        for (int i = 0; i < 20000; ++i) b.points.emplace_back(uni(g, box.min_x, box.max_x), uni(g, box.min_y, box.max_y));
+        for (CrossingMode m : {CrossingMode::C1, CrossingMode::C2, CrossingMode::Robust}) {
+            const BatchResult r = classify_batch(b, poly, m);
+            CHECK(r.stats.total() == b.size());
+            // identical for any "workers" value (batch_test.cpp:87-105)
+            CHECK(classify_batch(b, poly, m, 3) == r);
+            if (g_ref) {
+                std::vector<double> x, y;
+                std::vector<uint64_t> off{0};
+                for (const Ring& ring : poly.rings()) {
+                    for (const Point2& v : ring.vertices()) { x.push_back(v.x); y.push_back(v.y); }
+                    off.push_back(x.size());
+                }
+                std::vector<uint8_t> want(b.size());
+                uint64_t st[4];
+                g_ref(&b.points[0].x, b.size(), x.data(), y.data(), off.data(), (uint32_t)(off.size() - 1), (int)m,
+                      kDefaultBoundaryTol, 0, want.data(), st);
+                bool same = std::memcmp(want.data(), r.verdicts.data(), b.size()) == 0;
+                CHECK(same && "classify_batch bit-identical to the reference");
+                CHECK(st[0] == r.stats.inside && st[1] == r.stats.outside && st[2] == r.stats.boundary &&
+                      st[3] == r.stats.error);
+                ++compared;
+            }
+        }
+    }
+    // many-polygon extension == per-polygon classify_batch
+    std::vector<Polygon> polys;
+    std::vector<PointBatch> batches;
+    for (int i = 0; i < 50; ++i) {
+        polys.push_back(random_polygon(g, 4 + g() % 12));
+        const BBox box = bbox_of(polys.back()).inflated(0.5);
+        PointBatch b;
+        const int np = (int)(g() % 70);
+        for (int k = 0; k < np; ++k) b.points.emplace_back(uni(g, box.min_x, box.max_x), uni(g, box.min_y, box.max_y));
+        batches.push_back(std::move(b));
+    }
+    for (CrossingMode m : {CrossingMode::C1, CrossingMode::C2, CrossingMode::Robust}) {
+        const BatchResult many = classify_batch_many(batches, polys, m);
+        std::size_t off = 0;
+        bool ok = true;
+        for (std::size_t i = 0; i < polys.size(); ++i) {
+            const BatchResult one = classify_batch(batches[i], polys[i], m);
+            for (std::size_t k = 0; k < one.verdicts.size(); ++k) ok = ok && one.verdicts[k] == many.verdicts[off + k];
+            off += one.verdicts.size();
+        }
+        CHECK(ok && off == many.verdicts.size());
+    }
+    std::printf("randomized: %d polygon x mode cases compared against the reference\n", compared);
+}
+
+} // namespace
+
+int main(int argc, char** argv) {
+    const char* ref_path = argc > 1 ? argv[1] : "oracle/_ref/libpolycast_ref.so";
+    if (void* h = dlopen(ref_path, RTLD_NOW)) g_ref = reinterpret_cast<RefClassify>(dlsym(h, "ref_classify"));
+    else std::printf("note: reference shim not found at %s; reference cross-check skipped\n", ref_path);
+    try {
+        kats();
+        randomized();
+    } catch (const std::exception& e) {
+        std::fprintf(stderr, "FAIL: uncaught exception: %s\n", e.what());
+        return 100;
+    }
+    std::printf("api_test: %d checks, %d failed\n", g_checks, g_fail);
+    return g_fail;
+}

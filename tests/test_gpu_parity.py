@@ -1,0 +1,289 @@
+"""GPU parity: libpolycast_cuda.so (through the C-ABI) vs the oracle, bit-exact.
+
+Checker: the unmodified reference (oracle/_ref/libpolycast_ref.so, built from
+/root/reference and shipped prebuilt) wherever it can express the input, the C
+restatement (oracle/build/libpip_oracle.so, pinned to the reference in
+test_oracle.py) for duplicate-vertex inputs (P8) and for large CSR sets.
+Sizes: full BASELINE configs where the checker finishes in seconds, seeded
+subsamples of the same inputs otherwise, plus size-independent properties at
+full size.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import adversarial
+import oracle
+from paper_2306_04316_b200 import CrossingMode, DegenerateEdge, Engine, unpack_bits, verdicts_to_bits
+from paper_2306_04316_b200 import workloads as W
+from paper_2306_04316_b200.engine import Classification, CsrSet, Polygon
+
+pytestmark = pytest.mark.gpu
+MODES = (0, 1, 2)
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "golden_v1.npz")
+THREADS = os.cpu_count() or 8
+
+
+def check_single(xy, poly, mode, got, prefilter=True, source=None):
+    if source is None:
+        source = "reference" if oracle.ref_available() and prefilter else "port"
+    if source == "reference":
+        want_v, want_s = oracle.ref_classify(xy, poly.vx, poly.vy, poly.ring_off, mode)
+    else:
+        want_v, want_s = oracle.port_classify(xy, poly.vx, poly.vy, poly.ring_off, mode, prefilter=prefilter,
+                                              threads=THREADS)
+    assert np.array_equal(got.verdicts, want_v), f"mode {mode}: {(got.verdicts != want_v).sum()} verdicts differ"
+    assert np.array_equal(got.stats, want_s)
+    ib, ab = verdicts_to_bits(want_v, mode)
+    if got.inside_bits is not None:
+        assert np.array_equal(got.inside_bits, ib) and np.array_equal(got.aux_bits, ab)
+
+
+# ---- golden vectors -----------------------------------------------------------
+
+def test_golden_vectors(engine):
+    g = np.load(GOLDEN)
+    for name in (str(n) for n in g["__names__"]):
+        for mode in MODES:
+            if str(g[f"{name}/kind"]) == "single":
+                poly = Polygon(g[f"{name}/vx"], g[f"{name}/vy"], g[f"{name}/ring_off"])
+                xy = g[f"{name}/xy"]
+                r = engine.classify(xy, poly, mode)
+                assert np.array_equal(r.verdicts, g[f"{name}/verdicts{mode}"]), (name, mode)
+                assert np.array_equal(r.stats, g[f"{name}/stats{mode}"]), (name, mode)
+                r0 = engine.classify(xy, poly, mode, prefilter=False)
+                assert np.array_equal(r0.verdicts, g[f"{name}/contains{mode}"]), (name, mode, "contains")
+            else:
+                s = CsrSet(*(g[f"{name}/{k}"] for k in ("xy", "pt_off", "vx", "vy", "ring_off", "poly_ring_off")))
+                r = engine.classify_csr(s, mode)
+                assert np.array_equal(r.verdicts, g[f"{name}/verdicts{mode}"]), (name, mode)
+                assert np.array_equal(r.stats, g[f"{name}/stats{mode}"]), (name, mode)
+
+
+@pytest.mark.parametrize("case", adversarial.cases(), ids=[c[0] for c in adversarial.cases()])
+def test_adversarial(engine, case):
+    name, poly, xy = case
+    src = "port" if name == "dup_vertices" else None
+    for mode in MODES:
+        check_single(xy, poly, mode, engine.classify(xy, poly, mode), source=src)
+        check_single(xy, poly, mode, engine.classify(xy, poly, mode, prefilter=False), prefilter=False)
+
+
+# ---- KATs through the Python mirror of the reference API ------------------------
+
+def test_reference_kats(engine):
+    sq = Polygon.from_rings([adversarial.SQUARE])
+    for mode in (CrossingMode.C1, CrossingMode.C2, CrossingMode.Robust):
+        assert engine.contains((0.5, 0.5), sq, mode) == Classification.Inside
+        assert engine.contains((5.0, 5.0), sq, mode) == Classification.Outside
+    assert engine.contains((1.0, 0.5), sq, CrossingMode.Robust) == Classification.Boundary
+    with pytest.raises(DegenerateEdge):
+        engine.contains((0.5, 0.0), sq, CrossingMode.C2)
+    counts, deg = engine.count_crossings([[0.5, 0.5], [-1.0, 0.5], [2.0, 0.5]], sq.vx, sq.vy, CrossingMode.C1)
+    assert list(counts) == [1, 2, 0] and not deg.any()
+    dm = Polygon.from_rings([adversarial.DIAMOND])
+    counts, _ = engine.count_crossings([[-3.0, 0.0]], dm.vx, dm.vy, CrossingMode.C1)
+    assert counts[0] == 4
+    r = engine.classify_batch([[0.5, 0.0], [0.5, 0.5], [-2.0, 0.5]], sq, CrossingMode.C2)
+    assert list(r.verdicts) == [3, 0, 1] and r.stats[3] == 1
+
+
+def test_count_crossings_vs_reference(engine):
+    rng = np.random.default_rng(5)
+    for n in (5, 37, 400, 3000):
+        poly = W.star_polygon(n, seed=n)
+        xy = W.uniform_points(3000, W.bounds(poly), n)
+        xy[:200] = np.stack([rng.choice(poly.vx, 200), rng.choice(poly.vy, 200)], 1)  # rays through vertices
+        for mode in (0, 1):
+            c, d = engine.count_crossings(xy, poly.vx, poly.vy, mode)
+            wc, wd = oracle.port_count_crossings(xy, poly.vx, poly.vy, mode)
+            assert np.array_equal(d, wd)
+            assert np.array_equal(c[wd == 0], wc[wd == 0])
+            if oracle.ref_available():
+                for i in range(0, 3000, 97):
+                    want = oracle.ref_count_crossings(xy[i], poly.vx, poly.vy, mode)
+                    assert (want is None) == bool(d[i])
+                    if want is not None:
+                        assert c[i] == want
+
+
+# ---- configs ----------------------------------------------------------------------
+
+def test_config1_full(engine):
+    poly, xy = W.config1()
+    for mode in MODES:
+        check_single(xy, poly, mode, engine.classify_batch(xy, poly, mode))
+
+
+@pytest.mark.parametrize("n", W.SWEEP_N)
+def test_config2_sweep(engine, n):
+    poly, xy = W.config2(n)
+    for mode in MODES:
+        got = engine.classify_batch(xy, poly, mode)
+        assert int(got.stats.sum()) == len(xy)
+        if n <= 10_000:
+            check_single(xy, poly, mode, got)
+        else:  # seeded subsample keeps the CPU checker to seconds
+            idx = np.random.default_rng(n + mode).choice(len(xy), 20_000 if n == 100_000 else 2_000, replace=False)
+            sub = np.ascontiguousarray(xy[idx])
+            want_v, _ = (oracle.ref_classify(sub, poly.vx, poly.vy, poly.ring_off, mode) if oracle.ref_available()
+                         else oracle.port_classify(sub, poly.vx, poly.vy, poly.ring_off, mode, threads=THREADS))
+            assert np.array_equal(got.verdicts[idx], want_v)
+
+
+def test_config3_footprints(engine):
+    s = W.footprints(200_000)
+    for mode in MODES:
+        got = engine.classify_csr(s, mode)
+        want_v, want_s = oracle.port_classify_csr(s, mode, threads=THREADS)
+        assert np.array_equal(got.verdicts, want_v) and np.array_equal(got.stats, want_s)
+        ib, ab = verdicts_to_bits(want_v, mode)
+        assert np.array_equal(got.inside_bits, ib) and np.array_equal(got.aux_bits, ab)
+    if oracle.ref_available():
+        s = W.footprints(20_000, seed=77)
+        for mode in MODES:
+            want_v, _ = oracle.ref_classify_csr(s, mode)
+            assert np.array_equal(engine.classify_csr(s, mode).verdicts, want_v)
+
+
+def test_config4_subsample(engine):
+    poly = W.fractal_polygon(200_000)
+    xy = W.uniform_points(1_000_000, W.bounds(poly), 4)
+    for mode in MODES:
+        got = engine.classify_batch(xy, poly, mode)
+        idx = np.random.default_rng(mode).choice(len(xy), 10_000, replace=False)
+        sub = np.ascontiguousarray(xy[idx])
+        want_v, _ = (oracle.ref_classify(sub, poly.vx, poly.vy, poly.ring_off, mode) if oracle.ref_available()
+                     else oracle.port_classify(sub, poly.vx, poly.vy, poly.ring_off, mode, threads=THREADS))
+        assert np.array_equal(got.verdicts[idx], want_v)
+        assert int(got.stats.sum()) == len(xy)
+
+
+def test_config5_degenerate_full(engine):
+    s = W.degenerate(100_000, allow_dups=True)
+    assert s.n_points > 9_000_000
+    for mode in MODES:
+        got = engine.classify_csr(s, mode)
+        want_v, want_s = oracle.port_classify_csr(s, mode, threads=THREADS)
+        assert np.array_equal(got.verdicts, want_v), f"mode {mode}: {(got.verdicts != want_v).sum()} differ"
+        assert np.array_equal(got.stats, want_s)
+    if oracle.ref_available():
+        s = W.degenerate(10_000, allow_dups=False, seed=5)
+        for mode in MODES:
+            want_v, _ = oracle.ref_classify_csr(s, mode)
+            assert np.array_equal(engine.classify_csr(s, mode).verdicts, want_v)
+
+
+def test_config5_as_single_polygons(engine):
+    """Each degenerate polygon (with duplicates and holes) through the single-polygon kernel."""
+    s = W.degenerate(300, allow_dups=True, seed=9)
+    for p in range(0, 300, 7):
+        r0, r1 = int(s.poly_ring_off[p]), int(s.poly_ring_off[p + 1])
+        v0, v1 = int(s.ring_off[r0]), int(s.ring_off[r1])
+        poly = Polygon(s.vx[v0:v1], s.vy[v0:v1], s.ring_off[r0:r1 + 1] - s.ring_off[r0])
+        xy = np.ascontiguousarray(s.xy[int(s.pt_off[p]):int(s.pt_off[p + 1])])
+        for mode in MODES:
+            check_single(xy, poly, mode, engine.classify(xy, poly, mode), source="port")
+            check_single(xy, poly, mode, engine.classify(xy, poly, mode, prefilter=False), prefilter=False)
+
+
+# ---- sizes, layouts, sharding --------------------------------------------------
+
+@pytest.mark.parametrize("n", [0, 1, 31, 32, 33, 4095, 100_003])
+def test_ragged_point_counts(engine, n):
+    poly = W.star_polygon(777)
+    xy = W.uniform_points(max(n, 1), (-1.1, -1.1, 1.1, 1.1), n)[:n]
+    for mode in MODES:
+        got = engine.classify(xy, poly, mode)
+        assert len(got.verdicts) == n and int(got.stats.sum()) == n
+        if n:
+            check_single(xy, poly, mode, got)
+
+
+def test_many_holes_and_huge_ring(engine):
+    rng = np.random.default_rng(3)
+    rings = [np.stack([np.cos(t) * 100, np.sin(t) * 100], 1) for t in [np.linspace(0, 2 * np.pi, 5001)]]
+    rings[0][-1] = rings[0][0]
+    for k in range(150):  # 150 small square holes
+        cx, cy = rng.uniform(-60, 60, 2)
+        h = [(cx, cy), (cx + 1, cy), (cx + 1, cy + 1), (cx, cy + 1), (cx, cy)]
+        rings.append(np.array(h))
+    poly = Polygon.from_rings(rings)
+    xy = W.uniform_points(200_000, (-110, -110, 110, 110), 8)
+    for mode in MODES:
+        check_single(xy, poly, mode, engine.classify(xy, poly, mode))
+    # a 1e6-edge ring with few points: exercises the edge-chunk split
+    big = W.star_polygon(1_000_000)
+    xy = W.uniform_points(3000, W.bounds(big), 9)
+    for mode in MODES:
+        check_single(xy, big, mode, engine.classify(xy, big, mode))
+
+
+def test_multi_shard_identical():
+    """Shard logic across 'GPUs' (here: 3 shards on one device) gives identical output."""
+    poly, xy = W.config2(1000, n_points=300_017)
+    s = W.degenerate(20_000, allow_dups=True, seed=3)
+    with Engine(devices=[0]) as one, Engine(devices=[0, 0, 0]) as three:
+        assert three.device_count == 3
+        for mode in MODES:
+            a, b = one.classify_batch(xy, poly, mode), three.classify_batch(xy, poly, mode)
+            assert np.array_equal(a.verdicts, b.verdicts) and np.array_equal(a.inside_bits, b.inside_bits)
+            assert np.array_equal(a.aux_bits, b.aux_bits) and np.array_equal(a.stats, b.stats)
+            a, b = one.classify_csr(s, mode), three.classify_csr(s, mode)
+            assert np.array_equal(a.verdicts, b.verdicts) and np.array_equal(a.inside_bits, b.inside_bits)
+            assert np.array_equal(a.aux_bits, b.aux_bits) and np.array_equal(a.stats, b.stats)
+
+
+def test_device_pointer_api_matches_host_api(engine):
+    import torch
+    poly, xy = W.config2(1000, n_points=123_457)
+    dev = torch.device("cuda:0")
+    d_xy = torch.from_numpy(xy).to(dev)
+    d_vx, d_vy = torch.from_numpy(poly.vx).to(dev), torch.from_numpy(poly.vy).to(dev)
+    d_ro = torch.from_numpy(poly.ring_off.view(np.int64)).to(dev)
+    nw = (len(xy) + 31) // 32
+    for mode in MODES:
+        d_in = torch.empty(nw, dtype=torch.int32, device=dev)
+        d_aux = torch.empty(nw, dtype=torch.int32, device=dev)
+        d_st = torch.empty(4, dtype=torch.int64, device=dev)
+        d_v = torch.empty(len(xy), dtype=torch.uint8, device=dev)
+        st = torch.cuda.current_stream().cuda_stream
+        engine.classify_dev(0, st, d_xy, len(xy), d_vx, d_vy, d_ro, poly.n_rings, poly.n_verts, mode, 1e-12, True,
+                            d_in, d_aux, d_st, d_v)
+        torch.cuda.synchronize()
+        host = engine.classify_batch(xy, poly, mode)
+        assert np.array_equal(d_v.cpu().numpy(), host.verdicts)
+        assert np.array_equal(d_in.cpu().numpy().view(np.uint32), host.inside_bits)
+        assert np.array_equal(d_st.cpu().numpy().view(np.uint64), host.stats)
+    s = W.footprints(10_000)
+    t = {k: torch.from_numpy(getattr(s, k).view(np.int64) if getattr(s, k).dtype == np.uint64 else getattr(s, k))
+         .to(dev) for k in ("xy", "pt_off", "vx", "vy", "ring_off", "poly_ring_off")}
+    nw = (s.n_points + 31) // 32
+    d_in = torch.empty(nw, dtype=torch.int32, device=dev)
+    d_aux = torch.empty(nw, dtype=torch.int32, device=dev)
+    d_st = torch.empty(4, dtype=torch.int64, device=dev)
+    engine.classify_csr_dev(0, torch.cuda.current_stream().cuda_stream, t["xy"], t["pt_off"], s.n_polys, s.n_points,
+                            t["vx"], t["vy"], t["ring_off"], t["poly_ring_off"], 0, 1e-12, d_in, d_aux, d_st)
+    torch.cuda.synchronize()
+    host = engine.classify_csr(s, 0)
+    assert np.array_equal(d_in.cpu().numpy().view(np.uint32), host.inside_bits)
+
+
+def test_bits_match_verdicts_and_launch_count(engine):
+    poly, xy = W.config2(100, n_points=50_000)
+    r = engine.classify_batch(xy, poly, CrossingMode.Robust)
+    assert engine.last_launch_count >= 3  # prep, classify, finalize: native kernels ran
+    inside = unpack_bits(r.inside_bits, len(xy))
+    aux = unpack_bits(r.aux_bits, len(xy))
+    assert np.array_equal(inside, r.verdicts == 0) and np.array_equal(aux, r.verdicts == 2)
+
+
+def test_invalid_arguments_report_status(engine):
+    from paper_2306_04316_b200 import DeviceError
+    bad = Polygon(np.zeros(4), np.zeros(4), np.array([0, 2, 2], np.uint64))  # empty ring
+    with pytest.raises(DeviceError) as e:
+        engine.classify(np.zeros((4, 2)), bad, 0)
+    assert e.value.status == 1
+    with pytest.raises(DeviceError):
+        engine.classify(np.zeros((4, 2)), Polygon.from_rings([adversarial.SQUARE]), 7)
