@@ -215,7 +215,12 @@ def run_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    # an explicit stream: the library and the timing events must share it
+    # (the legacy default stream's handle is 0, which the C-ABI reads as "context stream")
+    torch.cuda.set_stream(torch.cuda.Stream(device=dev))
     eng = Engine(devices=[local_rank])
+    if args.bucket is not None:
+        eng.set_bucketing(args.bucket)
     items = build_items(args.workload, rank, world)
     log(f"[rank {rank}] workload {args.workload}: {len(items)} items, "
         f"{sum(i.tests for i in items):.3e} tests/step, {sum(i.n_points for i in items)} points/step")
@@ -460,6 +465,7 @@ def main():
     ap.add_argument("--mode", type=int, default=0, choices=[0, 1, 2])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--bucket", type=int, default=None, choices=[-1, 0, 1], help="y-bucketing: auto/off/on")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 1)
 

@@ -121,6 +121,12 @@ int pc_classify_csr_dev(pc_ctx* ctx, int dev_index, void* stream, const double* 
 /* Number of GPU kernels the last call on this context launched (all devices). */
 uint64_t pc_last_launch_count(const pc_ctx* ctx);
 
+/* Tuning options (none changes any result).
+ *  PC_OPT_BUCKET_POINTS: -1 auto (default), 0 off, 1 on — y-bucket the points of
+ *  a single-polygon call before classifying, for SIMT coherence (pip_sort.cu). */
+#define PC_OPT_BUCKET_POINTS 1
+int pc_set_option(pc_ctx* ctx, int option, int64_t value);
+
 /* Measurement hooks (bench.py).  With profiling on, every call records a pair
  * of CUDA events around its main classify kernel, on the stream that kernel is
  * launched on.  pc_profile_take() waits for the pairs recorded on device

@@ -41,6 +41,7 @@ SIGNATURES = {
                                       C.c_int, C.c_double, _vp, _vp, _vp, _vp]),
     "pc_last_launch_count": (C.c_uint64, [_vp]),
     "pc_set_profiling": (C.c_int, [_vp, C.c_int]),
+    "pc_set_option": (C.c_int, [_vp, C.c_int, C.c_int64]),
     "pc_profile_take": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_double), C.c_int]),
     "pc_measure_fp64_rate": (C.c_int, [_vp, C.c_int, C.c_double, C.POINTER(C.c_double)]),
 }

@@ -43,6 +43,7 @@ struct DevState {
     int dev = 0;
     cudaStream_t stream = nullptr;
     DevBuf pts, vx, vy, ring_off, pt_off, poly_ring_off, filt, rec, bbox, bits, verdicts, stats, counts, degen;
+    DevBuf bucket_scratch, sorted_pts, sorted_idx; // y-bucketing (pip_sort.cu)
     unsigned long long* h_stats = nullptr; // pinned 4 x u64
     // profiling: one event pair per main-kernel launch since the last take
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
@@ -57,6 +58,7 @@ struct pc_ctx {
     std::mutex mu;
     uint64_t launches = 0;
     bool profiling = false;
+    int64_t bucket_mode = -1; // PC_OPT_BUCKET_POINTS: -1 auto, 0 off, 1 on
 };
 
 namespace {
@@ -146,6 +148,8 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
     pa.n_zero_words = nwords;
     check(c, pcd::launch_prep(pa, st, d.dev, &c->launches), "prep kernel");
     check(c, cudaMemsetAsync(d_aux, 0, nwords * 4, st), "clear aux plane");
+    const bool bucket = n < 0xffffffffull &&
+                        (c->bucket_mode == 1 || (c->bucket_mode < 0 && n_edges >= 64 && n >= 4096));
     pcd::SingleArgs sa{};
     sa.mode = mode;
     sa.pts = d_pts;
@@ -159,9 +163,31 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
     sa.tol2 = tol * tol;
     sa.inside_bits = d_inside;
     sa.aux_bits = d_aux;
+    sa.n_dev = nullptr;
+    uint32_t* hist = nullptr;
+    if (bucket) {
+        const size_t hist_words = pcd::kBuckets + 2;
+        check(c, d.bucket_scratch.ensure((hist_words + 2 * nwords) * 4), "alloc bucket scratch");
+        check(c, d.sorted_pts.ensure(n * 16), "alloc bucketed points");
+        check(c, d.sorted_idx.ensure(n * 4), "alloc bucket index");
+        hist = d.bucket_scratch.as<uint32_t>();
+        check(c, cudaMemsetAsync(hist, 0, (hist_words + 2 * nwords) * 4, st), "clear bucket scratch");
+        pcd::BucketArgs ba{d_pts, n, d.bbox.as<unsigned long long>(), prefilter, hist, d.sorted_pts.as<double>(),
+                           d.sorted_idx.as<uint32_t>()};
+        check(c, pcd::launch_bucket(ba, st, d.dev, &c->launches), "bucket kernels");
+        sa.pts = d.sorted_pts.as<double>();
+        sa.prefilter = 0; // rejected points were left out of the bucketed prefix
+        sa.inside_bits = hist + hist_words;
+        sa.aux_bits = hist + hist_words + nwords;
+        sa.n_dev = hist + pcd::kBuckets + 1;
+    }
     mark_begin(c, d, st);
     check(c, pcd::launch_single(sa, st, d.dev, &c->launches), "classify kernel");
     mark_end(c, d, st);
+    if (bucket)
+        check(c, pcd::launch_unbucket(n, sa.n_dev, d.sorted_idx.as<uint32_t>(), sa.inside_bits, sa.aux_bits, d_inside,
+                                      d_aux, st, d.dev, &c->launches),
+              "unbucket kernel");
     check(c, pcd::launch_finalize(n, d_inside, d_aux, d_verdicts, mode, d_stats, st, d.dev, &c->launches),
           "finalize kernel");
 }
@@ -272,7 +298,8 @@ void pc_destroy(pc_ctx* c) {
         cudaSetDevice(d.dev);
         cudaStreamSynchronize(d.stream);
         for (DevBuf* b : {&d.pts, &d.vx, &d.vy, &d.ring_off, &d.pt_off, &d.poly_ring_off, &d.filt, &d.rec, &d.bbox,
-                          &d.bits, &d.verdicts, &d.stats, &d.counts, &d.degen})
+                          &d.bits, &d.verdicts, &d.stats, &d.counts, &d.degen, &d.bucket_scratch, &d.sorted_pts,
+                          &d.sorted_idx})
             b->release();
         if (d.h_stats) cudaFreeHost(d.h_stats);
         for (auto& e : d.evs) {
@@ -287,6 +314,17 @@ void pc_destroy(pc_ctx* c) {
 const char* pc_last_error(const pc_ctx* c) { return c ? c->err.c_str() : "null context"; }
 int pc_device_count(const pc_ctx* c) { return c ? (int)c->devs.size() : 0; }
 uint64_t pc_last_launch_count(const pc_ctx* c) { return c ? c->launches : 0; }
+
+int pc_set_option(pc_ctx* c, int option, int64_t value) {
+    if (!c) return PC_EINVAL;
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (option == PC_OPT_BUCKET_POINTS && value >= -1 && value <= 1) {
+        c->bucket_mode = value;
+        return PC_OK;
+    }
+    c->err = "unknown option or value";
+    return PC_EINVAL;
+}
 
 int pc_set_profiling(pc_ctx* c, int on) {
     if (!c) return PC_EINVAL;

@@ -45,23 +45,23 @@ __device__ __forceinline__ double dkey_inv(unsigned long long k) {
     return __longlong_as_double(static_cast<long long>(b));
 }
 
-// C1 exact test of one straddle candidate (geometry.hpp:189-200).
-__device__ __forceinline__ void exact_c1(double px, double py, const EdgeRec& r, int& cnt) {
+// C1 exact test of one straddle candidate (geometry.hpp:189-200).  `sure`:
+// the keys already prove min(a.y,b.y) < p.y < max(a.y,b.y) strictly, so the
+// reference's product f_prev*f_next is negative (or -0) and `<= 0.0` holds;
+// the product is only evaluated when a key tie leaves the order open.
+__device__ __forceinline__ void exact_c1(double px, double py, const EdgeRec& r, int& cnt, bool sure = false) {
     const double ax = r.d[0], ay = r.d[1], by = r.d[2], nx = r.d[3], ny = r.d[4];
-    const double f_prev = __dsub_rn(ay, py);
-    const double f_next = __dsub_rn(by, py);
-    if (__dmul_rn(f_prev, f_next) <= 0.0) {
+    if (sure || __dmul_rn(__dsub_rn(ay, py), __dsub_rn(by, py)) <= 0.0) {
         const double side = __dadd_rn(__dmul_rn(__dsub_rn(px, ax), nx), __dmul_rn(__dsub_rn(py, ay), ny));
         if (side <= 0.0) ++cnt;
     }
 }
 
 // C2 exact test (geometry.hpp:214-226); `err` marks the DegenerateEdge throw.
-__device__ __forceinline__ void exact_c2(double px, double py, const EdgeRec& r, int& cnt, bool& err) {
+__device__ __forceinline__ void exact_c2(double px, double py, const EdgeRec& r, int& cnt, bool& err,
+                                         bool sure = false) {
     const double ax = r.d[0], ay = r.d[1], by = r.d[2], dx = r.d[3], dy = r.d[4];
-    const double f_prev = __dsub_rn(ay, py);
-    const double f_next = __dsub_rn(by, py);
-    if (__dmul_rn(f_prev, f_next) <= 0.0) {
+    if (sure || __dmul_rn(__dsub_rn(ay, py), __dsub_rn(by, py)) <= 0.0) {
         if (dy == 0.0) {
             err = true;
         } else {

@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(kTPB) pip_single_kernel(
     const double2* __restrict__ pts, uint64_t n, const uint2* __restrict__ filt,
     const EdgeRec* __restrict__ rec, uint32_t n_edges, uint32_t edges_per_chunk,
     const unsigned long long* __restrict__ bbox_keys, int prefilter, double tol, double tol2,
-    uint32_t* __restrict__ inside_bits, uint32_t* __restrict__ aux_bits) {
+    uint32_t* __restrict__ inside_bits, uint32_t* __restrict__ aux_bits, const uint32_t* __restrict__ n_dev) {
     __shared__ uint2 s_filt[kTile];
     extern __shared__ __align__(16) unsigned char s_dyn[];
     EdgeRec* s_rec = reinterpret_cast<EdgeRec*>(s_dyn);
@@ -137,6 +137,8 @@ __global__ void __launch_bounds__(kTPB) pip_single_kernel(
     const uint32_t e_end = min(n_edges, e_begin + edges_per_chunk);
     const uint64_t base = (uint64_t)blockIdx.x * (kTPB * K);
     const int tid = threadIdx.x;
+    if (n_dev) n = min(n, (uint64_t)*n_dev); // bucketed input: only the in-box prefix is live
+    if (base >= n) return;
 
     double minx = 0, miny = 0, maxx = 0, maxy = 0;
     if (prefilter) {
@@ -203,9 +205,14 @@ __global__ void __launch_bounds__(kTPB) pip_single_kernel(
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
                     if (c[k]) {
-                        if (MODE == kC1) exact_c1(px[k], py[k], r, cnt[k]);
-                        else if (MODE == kC2) exact_c2(px[k], py[k], r, cnt[k], aux[k]);
-                        else exact_robust(px[k], py[k], tol, tol2, r, cnt[k], aux[k]);
+                        if (MODE == kRobust) {
+                            exact_robust(px[k], py[k], tol, tol2, r, cnt[k], aux[k]);
+                        } else {
+                            const uint32_t d = (uint32_t)(ka[k] - (int)f.x); // 0..range; strict inside => sure
+                            const bool sure = d != 0u && d != f.y;
+                            if (MODE == kC1) exact_c1(px[k], py[k], r, cnt[k], sure);
+                            else exact_c2(px[k], py[k], r, cnt[k], aux[k], sure);
+                        }
                     }
                 }
             }
@@ -432,7 +439,7 @@ cudaError_t launch_single_t(const SingleArgs& a, cudaStream_t st, int dev, uint6
     pip_single_kernel<MODE, K><<<grid, kTPB, dyn, st>>>(
         reinterpret_cast<const double2*>(a.pts), a.n, a.filt, reinterpret_cast<const EdgeRec*>(a.rec),
         a.n_edges, per_chunk ? per_chunk : 1, a.bbox_keys, a.prefilter, a.tol, a.tol2, a.inside_bits,
-        a.aux_bits);
+        a.aux_bits, a.n_dev);
     ++*launches;
     return cudaGetLastError();
 }

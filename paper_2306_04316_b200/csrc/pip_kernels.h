@@ -35,6 +35,7 @@ struct SingleArgs {
     double tol, tol2;
     uint32_t* inside_bits;
     uint32_t* aux_bits;
+    const uint32_t* n_dev; // optional device-side point count (bucketed input)
 };
 
 struct CsrArgs {
@@ -60,6 +61,25 @@ cudaError_t launch_finalize(uint64_t n, uint32_t* inside_bits, const uint32_t* a
                             int mode, unsigned long long* stats, cudaStream_t st, int dev, uint64_t* launches);
 cudaError_t launch_count(const double* pts, uint64_t n, const double* vx, const double* vy, uint64_t nv, int mode,
                          unsigned long long* counts, uint8_t* degenerate, cudaStream_t st, uint64_t* launches);
+
+// y-bucketing of the points of one polygon (pip_sort.cu): counting sort by
+// y over the outer ring's bbox into kBuckets bins; bbox-rejected points
+// (prefilter) go to a trailing bin that is not classified.
+constexpr int kBuckets = 4096;
+struct BucketArgs {
+    const double* pts;                    // n interleaved points
+    uint64_t n;
+    const unsigned long long* bbox_keys;  // from prep
+    int prefilter;
+    uint32_t* hist;                       // kBuckets + 2 words, zeroed; [kBuckets+1] receives n_in
+    double* sorted_pts;                   // n points (bucketed order)
+    uint32_t* sorted_idx;                 // original index of each bucketed point
+};
+cudaError_t launch_bucket(const BucketArgs& a, cudaStream_t st, int dev, uint64_t* launches);
+// ORs the set bits of the bucketed planes back to the original point order.
+cudaError_t launch_unbucket(uint64_t n, const uint32_t* n_dev, const uint32_t* sorted_idx, const uint32_t* s_inside,
+                            const uint32_t* s_aux, uint32_t* inside_bits, uint32_t* aux_bits, cudaStream_t st, int dev,
+                            uint64_t* launches);
 
 cudaError_t launch_fp64_probe(double* out, int iters, int dev, cudaStream_t st, double* flops);
 

@@ -176,6 +176,13 @@ class Engine:
         return int(self.lib.pc_last_launch_count(self.ctx))
 
     # ---- measurement hooks -----------------------------------------------------
+    def set_option(self, option: int, value: int):
+        self._check(self.lib.pc_set_option(self.ctx, int(option), int(value)), "pc_set_option")
+
+    def set_bucketing(self, mode: int):
+        """-1 auto, 0 off, 1 on (PC_OPT_BUCKET_POINTS); never changes results."""
+        self.set_option(1, mode)
+
     def set_profiling(self, on: bool = True):
         self._check(self.lib.pc_set_profiling(self.ctx, int(bool(on))), "pc_set_profiling")
 

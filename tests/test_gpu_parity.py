@@ -287,3 +287,21 @@ def test_invalid_arguments_report_status(engine):
     assert e.value.status == 1
     with pytest.raises(DeviceError):
         engine.classify(np.zeros((4, 2)), Polygon.from_rings([adversarial.SQUARE]), 7)
+
+
+@pytest.mark.parametrize("bucket", [0, 1])
+def test_bucketing_modes_identical(bucket):
+    """y-bucketing (pip_sort.cu) forced off / on: bit-identical to the reference, all modes,
+    with and without the bbox prefilter, including points outside the box."""
+    cases = [W.config2(1000, n_points=100_003), W.config2(64, n_points=50_001)]
+    poly = W.star_polygon(300, seed=4)
+    cases.append((poly, W.uniform_points(77_777, (-2.0, -2.0, 2.0, 2.0), 5)))  # many points outside the bbox
+    for name, p, xy in adversarial.cases():
+        cases.append((p, xy))
+    with Engine(devices=[0]) as eng:
+        eng.set_bucketing(bucket)
+        for i, (poly, xy) in enumerate(cases):
+            src = "port" if i == len(cases) - 1 else None  # last adversarial case has duplicate vertices
+            for mode in MODES:
+                check_single(xy, poly, mode, eng.classify(xy, poly, mode), source=src)
+                check_single(xy, poly, mode, eng.classify(xy, poly, mode, prefilter=False), prefilter=False)
