@@ -129,7 +129,7 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
     const uint64_t n_edges = n_verts - n_rings;
     if (n_edges > 0xffffffffull) invalid(c, "too many edges for one polygon (>= 2^32)");
     const uint64_t nwords = (n + 31) / 32;
-    check(c, d.filt.ensure(std::max<uint64_t>(n_edges, 1) * sizeof(uint2)), "alloc edge keys");
+    check(c, d.filt.ensure((n_edges + 2) * sizeof(uint2)), "alloc edge keys"); // +2: 16-byte bulk-copy padding
     check(c, d.rec.ensure(std::max<uint64_t>(n_edges, 1) * pcd::edge_rec_bytes()), "alloc edge records");
     check(c, d.bbox.ensure(4 * sizeof(unsigned long long)), "alloc bbox");
     pcd::PrepArgs pa{};

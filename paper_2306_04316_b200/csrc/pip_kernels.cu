@@ -1,9 +1,8 @@
 // sm_100a kernels of the batched point-in-polygon path.
 //
 //   prep_edges_kernel   raw rings -> per-edge filter keys + exact records, bbox
-//   pip_single_kernel   one polygon, (point tile x edge chunk) CTAs, edges staged
-//                       through shared memory, K points per thread, XOR parity
-//   pip_csr_kernel      many small polygons (CSR), one warp per polygon
+//   (the single-polygon kernel lives in pip_single.cu)
+//   (the CSR multi-polygon kernel lives in pip_csr.cu, bucketing in pip_sort.cu)
 //   finalize_kernel     bit planes -> verdict bytes + BatchStats
 //   count_kernel        per-ring crossing counts (count_crossings_c1/_c2)
 //
@@ -24,9 +23,6 @@ namespace pcd {
 
 namespace {
 
-constexpr int kTPB = 256;       // threads per CTA, single-polygon kernel
-constexpr int kTile = 512;      // edges per shared-memory tile
-constexpr int kWarpsCsr = 8;    // warps per CTA, CSR kernel
 
 __device__ __forceinline__ uint32_t ring_of(const uint64_t* ring_off, uint32_t n_rings, uint64_t v) {
     // largest r with ring_off[r] <= v
@@ -114,200 +110,6 @@ __global__ void __launch_bounds__(256) prep_edges_kernel(
         atomicMin(&bbox_keys[1], kminy);
         atomicMin(&bbox_keys[2], kmaxx);
         atomicMin(&bbox_keys[3], kmaxy);
-    }
-}
-
-// Single-polygon kernel.  CTA (bx, by) classifies points [bx*kTPB*K, +kTPB*K)
-// against edges [by*chunk, +chunk).  Thread t owns points base + k*kTPB + t.
-// Per staged edge: a 2-instruction integer range test per point decides
-// "certainly not straddling" (exactly, see fkey); only candidates run the
-// binary64 test of the reference.  Partial parities are XOR-ed into the
-// inside plane, Error/Boundary OR-ed into the aux plane.
-template <int MODE, int K>
-__global__ void __launch_bounds__(kTPB) pip_single_kernel(
-    const double2* __restrict__ pts, uint64_t n, const uint2* __restrict__ filt,
-    const EdgeRec* __restrict__ rec, uint32_t n_edges, uint32_t edges_per_chunk,
-    const unsigned long long* __restrict__ bbox_keys, int prefilter, double tol, double tol2,
-    uint32_t* __restrict__ inside_bits, uint32_t* __restrict__ aux_bits, const uint32_t* __restrict__ n_dev) {
-    __shared__ uint2 s_filt[kTile];
-    extern __shared__ __align__(16) unsigned char s_dyn[];
-    EdgeRec* s_rec = reinterpret_cast<EdgeRec*>(s_dyn);
-
-    const uint32_t e_begin = blockIdx.y * edges_per_chunk;
-    const uint32_t e_end = min(n_edges, e_begin + edges_per_chunk);
-    const uint64_t base = (uint64_t)blockIdx.x * (kTPB * K);
-    const int tid = threadIdx.x;
-    if (n_dev) n = min(n, (uint64_t)*n_dev); // bucketed input: only the in-box prefix is live
-    if (base >= n) return;
-
-    double minx = 0, miny = 0, maxx = 0, maxy = 0;
-    if (prefilter) {
-        minx = dkey_inv(bbox_keys[0]);
-        miny = dkey_inv(bbox_keys[1]);
-        maxx = dkey_inv(~bbox_keys[2]);
-        maxy = dkey_inv(~bbox_keys[3]);
-    }
-
-    double px[K], py[K];
-    int ka[K], kb[K]; // C1/C2: ka = kb = key(p.y); Robust: ka = key(p.y+tol), kb = key(p.y-tol)
-    int cnt[K];
-    bool aux[K], act[K];
-    bool any_act = false;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        const uint64_t i = base + (uint64_t)k * kTPB + tid;
-        cnt[k] = 0;
-        aux[k] = false;
-        act[k] = i < n;
-        double2 p = make_double2(0.0, 0.0);
-        if (act[k]) p = pts[i];
-        px[k] = p.x;
-        py[k] = p.y;
-        if (act[k] && prefilter)
-            act[k] = p.x >= minx && p.x <= maxx && p.y >= miny && p.y <= maxy; // batch.hpp:39-41
-        if (MODE == kRobust) {
-            ka[k] = act[k] ? fkey(__dadd_rn(p.y, tol)) : INT_MIN;
-            kb[k] = act[k] ? fkey(__dsub_rn(p.y, tol)) : INT_MAX;
-        } else {
-            ka[k] = act[k] ? fkey(p.y) : INT_MAX;
-            kb[k] = ka[k];
-        }
-        any_act |= act[k];
-    }
-    if (!__syncthreads_or(any_act)) return;
-
-    for (uint32_t t0 = e_begin; t0 < e_end; t0 += kTile) {
-        const uint32_t nt = min((uint32_t)kTile, e_end - t0);
-        __syncthreads();
-        for (uint32_t j = tid; j < nt; j += kTPB) s_filt[j] = filt[t0 + j];
-        {
-            const float4* src = reinterpret_cast<const float4*>(rec + t0);
-            float4* dst = reinterpret_cast<float4*>(s_rec);
-            for (uint32_t j = tid; j < nt * 4; j += kTPB) dst[j] = src[j];
-        }
-        __syncthreads();
-        if (!any_act) continue;
-#pragma unroll 2
-        for (uint32_t e = 0; e < nt; ++e) {
-            const uint2 f = s_filt[e];
-            bool c[K];
-            bool any = false;
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                if (MODE == kRobust)
-                    c[k] = ka[k] >= (int)f.x && kb[k] <= (int)f.y;
-                else
-                    c[k] = (uint32_t)(ka[k] - (int)f.x) <= f.y;
-                any |= c[k];
-            }
-            if (any) {
-                const EdgeRec r = s_rec[e];
-#pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    if (c[k]) {
-                        if (MODE == kRobust) {
-                            exact_robust(px[k], py[k], tol, tol2, r, cnt[k], aux[k]);
-                        } else {
-                            const uint32_t d = (uint32_t)(ka[k] - (int)f.x); // 0..range; strict inside => sure
-                            const bool sure = d != 0u && d != f.y;
-                            if (MODE == kC1) exact_c1(px[k], py[k], r, cnt[k], sure);
-                            else exact_c2(px[k], py[k], r, cnt[k], aux[k], sure);
-                        }
-                    }
-                }
-            }
-        }
-    }
-
-    const int lane = tid & 31;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        const uint64_t i0 = base + (uint64_t)k * kTPB + (tid & ~31);
-        const uint32_t b = __ballot_sync(0xffffffffu, act[k] && (cnt[k] & 1));
-        const uint32_t a = __ballot_sync(0xffffffffu, act[k] && aux[k]);
-        if (lane == 0 && i0 < n) {
-            if (b) atomicXor(&inside_bits[i0 >> 5], b);
-            if (a) atomicOr(&aux_bits[i0 >> 5], a);
-        }
-    }
-}
-
-// CSR kernel: one warp per polygon (grid-stride).  The warp reduces the outer
-// ring's bbox, then walks its points 32 at a time; each lane runs the literal
-// reference loop over every ring edge (vertex loads are warp-uniform
-// broadcasts).  Flags are OR-ed into the bit planes (polygon point ranges need
-// not be 32-aligned).
-template <int MODE>
-__global__ void __launch_bounds__(kWarpsCsr * 32) pip_csr_kernel(
-    const double2* __restrict__ pts, const uint64_t* __restrict__ pt_off, uint64_t n_polys,
-    const double* __restrict__ vx, const double* __restrict__ vy, const uint64_t* __restrict__ ring_off,
-    const uint64_t* __restrict__ poly_ring_off, uint64_t pt_base, uint64_t ring_base, uint64_t vert_base,
-    double tol, double tol2, uint32_t* __restrict__ inside_bits, uint32_t* __restrict__ aux_bits) {
-    const int lane = threadIdx.x & 31;
-    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t p = warp; p < n_polys; p += nwarps) {
-        const uint64_t r0 = poly_ring_off[p] - ring_base, r1 = poly_ring_off[p + 1] - ring_base;
-        const uint64_t s = pt_off[p] - pt_base, t = pt_off[p + 1] - pt_base;
-        if (s == t) continue;
-        double minx = INFINITY, miny = INFINITY, maxx = -INFINITY, maxy = -INFINITY;
-        if (r1 > r0) {
-            for (uint64_t v = ring_off[r0] - vert_base + lane; v < ring_off[r0 + 1] - vert_base; v += 32) {
-                const double x = vx[v], y = vy[v];
-                minx = x < minx ? x : minx;
-                miny = y < miny ? y : miny;
-                maxx = maxx < x ? x : maxx;
-                maxy = maxy < y ? y : maxy;
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const double a = __shfl_xor_sync(0xffffffffu, minx, o);
-                const double b = __shfl_xor_sync(0xffffffffu, miny, o);
-                const double c = __shfl_xor_sync(0xffffffffu, maxx, o);
-                const double d = __shfl_xor_sync(0xffffffffu, maxy, o);
-                minx = a < minx ? a : minx;
-                miny = b < miny ? b : miny;
-                maxx = maxx < c ? c : maxx;
-                maxy = maxy < d ? d : maxy;
-            }
-        }
-        for (uint64_t c0 = s; c0 < t; c0 += 32) {
-            const uint64_t i = c0 + lane;
-            bool act = i < t;
-            double2 q = make_double2(0.0, 0.0);
-            if (act) q = pts[i];
-            act = act && r1 > r0 && q.x >= minx && q.x <= maxx && q.y >= miny && q.y <= maxy;
-            int cnt = 0;
-            bool aux = false;
-            if (__any_sync(0xffffffffu, act)) {
-                for (uint64_t r = r0; r < r1; ++r) {
-                    const uint64_t lo = ring_off[r] - vert_base, hi = ring_off[r + 1] - vert_base;
-                    if (hi - lo < 2) continue;
-                    double ax = vx[lo], ay = vy[lo];
-                    double f_prev = __dsub_rn(ay, q.y);
-                    for (uint64_t v = lo + 1; v < hi; ++v) {
-                        const double bx = vx[v], by = vy[v];
-                        raw_edge<MODE>(q.x, q.y, tol, tol2, ax, ay, bx, by, f_prev, cnt, aux);
-                        ax = bx;
-                        ay = by;
-                    }
-                }
-            }
-            const uint32_t bi = __ballot_sync(0xffffffffu, act && (cnt & 1) && !aux);
-            const uint32_t ba = __ballot_sync(0xffffffffu, act && aux);
-            if (lane == 0) {
-                const uint64_t w = c0 >> 5;
-                const uint32_t sh = (uint32_t)(c0 & 31);
-                if (bi) {
-                    atomicOr(&inside_bits[w], bi << sh);
-                    if (sh && (bi >> (32 - sh))) atomicOr(&inside_bits[w + 1], bi >> (32 - sh));
-                }
-                if (ba) {
-                    atomicOr(&aux_bits[w], ba << sh);
-                    if (sh && (ba >> (32 - sh))) atomicOr(&aux_bits[w + 1], ba >> (32 - sh));
-                }
-            }
-        }
     }
 }
 
@@ -415,35 +217,6 @@ int sm_count(int dev) {
     return v;
 }
 
-template <int MODE, int K>
-cudaError_t launch_single_t(const SingleArgs& a, cudaStream_t st, int dev, uint64_t* launches) {
-    const uint32_t pts_per_cta = kTPB * K;
-    const uint64_t n_ptiles = (a.n + pts_per_cta - 1) / pts_per_cta;
-    const size_t dyn = sizeof(EdgeRec) * kTile;
-    static bool attr_set[64] = {};
-    if (dev < 64 && !attr_set[dev]) {
-        cudaFuncSetAttribute(pip_single_kernel<MODE, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-        attr_set[dev] = true;
-    }
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pip_single_kernel<MODE, K>, kTPB, dyn);
-    if (per_sm < 1) per_sm = 1;
-    const uint64_t slots = (uint64_t)sm_count(dev) * per_sm;
-    // Split the edge range so the grid covers >= ~4 waves, chunks >= one tile.
-    const uint64_t max_chunks = std::max<uint64_t>(1, (a.n_edges + kTile - 1) / kTile);
-    uint64_t chunks = std::max<uint64_t>(1, (4 * slots + n_ptiles - 1) / std::max<uint64_t>(n_ptiles, 1));
-    chunks = std::min<uint64_t>(std::min<uint64_t>(chunks, max_chunks), 65535);
-    const uint32_t per_chunk = (uint32_t)((a.n_edges + chunks - 1) / chunks);
-    chunks = a.n_edges ? (a.n_edges + per_chunk - 1) / per_chunk : 1;
-    dim3 grid((unsigned)n_ptiles, (unsigned)chunks);
-    pip_single_kernel<MODE, K><<<grid, kTPB, dyn, st>>>(
-        reinterpret_cast<const double2*>(a.pts), a.n, a.filt, reinterpret_cast<const EdgeRec*>(a.rec),
-        a.n_edges, per_chunk ? per_chunk : 1, a.bbox_keys, a.prefilter, a.tol, a.tol2, a.inside_bits,
-        a.aux_bits, a.n_dev);
-    ++*launches;
-    return cudaGetLastError();
-}
-
 } // namespace
 
 size_t edge_rec_bytes() { return sizeof(EdgeRec); }
@@ -476,40 +249,6 @@ cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st, int dev, uint64_t* l
                                                            a.filt, reinterpret_cast<EdgeRec*>(a.rec),
                                                            a.bbox_keys, a.zero_words, a.n_zero_words,
                                                            a.stats);
-        break;
-    }
-    ++*launches;
-    return cudaGetLastError();
-}
-
-cudaError_t launch_single(const SingleArgs& a, cudaStream_t st, int dev, uint64_t* launches) {
-    if (a.n == 0) return cudaSuccess;
-    switch (a.mode) {
-    case kC1: return launch_single_t<kC1, 8>(a, st, dev, launches);
-    case kC2: return launch_single_t<kC2, 8>(a, st, dev, launches);
-    default: return launch_single_t<kRobust, 8>(a, st, dev, launches);
-    }
-}
-
-cudaError_t launch_csr(const CsrArgs& a, cudaStream_t st, int dev, uint64_t* launches) {
-    if (a.n_polys == 0) return cudaSuccess;
-    const uint64_t want = (a.n_polys + kWarpsCsr - 1) / kWarpsCsr;
-    const unsigned blocks = (unsigned)std::min<uint64_t>(want, (uint64_t)sm_count(dev) * 64);
-    const dim3 tpb(kWarpsCsr * 32);
-    const double2* p = reinterpret_cast<const double2*>(a.pts);
-    switch (a.mode) {
-    case kC1:
-        pip_csr_kernel<kC1><<<blocks, tpb, 0, st>>>(p, a.pt_off, a.n_polys, a.vx, a.vy, a.ring_off, a.poly_ring_off,
-                                                    a.pt_base, a.ring_base, a.vert_base, a.tol, a.tol2, a.inside_bits, a.aux_bits);
-        break;
-    case kC2:
-        pip_csr_kernel<kC2><<<blocks, tpb, 0, st>>>(p, a.pt_off, a.n_polys, a.vx, a.vy, a.ring_off, a.poly_ring_off,
-                                                    a.pt_base, a.ring_base, a.vert_base, a.tol, a.tol2, a.inside_bits, a.aux_bits);
-        break;
-    default:
-        pip_csr_kernel<kRobust><<<blocks, tpb, 0, st>>>(p, a.pt_off, a.n_polys, a.vx, a.vy, a.ring_off,
-                                                        a.poly_ring_off, a.pt_base, a.ring_base, a.vert_base, a.tol, a.tol2, a.inside_bits,
-                                                        a.aux_bits);
         break;
     }
     ++*launches;

@@ -1,0 +1,272 @@
+// Single-polygon kernel (configs 1, 2, 4; classify_batch / contains over one
+// polygon with holes): the point-edge scan of count_crossings_c1/_c2 /
+// robust_ray_crossings (geometry.hpp:182-273) for every point of a batch.
+//
+// Work decomposition: CTA (bx, by) classifies points [bx*kTPB*K, +kTPB*K)
+// against edges [by*chunk, +chunk); partial parities are XOR-ed and
+// Error/Boundary flags OR-ed into the bit planes, so edge chunks combine
+// exactly like the reference's per-ring sums (geometry.hpp:285-299).
+//
+// Per thread: K points, of which only the 32-bit filter keys live in
+// registers; parity and aux flags are K-bit masks.  Warp w owns K*32
+// consecutive points (k-slice k = 32 consecutive points), which after
+// y-bucketing (pip_sort.cu) are y-adjacent, so an edge either misses the whole
+// warp or is a candidate for most of it.
+//
+// Per edge (fast path, all points): d_k = key(p.y) - key(ylo) (mod 2^32) and
+// the running minimum of the d_k — one fused add+min (VIADDMNMX) per point —
+// then a single compare of the minimum against key(yhi)-key(ylo) decides, for
+// the whole warp, whether any point may straddle the edge (exactness argument
+// in DESIGN.md §3).  Only then (warp-uniform branch) does the slow path
+// re-derive which points are candidates and run the binary64 test of the
+// reference for them.
+//
+// Edge tiles (filter keys + exact records, precomputed by prep_edges_kernel)
+// stream into shared memory with TMA bulk copies, double-buffered on
+// mbarriers, while the previous tile is scanned.
+#include "pip_kernels.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+
+#include "pip_device.cuh"
+
+namespace pcd {
+
+namespace {
+
+constexpr int kTPB = 256;
+constexpr int kK = 16;      // points per thread
+constexpr int kTile = 256;  // edges per shared-memory stage (multiple of 2: 16-byte bulk copies)
+
+struct __align__(128) TileStage {
+    EdgeRec rec[kTile];
+    uint2 filt[kTile];
+};
+
+struct SingleShared {
+    TileStage st[2];
+    unsigned long long full[2];
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+    unsigned done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(b)), "r"(parity)
+            : "memory");
+    }
+}
+
+// One elected thread: load tile [t0, t0+nt) of the edge arrays into stage s.
+__device__ __forceinline__ void issue_tile(SingleShared& sh, int s, const uint2* filt, const EdgeRec* rec,
+                                           uint32_t t0, uint32_t nt) {
+    const unsigned fb = ((nt + 1) & ~1u) * 8u; // filt padded to an even count (16-byte multiple)
+    const unsigned rb = nt * (unsigned)sizeof(EdgeRec);
+    const unsigned bar = smem_u32(&sh.full[s]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(fb + rb) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(sh.st[s].filt)),
+                 "l"(filt + t0), "r"(fb), "r"(bar)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(sh.st[s].rec)),
+                 "l"(rec + t0), "r"(rb), "r"(bar)
+                 : "memory");
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kTPB) pip_tile_kernel(const double2* __restrict__ pts, uint64_t n,
+                                                        const uint2* __restrict__ filt,
+                                                        const EdgeRec* __restrict__ rec, uint32_t n_edges,
+                                                        uint32_t edges_per_chunk,
+                                                        const unsigned long long* __restrict__ bbox_keys,
+                                                        int prefilter, double tol, double tol2,
+                                                        uint32_t* __restrict__ inside_bits,
+                                                        uint32_t* __restrict__ aux_bits,
+                                                        const uint32_t* __restrict__ n_dev) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    SingleShared& sh = *reinterpret_cast<SingleShared*>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (n_dev) n = min(n, (uint64_t)*n_dev); // bucketed input: only the in-box prefix is live
+    const uint64_t cta_base = (uint64_t)blockIdx.x * (kTPB * kK);
+    if (cta_base >= n) return;
+    const uint32_t e_begin = blockIdx.y * edges_per_chunk;
+    const uint32_t e_end = min(n_edges, e_begin + edges_per_chunk);
+    const uint64_t wbase = cta_base + (uint64_t)warp * 32 * kK; // this warp's first point
+
+    // ---- keys of this thread's points (coordinates stay in global / L1) ----
+    double minx = 0, miny = 0, maxx = 0, maxy = 0;
+    if (prefilter) {
+        minx = dkey_inv(bbox_keys[0]);
+        miny = dkey_inv(bbox_keys[1]);
+        maxx = dkey_inv(~bbox_keys[2]);
+        maxy = dkey_inv(~bbox_keys[3]);
+    }
+    int ka[kK], kb[kK];
+    uint32_t act = 0;
+#pragma unroll
+    for (int k = 0; k < kK; ++k) {
+        const uint64_t i = wbase + k * 32 + lane;
+        bool a = i < n;
+        double2 p = make_double2(0.0, 0.0);
+        if (a) p = pts[i];
+        if (a && prefilter) a = p.x >= minx && p.x <= maxx && p.y >= miny && p.y <= maxy; // batch.hpp:39-41
+        if (MODE == kRobust) {
+            ka[k] = a ? fkey(__dadd_rn(p.y, tol)) : INT_MIN;
+            kb[k] = a ? fkey(__dsub_rn(p.y, tol)) : INT_MAX;
+        } else {
+            ka[k] = a ? fkey(p.y) : INT_MAX; // INT_MAX is above every key: never a candidate
+            kb[k] = 0;
+        }
+        act |= (uint32_t)a << k;
+    }
+    const bool warp_live = __any_sync(0xffffffffu, act != 0);
+
+    // ---- edge tiles through a 2-deep TMA pipeline ----
+    if (tid == 0) {
+        mbar_init(&sh.full[0], 1);
+        mbar_init(&sh.full[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const uint32_t n_tiles = (e_end - e_begin + kTile - 1) / kTile;
+    if (tid == 0) {
+        for (uint32_t q = 0; q < 2 && q < n_tiles; ++q)
+            issue_tile(sh, (int)q, filt, rec, e_begin + q * kTile, min((uint32_t)kTile, e_end - e_begin - q * kTile));
+    }
+    uint32_t par = 0, auxm = 0;
+    for (uint32_t q = 0; q < n_tiles; ++q) {
+        const int s = (int)(q & 1);
+        const uint32_t t0 = e_begin + q * kTile;
+        const uint32_t nt = min((uint32_t)kTile, e_end - t0);
+        mbar_wait(&sh.full[s], (q >> 1) & 1);
+        const TileStage& T = sh.st[s];
+        if (warp_live) {
+            for (uint32_t e = 0; e < nt; ++e) {
+                const uint2 f = T.filt[e];
+                bool any;
+                if (MODE == kRobust) {
+                    bool c = false;
+#pragma unroll
+                    for (int k = 0; k < kK; ++k) c |= (ka[k] >= (int)f.x) & (kb[k] <= (int)f.y);
+                    any = __any_sync(0xffffffffu, c);
+                } else {
+                    const uint32_t neg = 0u - f.x;
+                    uint32_t m0 = (uint32_t)ka[0] + neg, m1 = (uint32_t)ka[1] + neg;
+                    uint32_t m2 = (uint32_t)ka[2] + neg, m3 = (uint32_t)ka[3] + neg;
+#pragma unroll
+                    for (int k = 4; k < kK; k += 4) {
+                        m0 = min(m0, (uint32_t)ka[k] + neg);
+                        m1 = min(m1, (uint32_t)ka[k + 1] + neg);
+                        m2 = min(m2, (uint32_t)ka[k + 2] + neg);
+                        m3 = min(m3, (uint32_t)ka[k + 3] + neg);
+                    }
+                    any = __any_sync(0xffffffffu, min(min(m0, m1), min(m2, m3)) <= f.y);
+                }
+                if (!any) continue;
+                // ---- slow path: exact binary64 test for the candidate points ----
+                const EdgeRec r = T.rec[e];
+#pragma unroll
+                for (int k = 0; k < kK; ++k) {
+                    bool c;
+                    bool sure = false;
+                    if (MODE == kRobust) {
+                        c = (ka[k] >= (int)f.x) & (kb[k] <= (int)f.y);
+                    } else {
+                        const uint32_t d = (uint32_t)ka[k] - f.x;
+                        c = d <= f.y;
+                        sure = d != 0u && d != f.y; // key order strict on both sides
+                    }
+                    if (!__any_sync(0xffffffffu, c)) continue;
+                    if (c) {
+                        const double2 p = pts[wbase + k * 32 + lane];
+                        int cnt = 0;
+                        bool ax = false;
+                        if (MODE == kC1) exact_c1(p.x, p.y, r, cnt, sure);
+                        else if (MODE == kC2) exact_c2(p.x, p.y, r, cnt, ax, sure);
+                        else exact_robust(p.x, p.y, tol, tol2, r, cnt, ax);
+                        par ^= (uint32_t)(cnt & 1) << k;
+                        auxm |= (uint32_t)ax << k;
+                    }
+                }
+            }
+        }
+        __syncthreads(); // stage s fully consumed
+        if (tid == 0 && q + 2 < n_tiles)
+            issue_tile(sh, s, filt, rec, t0 + 2 * kTile, min((uint32_t)kTile, e_end - (t0 + 2 * kTile)));
+    }
+
+    // ---- flags: one ballot word per k-slice ----
+#pragma unroll
+    for (int k = 0; k < kK; ++k) {
+        const uint32_t b = __ballot_sync(0xffffffffu, (par & act) >> k & 1u);
+        const uint32_t a = __ballot_sync(0xffffffffu, (auxm & act) >> k & 1u);
+        const uint64_t i0 = wbase + k * 32;
+        if (lane == 0 && i0 < n) {
+            if (b) atomicXor(&inside_bits[i0 >> 5], b);
+            if (a) atomicOr(&aux_bits[i0 >> 5], a);
+        }
+    }
+}
+
+int sms(int dev) {
+    int v = 148;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+}
+
+template <int MODE>
+cudaError_t launch_t(const SingleArgs& a, cudaStream_t st, int dev, uint64_t* launches) {
+    const size_t smem = sizeof(SingleShared);
+    static bool attr[64] = {};
+    if (dev < 64 && !attr[dev]) {
+        cudaFuncSetAttribute(pip_tile_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr[dev] = true;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pip_tile_kernel<MODE>, kTPB, smem);
+    per_sm = std::max(per_sm, 1);
+    const uint64_t pts_per_cta = (uint64_t)kTPB * kK;
+    const uint64_t n_ptiles = (a.n + pts_per_cta - 1) / pts_per_cta;
+    const uint64_t slots = (uint64_t)sms(dev) * per_sm;
+    // Split the edges so the grid covers >= ~4 waves; chunks are whole tiles.
+    const uint64_t tiles = std::max<uint64_t>(1, (a.n_edges + kTile - 1) / kTile);
+    uint64_t chunks = std::max<uint64_t>(1, (4 * slots + n_ptiles - 1) / std::max<uint64_t>(n_ptiles, 1));
+    chunks = std::min<uint64_t>(std::min<uint64_t>(chunks, tiles), 65535);
+    const uint64_t tiles_per_chunk = (tiles + chunks - 1) / chunks;
+    const uint32_t per_chunk = (uint32_t)(tiles_per_chunk * kTile);
+    chunks = (tiles + tiles_per_chunk - 1) / tiles_per_chunk;
+    dim3 grid((unsigned)n_ptiles, (unsigned)chunks);
+    pip_tile_kernel<MODE><<<grid, kTPB, smem, st>>>(reinterpret_cast<const double2*>(a.pts), a.n, a.filt,
+                                                   reinterpret_cast<const EdgeRec*>(a.rec), a.n_edges, per_chunk,
+                                                   a.bbox_keys, a.prefilter, a.tol, a.tol2, a.inside_bits,
+                                                   a.aux_bits, a.n_dev);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+} // namespace
+
+cudaError_t launch_single(const SingleArgs& a, cudaStream_t st, int dev, uint64_t* launches) {
+    if (a.n == 0) return cudaSuccess;
+    switch (a.mode) {
+    case kC1: return launch_t<kC1>(a, st, dev, launches);
+    case kC2: return launch_t<kC2>(a, st, dev, launches);
+    default: return launch_t<kRobust>(a, st, dev, launches);
+    }
+}
+
+} // namespace pcd

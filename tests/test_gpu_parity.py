@@ -305,3 +305,49 @@ def test_bucketing_modes_identical(bucket):
             for mode in MODES:
                 check_single(xy, poly, mode, eng.classify(xy, poly, mode), source=src)
                 check_single(xy, poly, mode, eng.classify(xy, poly, mode, prefilter=False), prefilter=False)
+
+
+def _concat_csr(parts):
+    """Concatenate CsrSets (offsets rebased)."""
+    xy, vx, vy = [], [], []
+    pt_off, ring_off, pring = [0], [0], [0]
+    for s in parts:
+        base_p, base_v, base_r = pt_off[-1], ring_off[-1], pring[-1]
+        xy.append(s.xy)
+        vx.append(s.vx)
+        vy.append(s.vy)
+        pt_off += [base_p + int(v) for v in s.pt_off[1:]]
+        ring_off += [base_v + int(v) for v in s.ring_off[1:]]
+        pring += [base_r + int(v) for v in s.poly_ring_off[1:]]
+    return CsrSet(np.ascontiguousarray(np.concatenate(xy)), np.array(pt_off, np.uint64), np.concatenate(vx),
+                  np.concatenate(vy), np.array(ring_off, np.uint64), np.array(pring, np.uint64))
+
+
+def _single_as_csr(poly, xy):
+    return CsrSet(np.ascontiguousarray(xy), np.array([0, len(xy)], np.uint64), poly.vx, poly.vy, poly.ring_off,
+                  np.array([0, poly.n_rings], np.uint64))
+
+
+def test_csr_oversize_and_mixed_polygons(engine):
+    """CSR stages hold <=1024 points / 512 vertices / 128 rings; bigger polygons take the
+    global-memory path.  Mix both, plus empty polygons and odd vertex offsets."""
+    rng = np.random.default_rng(11)
+    parts = [W.footprints(300, seed=1)]
+    big = W.star_polygon(2000, seed=3)                         # > kVmax vertices
+    parts.append(_single_as_csr(big, W.uniform_points(3000, W.bounds(big), 4)))  # > kPmax points
+    parts.append(W.degenerate(200, seed=5))
+    rings = [[(0, 0), (300, 0), (300, 300), (0, 300), (0, 0)]]
+    for k in range(140):                                       # > kRmax rings
+        x, y = 10 + 20 * (k % 14), 10 + 20 * (k // 14)
+        rings.append([(x, y), (x + 5, y), (x + 5, y + 5), (x, y + 5), (x, y)])
+    holed = Polygon.from_rings(rings)
+    parts.append(_single_as_csr(holed, rng.uniform(-10, 310, (500, 2))))
+    parts.append(CsrSet(np.zeros((0, 2)), np.array([0, 0], np.uint64), np.array([0., 1, 1, 0]),
+                        np.array([0., 0, 1, 0]), np.array([0, 4], np.uint64), np.array([0, 1], np.uint64)))
+    parts.append(W.footprints(500, seed=2, pts_per_poly=33))     # unaligned point runs
+    s = _concat_csr(parts)
+    for mode in MODES:
+        got = engine.classify_csr(s, mode)
+        want_v, want_s = oracle.port_classify_csr(s, mode, threads=THREADS)
+        assert np.array_equal(got.verdicts, want_v), f"mode {mode}: {(got.verdicts != want_v).sum()} differ"
+        assert np.array_equal(got.stats, want_s)
