@@ -8,7 +8,8 @@
 // exactly like the reference's per-ring sums (geometry.hpp:285-299).
 //
 // Per thread: K points, of which only the 32-bit filter keys live in
-// registers; parity and aux flags are K-bit masks.  Warp w owns K*32
+// registers (coordinates sit in shared memory, loaded once per CTA by one TMA
+// bulk copy); parity and aux flags are K-bit masks.  Warp w owns K*32
 // consecutive points (k-slice k = 32 consecutive points), which after
 // y-bucketing (pip_sort.cu) are y-adjacent, so an edge either misses the whole
 // warp or is a candidate for most of it.
@@ -39,7 +40,7 @@ namespace {
 
 constexpr int kTPB = 256;
 constexpr int kK = 16;      // points per thread
-constexpr int kTile = 256;  // edges per shared-memory stage (multiple of 2: 16-byte bulk copies)
+constexpr int kTile = 128;  // edges per shared-memory stage (multiple of 2: 16-byte bulk copies)
 
 struct __align__(128) TileStage {
     EdgeRec rec[kTile];
@@ -47,8 +48,10 @@ struct __align__(128) TileStage {
 };
 
 struct SingleShared {
+    double2 pts[kTPB * kK]; // this CTA's points (bucketed order), one TMA bulk copy
     TileStage st[2];
     unsigned long long full[2];
+    unsigned long long pbar;
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -87,8 +90,98 @@ __device__ __forceinline__ void issue_tile(SingleShared& sh, int s, const uint2*
                  : "memory");
 }
 
+// Fast path: may any of the warp's points straddle the edge?  d_k = key_k -
+// key(ylo) (mod 2^32) is a candidate iff d_k <= key(yhi) - key(ylo).  The
+// minimum over the 16 points is formed half on the FMA pipe (IMAD subtracts
+// + 3-input VIMNMX) and half as fused add+min (VIADDMNMX) on the ALU pipe, so
+// both integer pipes share the work.
 template <int MODE>
-__global__ void __launch_bounds__(kTPB) pip_tile_kernel(const double2* __restrict__ pts, uint64_t n,
+__device__ __forceinline__ bool warp_any_candidate(const int (&ka)[kK], const int (&kb)[kK], uint2 f) {
+    if (MODE == kRobust) {
+        bool c = false;
+#pragma unroll
+        for (int k = 0; k < kK; ++k) c |= (ka[k] >= (int)f.x) & (kb[k] <= (int)f.y);
+        return __any_sync(0xffffffffu, c);
+    }
+    uint32_t d[kK];
+#pragma unroll
+    for (int k = 4; k < kK; ++k) d[k] = (uint32_t)ka[k] - f.x;
+    uint32_t m = __vimin3_u32(d[4], d[5], d[6]);
+#pragma unroll
+    for (int k = 7; k + 1 < kK; k += 2) m = __vimin3_u32(m, d[k], d[k + 1]);
+    if (kK % 2 == 0) m = min(m, d[kK - 1]);
+    const uint32_t neg = 0u - f.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) m = __viaddmin_u32((uint32_t)ka[k], neg, m);
+    return __any_sync(0xffffffffu, m <= f.y);
+}
+
+// C1 slow path (geometry.hpp:189-200), branch-free over the 16 points: the
+// side test runs for every point with full ILP and counts only for
+// candidates.  Key ties (d == 0 or d == range), where the keys cannot decide
+// the straddle, take the reference product in a rare warp-uniform branch.
+__device__ __forceinline__ void slow_c1(const double2* my_pts, const int (&ka)[kK], uint2 f, const EdgeRec& r,
+                                        uint32_t& par) {
+    const double ax = r.d[0], ay = r.d[1], nx = r.d[3], ny = r.d[4];
+    uint32_t cm = 0, tm = 0;
+#pragma unroll
+    for (int k = 0; k < kK; ++k) {
+        const uint32_t d = (uint32_t)ka[k] - f.x;
+        cm |= (uint32_t)(d <= f.y) << k;
+        tm |= (uint32_t)(d - 1u >= f.y - 1u) << k; // d in {0, range} (only meaningful with cm)
+    }
+    tm &= cm;
+    if (__any_sync(0xffffffffu, tm != 0)) {
+        const double by = r.d[2];
+#pragma unroll 1
+        for (int k = 0; k < kK; ++k) {
+            if (tm >> k & 1u) {
+                const double py = my_pts[k * 32].y;
+                if (!(__dmul_rn(__dsub_rn(ay, py), __dsub_rn(by, py)) <= 0.0)) cm &= ~(1u << k);
+            }
+        }
+    }
+    uint32_t hit = 0;
+#pragma unroll
+    for (int k = 0; k < kK; ++k) {
+        const double2 p = my_pts[k * 32];
+        const double side = __dadd_rn(__dmul_rn(__dsub_rn(p.x, ax), nx), __dmul_rn(__dsub_rn(p.y, ay), ny));
+        hit |= (uint32_t)(side <= 0.0) << k;
+    }
+    par ^= hit & cm;
+}
+
+// C2 / Robust slow path: per point, only for candidates (division is costly).
+template <int MODE>
+__device__ __forceinline__ void slow_generic(const double2* my_pts, const int (&ka)[kK], const int (&kb)[kK], uint2 f,
+                                             const EdgeRec& r, double tol, double tol2, uint32_t& par,
+                                             uint32_t& auxm) {
+#pragma unroll
+    for (int k = 0; k < kK; ++k) {
+        bool c;
+        bool sure = false;
+        if (MODE == kRobust) {
+            c = (ka[k] >= (int)f.x) & (kb[k] <= (int)f.y);
+        } else {
+            const uint32_t d = (uint32_t)ka[k] - f.x;
+            c = d <= f.y;
+            sure = d - 1u < f.y - 1u; // key order strict on both sides
+        }
+        if (!__any_sync(0xffffffffu, c)) continue;
+        if (c) {
+            const double2 p = my_pts[k * 32];
+            int cnt = 0;
+            bool ax = false;
+            if (MODE == kC2) exact_c2(p.x, p.y, r, cnt, ax, sure);
+            else exact_robust(p.x, p.y, tol, tol2, r, cnt, ax);
+            par ^= (uint32_t)(cnt & 1) << k;
+            auxm |= (uint32_t)ax << k;
+        }
+    }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kTPB, 2) pip_tile_kernel(const double2* __restrict__ pts, uint64_t n,
                                                         const uint2* __restrict__ filt,
                                                         const EdgeRec* __restrict__ rec, uint32_t n_edges,
                                                         uint32_t edges_per_chunk,
@@ -105,9 +198,29 @@ __global__ void __launch_bounds__(kTPB) pip_tile_kernel(const double2* __restric
     if (cta_base >= n) return;
     const uint32_t e_begin = blockIdx.y * edges_per_chunk;
     const uint32_t e_end = min(n_edges, e_begin + edges_per_chunk);
-    const uint64_t wbase = cta_base + (uint64_t)warp * 32 * kK; // this warp's first point
+    const uint64_t wbase = cta_base + (uint64_t)warp * 32 * kK; // this warp's first point (global)
 
-    // ---- keys of this thread's points (coordinates stay in global / L1) ----
+    const uint32_t cta_n = (uint32_t)min((uint64_t)(kTPB * kK), n - cta_base);
+    if (tid == 0) {
+        mbar_init(&sh.full[0], 1);
+        mbar_init(&sh.full[1], 1);
+        mbar_init(&sh.pbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const uint32_t n_tiles = (e_end - e_begin + kTile - 1) / kTile;
+    if (tid == 0) {
+        const unsigned pb = cta_n * 16u, bar = smem_u32(&sh.pbar);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(pb) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(sh.pts)),
+                     "l"(pts + cta_base), "r"(pb), "r"(bar)
+                     : "memory");
+        for (uint32_t q = 0; q < 2 && q < n_tiles; ++q)
+            issue_tile(sh, (int)q, filt, rec, e_begin + q * kTile, min((uint32_t)kTile, e_end - e_begin - q * kTile));
+    }
+
+    // ---- keys of this thread's points (coordinates stay in shared memory) ----
     double minx = 0, miny = 0, maxx = 0, maxy = 0;
     if (prefilter) {
         minx = dkey_inv(bbox_keys[0]);
@@ -115,14 +228,16 @@ __global__ void __launch_bounds__(kTPB) pip_tile_kernel(const double2* __restric
         maxx = dkey_inv(~bbox_keys[2]);
         maxy = dkey_inv(~bbox_keys[3]);
     }
+    const uint32_t wloc = (uint32_t)warp * 32 * kK; // this warp's first point within the CTA
+    mbar_wait(&sh.pbar, 0);
     int ka[kK], kb[kK];
     uint32_t act = 0;
 #pragma unroll
     for (int k = 0; k < kK; ++k) {
-        const uint64_t i = wbase + k * 32 + lane;
-        bool a = i < n;
+        const uint32_t li = wloc + k * 32 + lane;
+        bool a = li < cta_n;
         double2 p = make_double2(0.0, 0.0);
-        if (a) p = pts[i];
+        if (a) p = sh.pts[li];
         if (a && prefilter) a = p.x >= minx && p.x <= maxx && p.y >= miny && p.y <= maxy; // batch.hpp:39-41
         if (MODE == kRobust) {
             ka[k] = a ? fkey(__dadd_rn(p.y, tol)) : INT_MIN;
@@ -135,18 +250,6 @@ __global__ void __launch_bounds__(kTPB) pip_tile_kernel(const double2* __restric
     }
     const bool warp_live = __any_sync(0xffffffffu, act != 0);
 
-    // ---- edge tiles through a 2-deep TMA pipeline ----
-    if (tid == 0) {
-        mbar_init(&sh.full[0], 1);
-        mbar_init(&sh.full[1], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    const uint32_t n_tiles = (e_end - e_begin + kTile - 1) / kTile;
-    if (tid == 0) {
-        for (uint32_t q = 0; q < 2 && q < n_tiles; ++q)
-            issue_tile(sh, (int)q, filt, rec, e_begin + q * kTile, min((uint32_t)kTile, e_end - e_begin - q * kTile));
-    }
     uint32_t par = 0, auxm = 0;
     for (uint32_t q = 0; q < n_tiles; ++q) {
         const int s = (int)(q & 1);
@@ -155,53 +258,15 @@ __global__ void __launch_bounds__(kTPB) pip_tile_kernel(const double2* __restric
         mbar_wait(&sh.full[s], (q >> 1) & 1);
         const TileStage& T = sh.st[s];
         if (warp_live) {
+#pragma unroll 2
             for (uint32_t e = 0; e < nt; ++e) {
                 const uint2 f = T.filt[e];
-                bool any;
-                if (MODE == kRobust) {
-                    bool c = false;
-#pragma unroll
-                    for (int k = 0; k < kK; ++k) c |= (ka[k] >= (int)f.x) & (kb[k] <= (int)f.y);
-                    any = __any_sync(0xffffffffu, c);
-                } else {
-                    const uint32_t neg = 0u - f.x;
-                    uint32_t m0 = (uint32_t)ka[0] + neg, m1 = (uint32_t)ka[1] + neg;
-                    uint32_t m2 = (uint32_t)ka[2] + neg, m3 = (uint32_t)ka[3] + neg;
-#pragma unroll
-                    for (int k = 4; k < kK; k += 4) {
-                        m0 = min(m0, (uint32_t)ka[k] + neg);
-                        m1 = min(m1, (uint32_t)ka[k + 1] + neg);
-                        m2 = min(m2, (uint32_t)ka[k + 2] + neg);
-                        m3 = min(m3, (uint32_t)ka[k + 3] + neg);
-                    }
-                    any = __any_sync(0xffffffffu, min(min(m0, m1), min(m2, m3)) <= f.y);
-                }
-                if (!any) continue;
+                if (!warp_any_candidate<MODE>(ka, kb, f)) continue;
                 // ---- slow path: exact binary64 test for the candidate points ----
-                const EdgeRec r = T.rec[e];
-#pragma unroll
-                for (int k = 0; k < kK; ++k) {
-                    bool c;
-                    bool sure = false;
-                    if (MODE == kRobust) {
-                        c = (ka[k] >= (int)f.x) & (kb[k] <= (int)f.y);
-                    } else {
-                        const uint32_t d = (uint32_t)ka[k] - f.x;
-                        c = d <= f.y;
-                        sure = d != 0u && d != f.y; // key order strict on both sides
-                    }
-                    if (!__any_sync(0xffffffffu, c)) continue;
-                    if (c) {
-                        const double2 p = pts[wbase + k * 32 + lane];
-                        int cnt = 0;
-                        bool ax = false;
-                        if (MODE == kC1) exact_c1(p.x, p.y, r, cnt, sure);
-                        else if (MODE == kC2) exact_c2(p.x, p.y, r, cnt, ax, sure);
-                        else exact_robust(p.x, p.y, tol, tol2, r, cnt, ax);
-                        par ^= (uint32_t)(cnt & 1) << k;
-                        auxm |= (uint32_t)ax << k;
-                    }
-                }
+                if (MODE == kC1)
+                    slow_c1(sh.pts + wloc + lane, ka, f, T.rec[e], par);
+                else
+                    slow_generic<MODE>(sh.pts + wloc + lane, ka, kb, f, T.rec[e], tol, tol2, par, auxm);
             }
         }
         __syncthreads(); // stage s fully consumed
