@@ -67,11 +67,11 @@ def build_items(workload, rank, world):
         return [Item("star1000", poly, W.uniform_points(1_000_000, (-1.0, -1.0, 1.0, 1.0), seed + 1))]
     if workload == "c4":
         poly = W.fractal_polygon(200_000, W.SEED)
+        from paper_2306_04316_b200.dist import shard_range
         total = 100_000_000
-        lo, hi = total * rank // world, total * (rank + 1) // world
-        xy = W.uniform_points(total, W.bounds(poly), W.SEED + 4)[lo:hi] if world > 1 else \
-            W.uniform_points(total, W.bounds(poly), W.SEED + 4)
-        return [Item("fractal200k", poly, np.ascontiguousarray(xy))]
+        lo, hi = shard_range(total, rank, world)
+        xy = W.uniform_points(total, W.bounds(poly), W.SEED + 4)
+        return [Item("fractal200k", poly, np.ascontiguousarray(xy[lo:hi]) if world > 1 else xy)]
     if workload == "c3":
         return [Item("footprints1e6", csr=W.footprints(1_000_000, seed=seed))]
     if workload == "c5":
@@ -292,10 +292,8 @@ def run_ours(args, rank, world, local_rank):
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     kern_ms = eng.profile_take(0)
     tot_ms = sum(step_ms)
-    t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    max_ms = float(t.item())
+    from paper_2306_04316_b200.dist import max_over_ranks
+    max_ms = max_over_ranks(tot_ms, world, dev)
     tot_units, tot_pts = job_totals(items, world, dev)
     value = tot_units / (max_ms / args.steps / 1e3)
 
@@ -357,15 +355,8 @@ def run_ours(args, rank, world, local_rank):
 
 def job_totals(items, world, dev):
     """(tests, points) processed by all ranks in one step."""
-    units = float(sum(i.tests for i in items))
-    pts = float(sum(i.n_points for i in items))
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-        u = torch.tensor([units, pts], dtype=torch.float64, device=dev)
-        dist.all_reduce(u)
-        units, pts = float(u[0]), float(u[1])
-    return units, pts
+    from paper_2306_04316_b200.dist import job_totals as jt
+    return jt(sum(i.tests for i in items), sum(i.n_points for i in items), world, dev)
 
 
 def run_e2e(args, eng, items, world, rank):
@@ -411,11 +402,10 @@ def run_e2e(args, eng, items, world, rank):
     for _ in range(args.steps):
         step()
     dt = time.perf_counter() - t0
-    t = torch.tensor([dt], dtype=torch.float64, device=torch.device("cuda", torch.cuda.current_device()))
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    dt = float(t.item()) / args.steps
-    units, _ = job_totals(items, world, t.device)
+    from paper_2306_04316_b200.dist import max_over_ranks
+    dev = torch.device("cuda", torch.cuda.current_device())
+    dt = max_over_ranks(dt, world, dev) / args.steps
+    units, _ = job_totals(items, world, dev)
     return {"value": units / dt, "unit": "tests/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "ms_per_step": dt * 1e3, "api": "pc_classify / pc_classify_csr (host pointers, pinned)"}
 

@@ -131,7 +131,7 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
     const uint64_t nwords = (n + 31) / 32;
     check(c, d.filt.ensure((n_edges + 2) * sizeof(uint2)), "alloc edge keys"); // +2: 16-byte bulk-copy padding
     check(c, d.rec.ensure(std::max<uint64_t>(n_edges, 1) * pcd::edge_rec_bytes()), "alloc edge records");
-    check(c, d.bbox.ensure(4 * sizeof(unsigned long long)), "alloc bbox");
+    check(c, d.bbox.ensure(8 * sizeof(unsigned long long)), "alloc bbox"); // 4 keys + key map
     pcd::PrepArgs pa{};
     pa.mode = mode;
     pa.vx = d_vx;

@@ -45,6 +45,42 @@ __device__ __forceinline__ double dkey_inv(unsigned long long k) {
     return __longlong_as_double(static_cast<long long>(b));
 }
 
+// 15-bit keys for the packed filter.  Two keys share a 32-bit register as
+// (q_a << 1) | (q_b << 17): one 32-bit IMAD then subtracts an edge's key from
+// both halves exactly (the low half's carry only reaches bit 0 of the high
+// half, which the compare ignores) and a 3-input packed VIMNMX3.U16x2 folds
+// four points into a running minimum.
+// q(y) = clamp(floor((c(y) - y0) * scale), 0, 32767) with
+// c(y) = 0 for |y| < 2^-480, else y.  Every step (collapse, RN subtract, RN
+// multiply by scale >= 0, clamp, floor) is monotone non-decreasing, so as for
+// fkey: q(u) < q(v) => u < v.  The collapse keeps the product-underflow cases
+// of the straddle test (both |y - p.y| < 2^-537, which forces all three values
+// below 2^-484) on equal keys, i.e. they are never rejected.  y0/scale come
+// from the outer ring's bbox (any values are correct; a tight range makes the
+// filter sharp).
+struct QMap {
+    double y0, scale;
+};
+
+__device__ __forceinline__ double q_collapse(double y) { return fabs(y) < 0x1p-480 ? 0.0 : y; }
+
+__device__ __forceinline__ QMap qmap_from_bbox(const unsigned long long* bbox_keys) {
+    QMap m;
+    const double lo = q_collapse(dkey_inv(bbox_keys[1])), hi = q_collapse(dkey_inv(~bbox_keys[3]));
+    const double h = __dsub_rn(hi, lo);
+    m.y0 = lo;
+    m.scale = (h > 0.0 && h < 1e300) ? __ddiv_rn(32767.0, h) : 0.0; // degenerate: all keys equal
+    if (!(lo == lo)) m.y0 = 0.0;                                     // empty outer ring
+    return m;
+}
+
+__device__ __forceinline__ uint32_t qkey15(double y, const QMap& m) {
+    double t = __dmul_rn(__dsub_rn(q_collapse(y), m.y0), m.scale);
+    t = t > 0.0 ? t : 0.0; // also maps a NaN product (0 * inf cannot occur: scale < inf) to 0
+    t = t < 32767.0 ? t : 32767.0;
+    return (uint32_t)t;
+}
+
 // C1 exact test of one straddle candidate (geometry.hpp:189-200).  `sure`:
 // the keys already prove min(a.y,b.y) < p.y < max(a.y,b.y) strictly, so the
 // reference's product f_prev*f_next is negative (or -0) and `<= 0.0` holds;

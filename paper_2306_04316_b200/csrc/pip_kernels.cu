@@ -1,6 +1,7 @@
 // sm_100a kernels of the batched point-in-polygon path.
 //
-//   prep_edges_kernel   raw rings -> per-edge filter keys + exact records, bbox
+//   prep_bbox_kernel    outer-ring bbox, zeroed planes/stats
+//   prep_edges_kernel   raw rings -> per-edge filter keys + exact records
 //   (the single-polygon kernel lives in pip_single.cu)
 //   (the CSR multi-polygon kernel lives in pip_csr.cu, bucketing in pip_sort.cu)
 //   finalize_kernel     bit planes -> verdict bytes + BatchStats
@@ -34,70 +35,27 @@ __device__ __forceinline__ uint32_t ring_of(const uint64_t* ring_off, uint32_t n
     return lo;
 }
 
-// One thread per vertex v: if (v, v+1) is an edge of the same ring, write its
-// filter key pair and exact record at edge index e = v - ring(v).  Also folds
-// the outer ring's vertices into the bbox (monotone-key atomics on memory
-// pre-set to 0xff) and zeroes the output bit planes and stats.
-template <int MODE>
-__global__ void __launch_bounds__(256) prep_edges_kernel(
-    const double* __restrict__ vx, const double* __restrict__ vy, const uint64_t* __restrict__ ring_off,
-    uint32_t n_rings, uint64_t n_verts, uint2* __restrict__ filt, EdgeRec* __restrict__ rec,
-    unsigned long long* __restrict__ bbox_keys, uint32_t* __restrict__ zero_words, uint64_t n_zero_words,
-    unsigned long long* __restrict__ stats) {
+// Outer-ring bbox (monotone-key atomics on memory pre-set to 0xff), plus
+// zeroing of the output plane and stats.  Runs before prep_edges_kernel, which
+// needs the bbox for the 16-bit key map.
+__global__ void __launch_bounds__(256) prep_bbox_kernel(const double* __restrict__ vx, const double* __restrict__ vy,
+                                                        const uint64_t* __restrict__ ring_off,
+                                                        unsigned long long* __restrict__ bbox_keys,
+                                                        uint32_t* __restrict__ zero_words, uint64_t n_zero_words,
+                                                        unsigned long long* __restrict__ stats) {
     const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t w = tid; w < n_zero_words; w += stride) zero_words[w] = 0u;
     if (tid < 4) stats[tid] = 0ull;
-
     const uint64_t outer_end = ring_off[1];
     unsigned long long kminx = ~0ull, kminy = ~0ull, kmaxx = ~0ull, kmaxy = ~0ull;
-    for (uint64_t v = tid; v < n_verts; v += stride) {
-        const double ax = vx[v], ay = vy[v];
-        if (v < outer_end) {
-            const unsigned long long kx = dkey(ax), ky = dkey(ay);
-            kminx = min(kminx, kx);
-            kminy = min(kminy, ky);
-            kmaxx = min(kmaxx, ~kx);
-            kmaxy = min(kmaxy, ~ky);
-        }
-        const uint32_t r = ring_of(ring_off, n_rings, v);
-        if (v + 1 >= ring_off[r + 1]) continue; // last (closing) vertex of its ring
-        const uint64_t e = v - r;
-        const double bx = vx[v + 1], by = vy[v + 1];
-        EdgeRec er;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) er.d[i] = 0.0;
-        er.d[0] = ax;
-        er.d[1] = ay;
-        er.d[2] = by;
-        const double ylo = by < ay ? by : ay; // std::min(a.y, b.y)
-        const double yhi = ay < by ? by : ay; // std::max(a.y, b.y)
-        const int klo = fkey(ylo), khi = fkey(yhi);
-        if (MODE == kC1) {
-            double nx = __dsub_rn(by, ay), ny = __dsub_rn(ax, bx);
-            if (nx < 0.0) {
-                nx = -nx;
-                ny = -ny;
-            }
-            er.d[3] = nx;
-            er.d[4] = ny;
-            filt[e] = make_uint2((uint32_t)klo, (uint32_t)khi - (uint32_t)klo);
-        } else if (MODE == kC2) {
-            er.d[3] = __dsub_rn(bx, ax);
-            er.d[4] = __dsub_rn(by, ay);
-            filt[e] = make_uint2((uint32_t)klo, (uint32_t)khi - (uint32_t)klo);
-        } else {
-            const double abx = __dsub_rn(bx, ax), aby = __dsub_rn(by, ay);
-            er.d[3] = abx;
-            er.d[4] = aby;
-            er.d[5] = __dadd_rn(__dmul_rn(abx, abx), __dmul_rn(aby, aby));
-            er.d[6] = ylo;
-            er.d[7] = yhi;
-            filt[e] = make_uint2((uint32_t)klo, (uint32_t)khi);
-        }
-        rec[e] = er;
+    for (uint64_t v = tid; v < outer_end; v += stride) {
+        const unsigned long long kx = dkey(vx[v]), ky = dkey(vy[v]);
+        kminx = min(kminx, kx);
+        kminy = min(kminy, ky);
+        kmaxx = min(kmaxx, ~kx);
+        kmaxy = min(kmaxy, ~ky);
     }
-    // warp-reduce then one atomic per warp and key
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         kminx = min(kminx, __shfl_xor_sync(0xffffffffu, kminx, o));
@@ -110,6 +68,64 @@ __global__ void __launch_bounds__(256) prep_edges_kernel(
         atomicMin(&bbox_keys[1], kminy);
         atomicMin(&bbox_keys[2], kmaxx);
         atomicMin(&bbox_keys[3], kmaxy);
+    }
+}
+
+// One thread per vertex v: if (v, v+1) is an edge of the same ring, write its
+// filter pair and exact record at edge index e = v - ring(v).
+//   C1/C2 filter: {(-q(ylo) mod 2^15) << 1 in both 16-bit halves, (q(yhi) - q(ylo)) << 1 | 1} (15-bit keys)
+//   Robust filter: {fkey(ylo), fkey(yhi)} (32-bit keys)
+template <int MODE>
+__global__ void __launch_bounds__(256) prep_edges_kernel(
+    const double* __restrict__ vx, const double* __restrict__ vy, const uint64_t* __restrict__ ring_off,
+    uint32_t n_rings, uint64_t n_verts, uint2* __restrict__ filt, EdgeRec* __restrict__ rec,
+    unsigned long long* __restrict__ bbox_keys) {
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const QMap qm = qmap_from_bbox(bbox_keys);
+    if (tid == 0) { // published for the classify kernels (bbox_keys[4..5])
+        reinterpret_cast<double*>(bbox_keys)[4] = qm.y0;
+        reinterpret_cast<double*>(bbox_keys)[5] = qm.scale;
+    }
+    for (uint64_t v = tid; v < n_verts; v += stride) {
+        const uint32_t r = ring_of(ring_off, n_rings, v);
+        if (v + 1 >= ring_off[r + 1]) continue; // last (closing) vertex of its ring
+        const uint64_t e = v - r;
+        const double ax = vx[v], ay = vy[v], bx = vx[v + 1], by = vy[v + 1];
+        EdgeRec er;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) er.d[i] = 0.0;
+        er.d[0] = ax;
+        er.d[1] = ay;
+        er.d[2] = by;
+        const double ylo = by < ay ? by : ay; // std::min(a.y, b.y)
+        const double yhi = ay < by ? by : ay; // std::max(a.y, b.y)
+        if (MODE == kRobust) {
+            const double abx = __dsub_rn(bx, ax), aby = __dsub_rn(by, ay);
+            er.d[3] = abx;
+            er.d[4] = aby;
+            er.d[5] = __dadd_rn(__dmul_rn(abx, abx), __dmul_rn(aby, aby));
+            er.d[6] = ylo;
+            er.d[7] = yhi;
+            filt[e] = make_uint2((uint32_t)fkey(ylo), (uint32_t)fkey(yhi));
+        } else {
+            if (MODE == kC1) {
+                double nx = __dsub_rn(by, ay), ny = __dsub_rn(ax, bx);
+                if (nx < 0.0) {
+                    nx = -nx;
+                    ny = -ny;
+                }
+                er.d[3] = nx;
+                er.d[4] = ny;
+            } else {
+                er.d[3] = __dsub_rn(bx, ax);
+                er.d[4] = __dsub_rn(by, ay);
+            }
+            const uint32_t klo = qkey15(ylo, qm), khi = qkey15(yhi, qm);
+            const uint32_t neg = ((0x8000u - klo) & 0x7fffu) << 1; // -q(ylo) mod 2^15, guard bit clear
+            filt[e] = make_uint2(neg | (neg << 16), ((khi - klo) << 1) | 1u);
+        }
+        rec[e] = er;
     }
 }
 
@@ -231,27 +247,25 @@ cudaError_t launch_fp64_probe(double* out, int iters, int dev, cudaStream_t st, 
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st, int dev, uint64_t* launches) {
     cudaError_t e = cudaMemsetAsync(a.bbox_keys, 0xff, 4 * sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
-    const uint64_t work = std::max<uint64_t>(a.n_verts, a.n_zero_words);
-    const unsigned blocks = (unsigned)std::min<uint64_t>((work + 255) / 256 + 1, (uint64_t)sm_count(dev) * 16);
+    const unsigned bb = (unsigned)std::min<uint64_t>(std::max<uint64_t>(a.n_verts, a.n_zero_words) / 256 + 1,
+                                                     (uint64_t)sm_count(dev) * 8);
+    prep_bbox_kernel<<<bb, 256, 0, st>>>(a.vx, a.vy, a.ring_off, a.bbox_keys, a.zero_words, a.n_zero_words, a.stats);
+    const unsigned blocks = (unsigned)std::min<uint64_t>(a.n_verts / 256 + 1, (uint64_t)sm_count(dev) * 16);
     switch (a.mode) {
     case kC1:
         prep_edges_kernel<kC1><<<blocks, 256, 0, st>>>(a.vx, a.vy, a.ring_off, a.n_rings, a.n_verts, a.filt,
-                                                       reinterpret_cast<EdgeRec*>(a.rec), a.bbox_keys,
-                                                       a.zero_words, a.n_zero_words, a.stats);
+                                                       reinterpret_cast<EdgeRec*>(a.rec), a.bbox_keys);
         break;
     case kC2:
         prep_edges_kernel<kC2><<<blocks, 256, 0, st>>>(a.vx, a.vy, a.ring_off, a.n_rings, a.n_verts, a.filt,
-                                                       reinterpret_cast<EdgeRec*>(a.rec), a.bbox_keys,
-                                                       a.zero_words, a.n_zero_words, a.stats);
+                                                       reinterpret_cast<EdgeRec*>(a.rec), a.bbox_keys);
         break;
     default:
-        prep_edges_kernel<kRobust><<<blocks, 256, 0, st>>>(a.vx, a.vy, a.ring_off, a.n_rings, a.n_verts,
-                                                           a.filt, reinterpret_cast<EdgeRec*>(a.rec),
-                                                           a.bbox_keys, a.zero_words, a.n_zero_words,
-                                                           a.stats);
+        prep_edges_kernel<kRobust><<<blocks, 256, 0, st>>>(a.vx, a.vy, a.ring_off, a.n_rings, a.n_verts, a.filt,
+                                                           reinterpret_cast<EdgeRec*>(a.rec), a.bbox_keys);
         break;
     }
-    ++*launches;
+    *launches += 2;
     return cudaGetLastError();
 }
 

@@ -17,7 +17,7 @@ struct PrepArgs {
     uint64_t n_verts;
     uint2* filt;                  // n_edges filter key pairs
     void* rec;                    // n_edges EdgeRec (edge_rec_bytes() each)
-    unsigned long long* bbox_keys; // 4 monotone keys: min x, min y, ~max x, ~max y
+    unsigned long long* bbox_keys; // 4 monotone keys: min x, min y, ~max x, ~max y; [4..5] 16-bit key map
     uint32_t* zero_words;          // output bit planes to clear (inside ++ aux, contiguous)
     uint64_t n_zero_words;
     unsigned long long* stats;     // 4 counters to clear

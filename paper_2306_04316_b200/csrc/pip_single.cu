@@ -90,46 +90,80 @@ __device__ __forceinline__ void issue_tile(SingleShared& sh, int s, const uint2*
                  : "memory");
 }
 
-// Fast path: may any of the warp's points straddle the edge?  d_k = key_k -
-// key(ylo) (mod 2^32) is a candidate iff d_k <= key(yhi) - key(ylo).  The
-// minimum over the 16 points is formed half on the FMA pipe (IMAD subtracts
-// + 3-input VIMNMX) and half as fused add+min (VIADDMNMX) on the ALU pipe, so
-// both integer pipes share the work.
+// Per-thread point keys.  C1/C2: 15-bit keys (qkey15), two points per
+// register as (q_2i << 1) | (q_2i+1 << 17).  Robust: 32-bit keys of p.y+tol
+// and p.y-tol.
 template <int MODE>
-__device__ __forceinline__ bool warp_any_candidate(const int (&ka)[kK], const int (&kb)[kK], uint2 f) {
-    if (MODE == kRobust) {
+struct Keys;
+template <>
+struct Keys<kC1> {
+    uint32_t k2[kK / 2];
+    // d_k = q_k - q(ylo) mod 2^15 for the edge whose filter word is fx
+    __device__ __forceinline__ uint32_t diff(int k, uint32_t fx) const {
+        return ((k2[k >> 1] + fx) >> (16 * (k & 1) + 1)) & 0x7fffu;
+    }
+};
+template <>
+struct Keys<kC2> : Keys<kC1> {};
+template <>
+struct Keys<kRobust> {
+    int ka[kK], kb[kK];
+};
+
+// Fast path: may any of this lane's points straddle the edge?
+// C1/C2: d_k = q_k - q(ylo) (mod 2^15); candidate iff d_k <= q(yhi) - q(ylo).
+// Per pair of points one 32-bit IMAD (FMA pipe) forms both d_k << 1 (+ a
+// guard bit); one VIMNMX3.U16x2 (ALU pipe) folds four points into the running
+// packed minimum, compared once against (range << 1) | 1.
+template <int MODE>
+__device__ __forceinline__ bool lane_candidate(const Keys<MODE>& K, uint2 f) {
+    if constexpr (MODE == kRobust) {
         bool c = false;
 #pragma unroll
-        for (int k = 0; k < kK; ++k) c |= (ka[k] >= (int)f.x) & (kb[k] <= (int)f.y);
-        return __any_sync(0xffffffffu, c);
+        for (int k = 0; k < kK; ++k) c |= (K.ka[k] >= (int)f.x) & (K.kb[k] <= (int)f.y);
+        return c;
+    } else {
+        uint32_t d[kK / 2];
+#pragma unroll
+        for (int i = 0; i < kK / 2; ++i) d[i] = K.k2[i] + f.x;
+        uint32_t m = __vimin3_u16x2(d[0], d[1], d[2]);
+#pragma unroll
+        for (int i = 3; i + 1 < kK / 2; i += 2) m = __vimin3_u16x2(m, d[i], d[i + 1]);
+        if ((kK / 2) % 2 == 0) m = __vminu2(m, d[kK / 2 - 1]);
+        return min(m & 0xffffu, m >> 16) <= f.y;
     }
-    uint32_t d[kK];
-#pragma unroll
-    for (int k = 4; k < kK; ++k) d[k] = (uint32_t)ka[k] - f.x;
-    uint32_t m = __vimin3_u32(d[4], d[5], d[6]);
-#pragma unroll
-    for (int k = 7; k + 1 < kK; k += 2) m = __vimin3_u32(m, d[k], d[k + 1]);
-    if (kK % 2 == 0) m = min(m, d[kK - 1]);
-    const uint32_t neg = 0u - f.x;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) m = __viaddmin_u32((uint32_t)ka[k], neg, m);
-    return __any_sync(0xffffffffu, m <= f.y);
 }
 
 // C1 slow path (geometry.hpp:189-200), branch-free over the 16 points: the
 // side test runs for every point with full ILP and counts only for
 // candidates.  Key ties (d == 0 or d == range), where the keys cannot decide
 // the straddle, take the reference product in a rare warp-uniform branch.
-__device__ __forceinline__ void slow_c1(const double2* my_pts, const int (&ka)[kK], uint2 f, const EdgeRec& r,
-                                        uint32_t& par) {
+__device__ __forceinline__ void slow_c1(const double2* my_pts, const Keys<kC1>& K, uint32_t act, uint2 f,
+                                        const EdgeRec& r, uint32_t& par, uint32_t wkey_lo, uint32_t wkey_hi) {
     const double ax = r.d[0], ay = r.d[1], nx = r.d[3], ny = r.d[4];
+    const uint32_t rng = f.y >> 1;
+    const uint32_t klo = (0x8000u - ((f.x & 0xffffu) >> 1)) & 0x7fffu;
+    if (klo < wkey_lo && wkey_hi < klo + rng) {
+        // every active point of the warp is strictly inside the edge's key range:
+        // all straddle for sure (no ties), only the side test remains
+        uint32_t hit = 0;
+#pragma unroll
+        for (int k = 0; k < kK; ++k) {
+            const double2 p = my_pts[k * 32];
+            const double side = __dadd_rn(__dmul_rn(__dsub_rn(p.x, ax), nx), __dmul_rn(__dsub_rn(p.y, ay), ny));
+            hit |= (uint32_t)(side <= 0.0) << k;
+        }
+        par ^= hit & act;
+        return;
+    }
     uint32_t cm = 0, tm = 0;
 #pragma unroll
     for (int k = 0; k < kK; ++k) {
-        const uint32_t d = (uint32_t)ka[k] - f.x;
-        cm |= (uint32_t)(d <= f.y) << k;
-        tm |= (uint32_t)(d - 1u >= f.y - 1u) << k; // d in {0, range} (only meaningful with cm)
+        const uint32_t d = K.diff(k, f.x);
+        cm |= (uint32_t)(d <= rng) << k;
+        tm |= (uint32_t)(d == 0u || d == rng) << k;
     }
+    cm &= act;
     tm &= cm;
     if (__any_sync(0xffffffffu, tm != 0)) {
         const double by = r.d[2];
@@ -153,19 +187,19 @@ __device__ __forceinline__ void slow_c1(const double2* my_pts, const int (&ka)[k
 
 // C2 / Robust slow path: per point, only for candidates (division is costly).
 template <int MODE>
-__device__ __forceinline__ void slow_generic(const double2* my_pts, const int (&ka)[kK], const int (&kb)[kK], uint2 f,
+__device__ __forceinline__ void slow_generic(const double2* my_pts, const Keys<MODE>& K, uint32_t act, uint2 f,
                                              const EdgeRec& r, double tol, double tol2, uint32_t& par,
                                              uint32_t& auxm) {
 #pragma unroll
     for (int k = 0; k < kK; ++k) {
         bool c;
         bool sure = false;
-        if (MODE == kRobust) {
-            c = (ka[k] >= (int)f.x) & (kb[k] <= (int)f.y);
+        if constexpr (MODE == kRobust) {
+            c = (K.ka[k] >= (int)f.x) & (K.kb[k] <= (int)f.y);
         } else {
-            const uint32_t d = (uint32_t)ka[k] - f.x;
-            c = d <= f.y;
-            sure = d - 1u < f.y - 1u; // key order strict on both sides
+            const uint32_t d = K.diff(k, f.x), rng = f.y >> 1;
+            c = d <= rng && (act >> k & 1u);
+            sure = d != 0u && d != rng; // key order strict on both sides
         }
         if (!__any_sync(0xffffffffu, c)) continue;
         if (c) {
@@ -230,8 +264,9 @@ __global__ void __launch_bounds__(kTPB, 2) pip_tile_kernel(const double2* __rest
     }
     const uint32_t wloc = (uint32_t)warp * 32 * kK; // this warp's first point within the CTA
     mbar_wait(&sh.pbar, 0);
-    int ka[kK], kb[kK];
+    Keys<MODE> K;
     uint32_t act = 0;
+    const QMap qm = {reinterpret_cast<const double*>(bbox_keys)[4], reinterpret_cast<const double*>(bbox_keys)[5]};
 #pragma unroll
     for (int k = 0; k < kK; ++k) {
         const uint32_t li = wloc + k * 32 + lane;
@@ -239,16 +274,32 @@ __global__ void __launch_bounds__(kTPB, 2) pip_tile_kernel(const double2* __rest
         double2 p = make_double2(0.0, 0.0);
         if (a) p = sh.pts[li];
         if (a && prefilter) a = p.x >= minx && p.x <= maxx && p.y >= miny && p.y <= maxy; // batch.hpp:39-41
-        if (MODE == kRobust) {
-            ka[k] = a ? fkey(__dadd_rn(p.y, tol)) : INT_MIN;
-            kb[k] = a ? fkey(__dsub_rn(p.y, tol)) : INT_MAX;
+        if constexpr (MODE == kRobust) {
+            K.ka[k] = a ? fkey(__dadd_rn(p.y, tol)) : INT_MIN;
+            K.kb[k] = a ? fkey(__dsub_rn(p.y, tol)) : INT_MAX;
         } else {
-            ka[k] = a ? fkey(p.y) : INT_MAX; // INT_MAX is above every key: never a candidate
-            kb[k] = 0;
+            const uint32_t q = (a ? qkey15(p.y, qm) : 0x7fffu) << 1; // inactive: masked by `act` (slow path)
+            if (k & 1) K.k2[k >> 1] |= q << 16;
+            else K.k2[k >> 1] = q;
         }
         act |= (uint32_t)a << k;
     }
     const bool warp_live = __any_sync(0xffffffffu, act != 0);
+    // key range of the warp's active points (C1 "all sure" shortcut)
+    uint32_t wkey_lo = 0xffffu, wkey_hi = 0u;
+    if constexpr (MODE != kRobust) {
+        uint32_t lo = 0xffffu, hi = 0u;
+#pragma unroll
+        for (int k = 0; k < kK; ++k) {
+            if (act >> k & 1u) {
+                const uint32_t q = (K.k2[k >> 1] >> (16 * (k & 1) + 1)) & 0x7fffu;
+                lo = min(lo, q);
+                hi = max(hi, q);
+            }
+        }
+        wkey_lo = __reduce_min_sync(0xffffffffu, lo);
+        wkey_hi = __reduce_max_sync(0xffffffffu, hi);
+    }
 
     uint32_t par = 0, auxm = 0;
     for (uint32_t q = 0; q < n_tiles; ++q) {
@@ -258,15 +309,24 @@ __global__ void __launch_bounds__(kTPB, 2) pip_tile_kernel(const double2* __rest
         mbar_wait(&sh.full[s], (q >> 1) & 1);
         const TileStage& T = sh.st[s];
         if (warp_live) {
-#pragma unroll 2
-            for (uint32_t e = 0; e < nt; ++e) {
-                const uint2 f = T.filt[e];
-                if (!warp_any_candidate<MODE>(ka, kb, f)) continue;
-                // ---- slow path: exact binary64 test for the candidate points ----
-                if (MODE == kC1)
-                    slow_c1(sh.pts + wloc + lane, ka, f, T.rec[e], par);
-                else
-                    slow_generic<MODE>(sh.pts + wloc + lane, ka, kb, f, T.rec[e], tol, tol2, par, auxm);
+            for (uint32_t e0 = 0; e0 < nt; e0 += 4) {
+                // filter 4 edges back to back (independent chains), then one
+                // warp-wide OR says which of them need the slow path
+                uint32_t bits = 0;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) bits |= (uint32_t)lane_candidate<MODE>(K, T.filt[e0 + u]) << u;
+                uint32_t todo = __reduce_or_sync(0xffffffffu, bits);
+                if (nt - e0 < 4) todo &= (1u << (nt - e0)) - 1u; // stale tail entries
+                while (todo) {
+                    const uint32_t e = e0 + (__ffs(todo) - 1);
+                    todo &= todo - 1;
+                    const uint2 f = T.filt[e];
+                    // ---- slow path: exact binary64 test for the candidate points ----
+                    if constexpr (MODE == kC1)
+                        slow_c1(sh.pts + wloc + lane, K, act, f, T.rec[e], par, wkey_lo, wkey_hi);
+                    else
+                        slow_generic<MODE>(sh.pts + wloc + lane, K, act, f, T.rec[e], tol, tol2, par, auxm);
+                }
             }
         }
         __syncthreads(); // stage s fully consumed

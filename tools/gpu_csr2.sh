@@ -1,0 +1,9 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -q -x --timeout 600 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+for w in c3 c5; do timeout 600 python bench.py --workload $w --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_$w.json 2> gpurun_out/bench_$w.err; done
+timeout 300 python tools/prof_kernel.py --workload c3 --polys 200000 --reps 2 > gpurun_out/plain_c3.log 2>&1 && \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:pip_csr -s 1 -c 1 -o gpurun_out/prof_c3e python tools/prof_kernel.py --workload c3 --polys 200000 --reps 2 > gpurun_out/ncu_c3.log 2>&1
+timeout 300 python bench.py --workload c1 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/plain_c1.log 2>&1 && \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c1.csv python bench.py --workload c1 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
+echo done
