@@ -65,7 +65,7 @@ cudaError_t launch_count(const double* pts, uint64_t n, const double* vx, const 
 // y-bucketing of the points of one polygon (pip_sort.cu): counting sort by
 // y over the outer ring's bbox into kBuckets bins; bbox-rejected points
 // (prefilter) go to a trailing bin that is not classified.
-constexpr int kBuckets = 4096;
+constexpr int kBuckets = 65536;
 struct BucketArgs {
     const double* pts;                    // n interleaved points
     uint64_t n;

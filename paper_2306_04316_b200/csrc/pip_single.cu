@@ -40,7 +40,7 @@ namespace {
 
 constexpr int kTPB = 256;
 constexpr int kK = 16;      // points per thread
-constexpr int kTile = 128;  // edges per shared-memory stage (multiple of 2: 16-byte bulk copies)
+constexpr int kTile = 256;  // edges per shared-memory stage (multiple of 2: 16-byte bulk copies)
 
 struct __align__(128) TileStage {
     EdgeRec rec[kTile];

@@ -5,7 +5,7 @@
 // binary64 test of an edge is ~1-(1-s)^32 (s = the edge's y-span fraction):
 // for the star polygons of configs 1/2, s ~ 0.05, so ~60% of edges take the
 // slow path for some lane and the whole warp pays for it.  Counting-sorting
-// the points by y over the polygon's bbox (kBuckets bins) makes each warp's
+// the points by y over the polygon's bbox (65536 bins) makes each warp's
 // points y-adjacent, so they straddle the same edges and the slow path runs
 // for ~s of the edges instead.  Points the bbox prefilter rejects
 // (classify_batch, batch.hpp:200) land in a trailing bin and are never
@@ -49,64 +49,65 @@ __device__ __forceinline__ BinMap make_map(const unsigned long long* bbox_keys, 
     return m;
 }
 
+// Histogram straight into global memory: with 65536 bins the same-address
+// atomics are few (n / 65536 per bin) and spread over all L2 slices.
 __global__ void __launch_bounds__(512) bucket_count_kernel(const double2* __restrict__ pts, uint64_t n,
                                                            const unsigned long long* __restrict__ bbox_keys,
                                                            int prefilter, uint32_t* __restrict__ hist) {
-    __shared__ uint32_t h[kBuckets + 1];
-    for (int j = threadIdx.x; j <= kBuckets; j += blockDim.x) h[j] = 0;
-    __syncthreads();
     const BinMap m = make_map(bbox_keys, prefilter);
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         const double2 p = pts[i];
-        atomicAdd(&h[m.bin(p.x, p.y)], 1u);
+        atomicAdd(&hist[m.bin(p.x, p.y)], 1u);
     }
-    __syncthreads();
-    for (int j = threadIdx.x; j <= kBuckets; j += blockDim.x)
-        if (h[j]) atomicAdd(&hist[j], h[j]);
 }
 
-// Exclusive scan of the kBuckets+1 counts (one CTA); hist becomes the write
-// cursor of each bin, hist[kBuckets+1] = number of in-box points.
+// Exclusive scan of the kBuckets+1 counts (one CTA of 1024 threads): every
+// thread loads its 64 counts of a coalesced tile layout up front (one memory
+// latency), then the CTA scans tile after tile with a carried running sum;
+// hist becomes the write cursor of each bin, hist[kBuckets+1] = in-box count.
 __global__ void __launch_bounds__(1024) bucket_scan_kernel(uint32_t* __restrict__ hist) {
-    constexpr int kPer = (kBuckets + 1 + 1023) / 1024;
+    constexpr int kTiles = (kBuckets + 1 + 1023) / 1024;
     __shared__ uint32_t warp_sums[32];
+    __shared__ uint32_t carry_s;
     const int t = threadIdx.x;
-    uint32_t v[kPer];
-    uint32_t local = 0;
+    uint32_t v[kTiles];
 #pragma unroll
-    for (int q = 0; q < kPer; ++q) {
-        const int j = t * kPer + q;
+    for (int q = 0; q < kTiles; ++q) {
+        const int j = q * 1024 + t;
         v[q] = j <= kBuckets ? hist[j] : 0u;
-        local += v[q];
     }
-    // block-wide exclusive scan of `local`
-    uint32_t incl = local;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if ((t & 31) >= o) incl += y;
-    }
-    if ((t & 31) == 31) warp_sums[t >> 5] = incl;
+    if (t == 0) carry_s = 0;
     __syncthreads();
-    if (t < 32) {
-        uint32_t w = warp_sums[t];
+#pragma unroll
+    for (int q = 0; q < kTiles; ++q) {
+        uint32_t incl = v[q];
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-            if (t >= o) w += y;
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if ((t & 31) >= o) incl += y;
         }
-        warp_sums[t] = w; // inclusive over warps
-    }
-    __syncthreads();
-    uint32_t run = incl - local + ((t >> 5) ? warp_sums[(t >> 5) - 1] : 0u);
+        if ((t & 31) == 31) warp_sums[t >> 5] = incl;
+        __syncthreads();
+        if (t < 32) {
+            uint32_t w = warp_sums[t];
 #pragma unroll
-    for (int q = 0; q < kPer; ++q) {
-        const int j = t * kPer + q;
-        if (j <= kBuckets) {
-            hist[j] = run;
-            if (j == kBuckets) hist[kBuckets + 1] = run; // in-box count = start of the reject bin
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+                if (t >= o) w += y;
+            }
+            warp_sums[t] = w;
         }
-        run += v[q];
+        __syncthreads();
+        const uint32_t carry = carry_s;
+        const uint32_t excl = carry + incl - v[q] + ((t >> 5) ? warp_sums[(t >> 5) - 1] : 0u);
+        const int j = q * 1024 + t;
+        if (j <= kBuckets) {
+            hist[j] = excl;
+            if (j == kBuckets) hist[kBuckets + 1] = excl; // in-box count = start of the reject bin
+        }
+        __syncthreads();
+        if (t == 1023) carry_s = carry + warp_sums[31];
+        __syncthreads();
     }
 }
 
