@@ -73,7 +73,7 @@ __device__ __forceinline__ unsigned long long warp_max_key(unsigned long long k)
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kCsrThreads, 2) pip_csr_warp_kernel(
+__global__ void __launch_bounds__(kCsrThreads, 4) pip_csr_warp_kernel(
     const double2* __restrict__ pts, const unsigned long long* __restrict__ pt_off, unsigned long long n_polys,
     const double* __restrict__ vx, const double* __restrict__ vy, const unsigned long long* __restrict__ ring_off,
     const unsigned long long* __restrict__ poly_ring_off, unsigned long long pt_base, unsigned long long ring_base,
