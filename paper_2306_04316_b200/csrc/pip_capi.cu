@@ -43,7 +43,7 @@ struct DevState {
     int dev = 0;
     cudaStream_t stream = nullptr;
     DevBuf pts, vx, vy, ring_off, pt_off, poly_ring_off, filt, rec, bbox, bits, verdicts, stats, counts, degen;
-    DevBuf bucket_scratch, sorted_pts, sorted_idx; // y-bucketing (pip_sort.cu)
+    DevBuf bucket_scratch, sorted_pts, sorted_idx, bucket_blk; // y-bucketing (pip_sort.cu)
     unsigned long long* h_stats = nullptr; // pinned 4 x u64
     // profiling: one event pair per main-kernel launch since the last take
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
@@ -172,8 +172,10 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
         check(c, d.sorted_idx.ensure(n * 4), "alloc bucket index");
         hist = d.bucket_scratch.as<uint32_t>();
         check(c, cudaMemsetAsync(hist, 0, (hist_words + 2 * nwords) * 4, st), "clear bucket scratch");
+        const int n_blk = pcd::bucket_blocks(n, d.dev);
+        check(c, d.bucket_blk.ensure((size_t)n_blk * (pcd::kBuckets + 1) * 4), "alloc bucket counts");
         pcd::BucketArgs ba{d_pts, n, d.bbox.as<unsigned long long>(), prefilter, hist, d.sorted_pts.as<double>(),
-                           d.sorted_idx.as<uint32_t>()};
+                           d.sorted_idx.as<uint32_t>(), d.bucket_blk.as<uint32_t>(), n_blk};
         check(c, pcd::launch_bucket(ba, st, d.dev, &c->launches), "bucket kernels");
         sa.pts = d.sorted_pts.as<double>();
         sa.prefilter = 0; // rejected points were left out of the bucketed prefix
@@ -299,7 +301,7 @@ void pc_destroy(pc_ctx* c) {
         cudaStreamSynchronize(d.stream);
         for (DevBuf* b : {&d.pts, &d.vx, &d.vy, &d.ring_off, &d.pt_off, &d.poly_ring_off, &d.filt, &d.rec, &d.bbox,
                           &d.bits, &d.verdicts, &d.stats, &d.counts, &d.degen, &d.bucket_scratch, &d.sorted_pts,
-                          &d.sorted_idx})
+                          &d.sorted_idx, &d.bucket_blk})
             b->release();
         if (d.h_stats) cudaFreeHost(d.h_stats);
         for (auto& e : d.evs) {

@@ -65,16 +65,19 @@ cudaError_t launch_count(const double* pts, uint64_t n, const double* vx, const 
 // y-bucketing of the points of one polygon (pip_sort.cu): counting sort by
 // y over the outer ring's bbox into kBuckets bins; bbox-rejected points
 // (prefilter) go to a trailing bin that is not classified.
-constexpr int kBuckets = 65536;
+constexpr int kBuckets = 4096;
 struct BucketArgs {
     const double* pts;                    // n interleaved points
     uint64_t n;
     const unsigned long long* bbox_keys;  // from prep
     int prefilter;
-    uint32_t* hist;                       // kBuckets + 2 words, zeroed; [kBuckets+1] receives n_in
+    uint32_t* hist;                       // kBuckets + 2 words; [kBuckets+1] receives n_in
     double* sorted_pts;                   // n points (bucketed order)
     uint32_t* sorted_idx;                 // original index of each bucketed point
+    uint32_t* blk;                        // n_blk x (kBuckets + 1) per-CTA counts
+    int n_blk;                            // bucket_blocks(n, dev)
 };
+int bucket_blocks(uint64_t n, int dev);
 cudaError_t launch_bucket(const BucketArgs& a, cudaStream_t st, int dev, uint64_t* launches);
 // ORs the set bits of the bucketed planes back to the original point order.
 cudaError_t launch_unbucket(uint64_t n, const uint32_t* n_dev, const uint32_t* sorted_idx, const uint32_t* s_inside,

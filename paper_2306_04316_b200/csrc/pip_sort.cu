@@ -5,7 +5,7 @@
 // binary64 test of an edge is ~1-(1-s)^32 (s = the edge's y-span fraction):
 // for the star polygons of configs 1/2, s ~ 0.05, so ~60% of edges take the
 // slow path for some lane and the whole warp pays for it.  Counting-sorting
-// the points by y over the polygon's bbox (65536 bins) makes each warp's
+// the points by y over the polygon's bbox (4096 bins) makes each warp's
 // points y-adjacent, so they straddle the same edges and the slow path runs
 // for ~s of the edges instead.  Points the bbox prefilter rejects
 // (classify_batch, batch.hpp:200) land in a trailing bin and are never
@@ -49,16 +49,44 @@ __device__ __forceinline__ BinMap make_map(const unsigned long long* bbox_keys, 
     return m;
 }
 
-// Histogram straight into global memory: with 65536 bins the same-address
-// atomics are few (n / 65536 per bin) and spread over all L2 slices.
-__global__ void __launch_bounds__(512) bucket_count_kernel(const double2* __restrict__ pts, uint64_t n,
-                                                           const unsigned long long* __restrict__ bbox_keys,
-                                                           int prefilter, uint32_t* __restrict__ hist) {
+// Atomic-free (in global memory) counting sort over P CTAs:
+//   count    CTA b histograms its contiguous chunk of points in shared memory
+//            and writes the counts to blk[b][bin];
+//   colscan  per bin, an exclusive prefix over the CTAs (blk[b][bin] becomes
+//            CTA b's offset inside the bin) and the bin total;
+//   scan     exclusive scan of the bin totals -> bin base (and n_in);
+//   scatter  CTA b re-reads its chunk and places each point at base[bin] +
+//            blk[b][bin] + (shared-memory cursor), no global atomics.
+__global__ void __launch_bounds__(1024) bucket_count_kernel(const double2* __restrict__ pts, uint64_t n,
+                                                            uint64_t chunk,
+                                                            const unsigned long long* __restrict__ bbox_keys,
+                                                            int prefilter, uint32_t* __restrict__ blk) {
+    __shared__ uint32_t h[kBuckets + 1];
+    for (int j = threadIdx.x; j <= kBuckets; j += blockDim.x) h[j] = 0;
+    __syncthreads();
     const BinMap m = make_map(bbox_keys, prefilter);
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
+    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
         const double2 p = pts[i];
-        atomicAdd(&hist[m.bin(p.x, p.y)], 1u);
+        atomicAdd(&h[m.bin(p.x, p.y)], 1u);
     }
+    __syncthreads();
+    uint32_t* row = blk + (uint64_t)blockIdx.x * (kBuckets + 1);
+    for (int j = threadIdx.x; j <= kBuckets; j += blockDim.x) row[j] = h[j];
+}
+
+__global__ void __launch_bounds__(128) bucket_colscan_kernel(uint32_t* __restrict__ blk, int n_blk,
+                                                             uint32_t* __restrict__ hist) {
+    const int bin = blockIdx.x * blockDim.x + threadIdx.x;
+    if (bin > kBuckets) return;
+    uint32_t run = 0;
+    for (int b = 0; b < n_blk; ++b) {
+        uint32_t* p = blk + (uint64_t)b * (kBuckets + 1) + bin;
+        const uint32_t v = *p;
+        *p = run;
+        run += v;
+    }
+    hist[bin] = run;
 }
 
 // Exclusive scan of the kBuckets+1 counts (one CTA of 1024 threads): every
@@ -111,17 +139,24 @@ __global__ void __launch_bounds__(1024) bucket_scan_kernel(uint32_t* __restrict_
     }
 }
 
-__global__ void __launch_bounds__(512) bucket_scatter_kernel(const double2* __restrict__ pts, uint64_t n,
-                                                             const unsigned long long* __restrict__ bbox_keys,
-                                                             int prefilter, uint32_t* __restrict__ cursor,
-                                                             double2* __restrict__ sorted_pts,
-                                                             uint32_t* __restrict__ sorted_idx) {
+__global__ void __launch_bounds__(1024) bucket_scatter_kernel(const double2* __restrict__ pts, uint64_t n,
+                                                              uint64_t chunk,
+                                                              const unsigned long long* __restrict__ bbox_keys,
+                                                              int prefilter, const uint32_t* __restrict__ blk,
+                                                              const uint32_t* __restrict__ base,
+                                                              double2* __restrict__ sorted_pts,
+                                                              uint32_t* __restrict__ sorted_idx) {
+    __shared__ uint32_t cur[kBuckets + 1];
+    const uint32_t* row = blk + (uint64_t)blockIdx.x * (kBuckets + 1);
+    for (int j = threadIdx.x; j <= kBuckets; j += blockDim.x) cur[j] = base[j] + row[j];
+    __syncthreads();
     const BinMap m = make_map(bbox_keys, prefilter);
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
+    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
         const double2 p = pts[i];
         const int b = m.bin(p.x, p.y);
         if (b == kBuckets) continue; // rejected by the bbox prefilter: Outside, never classified
-        const uint32_t pos = atomicAdd(&cursor[b], 1u);
+        const uint32_t pos = atomicAdd(&cur[b], 1u);
         sorted_pts[pos] = p;
         sorted_idx[pos] = (uint32_t)i;
     }
@@ -157,13 +192,19 @@ int sms(int dev) {
 
 cudaError_t launch_bucket(const BucketArgs& a, cudaStream_t st, int dev, uint64_t* launches) {
     const double2* p = reinterpret_cast<const double2*>(a.pts);
-    const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((a.n + 511) / 512, (uint64_t)sms(dev) * 4));
-    bucket_count_kernel<<<blocks, 512, 0, st>>>(p, a.n, a.bbox_keys, a.prefilter, a.hist);
+    const int n_blk = a.n_blk;
+    const uint64_t chunk = (a.n + n_blk - 1) / n_blk;
+    bucket_count_kernel<<<n_blk, 1024, 0, st>>>(p, a.n, chunk, a.bbox_keys, a.prefilter, a.blk);
+    bucket_colscan_kernel<<<(kBuckets + 1 + 127) / 128, 128, 0, st>>>(a.blk, n_blk, a.hist);
     bucket_scan_kernel<<<1, 1024, 0, st>>>(a.hist);
-    bucket_scatter_kernel<<<blocks, 512, 0, st>>>(p, a.n, a.bbox_keys, a.prefilter, a.hist,
+    bucket_scatter_kernel<<<n_blk, 1024, 0, st>>>(p, a.n, chunk, a.bbox_keys, a.prefilter, a.blk, a.hist,
                                                   reinterpret_cast<double2*>(a.sorted_pts), a.sorted_idx);
-    *launches += 3;
+    *launches += 4;
     return cudaGetLastError();
+}
+
+int bucket_blocks(uint64_t n, int dev) {
+    return (int)std::max<uint64_t>(1, std::min<uint64_t>((n + 4095) / 4096, (uint64_t)sms(dev)));
 }
 
 cudaError_t launch_unbucket(uint64_t n, const uint32_t* n_dev, const uint32_t* sorted_idx, const uint32_t* s_inside,
