@@ -351,3 +351,23 @@ def test_csr_oversize_and_mixed_polygons(engine):
         want_v, want_s = oracle.port_classify_csr(s, mode, threads=THREADS)
         assert np.array_equal(got.verdicts, want_v), f"mode {mode}: {(got.verdicts != want_v).sum()} differ"
         assert np.array_equal(got.stats, want_s)
+
+
+def test_bucketing_skewed_inputs(engine):
+    """All points on a handful of y values / one bin (counting-sort edge cases), and
+    points far outside the bbox with and without the prefilter."""
+    rng = np.random.default_rng(21)
+    poly = W.star_polygon(500, seed=8)
+    n = 70_001
+    xy = np.empty((n, 2))
+    xy[:, 0] = rng.uniform(-1.2, 1.2, n)
+    xy[:, 1] = rng.choice(np.array([0.0, 0.25, -0.5, poly.vy[3], poly.vy[77]]), n)
+    xy[:1000, 1] = 1e300
+    xy[1000:2000, 1] = -1e300
+    engine.set_bucketing(1)
+    try:
+        for mode in MODES:
+            check_single(xy, poly, mode, engine.classify(xy, poly, mode))
+            check_single(xy, poly, mode, engine.classify(xy, poly, mode, prefilter=False), prefilter=False)
+    finally:
+        engine.set_bucketing(-1)
