@@ -44,6 +44,7 @@ struct DevState {
     cudaStream_t stream = nullptr;
     DevBuf pts, vx, vy, ring_off, pt_off, poly_ring_off, filt, rec, bbox, bits, verdicts, stats, counts, degen;
     DevBuf bucket_scratch, sorted_pts, sorted_idx, bucket_blk; // y-bucketing (pip_sort.cu)
+    DevBuf csr_meta;                                          // per-polygon records (pip_csr.cu)
     unsigned long long* h_stats = nullptr; // pinned 4 x u64
     // profiling: one event pair per main-kernel launch since the last take
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
@@ -219,6 +220,8 @@ void enqueue_csr(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts, u
     a.tol2 = tol * tol;
     a.inside_bits = d_inside;
     a.aux_bits = d_aux;
+    check(c, d.csr_meta.ensure(std::max<size_t>(pcd::csr_meta_bytes(n_polys), 16)), "alloc polygon metadata");
+    a.meta = d.csr_meta.p;
     mark_begin(c, d, st);
     check(c, pcd::launch_csr(a, st, d.dev, &c->launches), "csr kernel");
     mark_end(c, d, st);

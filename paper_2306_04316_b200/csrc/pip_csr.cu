@@ -1,10 +1,10 @@
 // CSR multi-polygon kernel (configs 3 and 5): many small
 // polygons, each with its own contiguous run of query points.
 //
-// One warp per polygon (grid-stride, next polygon's offsets prefetched).  Per
-// polygon the warp:
-//   1. reads the polygon's CSR offsets with a single load (lanes 0-3) and
-//      broadcasts them with shuffles;
+// A metadata prepass (csr_meta_kernel, one thread per polygon) resolves each
+// polygon's point / vertex / ring ranges and the exact bbox of its outer ring.
+// Then one warp per polygon (grid-stride, next polygon's record prefetched):
+//   1. reads the polygon's 80-byte metadata record (uniform loads);
 //   2. walks its points 64 at a time (2 per lane) and, for each chunk of up to
 //      31 edges, loads the chunk's 32 vertices (one per lane), derives the
 //      per-edge data (filter keys, normal / direction) lane-parallel into a
@@ -13,9 +13,9 @@
 //      own candidate edges (ffs loop) running the reference's binary64 test --
 //      the warp iterates max-popcount (~2-4 for footprints) times, not once
 //      per edge, so the FP64 work follows the candidates, not the SIMT width;
-//   3. masks the result with the closed bbox of the outer ring (reduced from
-//      the same vertex loads) — points outside it are Outside with no Error /
-//      Boundary, exactly as classify_batch's short-circuit (batch.hpp:200);
+//   3. masks the result with the closed bbox of the outer ring -- points
+//      outside it are Outside with no Error / Boundary, exactly as
+//      classify_batch's short-circuit (batch.hpp:200);
 //   4. ORs one ballot word per 32 points into the bit planes.
 //
 // Reference semantics per polygon: classify_batch(points_i, poly_i, mode)
@@ -47,10 +47,6 @@ struct __align__(16) EdgeScratch { // one warp's current chunk of <= 31 edges
     double len2[32];                 // Robust only
 };
 
-__device__ __forceinline__ unsigned long long shfl64(unsigned long long v, int src) {
-    return __shfl_sync(kFull, v, src);
-}
-
 __device__ __forceinline__ void or_bits(uint32_t* plane, unsigned long long g0, uint32_t bits) {
     if (!bits) return;
     const unsigned long long w = g0 >> 5;
@@ -59,17 +55,52 @@ __device__ __forceinline__ void or_bits(uint32_t* plane, unsigned long long g0, 
     if (sh && (bits >> (32 - sh))) atomicOr(&plane[w + 1], bits >> (32 - sh));
 }
 
-// Warp-wide exact min / max of a double via its monotone 64-bit key and two
-// 32-bit REDUX steps (high word, then low word among the lanes that tie).
-__device__ __forceinline__ unsigned long long warp_min_key(unsigned long long k) {
-    const unsigned hi = __reduce_min_sync(kFull, (unsigned)(k >> 32));
-    const unsigned lo = __reduce_min_sync(kFull, (unsigned)(k >> 32) == hi ? (unsigned)k : 0xffffffffu);
-    return ((unsigned long long)hi << 32) | lo;
-}
-__device__ __forceinline__ unsigned long long warp_max_key(unsigned long long k) {
-    const unsigned hi = __reduce_max_sync(kFull, (unsigned)(k >> 32));
-    const unsigned lo = __reduce_max_sync(kFull, (unsigned)(k >> 32) == hi ? (unsigned)k : 0u);
-    return ((unsigned long long)hi << 32) | lo;
+// Per-polygon metadata, one thread per polygon (csr_meta_kernel): the exact
+// closed bbox of the outer ring (batch.hpp:121-133, std::min/std::max order)
+// and the resolved point / vertex / ring ranges.  A thread per polygon costs
+// ~1/32 of a warp per polygon, so the classify kernel's warps start straight
+// at the points and edges.
+struct __align__(16) PolyMeta {
+    double bx0, by0, bx1, by1;        // empty outer ring: +inf/-inf (nothing inside)
+    unsigned long long s;             // first point (local index)
+    unsigned long long v0;            // first vertex (local index)
+    unsigned long long r0;            // first ring (local index)
+    uint32_t np, nv, nvo, nr;         // points, vertices (all rings), outer-ring vertices, rings
+};
+
+__global__ void __launch_bounds__(256) csr_meta_kernel(
+    const unsigned long long* __restrict__ pt_off, unsigned long long n_polys, const double* __restrict__ vx,
+    const double* __restrict__ vy, const unsigned long long* __restrict__ ring_off,
+    const unsigned long long* __restrict__ poly_ring_off, unsigned long long pt_base, unsigned long long ring_base,
+    unsigned long long vert_base, PolyMeta* __restrict__ meta) {
+    const unsigned long long p = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+    if (p >= n_polys) return;
+    PolyMeta m;
+    const unsigned long long s = pt_off[p] - pt_base, t = pt_off[p + 1] - pt_base;
+    const unsigned long long r0 = poly_ring_off[p] - ring_base, r1 = poly_ring_off[p + 1] - ring_base;
+    m.s = s;
+    m.r0 = r0;
+    m.np = (uint32_t)(t - s);
+    m.nr = (uint32_t)min(r1 - r0, 0xffffffffull);
+    m.bx0 = m.by0 = INFINITY;
+    m.bx1 = m.by1 = -INFINITY;
+    m.v0 = 0;
+    m.nv = m.nvo = 0;
+    if (r1 > r0) {
+        const unsigned long long v0 = ring_off[r0] - vert_base, vo1 = ring_off[r0 + 1] - vert_base;
+        const unsigned long long vend = ring_off[r1] - vert_base;
+        m.v0 = v0;
+        m.nv = (uint32_t)(vend - v0);
+        m.nvo = (uint32_t)(vo1 - v0);
+        for (unsigned long long v = v0; v < vo1; ++v) {
+            const double x = vx[v], y = vy[v];
+            m.bx0 = x < m.bx0 ? x : m.bx0;
+            m.by0 = y < m.by0 ? y : m.by0;
+            m.bx1 = m.bx1 < x ? x : m.bx1;
+            m.by1 = m.by1 < y ? y : m.by1;
+        }
+    }
+    meta[p] = m;
 }
 
 template <int MODE>
@@ -78,50 +109,45 @@ __global__ void __launch_bounds__(kCsrThreads, 4) pip_csr_warp_kernel(
     const double* __restrict__ vx, const double* __restrict__ vy, const unsigned long long* __restrict__ ring_off,
     const unsigned long long* __restrict__ poly_ring_off, unsigned long long pt_base, unsigned long long ring_base,
     unsigned long long vert_base, double tol, double tol2, uint32_t* __restrict__ inside_bits,
-    uint32_t* __restrict__ aux_bits) {
+    uint32_t* __restrict__ aux_bits, const PolyMeta* __restrict__ meta) {
     __shared__ EdgeScratch scratch[kWarps];
     const int lane = threadIdx.x & 31;
     EdgeScratch& es = scratch[threadIdx.x >> 5];
     const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
     unsigned long long p = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
 
-    // offsets of the first polygon; later ones are prefetched one polygon ahead
-    unsigned long long hv = 0;
-    if (p < n_polys) hv = lane < 2 ? pt_off[p + lane] : (lane < 4 ? poly_ring_off[p + lane - 2] : 0ull);
-    for (; p < n_polys; p += nwarps) {
-        const unsigned long long s = shfl64(hv, 0) - pt_base, t = shfl64(hv, 1) - pt_base;
-        const unsigned long long r0 = shfl64(hv, 2) - ring_base, r1 = shfl64(hv, 3) - ring_base;
+    // metadata records: lanes 0-4 copy the next polygon's 80 bytes into this
+    // warp's shared double buffer (cp.async) while the warp works on the current one
+    __shared__ PolyMeta meta_s[kWarps][2];
+    PolyMeta* mbuf = meta_s[threadIdx.x >> 5];
+    auto fetch = [&](unsigned long long q, int slot) {
+        if (lane < 5) {
+            const unsigned dst = (unsigned)__cvta_generic_to_shared(reinterpret_cast<char*>(mbuf + slot) + 16 * lane);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                         "l"(reinterpret_cast<const char*>(meta + q) + 16 * lane)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    int slot = 0;
+    if (p < n_polys) fetch(p, 0);
+    for (; p < n_polys; p += nwarps, slot ^= 1) {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp();
+        const PolyMeta& m = mbuf[slot];
         const unsigned long long pn = p + nwarps;
-        if (pn < n_polys) hv = lane < 2 ? pt_off[pn + lane] : (lane < 4 ? poly_ring_off[pn + lane - 2] : 0ull);
-        if (t <= s || r1 <= r0) continue; // no points, or no rings (nothing is inside)
-        const int nr = (int)min(r1 - r0, 1ull << 20);
-        // lane i holds ring_off[r0 + i] (i <= nr, i < 32); further rings are read from global
-        const unsigned long long ro = lane <= nr ? ring_off[r0 + lane] - vert_base : 0ull;
-        const unsigned long long v0 = shfl64(ro, 0);
-        const unsigned long long vend = nr < 32 ? shfl64(ro, nr) : ring_off[r1] - vert_base;
-        // local (32-bit) indexing from here on
+        if (pn < n_polys) fetch(pn, slot ^ 1); // the slot last read one polygon ago
+        if (m.np == 0 || m.nr == 0) continue;  // no points, or no rings (nothing is inside)
+        const int nr = (int)min(m.nr, 1u << 20);
+        const unsigned long long v0 = m.v0, r0 = m.r0;
+        // ring starts (only for polygons with holes): lane i holds ring_off[r0 + i]
+        const uint32_t rs_lane = (nr > 1 && lane < nr) ? (uint32_t)(ring_off[r0 + lane] - vert_base - v0) : 0u;
         const double* X = vx + v0;
         const double* Y = vy + v0;
-        const double2* P = pts + s;
-        const uint32_t np = (uint32_t)(t - s), nv = (uint32_t)(vend - v0);
-        const uint32_t nvo = (uint32_t)(shfl64(ro, 1) - v0); // outer ring vertices
-        const uint32_t rs_lane = (uint32_t)(ro - v0);          // ring start of lane's ring (lane < nr)
-
-        // closed bbox of the outer ring, exactly, via monotone keys + REDUX
-        unsigned long long kx0 = ~0ull, ky0 = ~0ull, kx1 = 0ull, ky1 = 0ull;
-        for (uint32_t cv = 0; cv < nvo; cv += 32) {
-            const uint32_t v = cv + lane;
-            unsigned long long kx = ~0ull, ky = ~0ull, qx = 0ull, qy = 0ull;
-            if (v < nvo) {
-                kx = qx = dkey(X[v]);
-                ky = qy = dkey(Y[v]);
-            }
-            kx0 = min(kx0, warp_min_key(kx));
-            ky0 = min(ky0, warp_min_key(ky));
-            kx1 = max(kx1, warp_max_key(qx));
-            ky1 = max(ky1, warp_max_key(qy));
-        }
-        const double bx0 = dkey_inv(kx0), by0 = dkey_inv(ky0), bx1 = dkey_inv(kx1), by1 = dkey_inv(ky1);
+        const double2* P = pts + m.s;
+        const unsigned long long s = m.s;
+        const uint32_t np = m.np, nv = m.nv;
+        const double bx0 = m.bx0, by0 = m.by0, bx1 = m.bx1, by1 = m.by1;
 
         for (uint32_t c = 0; c < np; c += 64) {
             double px[2], py[2];
@@ -267,6 +293,12 @@ int sms(int dev) {
 
 template <int MODE>
 cudaError_t launch_t(const CsrArgs& a, cudaStream_t st, int dev, uint64_t* launches) {
+    PolyMeta* meta = reinterpret_cast<PolyMeta*>(a.meta);
+    csr_meta_kernel<<<(unsigned)((a.n_polys + 255) / 256), 256, 0, st>>>(
+        reinterpret_cast<const unsigned long long*>(a.pt_off), a.n_polys, a.vx, a.vy,
+        reinterpret_cast<const unsigned long long*>(a.ring_off), reinterpret_cast<const unsigned long long*>(a.poly_ring_off),
+        a.pt_base, a.ring_base, a.vert_base, meta);
+    ++*launches;
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pip_csr_warp_kernel<MODE>, kCsrThreads, 0);
     per_sm = std::max(per_sm, 1);
@@ -276,12 +308,14 @@ cudaError_t launch_t(const CsrArgs& a, cudaStream_t st, int dev, uint64_t* launc
         reinterpret_cast<const double2*>(a.pts), reinterpret_cast<const unsigned long long*>(a.pt_off), a.n_polys,
         a.vx, a.vy, reinterpret_cast<const unsigned long long*>(a.ring_off),
         reinterpret_cast<const unsigned long long*>(a.poly_ring_off), a.pt_base, a.ring_base, a.vert_base, a.tol,
-        a.tol2, a.inside_bits, a.aux_bits);
+        a.tol2, a.inside_bits, a.aux_bits, meta);
     ++*launches;
     return cudaGetLastError();
 }
 
 } // namespace
+
+size_t csr_meta_bytes(uint64_t n_polys) { return (size_t)n_polys * sizeof(PolyMeta); }
 
 cudaError_t launch_csr(const CsrArgs& a, cudaStream_t st, int dev, uint64_t* launches) {
     if (a.n_polys == 0) return cudaSuccess;

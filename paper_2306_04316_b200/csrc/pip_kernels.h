@@ -51,9 +51,11 @@ struct CsrArgs {
     double tol, tol2;
     uint32_t* inside_bits;
     uint32_t* aux_bits;
+    void* meta; // csr_meta_bytes(n_polys) of device scratch (per-polygon records)
 };
 
 size_t edge_rec_bytes();
+size_t csr_meta_bytes(uint64_t n_polys);
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st, int dev, uint64_t* launches);
 cudaError_t launch_single(const SingleArgs& a, cudaStream_t st, int dev, uint64_t* launches);
 cudaError_t launch_csr(const CsrArgs& a, cudaStream_t st, int dev, uint64_t* launches);

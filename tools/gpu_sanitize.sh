@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 300 python tools/sanitize_cases.py > gpurun_out/sanitize_plain.log 2>&1 && \
+timeout 1500 compute-sanitizer --tool memcheck --leak-check no --print-limit 50 python tools/sanitize_cases.py > gpurun_out/sanitize_memcheck.log 2>&1
+echo "rc=$?" >> gpurun_out/sanitize_memcheck.log
+echo done
