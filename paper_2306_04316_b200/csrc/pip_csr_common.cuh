@@ -1,0 +1,61 @@
+// Helpers shared by the CSR kernels (pip_csr.cu warp kernel, pip_csr_tile.cu
+// tile kernel): the C1 certified fast path and bit-plane output.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace pcd {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// ---- C1 certified fast path -------------------------------------------------
+// For a polygon whose bbox W x H is well scaled (2^-300 <= W, H <= 2^300), map
+// coordinates to polygon-local units: L = (v - o) * s with o the bbox min and s
+// a power of two with W*s, H*s in [1/2, 1).  Then, per (point, edge):
+//   * y: q(y) = trunc((y - o_y) * s_y * 2^30) is monotone, so
+//       q_lo < q(p.y) < q_hi        =>  y_lo < p.y < y_hi  => the reference's
+//                                       f_prev * f_next <= 0 holds (P2);
+//       q(p.y) outside [q_lo, q_hi] =>  p.y outside [y_lo, y_hi] strictly, and
+//       with |p.y| >= 2^-400 both differences are >= 2^-453 so the product is
+//       > 0 (no underflow): the edge is not a straddle;
+//     q(p.y) equal to some vertex key is a tie -> the exact path.
+//   * side: s = fma(lx, Nx, fma(ly, Ny, c)) in fp32 approximates
+//       S' = (p - a) . n * s_x * s_y  (n = the reference's rounded, flipped
+//       normal) with |s - S'| <= 13.1 * 2^-24 (all local terms are <= 1 in
+//       magnitude, |c| <= 2), while the reference's binary64
+//       value differs from S' by <= 4.1 * 2^-53 (+ underflow terms < 2^-470).
+//       So |s| > kFastBand = 2^-20 decides the sign of the reference's side;
+//       |s| <= kFastBand is sent to the exact path.
+// A point with any tie / band hit in a chunk of edges takes the exact binary64
+// path (binary64, the reference's expression order) for that chunk; every other (point, edge)
+// contribution is the reference's, so parities stay bit-exact.
+constexpr float kFastBand = 0x1p-20f;
+constexpr int kFastSentinelLo = 0x40000000; // qlo+1 of a non-edge: never "sure"
+
+// fpar ^= bit when d1 < rng1 (unsigned: q_lo < q(p.y) < q_hi) and s < -kFastBand,
+// as two predicate-combining compares and one predicated xor
+__device__ __forceinline__ void fast_toggle(uint32_t& fpar, uint32_t bit, unsigned d1, unsigned rng1, float s) {
+    asm("{\n\t.reg .pred p, q;\n\t"
+        "setp.lt.f32 p, %2, %5;\n\t"
+        "setp.lt.and.u32 q, %3, %4, p;\n\t"
+        "@q xor.b32 %0, %0, %1;\n\t}"
+        : "+r"(fpar)
+        : "r"(bit), "f"(s), "r"(d1), "r"(rng1), "f"(-kFastBand));
+}
+
+__device__ __forceinline__ double pow2_below_inv(double w) { // 2^-(E+1) for w in [2^E, 2^(E+1))
+    const int e = (__double2hiint(w) >> 20) & 0x7ff;
+    return __hiloint2double((2045 - e) << 20, 0);
+}
+
+__device__ __forceinline__ void or_bits(uint32_t* plane, unsigned long long g0, uint32_t bits) {
+    if (!bits) return;
+    const unsigned long long w = g0 >> 5;
+    const unsigned sh = (unsigned)(g0 & 31);
+    atomicOr(&plane[w], bits << sh);
+    if (sh && (bits >> (32 - sh))) atomicOr(&plane[w + 1], bits >> (32 - sh));
+}
+
+} // namespace pcd

@@ -1,0 +1,413 @@
+// CSR batch kernel for C1 (the paper's side-of-normal test, configs 3 and 5):
+// many small polygons, each with its own contiguous run of query points.
+//
+// Every warp works on its own: it takes a group of 32 consecutive polygons
+// (lane = polygon), resolves their point / vertex / ring ranges, and then
+// processes them in batches whose vertices fit its shared-memory slice
+// (kWV vertices).  Per batch the warp
+//   1. loads the batch's vertices into shared memory (lanes stride over the
+//      batch's vertices, so a 10-vertex footprint does not leave 22 lanes
+//      idle), and marks ring ends;
+//   2. lane per polygon: the exact closed bbox of the outer ring with the
+//      reference's std::min / std::max order (batch.hpp:121-133) and the
+//      polygon-local scaling of the C1 fast path (pip_csr_common.cuh);
+//   3. lanes stride over the vertices again: one fast-path record per edge;
+//   4. classifies each polygon of the batch, 64 points per step (2 per lane):
+//      ~9 instructions per (point, edge) pair; the rare undecided points (a
+//      tie, or |s| within the band) re-run the polygon in binary64 in the
+//      reference's expression order (geometry.hpp:182-203).
+// No block-wide barriers: a warp waiting on its loads never holds up others.
+// Polygons with more than kWV vertices are appended to a list and handled
+// afterwards by the warp-per-polygon kernel (pip_csr.cu), which streams
+// edges in chunks.
+//
+// Reference semantics per polygon: classify_batch(points_i, poly_i, C1)
+// (batch.hpp:184-230) -> bbox short-circuit (batch.hpp:200) -> contains
+// (geometry.hpp:281-300) -> count_crossings_c1 over every ring.
+#include "pip_kernels.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "pip_csr_common.cuh"
+#include "pip_device.cuh"
+
+namespace pcd {
+
+namespace {
+
+constexpr int kBThreads = 128;
+constexpr int kBWarps = kBThreads / 32;
+constexpr int kWV = 96; // vertex budget of one batch (per warp)
+
+struct BPoly {
+    double bx0, by0, bx1, by1; // exact closed bbox of the outer ring
+    double sx, sy;             // fast-path scaling (powers of two)
+    unsigned long long s;      // first point (shard-local index)
+    uint32_t np;               // points
+    uint32_t e0, e1;           // vertex range in the batch
+    int fast;                  // fast path usable
+};
+
+struct WarpSmem {
+    double2 vert[kWV];
+    int4 rec[kWV];    // (qlo+1, max(qhi-qlo-1,0), q(a), Nx) -- see pip_csr_common.cuh
+    float2 rec2[kWV]; // (Ny, c)
+    BPoly bp[32];
+    unsigned long long v0s[32]; // first vertex (shard-local) of batch polygon k
+    uint32_t off[32];           // batch offset of batch polygon k's first vertex
+    uint32_t ring_end[kWV / 32]; // bit i: batch vertex i is the last vertex of its ring
+    unsigned char owner[kWV];
+    // the current group of 32 polygons (lane = polygon), kept here rather than
+    // in registers across the batches
+    unsigned long long gs[32], gr0[32], gv0[32];
+    uint32_t gnp[32], gnr[32], gnv[32], gnvo[32];
+};
+
+__device__ __forceinline__ bool is_ring_end(const WarpSmem& ws, uint32_t i) {
+    return (ws.ring_end[i >> 5] >> (i & 31)) & 1u;
+}
+
+// One step of a batch polygon: points cc .. cc+63 (2 per lane, already loaded
+// into qc) against all of its edges.
+// walk_all (warp-uniform): skip the fp32 pass and walk every candidate edge in
+// binary64 -- cheaper when most points tie vertex keys anyway (returns the
+// number of undecided points so the caller can pick the mode adaptively).
+__device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t cc, const double2 (&qc)[2],
+                                             int lane, const double2* __restrict__ pts,
+                                             uint32_t* __restrict__ inside_bits, bool walk_all) {
+    const BPoly& tp = ws.bp[j];
+    const uint32_t np = tp.np, e0 = tp.e0, e1 = tp.e1;
+    const double bx0 = tp.bx0, by0 = tp.by0, bx1 = tp.bx1, by1 = tp.by1;
+    const double sx = tp.sx, sy = tp.sy;
+    const bool fast = tp.fast != 0;
+    float lx[2], ly[2];
+    int qy[2];
+    uint32_t act = 0, qok = 0;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const double2 q = qc[k];
+        // classify_batch short-circuit (batch.hpp:200): outside the closed bbox -> Outside
+        const bool a = cc + 32 * k + lane < np && q.x >= bx0 && q.x <= bx1 && q.y >= by0 && q.y <= by1;
+        act |= (uint32_t)a << k;
+        const double yl = __dmul_rn(__dsub_rn(q.y, by0), sy);
+        lx[k] = __double2float_rn(__dmul_rn(__dsub_rn(q.x, bx0), sx));
+        ly[k] = __double2float_rn(yl);
+        qy[k] = __double2int_rz(__dmul_rn(yl, 0x1p30)); // = trunc((y - o_y) * s_y * 2^30): exact scaling
+        // the key filters are exact only for |p.y| >= 2^-400 (pip_csr_common.cuh)
+        qok |= (uint32_t)(a && fast && fabs(q.y) >= 0x1p-400) << k;
+    }
+    if (!__any_sync(kFull, act != 0)) return 0;
+    uint32_t par = 0, slow = act & ~qok, band = 0;
+    if (fast && walk_all) {
+        slow = act;
+        band = act; // every candidate edge of every point
+    } else if (fast) {
+        uint32_t fpar = 0, t0 = 0xffffffffu, t1 = 0xffffffffu;
+        float m0 = 1.f, m1 = 1.f;
+        auto rec = [&](uint32_t i) {
+            const int4 f = ws.rec[i];
+            const float2 g = ws.rec2[i];
+            const float nxf = __int_as_float(f.w);
+            const float s0 = fmaf(lx[0], nxf, fmaf(ly[0], g.x, g.y));
+            const float s1 = fmaf(lx[1], nxf, fmaf(ly[1], g.x, g.y));
+            fast_toggle(fpar, 1u, (unsigned)(qy[0] - f.x), (unsigned)f.y, s0);
+            fast_toggle(fpar, 2u, (unsigned)(qy[1] - f.x), (unsigned)f.y, s1);
+            m0 = fminf(m0, fabsf(s0)); // band hits
+            m1 = fminf(m1, fabsf(s1));
+            t0 = min(t0, (unsigned)(qy[0] - f.z)); // ties: 0 iff q(p.y) == q(vertex)
+            t1 = min(t1, (unsigned)(qy[1] - f.z));
+        };
+        uint32_t i = e0;
+        for (; i + 4 <= e1; i += 4) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) rec(i + k);
+        }
+        for (; i < e1; ++i) rec(i);
+        band = ((uint32_t)(m0 <= kFastBand) | ((uint32_t)(m1 <= kFastBand) << 1)) & act;
+        const uint32_t tie = ((uint32_t)(t0 == 0u) | ((uint32_t)(t1 == 0u) << 1)) & act;
+        slow |= band | tie;
+        // decided contributions (ties never toggle fpar); points with a band hit
+        // redo every candidate edge
+        par = fpar & qok & ~band;
+    }
+    if (__any_sync(kFull, slow != 0)) {
+        // exact binary64 path, count_crossings_c1 (geometry.hpp:182-203), on the
+        // undecided (point, edge) pairs: a point with only key ties redoes the
+        // edges whose key range it ties (q == q_lo or q == q_hi); a point with a
+        // band hit redoes every candidate edge (q_lo <= q <= q_hi); a point whose
+        // key filter is not exact redoes every edge
+        const double2* P = pts + tp.s;
+        double px[2], py[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const double2 q = (slow >> k & 1u) ? P[cc + 32 * k + lane] : make_double2(0.0, 0.0);
+            px[k] = q.x;
+            py[k] = q.y;
+        }
+        // one selection rule per warp: if any point has a band hit, every
+        // undecided point redoes all its candidate edges (and drops fpar)
+        const bool cand_mode = __any_sync(kFull, band != 0);
+        if (cand_mode) par &= ~slow;
+        const int qy1[2] = {qy[0] + 1, qy[1] + 1};
+        for (uint32_t i0 = e0; i0 < e1; i0 += 32) {
+            const int n = (int)min(32u, e1 - i0);
+            // real edges of the chunk: not a ring's last vertex, inside the chunk
+            const uint32_t w = i0 >> 5, sh = i0 & 31;
+            uint32_t ends = ws.ring_end[w] >> sh;
+            if (sh && w + 1 < (uint32_t)(kWV / 32)) ends |= ws.ring_end[w + 1] << (32 - sh);
+            const uint32_t real = ~ends & (n == 32 ? 0xffffffffu : ((1u << n) - 1u));
+            uint32_t cm0 = 0u, cm1 = 0u;
+            if (cand_mode) { // q_lo <= q <= q_hi (a superset when q_hi == q_lo)
+                for (int u = n - 1; u >= 0; --u) {
+                    const int2 f = *reinterpret_cast<const int2*>(&ws.rec[i0 + u]);
+                    const unsigned r = (unsigned)f.y + 1u;
+                    cm0 = (cm0 << 1) | (uint32_t)((unsigned)(qy1[0] - f.x) <= r);
+                    cm1 = (cm1 << 1) | (uint32_t)((unsigned)(qy1[1] - f.x) <= r);
+                }
+            } else { // ties only: q == q_lo (d == -1) or q == q_hi (d == f.y)
+                for (int u = n - 1; u >= 0; --u) {
+                    const int2 f = *reinterpret_cast<const int2*>(&ws.rec[i0 + u]);
+                    const unsigned d0 = (unsigned)(qy[0] - f.x), d1 = (unsigned)(qy[1] - f.x);
+                    cm0 = (cm0 << 1) | (uint32_t)(d0 == 0xffffffffu || d0 == (unsigned)f.y);
+                    cm1 = (cm1 << 1) | (uint32_t)(d1 == 0xffffffffu || d1 == (unsigned)f.y);
+                }
+            }
+            // points whose key filter is not exact: every edge
+            cm0 = (slow & 1u) ? real & ((qok & 1u) ? cm0 : 0xffffffffu) : 0u;
+            cm1 = (slow & 2u) ? real & ((qok & 2u) ? cm1 : 0xffffffffu) : 0u;
+            // walk both points' undecided edges side by side
+            while (__any_sync(kFull, (cm0 | cm1) != 0)) {
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    uint32_t& m = k ? cm1 : cm0;
+                    if (m == 0) continue;
+                    const uint32_t i = i0 + __ffs(m) - 1;
+                    m &= m - 1;
+                    const double2 a = ws.vert[i], b = ws.vert[i + 1];
+                    if (__dmul_rn(__dsub_rn(a.y, py[k]), __dsub_rn(b.y, py[k])) <= 0.0) {
+                        double nx = __dsub_rn(b.y, a.y), ny = __dsub_rn(a.x, b.x);
+                        if (nx < 0.0) {
+                            nx = -nx;
+                            ny = -ny;
+                        }
+                        const double side =
+                            __dadd_rn(__dmul_rn(__dsub_rn(px[k], a.x), nx), __dmul_rn(__dsub_rn(py[k], a.y), ny));
+                        if (side <= 0.0) par ^= 1u << k;
+                    }
+                }
+            }
+        }
+    }
+    const uint32_t b0 = __ballot_sync(kFull, act & par & 1u);
+    const uint32_t b1 = __ballot_sync(kFull, (act & par) >> 1 & 1u);
+    if (lane < 2) or_bits(inside_bits, tp.s + cc + 32 * lane, lane ? b1 : b0);
+    return __popc(__ballot_sync(kFull, slow & 1u)) + __popc(__ballot_sync(kFull, slow >> 1 & 1u));
+}
+
+__global__ void __launch_bounds__(kBThreads, 8) pip_csr_tile_kernel(
+    const double2* __restrict__ pts, const unsigned long long* __restrict__ pt_off, unsigned long long n_polys,
+    const double* __restrict__ vx, const double* __restrict__ vy, const unsigned long long* __restrict__ ring_off,
+    const unsigned long long* __restrict__ poly_ring_off, unsigned long long pt_base, unsigned long long ring_base,
+    unsigned long long vert_base, uint32_t* __restrict__ inside_bits, uint32_t* __restrict__ defer_list,
+    uint32_t* __restrict__ defer_count) {
+    __shared__ WarpSmem smem[kBWarps];
+    const int lane = threadIdx.x & 31;
+    WarpSmem& ws = smem[threadIdx.x >> 5];
+    const unsigned long long nw = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+    const unsigned long long ngroups = (n_polys + 31) / 32;
+
+    int walk_left = 0; // adaptive mode of classify_item (warp-uniform)
+    for (unsigned long long g = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < ngroups; g += nw) {
+        // ---- ranges: lane = polygon g*32 + lane --------------------------------
+        const unsigned long long p = g * 32 + lane;
+        unsigned long long s = 0, e = 0, r0 = 0, r1 = 0, v0 = 0, vo1 = 0, vend = 0;
+        if (p < n_polys) {
+            s = pt_off[p] - pt_base;
+            e = pt_off[p + 1] - pt_base;
+            r0 = poly_ring_off[p] - ring_base;
+            r1 = poly_ring_off[p + 1] - ring_base;
+            v0 = ring_off[r0] - vert_base;
+            vend = ring_off[r1] - vert_base;
+            vo1 = r1 > r0 ? ring_off[r0 + 1] - vert_base : v0;
+        }
+        // no points or no rings: nothing to classify (no rings -> nothing is inside)
+        const bool work = p < n_polys && e > s && r1 > r0;
+        const bool big = work && vend - v0 > (unsigned long long)kWV;
+        if (big) defer_list[atomicAdd(defer_count, 1u)] = (uint32_t)p;
+        ws.gs[lane] = s;
+        ws.gr0[lane] = r0;
+        ws.gv0[lane] = v0;
+        ws.gnp[lane] = (uint32_t)(e - s);
+        ws.gnr[lane] = (uint32_t)(r1 - r0);
+        ws.gnv[lane] = work && !big ? (uint32_t)(vend - v0) : 0u;
+        ws.gnvo[lane] = (uint32_t)(vo1 - v0);
+        uint32_t todo = __ballot_sync(kFull, work && !big);
+        while (todo) {
+            // ---- batch: a prefix of the remaining polygons that fits kWV ----------
+            const uint32_t nv = ws.gnv[lane];
+            const uint32_t mine = (todo >> lane & 1u) ? nv : 0u;
+            uint32_t cum = mine;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(kFull, cum, o);
+                if (lane >= o) cum += y;
+            }
+            const uint32_t batch = todo & __ballot_sync(kFull, cum <= (uint32_t)kWV);
+            const int nb = __popc(batch);
+            const bool inb = batch >> lane & 1u;
+            const uint32_t excl = cum - mine;
+            const int k = __popc(batch & ((1u << lane) - 1u)); // compact index of this lane's polygon
+            const uint32_t total = __shfl_sync(kFull, cum, 31 - __clz(batch));
+            if (lane < kWV / 32) ws.ring_end[lane] = 0u;
+            if (inb) {
+                ws.off[k] = excl;
+                ws.v0s[k] = ws.gv0[lane];
+            }
+            __syncwarp();
+            if (inb) { // ring ends
+                const unsigned long long r0 = ws.gr0[lane], r1 = r0 + ws.gnr[lane], v0 = ws.gv0[lane];
+                if (r1 - r0 == 1) {
+                    atomicOr(&ws.ring_end[(excl + nv - 1) >> 5], 1u << ((excl + nv - 1) & 31));
+                } else {
+                    for (unsigned long long r = r0; r < r1; ++r) {
+                        const uint32_t i = excl + (uint32_t)(ring_off[r + 1] - vert_base - v0) - 1u;
+                        atomicOr(&ws.ring_end[i >> 5], 1u << (i & 31));
+                    }
+                }
+            }
+            // ---- 1. vertices -> shared memory ------------------------------------
+#pragma unroll
+            for (int u = 0; u < kWV / 32; ++u) {
+                const uint32_t i = lane + 32 * u;
+                if (i < total) {
+                    int o = 0; // owner: the last batch polygon whose first vertex is <= i
+#pragma unroll
+                    for (int step = 16; step > 0; step >>= 1)
+                        if (o + step < nb && ws.off[o + step] <= i) o += step;
+                    ws.owner[i] = (unsigned char)o;
+                    const unsigned long long v = ws.v0s[o] + (i - ws.off[o]);
+                    ws.vert[i] = make_double2(vx[v], vy[v]);
+                }
+            }
+            __syncwarp();
+            // ---- 2. bbox of the outer ring (lane per polygon) and scaling ------------
+            if (inb) {
+                double bx0 = INFINITY, by0 = INFINITY, bx1 = -INFINITY, by1 = -INFINITY;
+                const uint32_t nvo = ws.gnvo[lane];
+                for (uint32_t i = excl; i < excl + nvo; ++i) {
+                    const double2 q = ws.vert[i];
+                    bx0 = q.x < bx0 ? q.x : bx0; // std::min(min_x, v.x)
+                    by0 = q.y < by0 ? q.y : by0;
+                    bx1 = bx1 < q.x ? q.x : bx1; // std::max(max_x, v.x)
+                    by1 = by1 < q.y ? q.y : by1;
+                }
+                BPoly& b = ws.bp[k];
+                b.bx0 = bx0;
+                b.by0 = by0;
+                b.bx1 = bx1;
+                b.by1 = by1;
+                const double W = __dsub_rn(bx1, bx0), H = __dsub_rn(by1, by0);
+                const bool fast = W >= 0x1p-300 && W <= 0x1p300 && H >= 0x1p-300 && H <= 0x1p300;
+                b.fast = fast;
+                b.sx = fast ? pow2_below_inv(W) : 1.0;
+                b.sy = fast ? pow2_below_inv(H) : 1.0;
+                b.s = ws.gs[lane];
+                b.np = ws.gnp[lane];
+                b.e0 = excl;
+                b.e1 = excl + nv;
+            }
+            __syncwarp();
+            // ---- 3. fast-path record per edge -----------------------------------
+            for (uint32_t i = lane; i < total; i += 32) {
+                const int o = ws.owner[i];
+                const double bx0 = ws.bp[o].bx0, by0 = ws.bp[o].by0;
+                const double sx = ws.bp[o].sx, sy = ws.bp[o].sy;
+                const double2 a = ws.vert[i];
+                const double axl = __dmul_rn(__dsub_rn(a.x, bx0), sx), ayl = __dmul_rn(__dsub_rn(a.y, by0), sy);
+                const int qa = __double2int_rz(__dmul_rn(ayl, 0x1p30));
+                if (!(axl >= 0.0 && axl < 1.0 && ayl >= 0.0 && ayl < 1.0)) ws.bp[o].fast = 0; // a hole poking out
+                int4 f = make_int4(kFastSentinelLo, 0, qa, 0);
+                float2 gg = make_float2(0.f, 1.f);
+                if (!is_ring_end(ws, i)) {
+                    const double2 b = ws.vert[i + 1];
+                    const int qb = __double2int_rz(__dmul_rn(__dmul_rn(__dsub_rn(b.y, by0), sy), 0x1p30));
+                    // the reference's normal (geometry.hpp:190-195)
+                    double nx = __dsub_rn(b.y, a.y), ny = __dsub_rn(a.x, b.x);
+                    if (nx < 0.0) {
+                        nx = -nx;
+                        ny = -ny;
+                    }
+                    const int qlo = min(qa, qb), qhi = max(qa, qb);
+                    const double Nx = __dmul_rn(nx, sy), Ny = __dmul_rn(ny, sx);
+                    const double cd = __dadd_rn(__dmul_rn(axl, Nx), __dmul_rn(ayl, Ny));
+                    f = make_int4(qlo + 1, max(qhi - qlo - 1, 0), qa, __float_as_int(__double2float_rn(Nx)));
+                    gg = make_float2(__double2float_rn(Ny), __double2float_rn(-cd));
+                }
+                ws.rec[i] = f;
+                ws.rec2[i] = gg;
+            }
+            __syncwarp();
+            // ---- 4. classify the batch's polygons ---------------------------------
+            // items (polygon j, points c..c+63) in order; the points of the next
+            // item are loaded while the current one is classified
+            int j = 0;
+            uint32_t c = 0;
+            double2 qn0, qn1;
+            auto load = [&](int jj, uint32_t cc, double2& a0, double2& a1) {
+                const uint32_t n = ws.bp[jj].np;
+                const double2* P = pts + ws.bp[jj].s;
+                a0 = cc + lane < n ? P[cc + lane] : make_double2(0.0, 0.0);
+                a1 = cc + 32 + lane < n ? P[cc + 32 + lane] : make_double2(0.0, 0.0);
+            };
+            load(0, 0, qn0, qn1);
+            while (j < nb) {
+                const double2 qc[2] = {qn0, qn1};
+                const int cj = j;
+                const uint32_t cc = c;
+                c += 64;
+                if (c >= ws.bp[j].np) {
+                    c = 0;
+                    ++j;
+                }
+                if (j < nb) load(j, c, qn0, qn1);
+                const int ns = classify_item(ws, cj, cc, qc, lane, pts, inside_bits, walk_left > 0);
+                // mode choice: after an fp32 pass that left >= 1/4 of the points
+                // undecided, walk everything for the next 16 steps, then probe again
+                if (walk_left > 0) --walk_left;
+                else if (ns >= 16) walk_left = 16;
+            }
+            __syncwarp(); // the next batch rewrites this warp's shared slice
+            todo &= ~batch;
+        }
+    }
+}
+
+int sms(int dev) {
+    int v = 148;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+}
+
+} // namespace
+
+cudaError_t launch_csr_tile(const CsrArgs& a, uint32_t* list, uint32_t* count, cudaStream_t st, int dev,
+                            uint64_t* launches) {
+    if (a.n_polys > 0xffffffffull) return cudaErrorInvalidValue; // 32-bit deferred-polygon list
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pip_csr_tile_kernel, kBThreads, 0);
+    per_sm = std::max(per_sm, 1);
+    const uint64_t ngroups = (a.n_polys + 31) / 32;
+    const uint64_t want = (ngroups + kBWarps - 1) / kBWarps;
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)sms(dev) * per_sm));
+    pip_csr_tile_kernel<<<grid, kBThreads, 0, st>>>(
+        reinterpret_cast<const double2*>(a.pts), reinterpret_cast<const unsigned long long*>(a.pt_off), a.n_polys,
+        a.vx, a.vy, reinterpret_cast<const unsigned long long*>(a.ring_off),
+        reinterpret_cast<const unsigned long long*>(a.poly_ring_off), a.pt_base, a.ring_base, a.vert_base,
+        a.inside_bits, list, count);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+} // namespace pcd

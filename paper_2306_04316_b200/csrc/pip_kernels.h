@@ -59,6 +59,10 @@ size_t csr_meta_bytes(uint64_t n_polys);
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st, int dev, uint64_t* launches);
 cudaError_t launch_single(const SingleArgs& a, cudaStream_t st, int dev, uint64_t* launches);
 cudaError_t launch_csr(const CsrArgs& a, cudaStream_t st, int dev, uint64_t* launches);
+// C1 tile kernel (pip_csr_tile.cu): appends the polygons of oversized tiles to
+// list[*count ...] for the warp-per-polygon kernel
+cudaError_t launch_csr_tile(const CsrArgs& a, uint32_t* list, uint32_t* count, cudaStream_t st, int dev,
+                            uint64_t* launches);
 cudaError_t launch_finalize(uint64_t n, uint32_t* inside_bits, const uint32_t* aux_bits, uint8_t* verdicts,
                             int mode, unsigned long long* stats, cudaStream_t st, int dev, uint64_t* launches);
 cudaError_t launch_count(const double* pts, uint64_t n, const double* vx, const double* vy, uint64_t nv, int mode,

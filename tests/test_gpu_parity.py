@@ -371,3 +371,73 @@ def test_bucketing_skewed_inputs(engine):
             check_single(xy, poly, mode, engine.classify(xy, poly, mode, prefilter=False), prefilter=False)
     finally:
         engine.set_bucketing(-1)
+
+
+def _near_edge_points(s, deltas, ts=(0.25, 0.5, 0.75)):
+    """Per polygon of CsrSet s: points on every outer-ring edge (a + t (b - a) in
+    binary64) and nudged off it along the edge normal by each delta (relative to
+    the polygon's bbox size), so that they fall inside, on and just outside the
+    fp32 fast path's band (pip_csr_common.cuh)."""
+    xy, pt_off = [], [0]
+    for p in range(s.n_polys):
+        r0 = int(s.poly_ring_off[p])
+        v0, v1 = int(s.ring_off[r0]), int(s.ring_off[r0 + 1])
+        x, y = s.vx[v0:v1], s.vy[v0:v1]
+        size = max(x.max() - x.min(), y.max() - y.min())
+        pts = []
+        for i in range(len(x) - 1):
+            ax, ay, bx, by = x[i], y[i], x[i + 1], y[i + 1]
+            ln = np.hypot(bx - ax, by - ay) or 1.0
+            nx, ny = (by - ay) / ln, (ax - bx) / ln
+            for t in ts:
+                px, py = ax + t * (bx - ax), ay + t * (by - ay)
+                pts.append((px, py))
+                for d in deltas:
+                    pts.append((px + d * size * nx, py + d * size * ny))
+                    pts.append((px - d * size * nx, py - d * size * ny))
+            pts.append((ax, ay))                       # the vertex itself (tie)
+            pts.append((ax + 0.3 * size, ay))          # on the vertex's y-level (tie)
+        xy.extend(pts)
+        pt_off.append(len(xy))
+    return CsrSet(np.ascontiguousarray(np.array(xy, np.float64)), np.array(pt_off, np.uint64), s.vx, s.vy,
+                  s.ring_off, s.poly_ring_off)
+
+
+def test_csr_fast_path_band_and_ties(engine):
+    """C1 CSR fast path (fp32 side test with a certified band, integer y keys):
+    points on / within / just outside the band of every edge, vertex ties, for
+    footprints in lon/lat degrees and for integer-grid polygons."""
+    deltas = (1e-16, 1e-12, 1e-9, 2e-7, 4e-7, 1e-6, 3e-6, 1e-4)
+    for base in (W.footprints(400, seed=31), W.degenerate(150, seed=32, allow_dups=False)):
+        s = _near_edge_points(base, deltas)
+        for mode in MODES:
+            got = engine.classify_csr(s, mode)
+            want_v, want_s = oracle.port_classify_csr(s, mode, threads=THREADS)
+            assert np.array_equal(got.verdicts, want_v), f"mode {mode}: {(got.verdicts != want_v).sum()} differ"
+            assert np.array_equal(got.stats, want_s)
+
+
+def test_csr_fast_path_gates(engine):
+    """Polygons where the fast path must switch itself off or route points to the
+    exact path: the adversarial cases as CSR polygons (tiny / subnormal / huge
+    extents, signed zeros, slivers), a hole poking outside the outer ring, and a
+    polygon straddling y = 0 with points at |y| < 2^-400."""
+    rng = np.random.default_rng(41)
+    parts = []
+    for name, poly, xy in adversarial.cases(include_dups=False):
+        parts.append(_single_as_csr(poly, xy))
+    out = [(0, 0), (4, 0), (4, 4), (0, 4), (0, 0)]
+    hole = [(1, 1), (6, 1), (6, 3), (1, 3), (1, 1)]  # extends past the outer ring's bbox
+    ph = Polygon.from_rings([out, hole])
+    parts.append(_single_as_csr(ph, np.concatenate([rng.uniform(-1, 7, (800, 2)), adversarial._special_points(ph, rng)])))
+    eq = [(-1.0, -1.0), (1.0, -1.0), (1.0, 1.0), (-1.0, 1.0), (-1.0, -1.0)]
+    pe = Polygon.from_rings([eq, [(-0.5, -1e-310), (0.5, -1e-310), (0.5, 1e-310), (-0.5, 1e-310), (-0.5, -1e-310)]])
+    ys = np.array([0.0, -0.0, 1e-320, -1e-320, 1e-310, -1e-310, 2e-310, 1e-130, 1e-121, 3e-121, -3e-121])
+    exy = np.stack([np.repeat(np.linspace(-1.2, 1.2, 13), len(ys)), np.tile(ys, 13)], 1)
+    parts.append(_single_as_csr(pe, np.concatenate([exy, rng.uniform(-1.2, 1.2, (500, 2))])))
+    s = _concat_csr(parts)
+    for mode in MODES:
+        got = engine.classify_csr(s, mode)
+        want_v, want_s = oracle.port_classify_csr(s, mode, threads=THREADS)
+        assert np.array_equal(got.verdicts, want_v), f"mode {mode}: {(got.verdicts != want_v).sum()} differ"
+        assert np.array_equal(got.stats, want_s)
