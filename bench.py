@@ -349,6 +349,9 @@ def run_ours(args, rank, world, local_rank):
             "per_item_tests_per_s": {i.label: i.tests / (ms / 1e3) for i, ms in zip(items, per_item_ms)},
             "roofline": roof, "gpu_launches": launches[0]}
 
+    if args.workload == "c2_sweep":
+        line["sweep_fit"] = sweep_fit(items, per_item_ms)
+
     # ---- clocks -------------------------------------------------------------------------
     line["clocks"] = clk.summary()
 
@@ -363,6 +366,23 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0:
         print(json.dumps(line), flush=True)
     eng.close()
+
+
+def sweep_fit(items, per_item_ms):
+    """The paper's O(n) claim on the GPU: least-squares line of kernel time vs n
+    (vertices) over the sweep, solved on centred data as the reference's
+    least_squares_fit (bench.hpp:120-148), with its per-sample relative
+    prediction error (error_report, bench.hpp:172-199) and R^2."""
+    n = np.array([it.tests / it.n_points for it in items], dtype=np.float64)  # edges
+    t = np.asarray(per_item_ms, dtype=np.float64) / 1e3
+    dn, dt = n - n.mean(), t - t.mean()
+    slope = float((dn * dt).sum() / (dn * dn).sum())
+    icpt = float(t.mean() - slope * n.mean())
+    pred = slope * n + icpt
+    ss_res, ss_tot = float(((t - pred) ** 2).sum()), float((dt * dt).sum())
+    return {"x": "edges n", "y": "kernel seconds per 1e6-point launch", "slope_s_per_edge": slope,
+            "intercept_s": icpt, "r2": 1.0 - ss_res / ss_tot if ss_tot > 0 else 1.0,
+            "rel_err": {it.label: float(abs(p - a) / a) for it, p, a in zip(items, pred, t)}}
 
 
 def job_totals(items, world, dev):

@@ -118,6 +118,30 @@ int pc_classify_csr_dev(pc_ctx* ctx, int dev_index, void* stream, const double* 
                         uint8_t* d_verdicts, uint32_t* d_inside_bits, uint32_t* d_aux_bits,
                         uint64_t* d_stats);
 
+/* prefilter_bbox (batch.hpp:137-153) on the GPU: the points of pts_xy[n]
+ * inside the closed box {min_x, min_y, max_x, max_y} (BBox::contains,
+ * batch.hpp:39-41), in input order, to out_xy (capacity n points) with their
+ * original indices to out_idx (capacity n); *n_inside = how many.  The
+ * outside count is n - *n_inside.  PC_EINVAL if min > max on an axis (the
+ * BBox constructor's check, batch.hpp:32-36) or a needed pointer is NULL. */
+int pc_prefilter_bbox(pc_ctx* ctx, const double* pts_xy, uint64_t n, const double box[4], double* out_xy,
+                      uint64_t* out_idx, uint64_t* n_inside);
+
+/* scatter_verdicts (batch.hpp:157-168) on the GPU: out[n_total] = Outside,
+ * then out[idx[k]] = inbox_verdicts[k] for k < n_inbox.  PC_EINVAL if
+ * n_inbox > n_total (the reference's size check) or an index is >= n_total. */
+int pc_scatter_verdicts(pc_ctx* ctx, const uint64_t* idx, const uint8_t* inbox_verdicts, uint64_t n_inbox,
+                        uint64_t n_total, uint8_t* out);
+
+/* Device-pointer variants (not synchronised).  d_n_inside receives the count
+ * (one u64 in device memory); d_bad (one u32, zeroed by the caller) is set
+ * to non-zero when an index is out of range. */
+int pc_prefilter_bbox_dev(pc_ctx* ctx, int dev_index, void* stream, const double* d_pts_xy, uint64_t n,
+                          const double box[4], double* d_out_xy, uint64_t* d_out_idx, uint64_t* d_n_inside);
+int pc_scatter_verdicts_dev(pc_ctx* ctx, int dev_index, void* stream, const uint64_t* d_idx,
+                            const uint8_t* d_inbox_verdicts, uint64_t n_inbox, uint64_t n_total,
+                            uint8_t* d_out, uint32_t* d_bad);
+
 /* Number of GPU kernels the last call on this context launched (all devices). */
 uint64_t pc_last_launch_count(const pc_ctx* ctx);
 

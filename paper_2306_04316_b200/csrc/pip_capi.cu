@@ -45,6 +45,7 @@ struct DevState {
     DevBuf pts, vx, vy, ring_off, pt_off, poly_ring_off, filt, rec, bbox, bits, verdicts, stats, counts, degen;
     DevBuf bucket_scratch, sorted_pts, sorted_idx, bucket_blk; // y-bucketing (pip_sort.cu)
     DevBuf csr_meta;                                          // per-polygon records (pip_csr.cu)
+    DevBuf cmp_blk, cmp_pts, cmp_idx, cmp_v, cmp_out;         // prefilter / scatter (pip_compact.cu)
     unsigned long long* h_stats = nullptr; // pinned 4 x u64
     // profiling: one event pair per main-kernel launch since the last take
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
@@ -556,6 +557,117 @@ int pc_count_crossings(pc_ctx* c, const double* pts_xy, uint64_t n, const double
         check(c, cudaMemcpyAsync(counts, d.counts.p, n * 8, cudaMemcpyDeviceToHost, st), "download counts");
         check(c, cudaMemcpyAsync(degenerate, d.degen.p, n, cudaMemcpyDeviceToHost, st), "download flags");
         check(c, cudaStreamSynchronize(st), "count_crossings");
+    });
+}
+
+namespace {
+
+void check_box(pc_ctx* c, const double* box) {
+    if (!box) invalid(c, "null box");
+    if (!(box[0] <= box[2]) || !(box[1] <= box[3])) invalid(c, "BBox: min must not exceed max");
+}
+
+// prefilter on device d, stream st; blk scratch from d; count left at blk[n_blk]
+unsigned long long* enqueue_prefilter(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts, uint64_t n,
+                                      const double* box, double* d_out, unsigned long long* d_idx) {
+    const int nb = pcd::compact_blocks(n, d.dev);
+    check(c, d.cmp_blk.ensure((size_t)(nb + 1) * 8), "alloc prefilter scratch");
+    unsigned long long* blk = d.cmp_blk.as<unsigned long long>();
+    check(c, pcd::launch_prefilter(d_pts, n, box, nb, blk, d_out, d_idx, st, &c->launches), "prefilter kernels");
+    return blk + nb;
+}
+
+} // namespace
+
+int pc_prefilter_bbox(pc_ctx* c, const double* pts_xy, uint64_t n, const double box[4], double* out_xy,
+                      uint64_t* out_idx, uint64_t* n_inside) {
+    return guarded(c, [&] {
+        check_box(c, box);
+        if (!n_inside) invalid(c, "null n_inside");
+        *n_inside = 0;
+        if (n == 0) return;
+        if (!pts_xy || !out_xy || !out_idx) invalid(c, "null arrays");
+        DevState& d = c->devs[0];
+        check(c, cudaSetDevice(d.dev), "cudaSetDevice");
+        cudaStream_t st = d.stream;
+        h2d(c, d.cmp_pts, pts_xy, n * 16, st, "upload points");
+        check(c, d.cmp_out.ensure(n * 16), "alloc compacted points");
+        check(c, d.cmp_idx.ensure(n * 8), "alloc indices");
+        const unsigned long long* cnt = enqueue_prefilter(c, d, st, d.cmp_pts.as<double>(), n, box,
+                                                          d.cmp_out.as<double>(), d.cmp_idx.as<unsigned long long>());
+        unsigned long long k = 0;
+        check(c, cudaMemcpyAsync(&k, cnt, 8, cudaMemcpyDeviceToHost, st), "download count");
+        check(c, cudaStreamSynchronize(st), "prefilter");
+        if (k) {
+            check(c, cudaMemcpyAsync(out_xy, d.cmp_out.p, k * 16, cudaMemcpyDeviceToHost, st), "download points");
+            check(c, cudaMemcpyAsync(out_idx, d.cmp_idx.p, k * 8, cudaMemcpyDeviceToHost, st), "download indices");
+            check(c, cudaStreamSynchronize(st), "prefilter");
+        }
+        *n_inside = k;
+    });
+}
+
+int pc_scatter_verdicts(pc_ctx* c, const uint64_t* idx, const uint8_t* inbox_verdicts, uint64_t n_inbox,
+                        uint64_t n_total, uint8_t* out) {
+    return guarded(c, [&] {
+        if (n_inbox > n_total) invalid(c, "scatter_verdicts: verdict count does not match index map");
+        if (n_total == 0) return;
+        if (!out || (n_inbox && (!idx || !inbox_verdicts))) invalid(c, "null arrays");
+        DevState& d = c->devs[0];
+        check(c, cudaSetDevice(d.dev), "cudaSetDevice");
+        cudaStream_t st = d.stream;
+        h2d(c, d.cmp_idx, idx, n_inbox * 8, st, "upload indices");
+        h2d(c, d.cmp_v, inbox_verdicts, n_inbox, st, "upload verdicts");
+        const size_t off = (n_total + 7) & ~7ull; // the out-of-range flag after the verdicts
+        check(c, d.cmp_out.ensure(off + 16), "alloc verdicts");
+        uint8_t* o = d.cmp_out.as<uint8_t>();
+        unsigned* bad = reinterpret_cast<unsigned*>(o + off);
+        check(c, cudaMemsetAsync(bad, 0, 4, st), "clear flag");
+        check(c, pcd::launch_scatter_verdicts(d.cmp_idx.as<unsigned long long>(), d.cmp_v.as<uint8_t>(), n_inbox,
+                                              n_total, o, bad, st, d.dev, &c->launches),
+              "scatter kernel");
+        unsigned b = 0;
+        check(c, cudaMemcpyAsync(&b, bad, 4, cudaMemcpyDeviceToHost, st), "download flag");
+        check(c, cudaMemcpyAsync(out, o, n_total, cudaMemcpyDeviceToHost, st), "download verdicts");
+        check(c, cudaStreamSynchronize(st), "scatter_verdicts");
+        if (b) invalid(c, "scatter_verdicts: original index out of range");
+    });
+}
+
+int pc_prefilter_bbox_dev(pc_ctx* c, int dev_index, void* stream, const double* d_pts_xy, uint64_t n,
+                          const double box[4], double* d_out_xy, uint64_t* d_out_idx, uint64_t* d_n_inside) {
+    return guarded(c, [&] {
+        if (dev_index < 0 || dev_index >= (int)c->devs.size()) invalid(c, "bad device index");
+        check_box(c, box);
+        if (!d_n_inside) invalid(c, "null count");
+        DevState& d = c->devs[dev_index];
+        check(c, cudaSetDevice(d.dev), "cudaSetDevice");
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d.stream;
+        if (n == 0) {
+            check(c, cudaMemsetAsync(d_n_inside, 0, 8, st), "clear count");
+            return;
+        }
+        if (!d_pts_xy || !d_out_xy || !d_out_idx) invalid(c, "null arrays");
+        const unsigned long long* cnt = enqueue_prefilter(c, d, st, d_pts_xy, n, box, d_out_xy,
+                                                          reinterpret_cast<unsigned long long*>(d_out_idx));
+        check(c, cudaMemcpyAsync(d_n_inside, cnt, 8, cudaMemcpyDeviceToDevice, st), "copy count");
+    });
+}
+
+int pc_scatter_verdicts_dev(pc_ctx* c, int dev_index, void* stream, const uint64_t* d_idx,
+                            const uint8_t* d_inbox_verdicts, uint64_t n_inbox, uint64_t n_total, uint8_t* d_out,
+                            uint32_t* d_bad) {
+    return guarded(c, [&] {
+        if (dev_index < 0 || dev_index >= (int)c->devs.size()) invalid(c, "bad device index");
+        if (n_inbox > n_total) invalid(c, "scatter_verdicts: verdict count does not match index map");
+        if (n_total == 0) return;
+        if (!d_out || !d_bad || (n_inbox && (!d_idx || !d_inbox_verdicts))) invalid(c, "null arrays");
+        DevState& d = c->devs[dev_index];
+        check(c, cudaSetDevice(d.dev), "cudaSetDevice");
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d.stream;
+        check(c, pcd::launch_scatter_verdicts(reinterpret_cast<const unsigned long long*>(d_idx), d_inbox_verdicts,
+                                              n_inbox, n_total, d_out, d_bad, st, d.dev, &c->launches),
+              "scatter kernel");
     });
 }
 

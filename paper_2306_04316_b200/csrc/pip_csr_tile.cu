@@ -47,7 +47,9 @@ struct BPoly {
     unsigned long long s;      // first point (shard-local index)
     uint32_t np;               // points
     uint32_t e0, e1;           // vertex range in the batch
-    int fast;                  // fast path usable
+    uint32_t nloop;            // records the fast pass must visit (a closed single ring's
+                               // last vertex repeats the first: its sentinel is skipped),
+                               // bit 31: fast path usable
 };
 
 struct WarpSmem {
@@ -81,7 +83,7 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
     const uint32_t np = tp.np, e0 = tp.e0, e1 = tp.e1;
     const double bx0 = tp.bx0, by0 = tp.by0, bx1 = tp.bx1, by1 = tp.by1;
     const double sx = tp.sx, sy = tp.sy;
-    const bool fast = tp.fast != 0;
+    const bool fast = tp.nloop >> 31;
     float lx[2], ly[2];
     int qy[2];
     uint32_t act = 0, qok = 0;
@@ -119,12 +121,14 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
             t0 = min(t0, (unsigned)(qy[0] - f.z)); // ties: 0 iff q(p.y) == q(vertex)
             t1 = min(t1, (unsigned)(qy[1] - f.z));
         };
-        uint32_t i = e0;
-        for (; i + 4 <= e1; i += 4) {
+        // four records per iteration; reads past the polygon's last record
+        // re-read it (the final vertex's sentinel: no toggle, no band hit, a
+        // repeated tie check), so no remainder loop is needed
+        const uint32_t last = e1 - 1u;
+        for (uint32_t i = e0; i < e0 + (tp.nloop & 0x7fffffffu); i += 4) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) rec(i + k);
+            for (int k = 0; k < 4; ++k) rec(min(i + k, last));
         }
-        for (; i < e1; ++i) rec(i);
         band = ((uint32_t)(m0 <= kFastBand) | ((uint32_t)(m1 <= kFastBand) << 1)) & act;
         const uint32_t tie = ((uint32_t)(t0 == 0u) | ((uint32_t)(t1 == 0u) << 1)) & act;
         slow |= band | tie;
@@ -310,13 +314,15 @@ __global__ void __launch_bounds__(kBThreads, 8) pip_csr_tile_kernel(
                 b.by1 = by1;
                 const double W = __dsub_rn(bx1, bx0), H = __dsub_rn(by1, by0);
                 const bool fast = W >= 0x1p-300 && W <= 0x1p300 && H >= 0x1p-300 && H <= 0x1p300;
-                b.fast = fast;
                 b.sx = fast ? pow2_below_inv(W) : 1.0;
                 b.sy = fast ? pow2_below_inv(H) : 1.0;
                 b.s = ws.gs[lane];
                 b.np = ws.gnp[lane];
                 b.e0 = excl;
                 b.e1 = excl + nv;
+                const double2 vf = ws.vert[excl], vl = ws.vert[excl + nv - 1];
+                b.nloop = (ws.gnr[lane] == 1 && nv > 1 && vf.x == vl.x && vf.y == vl.y ? nv - 1 : nv) |
+                          ((uint32_t)fast << 31);
             }
             __syncwarp();
             // ---- 3. fast-path record per edge -----------------------------------
@@ -327,7 +333,7 @@ __global__ void __launch_bounds__(kBThreads, 8) pip_csr_tile_kernel(
                 const double2 a = ws.vert[i];
                 const double axl = __dmul_rn(__dsub_rn(a.x, bx0), sx), ayl = __dmul_rn(__dsub_rn(a.y, by0), sy);
                 const int qa = __double2int_rz(__dmul_rn(ayl, 0x1p30));
-                if (!(axl >= 0.0 && axl < 1.0 && ayl >= 0.0 && ayl < 1.0)) ws.bp[o].fast = 0; // a hole poking out
+                if (!(axl >= 0.0 && axl < 1.0 && ayl >= 0.0 && ayl < 1.0)) atomicAnd(&ws.bp[o].nloop, 0x7fffffffu); // a hole poking out
                 int4 f = make_int4(kFastSentinelLo, 0, qa, 0);
                 float2 gg = make_float2(0.f, 1.f);
                 if (!is_ring_end(ws, i)) {

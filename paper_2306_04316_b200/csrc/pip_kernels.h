@@ -68,6 +68,16 @@ cudaError_t launch_finalize(uint64_t n, uint32_t* inside_bits, const uint32_t* a
 cudaError_t launch_count(const double* pts, uint64_t n, const double* vx, const double* vy, uint64_t nv, int mode,
                          unsigned long long* counts, uint8_t* degenerate, cudaStream_t st, uint64_t* launches);
 
+// GPU prefilter_bbox / scatter_verdicts (pip_compact.cu): blk needs
+// compact_blocks(n)+1 entries; box = {min_x, min_y, max_x, max_y}; the in-box
+// count lands in blk[n_blk].
+int compact_blocks(uint64_t n, int dev);
+cudaError_t launch_prefilter(const double* pts, uint64_t n, const double box[4], int n_blk,
+                             unsigned long long* blk, double* out_pts, unsigned long long* out_idx, cudaStream_t st,
+                             uint64_t* launches);
+cudaError_t launch_scatter_verdicts(const unsigned long long* idx, const uint8_t* v, uint64_t n_in, uint64_t n_total,
+                                    uint8_t* out, unsigned* bad, cudaStream_t st, int dev, uint64_t* launches);
+
 // y-bucketing of the points of one polygon (pip_sort.cu): counting sort by
 // y over the outer ring's bbox into kBuckets bins; bbox-rejected points
 // (prefilter) go to a trailing bin that is not classified.

@@ -264,6 +264,30 @@ class Engine:
         self._check(rc, "pc_count_crossings")
         return counts, deg
 
+    def prefilter_bbox(self, xy, box):
+        """prefilter_bbox (batch.hpp:137-153) on the GPU: (inside_xy, original_indices,
+        outside_count) for the closed box (min_x, min_y, max_x, max_y), input order kept."""
+        xy = np.ascontiguousarray(xy, dtype=np.float64).reshape(-1, 2)
+        b = np.ascontiguousarray(box, dtype=np.float64).reshape(4)
+        n = len(xy)
+        out = np.empty((n, 2), np.float64)
+        idx = np.empty(n, np.uint64)
+        k = C.c_uint64(0)
+        rc = self.lib.pc_prefilter_bbox(self.ctx, _ptr(xy), n, _ptr(b), _ptr(out), _ptr(idx), C.byref(k))
+        self._check(rc, "pc_prefilter_bbox")
+        return out[:k.value], idx[:k.value], n - k.value
+
+    def scatter_verdicts(self, original_indices, inbox_verdicts, n_total):
+        """scatter_verdicts (batch.hpp:157-168) on the GPU: full-length verdicts, Outside where filtered."""
+        idx = np.ascontiguousarray(original_indices, dtype=np.uint64)
+        v = np.ascontiguousarray(inbox_verdicts, dtype=np.uint8)
+        if len(idx) != len(v):
+            raise ValueError("scatter_verdicts: verdict count does not match index map")
+        out = np.empty(int(n_total), np.uint8)
+        rc = self.lib.pc_scatter_verdicts(self.ctx, _ptr(idx), _ptr(v), len(v), int(n_total), _ptr(out))
+        self._check(rc, "pc_scatter_verdicts")
+        return out
+
     # ---- device-pointer API (torch tensors as HBM buffers) ------------------
     def classify_dev(self, dev_index, stream_ptr, d_xy, n, d_vx, d_vy, d_ring_off, n_rings, n_verts, mode,
                      boundary_tol, prefilter, d_inside, d_aux, d_stats, d_verdicts=None):

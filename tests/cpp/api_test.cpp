@@ -200,6 +200,51 @@ void randomized() {
     std::printf("randomized: %d polygon x mode cases compared against the reference\n", compared);
 }
 
+// batch_test.cpp:37-63 (prefilter_bbox, scatter_verdicts) and the bbox
+// property of :107-124, now GPU compaction / scatter behind the same API
+void prefilter_scatter() {
+    PointBatch batch;
+    batch.points = {{0.5, 0.5}, {2, 2}};
+    const PrefilterResult pre = prefilter_bbox(batch, BBox(0, 0, 1, 1));
+    CHECK(pre.inside_box.size() == 1);
+    CHECK(pre.inside_box.size() == 1 && pre.inside_box.points[0] == Point2(0.5, 0.5));
+    CHECK(pre.original_indices == std::vector<std::size_t>{0});
+    CHECK(pre.outside_count == 1);
+    PointBatch edge_case;
+    edge_case.points = {{1.0, 0.5}};
+    CHECK(prefilter_bbox(edge_case, BBox(0, 0, 1, 1)).inside_box.size() == 1); // closed interval
+
+    PointBatch b2;
+    b2.points = {{0.5, 0.5}, {2, 2}, {0.1, 0.1}, {-3, 0}};
+    const PrefilterResult p2 = prefilter_bbox(b2, BBox(0, 0, 1, 1));
+    CHECK(p2.inside_box.size() == 2);
+    const std::vector<Verdict> sc = scatter_verdicts(p2, {Verdict::Inside, Verdict::Boundary});
+    CHECK((sc == std::vector<Verdict>{Verdict::Inside, Verdict::Outside, Verdict::Boundary, Verdict::Outside}));
+    CHECK_THROWS(scatter_verdicts(p2, {Verdict::Inside}), std::invalid_argument);
+    CHECK(prefilter_bbox(PointBatch{}, BBox(0, 0, 1, 1)).inside_box.empty());
+
+    // order, indices and counts vs the reference loop on random batches (1e5 points)
+    std::mt19937_64 g(17);
+    for (int trial = 0; trial < 5; ++trial) {
+        const Polygon poly = random_polygon(g, 5 + g() % 50);
+        const BBox box = bbox_of(poly);
+        const BBox big = box.inflated(1.0);
+        PointBatch pb;
+        for (int k = 0; k < 100000; ++k) pb.points.emplace_back(uni(g, big.min_x, big.max_x), uni(g, big.min_y, big.max_y));
+        pb.points.emplace_back(box.min_x, box.max_y); // corners are inside (closed)
+        const PrefilterResult pr = prefilter_bbox(pb, box);
+        std::vector<std::size_t> want;
+        for (std::size_t i = 0; i < pb.size(); ++i)
+            if (box.contains(pb.points[i])) want.push_back(i);
+        bool ok = pr.original_indices == want && pr.outside_count + want.size() == pb.size();
+        for (std::size_t k = 0; ok && k < want.size(); ++k) ok = pr.inside_box.points[k] == pb.points[want[k]];
+        CHECK(ok);
+        const BatchResult in = classify_batch(pr.inside_box, poly, CrossingMode::C1);
+        const std::vector<Verdict> full = scatter_verdicts(pr, in.verdicts);
+        CHECK(full == classify_batch(pb, poly, CrossingMode::C1).verdicts); // the CLI pipeline == classify_batch
+    }
+}
+
 } // namespace
 
 int main(int argc, char** argv) {
@@ -209,6 +254,7 @@ int main(int argc, char** argv) {
     try {
         kats();
         randomized();
+        prefilter_scatter();
     } catch (const std::exception& e) {
         std::fprintf(stderr, "FAIL: uncaught exception: %s\n", e.what());
         return 100;

@@ -441,3 +441,50 @@ def test_csr_fast_path_gates(engine):
         want_v, want_s = oracle.port_classify_csr(s, mode, threads=THREADS)
         assert np.array_equal(got.verdicts, want_v), f"mode {mode}: {(got.verdicts != want_v).sum()} differ"
         assert np.array_equal(got.stats, want_s)
+
+
+# ---- GPU prefilter_bbox / scatter_verdicts ------------------------
+
+def _prefilter_ref(xy, box):
+    """batch.hpp:137-153 restated: closed-interval membership, input order kept."""
+    x0, y0, x1, y1 = box
+    m = (xy[:, 0] >= x0) & (xy[:, 0] <= x1) & (xy[:, 1] >= y0) & (xy[:, 1] <= y1)
+    idx = np.nonzero(m)[0].astype(np.uint64)
+    return xy[m], idx, len(xy) - len(idx)
+
+
+@pytest.mark.parametrize("n", [0, 1, 31, 1000, 16385, 5_000_003])
+def test_prefilter_bbox_matches_reference_loop(engine, n):
+    rng = np.random.default_rng(n + 5)
+    xy = rng.uniform(-2, 2, (n, 2))
+    if n > 10:
+        xy[:5] = [[1.0, 0.5], [-1.0, -1.0], [1.0, 1.0], [np.nan, 0.0], [0.0, np.inf]]  # edges, corner, NaN, inf
+    for box in ((-1.0, -1.0, 1.0, 1.0), (0.0, 0.0, 0.0, 0.0), (-5.0, -5.0, 5.0, 5.0), (3.0, 3.0, 4.0, 4.0)):
+        got_xy, got_idx, got_out = engine.prefilter_bbox(xy, box)
+        want_xy, want_idx, want_out = _prefilter_ref(xy, box)
+        assert got_out == want_out
+        assert np.array_equal(got_idx, want_idx)
+        assert np.array_equal(got_xy.view(np.uint64), want_xy.view(np.uint64))  # bit-identical points
+
+
+def test_scatter_verdicts_and_cli_pipeline(engine):
+    """CLI pipeline (polycast_cli.cpp:78-80): prefilter -> classify the in-box points ->
+    scatter == classify_batch of the whole batch; plus the reference's error cases."""
+    poly = W.star_polygon(300, seed=9)
+    rng = np.random.default_rng(3)
+    b = W.bounds(poly)
+    xy = np.stack([rng.uniform(b[0] - 1, b[2] + 1, 200_001), rng.uniform(b[1] - 1, b[3] + 1, 200_001)], 1)
+    box = (float(poly.vx.min()), float(poly.vy.min()), float(poly.vx.max()), float(poly.vy.max()))
+    for mode in MODES:
+        ixy, idx, n_out = engine.prefilter_bbox(xy, box)
+        inbox = engine.classify(ixy, poly, mode, prefilter=False).verdicts
+        full = engine.scatter_verdicts(idx, inbox, len(xy))
+        assert np.array_equal(full, engine.classify(xy, poly, mode).verdicts)
+        assert n_out == int((full == 1).sum()) - int((inbox == 1).sum())
+    with pytest.raises(Exception):
+        engine.prefilter_bbox(xy, (1.0, 0.0, 0.0, 1.0))  # BBox: min must not exceed max
+    with pytest.raises(Exception):
+        engine.scatter_verdicts(np.array([0, 7], np.uint64), np.zeros(2, np.uint8), 5)  # index out of range
+    with pytest.raises(Exception):
+        engine.scatter_verdicts(np.arange(6, dtype=np.uint64), np.zeros(6, np.uint8), 5)  # more verdicts than total
+    assert np.array_equal(engine.scatter_verdicts(np.zeros(0, np.uint64), np.zeros(0, np.uint8), 4), np.ones(4))
