@@ -50,7 +50,7 @@ __device__ __forceinline__ double dkey_inv(unsigned long long k) {
 // both halves exactly (the low half's carry only reaches bit 0 of the high
 // half, which the compare ignores) and a 3-input packed VIMNMX3.U16x2 folds
 // four points into a running minimum.
-// q(y) = clamp(floor((c(y) - y0) * scale), 0, 32767) with
+// q(y) = clamp(floor((c(y) - y0) * scale), 0, 32766) with
 // c(y) = 0 for |y| < 2^-480, else y.  Every step (collapse, RN subtract, RN
 // multiply by scale >= 0, clamp, floor) is monotone non-decreasing, so as for
 // fkey: q(u) < q(v) => u < v.  The collapse keeps the product-underflow cases
@@ -69,7 +69,7 @@ __device__ __forceinline__ QMap qmap_from_bbox(const unsigned long long* bbox_ke
     const double lo = q_collapse(dkey_inv(bbox_keys[1])), hi = q_collapse(dkey_inv(~bbox_keys[3]));
     const double h = __dsub_rn(hi, lo);
     m.y0 = lo;
-    m.scale = (h > 0.0 && h < 1e300) ? __ddiv_rn(32767.0, h) : 0.0; // degenerate: all keys equal
+    m.scale = (h > 0.0 && h < 1e300) ? __ddiv_rn(32766.0, h) : 0.0; // degenerate: all keys equal
     if (!(lo == lo)) m.y0 = 0.0;                                     // empty outer ring
     return m;
 }
@@ -77,7 +77,7 @@ __device__ __forceinline__ QMap qmap_from_bbox(const unsigned long long* bbox_ke
 __device__ __forceinline__ uint32_t qkey15(double y, const QMap& m) {
     double t = __dmul_rn(__dsub_rn(q_collapse(y), m.y0), m.scale);
     t = t > 0.0 ? t : 0.0; // also maps a NaN product (0 * inf cannot occur: scale < inf) to 0
-    t = t < 32767.0 ? t : 32767.0;
+    t = t < 32766.0 ? t : 32766.0; // 32767 stays free: inactive points' key, never a candidate
     return (uint32_t)t;
 }
 

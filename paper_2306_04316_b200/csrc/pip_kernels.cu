@@ -123,7 +123,10 @@ __global__ void __launch_bounds__(256) prep_edges_kernel(
             }
             const uint32_t klo = qkey15(ylo, qm), khi = qkey15(yhi, qm);
             const uint32_t neg = ((0x8000u - klo) & 0x7fffu) << 1; // -q(ylo) mod 2^15, guard bit clear
-            filt[e] = make_uint2(neg | (neg << 16), ((khi - klo) << 1) | 1u);
+            // threshold + 1 in both halves: candidate iff min(d_lo, d_hi) < ((khi - klo) << 1) + 2
+            // (<= 65534 since keys are <= 32766), see lane_candidate (pip_single.cu)
+            const uint32_t thr1 = ((khi - klo) << 1) + 2u;
+            filt[e] = make_uint2(neg | (neg << 16), thr1 | (thr1 << 16));
         }
         rec[e] = er;
     }

@@ -123,14 +123,17 @@ __device__ __forceinline__ bool lane_candidate(const Keys<MODE>& K, uint2 f) {
         for (int k = 0; k < kK; ++k) c |= (K.ka[k] >= (int)f.x) & (K.kb[k] <= (int)f.y);
         return c;
     } else {
+        static_assert(kK / 2 >= 4 && (kK / 2) % 2 == 0, "fold below assumes an even number of key registers");
         uint32_t d[kK / 2];
 #pragma unroll
         for (int i = 0; i < kK / 2; ++i) d[i] = K.k2[i] + f.x;
         uint32_t m = __vimin3_u16x2(d[0], d[1], d[2]);
 #pragma unroll
         for (int i = 3; i + 1 < kK / 2; i += 2) m = __vimin3_u16x2(m, d[i], d[i + 1]);
-        if ((kK / 2) % 2 == 0) m = __vminu2(m, d[kK / 2 - 1]);
-        return min(m & 0xffffu, m >> 16) <= f.y;
+        // f.y = (threshold + 1) in both halves: the fold's last input, so the
+        // result differs from f.y iff some half of some d is below it
+        m = __vimin3_u16x2(m, d[kK / 2 - 1], f.y);
+        return m != f.y;
     }
 }
 
@@ -141,7 +144,7 @@ __device__ __forceinline__ bool lane_candidate(const Keys<MODE>& K, uint2 f) {
 __device__ __forceinline__ void slow_c1(const double2* my_pts, const Keys<kC1>& K, uint32_t act, uint2 f,
                                         const EdgeRec& r, uint32_t& par, uint32_t wkey_lo, uint32_t wkey_hi) {
     const double ax = r.d[0], ay = r.d[1], nx = r.d[3], ny = r.d[4];
-    const uint32_t rng = f.y >> 1;
+    const uint32_t rng = ((f.y & 0xffffu) - 2u) >> 1;
     const uint32_t klo = (0x8000u - ((f.x & 0xffffu) >> 1)) & 0x7fffu;
     if (klo < wkey_lo && wkey_hi < klo + rng) {
         // every active point of the warp is strictly inside the edge's key range:
@@ -197,7 +200,7 @@ __device__ __forceinline__ void slow_generic(const double2* my_pts, const Keys<M
         if constexpr (MODE == kRobust) {
             c = (K.ka[k] >= (int)f.x) & (K.kb[k] <= (int)f.y);
         } else {
-            const uint32_t d = K.diff(k, f.x), rng = f.y >> 1;
+            const uint32_t d = K.diff(k, f.x), rng = ((f.y & 0xffffu) - 2u) >> 1;
             c = d <= rng && (act >> k & 1u);
             sure = d != 0u && d != rng; // key order strict on both sides
         }
@@ -312,9 +315,14 @@ __global__ void __launch_bounds__(kTPB, 2) pip_tile_kernel(const double2* __rest
             for (uint32_t e0 = 0; e0 < nt; e0 += 4) {
                 // filter 4 edges back to back (independent chains), then one
                 // warp-wide OR says which of them need the slow path
+                bool c[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) c[u] = lane_candidate<MODE>(K, T.filt[e0 + u]);
+                // common case: no candidate in the warp for any of the 4 edges
+                if (!__any_sync(0xffffffffu, c[0] | c[1] | c[2] | c[3])) continue;
                 uint32_t bits = 0;
 #pragma unroll
-                for (int u = 0; u < 4; ++u) bits |= (uint32_t)lane_candidate<MODE>(K, T.filt[e0 + u]) << u;
+                for (int u = 0; u < 4; ++u) bits |= (uint32_t)c[u] << u;
                 uint32_t todo = __reduce_or_sync(0xffffffffu, bits);
                 if (nt - e0 < 4) todo &= (1u << (nt - e0)) - 1u; // stale tail entries
                 while (todo) {

@@ -80,7 +80,19 @@ __global__ void __launch_bounds__(128) bucket_colscan_kernel(uint32_t* __restric
     const int bin = blockIdx.x * blockDim.x + threadIdx.x;
     if (bin > kBuckets) return;
     uint32_t run = 0;
-    for (int b = 0; b < n_blk; ++b) {
+    // eight rows per step: the loads are independent, so their latencies overlap
+    int b = 0;
+    for (; b + 8 <= n_blk; b += 8) {
+        uint32_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = blk[(uint64_t)(b + u) * (kBuckets + 1) + bin];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            blk[(uint64_t)(b + u) * (kBuckets + 1) + bin] = run;
+            run += v[u];
+        }
+    }
+    for (; b < n_blk; ++b) {
         uint32_t* p = blk + (uint64_t)b * (kBuckets + 1) + bin;
         const uint32_t v = *p;
         *p = run;
