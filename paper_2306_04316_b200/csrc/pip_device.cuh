@@ -81,6 +81,47 @@ __device__ __forceinline__ uint32_t qkey15(double y, const QMap& m) {
     return (uint32_t)t;
 }
 
+// Polygon-local scaling of the C1 certified fp32 side test:
+// local coordinate L = RN(v - o) * s with o = the outer ring's bbox min and s a
+// power of two with W*s, H*s in [1/2, 1); valid when 2^-300 <= W, H <= 2^300
+// (sx = sy = 0 otherwise).  A point inside the bbox and an edge with both
+// endpoints inside get |s_fp32 - S'| <= 13.1 * 2^-24 against the reference's
+// side scaled by sx*sy, so |s| > kLocalBand = 2^-20 decides its sign.
+struct LocalMap {
+    double x0, y0, sx, sy;
+};
+constexpr float kLocalBand = 0x1p-20f;
+
+__device__ __forceinline__ double pow2_inv_above(double w) { // 2^-(E+1) for w in [2^E, 2^(E+1))
+    const int e = (__double2hiint(w) >> 20) & 0x7ff;
+    return __hiloint2double((2045 - e) << 20, 0);
+}
+
+__device__ __forceinline__ LocalMap local_map_from_bbox(const unsigned long long* bbox_keys) {
+    LocalMap m;
+    m.x0 = dkey_inv(bbox_keys[0]);
+    m.y0 = dkey_inv(bbox_keys[1]);
+    const double W = __dsub_rn(dkey_inv(~bbox_keys[2]), m.x0), H = __dsub_rn(dkey_inv(~bbox_keys[3]), m.y0);
+    const bool ok = W >= 0x1p-300 && W <= 0x1p300 && H >= 0x1p-300 && H <= 0x1p300;
+    m.sx = ok ? pow2_inv_above(W) : 0.0;
+    m.sy = ok ? pow2_inv_above(H) : 0.0;
+    return m;
+}
+
+// {Nx, Ny, c} of edge a->b with the reference's flipped normal (nx, ny); NaN
+// when the map is off or an endpoint lies outside the bbox (a hole poking out)
+__device__ __forceinline__ float3 local_side_record(const LocalMap& m, double ax, double ay, double bx, double by,
+                                                    double nx, double ny) {
+    const double axl = __dmul_rn(__dsub_rn(ax, m.x0), m.sx), ayl = __dmul_rn(__dsub_rn(ay, m.y0), m.sy);
+    const double bxl = __dmul_rn(__dsub_rn(bx, m.x0), m.sx), byl = __dmul_rn(__dsub_rn(by, m.y0), m.sy);
+    const bool ok = m.sx != 0.0 && axl >= 0.0 && axl < 1.0 && ayl >= 0.0 && ayl < 1.0 && bxl >= 0.0 && bxl < 1.0 &&
+                    byl >= 0.0 && byl < 1.0;
+    if (!ok) return make_float3(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
+    const double Nx = __dmul_rn(nx, m.sy), Ny = __dmul_rn(ny, m.sx);
+    const double cd = __dadd_rn(__dmul_rn(axl, Nx), __dmul_rn(ayl, Ny));
+    return make_float3(__double2float_rn(Nx), __double2float_rn(Ny), __double2float_rn(-cd));
+}
+
 // C1 exact test of one straddle candidate (geometry.hpp:189-200).  `sure`:
 // the keys already prove min(a.y,b.y) < p.y < max(a.y,b.y) strictly, so the
 // reference's product f_prev*f_next is negative (or -0) and `<= 0.0` holds;

@@ -83,9 +83,12 @@ __global__ void __launch_bounds__(256) prep_edges_kernel(
     const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const QMap qm = qmap_from_bbox(bbox_keys);
-    if (tid == 0) { // published for the classify kernels (bbox_keys[4..5])
+    const LocalMap lm = local_map_from_bbox(bbox_keys);
+    if (tid == 0) { // published for the classify kernels (bbox_keys[4..7])
         reinterpret_cast<double*>(bbox_keys)[4] = qm.y0;
         reinterpret_cast<double*>(bbox_keys)[5] = qm.scale;
+        reinterpret_cast<double*>(bbox_keys)[6] = lm.sx;
+        reinterpret_cast<double*>(bbox_keys)[7] = lm.sy;
     }
     for (uint64_t v = tid; v < n_verts; v += stride) {
         const uint32_t r = ring_of(ring_off, n_rings, v);
@@ -117,6 +120,11 @@ __global__ void __launch_bounds__(256) prep_edges_kernel(
                 }
                 er.d[3] = nx;
                 er.d[4] = ny;
+                // fp32 side-test record (d[5] = {Nx, Ny}, d[6] = {c, 0}): see
+                // LocalMap; NaN when unusable (every test then goes exact)
+                const float3 fr = local_side_record(lm, ax, ay, bx, by, nx, ny);
+                er.d[5] = __hiloint2double(__float_as_int(fr.y), __float_as_int(fr.x));
+                er.d[6] = __hiloint2double(0, __float_as_int(fr.z));
             } else {
                 er.d[3] = __dsub_rn(bx, ax);
                 er.d[4] = __dsub_rn(by, ay);

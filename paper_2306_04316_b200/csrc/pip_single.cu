@@ -31,6 +31,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <type_traits>
 
 #include "pip_device.cuh"
 
@@ -47,8 +48,13 @@ struct __align__(128) TileStage {
     uint2 filt[kTile];
 };
 
+// C1 keeps only the polygon-local fp32 coordinates of its points in shared
+// memory (the fp32 side test; the rare exact fallbacks re-read the binary64
+// point from global memory / L2); C2 and Robust keep the binary64 points.
+template <int MODE>
 struct SingleShared {
-    double2 pts[kTPB * kK]; // this CTA's points (bucketed order), one TMA bulk copy
+    using PointT = std::conditional_t<MODE == kC1, float2, double2>;
+    PointT pts[kTPB * kK]; // this CTA's points (bucketed order)
     TileStage st[2];
     unsigned long long full[2];
     unsigned long long pbar;
@@ -74,7 +80,8 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
 }
 
 // One elected thread: load tile [t0, t0+nt) of the edge arrays into stage s.
-__device__ __forceinline__ void issue_tile(SingleShared& sh, int s, const uint2* filt, const EdgeRec* rec,
+template <class Shared>
+__device__ __forceinline__ void issue_tile(Shared& sh, int s, const uint2* filt, const EdgeRec* rec,
                                            uint32_t t0, uint32_t nt) {
     const unsigned fb = ((nt + 1) & ~1u) * 8u; // filt padded to an even count (16-byte multiple)
     const unsigned rb = nt * (unsigned)sizeof(EdgeRec);
@@ -137,53 +144,64 @@ __device__ __forceinline__ bool lane_candidate(const Keys<MODE>& K, uint2 f) {
     }
 }
 
-// C1 slow path (geometry.hpp:189-200), branch-free over the 16 points: the
-// side test runs for every point with full ILP and counts only for
-// candidates.  Key ties (d == 0 or d == range), where the keys cannot decide
-// the straddle, take the reference product in a rare warp-uniform branch.
-__device__ __forceinline__ void slow_c1(const double2* my_pts, const Keys<kC1>& K, uint32_t act, uint2 f,
-                                        const EdgeRec& r, uint32_t& par, uint32_t wkey_lo, uint32_t wkey_hi) {
-    const double ax = r.d[0], ay = r.d[1], nx = r.d[3], ny = r.d[4];
+// C1 slow path (geometry.hpp:189-200) for one candidate edge, branch-free
+// over the 16 points.  Straddle: if the warp's whole key range lies strictly
+// inside the edge's, every active point straddles for sure; otherwise per-point
+// candidate / tie masks, ties evaluating the reference product.  Side: the
+// certified fp32 test on the polygon-local coordinates (LocalMap, DESIGN.md
+// §3.4) -- two FFMAs per point; a point within the band (or without local
+// coordinates) re-reads its binary64 coordinates and runs the reference's
+// expression.
+__device__ __forceinline__ void slow_c1(const float2* my_l, const double2* __restrict__ my_g, const Keys<kC1>& K,
+                                        uint32_t act, uint2 f, const EdgeRec& r, uint32_t& par, uint32_t wkey_lo,
+                                        uint32_t wkey_hi) {
+    const double ax = r.d[0], ay = r.d[1];
     const uint32_t rng = ((f.y & 0xffffu) - 2u) >> 1;
     const uint32_t klo = (0x8000u - ((f.x & 0xffffu) >> 1)) & 0x7fffu;
-    if (klo < wkey_lo && wkey_hi < klo + rng) {
-        // every active point of the warp is strictly inside the edge's key range:
-        // all straddle for sure (no ties), only the side test remains
-        uint32_t hit = 0;
+    uint32_t cm = act;
+    if (!(klo < wkey_lo && wkey_hi < klo + rng)) {
+        uint32_t tm = 0;
+        cm = 0;
 #pragma unroll
         for (int k = 0; k < kK; ++k) {
-            const double2 p = my_pts[k * 32];
-            const double side = __dadd_rn(__dmul_rn(__dsub_rn(p.x, ax), nx), __dmul_rn(__dsub_rn(p.y, ay), ny));
-            hit |= (uint32_t)(side <= 0.0) << k;
+            const uint32_t d = K.diff(k, f.x);
+            cm |= (uint32_t)(d <= rng) << k;
+            tm |= (uint32_t)(d == 0u || d == rng) << k;
         }
-        par ^= hit & act;
-        return;
-    }
-    uint32_t cm = 0, tm = 0;
-#pragma unroll
-    for (int k = 0; k < kK; ++k) {
-        const uint32_t d = K.diff(k, f.x);
-        cm |= (uint32_t)(d <= rng) << k;
-        tm |= (uint32_t)(d == 0u || d == rng) << k;
-    }
-    cm &= act;
-    tm &= cm;
-    if (__any_sync(0xffffffffu, tm != 0)) {
-        const double by = r.d[2];
+        cm &= act;
+        tm &= cm;
+        if (__any_sync(0xffffffffu, tm != 0)) {
+            const double by = r.d[2];
 #pragma unroll 1
-        for (int k = 0; k < kK; ++k) {
-            if (tm >> k & 1u) {
-                const double py = my_pts[k * 32].y;
-                if (!(__dmul_rn(__dsub_rn(ay, py), __dsub_rn(by, py)) <= 0.0)) cm &= ~(1u << k);
+            for (int k = 0; k < kK; ++k) {
+                if (tm >> k & 1u) {
+                    const double py = my_g[k * 32].y;
+                    if (!(__dmul_rn(__dsub_rn(ay, py), __dsub_rn(by, py)) <= 0.0)) cm &= ~(1u << k);
+                }
             }
         }
     }
-    uint32_t hit = 0;
+    const float nxf = __int_as_float(__double2loint(r.d[5])), nyf = __int_as_float(__double2hiint(r.d[5]));
+    const float cf = __int_as_float(__double2loint(r.d[6]));
+    uint32_t hit = 0, und = 0;
 #pragma unroll
     for (int k = 0; k < kK; ++k) {
-        const double2 p = my_pts[k * 32];
-        const double side = __dadd_rn(__dmul_rn(__dsub_rn(p.x, ax), nx), __dmul_rn(__dsub_rn(p.y, ay), ny));
-        hit |= (uint32_t)(side <= 0.0) << k;
+        const float2 l = my_l[k * 32];
+        const float sk = fmaf(l.x, nxf, fmaf(l.y, nyf, cf));
+        hit |= (uint32_t)(sk < -kLocalBand) << k;
+        und |= (uint32_t)!(fabsf(sk) > kLocalBand) << k; // band hit, or NaN (no local coordinates)
+    }
+    und &= cm;
+    if (__any_sync(0xffffffffu, und != 0)) {
+        const double nx = r.d[3], ny = r.d[4];
+#pragma unroll 1
+        for (int k = 0; k < kK; ++k) {
+            if (und >> k & 1u) {
+                const double2 p = my_g[k * 32];
+                const double side = __dadd_rn(__dmul_rn(__dsub_rn(p.x, ax), nx), __dmul_rn(__dsub_rn(p.y, ay), ny));
+                hit = (hit & ~(1u << k)) | ((uint32_t)(side <= 0.0) << k);
+            }
+        }
     }
     par ^= hit & cm;
 }
@@ -218,7 +236,7 @@ __device__ __forceinline__ void slow_generic(const double2* my_pts, const Keys<M
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kTPB, 2) pip_tile_kernel(const double2* __restrict__ pts, uint64_t n,
+__global__ void __launch_bounds__(kTPB, MODE == kC1 ? 3 : 2) pip_tile_kernel(const double2* __restrict__ pts, uint64_t n,
                                                         const uint2* __restrict__ filt,
                                                         const EdgeRec* __restrict__ rec, uint32_t n_edges,
                                                         uint32_t edges_per_chunk,
@@ -228,7 +246,7 @@ __global__ void __launch_bounds__(kTPB, 2) pip_tile_kernel(const double2* __rest
                                                         uint32_t* __restrict__ aux_bits,
                                                         const uint32_t* __restrict__ n_dev) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    SingleShared& sh = *reinterpret_cast<SingleShared*>(smem_raw);
+    SingleShared<MODE>& sh = *reinterpret_cast<SingleShared<MODE>*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (n_dev) n = min(n, (uint64_t)*n_dev); // bucketed input: only the in-box prefix is live
     const uint64_t cta_base = (uint64_t)blockIdx.x * (kTPB * kK);
@@ -247,12 +265,15 @@ __global__ void __launch_bounds__(kTPB, 2) pip_tile_kernel(const double2* __rest
     __syncthreads();
     const uint32_t n_tiles = (e_end - e_begin + kTile - 1) / kTile;
     if (tid == 0) {
-        const unsigned pb = cta_n * 16u, bar = smem_u32(&sh.pbar);
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(pb) : "memory");
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                         smem_u32(sh.pts)),
-                     "l"(pts + cta_base), "r"(pb), "r"(bar)
-                     : "memory");
+        if constexpr (MODE != kC1) { // C1 reads its points directly (they become fp32 local coordinates)
+            const unsigned pb = cta_n * 16u, bar = smem_u32(&sh.pbar);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(pb) : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_u32(sh.pts)),
+                "l"(pts + cta_base), "r"(pb), "r"(bar)
+                : "memory");
+        }
         for (uint32_t q = 0; q < 2 && q < n_tiles; ++q)
             issue_tile(sh, (int)q, filt, rec, e_begin + q * kTile, min((uint32_t)kTile, e_end - e_begin - q * kTile));
     }
@@ -266,7 +287,14 @@ __global__ void __launch_bounds__(kTPB, 2) pip_tile_kernel(const double2* __rest
         maxy = dkey_inv(~bbox_keys[3]);
     }
     const uint32_t wloc = (uint32_t)warp * 32 * kK; // this warp's first point within the CTA
-    mbar_wait(&sh.pbar, 0);
+    if constexpr (MODE != kC1) mbar_wait(&sh.pbar, 0);
+    LocalMap lm{};
+    if constexpr (MODE == kC1) {
+        lm.x0 = dkey_inv(bbox_keys[0]);
+        lm.y0 = dkey_inv(bbox_keys[1]);
+        lm.sx = reinterpret_cast<const double*>(bbox_keys)[6];
+        lm.sy = reinterpret_cast<const double*>(bbox_keys)[7];
+    }
     Keys<MODE> K;
     uint32_t act = 0;
     const QMap qm = {reinterpret_cast<const double*>(bbox_keys)[4], reinterpret_cast<const double*>(bbox_keys)[5]};
@@ -275,8 +303,20 @@ __global__ void __launch_bounds__(kTPB, 2) pip_tile_kernel(const double2* __rest
         const uint32_t li = wloc + k * 32 + lane;
         bool a = li < cta_n;
         double2 p = make_double2(0.0, 0.0);
-        if (a) p = sh.pts[li];
+        if constexpr (MODE == kC1) {
+            if (a) p = pts[cta_base + li];
+            if ((k & 3) == 3) asm volatile("" ::: "memory"); // at most 4 point loads in flight (registers)
+        } else {
+            if (a) p = sh.pts[li];
+        }
         if (a && prefilter) a = p.x >= minx && p.x <= maxx && p.y >= miny && p.y <= maxy; // batch.hpp:39-41
+        if constexpr (MODE == kC1) {
+            // polygon-local fp32 coordinates; NaN outside the bbox / without a map (-> exact side test)
+            const double lxd = __dmul_rn(__dsub_rn(p.x, lm.x0), lm.sx), lyd = __dmul_rn(__dsub_rn(p.y, lm.y0), lm.sy);
+            const bool ok = lm.sx != 0.0 && lxd >= 0.0 && lxd < 1.0 && lyd >= 0.0 && lyd < 1.0;
+            const float nan = __int_as_float(0x7fc00000);
+            sh.pts[li] = ok ? make_float2(__double2float_rn(lxd), __double2float_rn(lyd)) : make_float2(nan, nan);
+        }
         if constexpr (MODE == kRobust) {
             K.ka[k] = a ? fkey(__dadd_rn(p.y, tol)) : INT_MIN;
             K.kb[k] = a ? fkey(__dsub_rn(p.y, tol)) : INT_MAX;
@@ -331,7 +371,8 @@ __global__ void __launch_bounds__(kTPB, 2) pip_tile_kernel(const double2* __rest
                     const uint2 f = T.filt[e];
                     // ---- slow path: exact binary64 test for the candidate points ----
                     if constexpr (MODE == kC1)
-                        slow_c1(sh.pts + wloc + lane, K, act, f, T.rec[e], par, wkey_lo, wkey_hi);
+                        slow_c1(sh.pts + wloc + lane, pts + cta_base + wloc + lane, K, act, f, T.rec[e], par, wkey_lo,
+                                wkey_hi);
                     else
                         slow_generic<MODE>(sh.pts + wloc + lane, K, act, f, T.rec[e], tol, tol2, par, auxm);
                 }
@@ -363,7 +404,7 @@ int sms(int dev) {
 
 template <int MODE>
 cudaError_t launch_t(const SingleArgs& a, cudaStream_t st, int dev, uint64_t* launches) {
-    const size_t smem = sizeof(SingleShared);
+    const size_t smem = sizeof(SingleShared<MODE>);
     static bool attr[64] = {};
     if (dev < 64 && !attr[dev]) {
         cudaFuncSetAttribute(pip_tile_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
