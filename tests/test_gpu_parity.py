@@ -488,3 +488,24 @@ def test_scatter_verdicts_and_cli_pipeline(engine):
     with pytest.raises(Exception):
         engine.scatter_verdicts(np.arange(6, dtype=np.uint64), np.zeros(6, np.uint8), 5)  # more verdicts than total
     assert np.array_equal(engine.scatter_verdicts(np.zeros(0, np.uint64), np.zeros(0, np.uint8), 4), np.ones(4))
+
+
+def test_single_fast_side_band(engine):
+    """Single-polygon C1 slow path (certified fp32 side test, LocalMap): points on,
+    inside, at and just outside the band of every edge of a star polygon and of a
+    lon/lat footprint-like polygon, with and without the bbox prefilter, bucketed
+    and not."""
+    deltas = (1e-16, 1e-12, 1e-9, 2e-7, 4e-7, 1e-6, 3e-6, 1e-4)
+    ring = [(5.0 + 0.0004 * np.cos(t), 0.5 + 0.0003 * np.sin(t)) for t in np.linspace(0, 2 * np.pi, 41)[:-1]]
+    polys = [W.star_polygon(300, seed=12), Polygon.from_rings([ring + [ring[0]]])]
+    for poly in polys:
+        s = _near_edge_points(_single_as_csr(poly, np.zeros((1, 2))), deltas)
+        xy = s.xy
+        for bucket in (0, 1):
+            engine.set_bucketing(bucket)
+            try:
+                for mode in MODES:
+                    check_single(xy, poly, mode, engine.classify(xy, poly, mode))
+                    check_single(xy, poly, mode, engine.classify(xy, poly, mode, prefilter=False), prefilter=False)
+            finally:
+                engine.set_bucketing(-1)
