@@ -73,12 +73,13 @@ __global__ void __launch_bounds__(256) prep_bbox_kernel(const double* __restrict
 
 // One thread per vertex v: if (v, v+1) is an edge of the same ring, write its
 // filter pair and exact record at edge index e = v - ring(v).
-//   C1/C2 filter: {(-q(ylo) mod 2^15) << 1 in both 16-bit halves, (q(yhi) - q(ylo)) << 1 | 1} (15-bit keys)
-//   Robust filter: {fkey(ylo), fkey(yhi)} (32-bit keys)
+//   C1/C2 filter: {(-q(ylo) mod 2^15) << 1 in both 16-bit halves,
+//                  ((q(yhi) - q(ylo)) << 1) + 2 in both halves, q(ylo), q(yhi)} (15-bit keys)
+//   Robust filter: {fkey(ylo), fkey(yhi), 0, 0} (32-bit keys)
 template <int MODE>
 __global__ void __launch_bounds__(256) prep_edges_kernel(
     const double* __restrict__ vx, const double* __restrict__ vy, const uint64_t* __restrict__ ring_off,
-    uint32_t n_rings, uint64_t n_verts, uint2* __restrict__ filt, EdgeRec* __restrict__ rec,
+    uint32_t n_rings, uint64_t n_verts, uint4* __restrict__ filt, EdgeRec* __restrict__ rec,
     unsigned long long* __restrict__ bbox_keys) {
     const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -110,7 +111,7 @@ __global__ void __launch_bounds__(256) prep_edges_kernel(
             er.d[5] = __dadd_rn(__dmul_rn(abx, abx), __dmul_rn(aby, aby));
             er.d[6] = ylo;
             er.d[7] = yhi;
-            filt[e] = make_uint2((uint32_t)fkey(ylo), (uint32_t)fkey(yhi));
+            filt[e] = make_uint4((uint32_t)fkey(ylo), (uint32_t)fkey(yhi), 0u, 0u);
         } else {
             if (MODE == kC1) {
                 double nx = __dsub_rn(by, ay), ny = __dsub_rn(ax, bx);
@@ -134,7 +135,7 @@ __global__ void __launch_bounds__(256) prep_edges_kernel(
             // threshold + 1 in both halves: candidate iff min(d_lo, d_hi) < ((khi - klo) << 1) + 2
             // (<= 65534 since keys are <= 32766), see lane_candidate (pip_single.cu)
             const uint32_t thr1 = ((khi - klo) << 1) + 2u;
-            filt[e] = make_uint2(neg | (neg << 16), thr1 | (thr1 << 16));
+            filt[e] = make_uint4(neg | (neg << 16), thr1 | (thr1 << 16), klo, khi); // .z/.w: warp-level test
         }
         rec[e] = er;
     }

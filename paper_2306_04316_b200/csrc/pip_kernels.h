@@ -15,7 +15,7 @@ struct PrepArgs {
     const uint64_t* ring_off;
     uint32_t n_rings;
     uint64_t n_verts;
-    uint2* filt;                  // n_edges filter key pairs
+    uint4* filt;                  // n_edges filter words (see prep_edges_kernel)
     void* rec;                    // n_edges EdgeRec (edge_rec_bytes() each)
     unsigned long long* bbox_keys; // 4 monotone keys: min x, min y, ~max x, ~max y; [4..5] 16-bit key map
     uint32_t* zero_words;          // output bit planes to clear (inside ++ aux, contiguous)
@@ -27,7 +27,7 @@ struct SingleArgs {
     int mode;
     const double* pts;
     uint64_t n;
-    const uint2* filt;
+    const uint4* filt;
     const void* rec;
     uint32_t n_edges;
     const unsigned long long* bbox_keys;

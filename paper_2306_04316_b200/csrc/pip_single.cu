@@ -45,7 +45,7 @@ constexpr int kTile = 256;  // edges per shared-memory stage (multiple of 2: 16-
 
 struct __align__(128) TileStage {
     EdgeRec rec[kTile];
-    uint2 filt[kTile];
+    uint4 filt[kTile];
 };
 
 // C1 keeps only the polygon-local fp32 coordinates of its points in shared
@@ -81,9 +81,9 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
 
 // One elected thread: load tile [t0, t0+nt) of the edge arrays into stage s.
 template <class Shared>
-__device__ __forceinline__ void issue_tile(Shared& sh, int s, const uint2* filt, const EdgeRec* rec,
+__device__ __forceinline__ void issue_tile(Shared& sh, int s, const uint4* filt, const EdgeRec* rec,
                                            uint32_t t0, uint32_t nt) {
-    const unsigned fb = ((nt + 1) & ~1u) * 8u; // filt padded to an even count (16-byte multiple)
+    const unsigned fb = nt * 16u;
     const unsigned rb = nt * (unsigned)sizeof(EdgeRec);
     const unsigned bar = smem_u32(&sh.full[s]);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(fb + rb) : "memory");
@@ -237,7 +237,7 @@ __device__ __forceinline__ void slow_generic(const double2* my_pts, const Keys<M
 
 template <int MODE>
 __global__ void __launch_bounds__(kTPB, MODE == kC1 ? 3 : 2) pip_tile_kernel(const double2* __restrict__ pts, uint64_t n,
-                                                        const uint2* __restrict__ filt,
+                                                        const uint4* __restrict__ filt,
                                                         const EdgeRec* __restrict__ rec, uint32_t n_edges,
                                                         uint32_t edges_per_chunk,
                                                         const unsigned long long* __restrict__ bbox_keys,
@@ -343,6 +343,27 @@ __global__ void __launch_bounds__(kTPB, MODE == kC1 ? 3 : 2) pip_tile_kernel(con
         wkey_lo = __reduce_min_sync(0xffffffffu, lo);
         wkey_hi = __reduce_max_sync(0xffffffffu, hi);
     }
+    // warp-level interval test (Robust): some point may straddle only if
+    // max key(p.y + tol) >= key(ylo) and min key(p.y - tol) <= key(yhi)
+    int wka_max = INT_MIN, wkb_min = INT_MAX;
+    if constexpr (MODE == kRobust) {
+        int hi = INT_MIN, lo = INT_MAX;
+#pragma unroll
+        for (int k = 0; k < kK; ++k) {
+            if (act >> k & 1u) {
+                hi = max(hi, K.ka[k]);
+                lo = min(lo, K.kb[k]);
+            }
+        }
+        wka_max = __reduce_max_sync(0xffffffffu, hi);
+        wkb_min = __reduce_min_sync(0xffffffffu, lo);
+    }
+    // may any active point of the warp straddle edge f?  (exact: the keys are
+    // monotone; the per-point filter and the slow path then decide per point)
+    auto warp_may = [&](const uint4& f) {
+        if constexpr (MODE == kRobust) return (int)f.x <= wka_max && (int)f.y >= wkb_min;
+        else return f.z <= wkey_hi && f.w >= wkey_lo;
+    };
 
     uint32_t par = 0, auxm = 0;
     for (uint32_t q = 0; q < n_tiles; ++q) {
@@ -353,11 +374,17 @@ __global__ void __launch_bounds__(kTPB, MODE == kC1 ? 3 : 2) pip_tile_kernel(con
         const TileStage& T = sh.st[s];
         if (warp_live) {
             for (uint32_t e0 = 0; e0 < nt; e0 += 4) {
-                // filter 4 edges back to back (independent chains), then one
-                // warp-wide OR says which of them need the slow path
+                // warp-level interval test of 4 edges (warp-uniform: the key
+                // ranges of the warp's points against each edge's key range)
+                const uint4 f0 = T.filt[e0], f1 = T.filt[e0 + 1], f2 = T.filt[e0 + 2], f3 = T.filt[e0 + 3];
+                if (!(warp_may(f0) || warp_may(f1) || warp_may(f2) || warp_may(f3))) continue;
+                // per-point filter of the 4 edges, then one warp-wide OR says
+                // which of them need the slow path
                 bool c[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) c[u] = lane_candidate<MODE>(K, T.filt[e0 + u]);
+                c[0] = lane_candidate<MODE>(K, make_uint2(f0.x, f0.y));
+                c[1] = lane_candidate<MODE>(K, make_uint2(f1.x, f1.y));
+                c[2] = lane_candidate<MODE>(K, make_uint2(f2.x, f2.y));
+                c[3] = lane_candidate<MODE>(K, make_uint2(f3.x, f3.y));
                 // common case: no candidate in the warp for any of the 4 edges
                 if (!__any_sync(0xffffffffu, c[0] | c[1] | c[2] | c[3])) continue;
                 uint32_t bits = 0;
@@ -368,7 +395,7 @@ __global__ void __launch_bounds__(kTPB, MODE == kC1 ? 3 : 2) pip_tile_kernel(con
                 while (todo) {
                     const uint32_t e = e0 + (__ffs(todo) - 1);
                     todo &= todo - 1;
-                    const uint2 f = T.filt[e];
+                    const uint2 f = make_uint2(T.filt[e].x, T.filt[e].y);
                     // ---- slow path: exact binary64 test for the candidate points ----
                     if constexpr (MODE == kC1)
                         slow_c1(sh.pts + wloc + lane, pts + cta_base + wloc + lane, K, act, f, T.rec[e], par, wkey_lo,
