@@ -119,7 +119,11 @@ __device__ __forceinline__ float3 local_side_record(const LocalMap& m, double ax
     if (!ok) return make_float3(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
     const double Nx = __dmul_rn(nx, m.sy), Ny = __dmul_rn(ny, m.sx);
     const double cd = __dadd_rn(__dmul_rn(axl, Nx), __dmul_rn(ayl, Ny));
-    return make_float3(__double2float_rn(Nx), __double2float_rn(Ny), __double2float_rn(-cd));
+    // c + kLocalBand: the kernel's s' = s + B is then <= -0 (sign bit) for a sure
+    // count and in [+0, 2B] for a band hit; the extra fp32 rounding of c + B
+    // (<= 2 * 2^-24) keeps the total error at 15.1 * 2^-24 < B
+    return make_float3(__double2float_rn(Nx), __double2float_rn(Ny),
+                       __double2float_rn(__dadd_rn(-cd, (double)kLocalBand)));
 }
 
 // C1 exact test of one straddle candidate (geometry.hpp:189-200).  `sure`:

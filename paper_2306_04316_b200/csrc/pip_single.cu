@@ -153,8 +153,8 @@ __device__ __forceinline__ bool lane_candidate(const Keys<MODE>& K, uint2 f) {
 // coordinates) re-reads its binary64 coordinates and runs the reference's
 // expression.
 __device__ __forceinline__ void slow_c1(const float2* my_l, const double2* __restrict__ my_g, const Keys<kC1>& K,
-                                        uint32_t act, uint2 f, const EdgeRec& r, uint32_t& par, uint32_t wkey_lo,
-                                        uint32_t wkey_hi) {
+                                        uint32_t act, uint32_t nonloc, uint2 f, const EdgeRec& r, uint32_t& par,
+                                        uint32_t wkey_lo, uint32_t wkey_hi) {
     const double ax = r.d[0], ay = r.d[1];
     const uint32_t rng = ((f.y & 0xffffu) - 2u) >> 1;
     const uint32_t klo = (0x8000u - ((f.x & 0xffffu) >> 1)) & 0x7fffu;
@@ -182,14 +182,27 @@ __device__ __forceinline__ void slow_c1(const float2* my_l, const double2* __res
         }
     }
     const float nxf = __int_as_float(__double2loint(r.d[5])), nyf = __int_as_float(__double2hiint(r.d[5]));
-    const float cf = __int_as_float(__double2loint(r.d[6]));
-    uint32_t hit = 0, und = 0;
+    const float cf = __int_as_float(__double2loint(r.d[6])); // c + B
+    // s' = s + B: counted iff the sign bit is set (s' <= -0); band hit iff
+    // +0 <= s' <= 2B, i.e. its bits (as unsigned) are <= those of 2B
+    constexpr uint32_t k2B = 0x36000000u; // bits of 2^-19 = 2 * kLocalBand
+    uint32_t hit = 0, umin = 0xffffffffu;
 #pragma unroll
-    for (int k = 0; k < kK; ++k) {
+    for (int k = kK - 1; k >= 0; --k) {
         const float2 l = my_l[k * 32];
-        const float sk = fmaf(l.x, nxf, fmaf(l.y, nyf, cf));
-        hit |= (uint32_t)(sk < -kLocalBand) << k;
-        und |= (uint32_t)!(fabsf(sk) > kLocalBand) << k; // band hit, or NaN (no local coordinates)
+        const uint32_t u = __float_as_uint(fmaf(l.x, nxf, fmaf(l.y, nyf, cf)));
+        hit = (hit << 1) | (u >> 31);
+        umin = min(umin, u);
+    }
+    // undecided: band hits (rare: per point only then), points without local
+    // coordinates (nonloc) and edges without a record (NaN: every point)
+    uint32_t und = nonloc | ((nxf == nxf) ? 0u : 0xffffu);
+    if (umin <= k2B) {
+#pragma unroll
+        for (int k = 0; k < kK; ++k) {
+            const float2 l = my_l[k * 32];
+            und |= (uint32_t)(__float_as_uint(fmaf(l.x, nxf, fmaf(l.y, nyf, cf))) <= k2B) << k;
+        }
     }
     und &= cm;
     if (__any_sync(0xffffffffu, und != 0)) {
@@ -296,7 +309,7 @@ __global__ void __launch_bounds__(kTPB, MODE == kC1 ? 3 : 2) pip_tile_kernel(con
         lm.sy = reinterpret_cast<const double*>(bbox_keys)[7];
     }
     Keys<MODE> K;
-    uint32_t act = 0;
+    uint32_t act = 0, nonloc = 0; // nonloc (C1): active points without local fp32 coordinates
     const QMap qm = {reinterpret_cast<const double*>(bbox_keys)[4], reinterpret_cast<const double*>(bbox_keys)[5]};
 #pragma unroll
     for (int k = 0; k < kK; ++k) {
@@ -316,6 +329,7 @@ __global__ void __launch_bounds__(kTPB, MODE == kC1 ? 3 : 2) pip_tile_kernel(con
             const bool ok = lm.sx != 0.0 && lxd >= 0.0 && lxd < 1.0 && lyd >= 0.0 && lyd < 1.0;
             const float nan = __int_as_float(0x7fc00000);
             sh.pts[li] = ok ? make_float2(__double2float_rn(lxd), __double2float_rn(lyd)) : make_float2(nan, nan);
+            nonloc |= (uint32_t)(a && !ok) << k;
         }
         if constexpr (MODE == kRobust) {
             K.ka[k] = a ? fkey(__dadd_rn(p.y, tol)) : INT_MIN;
@@ -398,8 +412,8 @@ __global__ void __launch_bounds__(kTPB, MODE == kC1 ? 3 : 2) pip_tile_kernel(con
                     const uint2 f = make_uint2(T.filt[e].x, T.filt[e].y);
                     // ---- slow path: exact binary64 test for the candidate points ----
                     if constexpr (MODE == kC1)
-                        slow_c1(sh.pts + wloc + lane, pts + cta_base + wloc + lane, K, act, f, T.rec[e], par, wkey_lo,
-                                wkey_hi);
+                        slow_c1(sh.pts + wloc + lane, pts + cta_base + wloc + lane, K, act, nonloc, f, T.rec[e], par,
+                                wkey_lo, wkey_hi);
                     else
                         slow_generic<MODE>(sh.pts + wloc + lane, K, act, f, T.rec[e], tol, tol2, par, auxm);
                 }
