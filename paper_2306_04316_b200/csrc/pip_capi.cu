@@ -131,7 +131,7 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
     const uint64_t n_edges = n_verts - n_rings;
     if (n_edges > 0xffffffffull) invalid(c, "too many edges for one polygon (>= 2^32)");
     const uint64_t nwords = (n + 31) / 32;
-    check(c, d.filt.ensure((n_edges + 2) * sizeof(uint4)), "alloc edge keys");
+    check(c, d.filt.ensure(pcd::filt_words(n_edges) * sizeof(uint2)), "alloc edge keys");
     check(c, d.rec.ensure(std::max<uint64_t>(n_edges, 1) * pcd::edge_rec_bytes()), "alloc edge records");
     check(c, d.bbox.ensure(8 * sizeof(unsigned long long)), "alloc bbox"); // 4 keys + key map
     pcd::PrepArgs pa{};
@@ -141,7 +141,7 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
     pa.ring_off = d_ring_off;
     pa.n_rings = n_rings;
     pa.n_verts = n_verts;
-    pa.filt = d.filt.as<uint4>();
+    pa.filt = d.filt.as<uint2>();
     pa.rec = d.rec.p;
     pa.bbox_keys = d.bbox.as<unsigned long long>();
     pa.stats = d_stats;
@@ -156,7 +156,7 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
     sa.mode = mode;
     sa.pts = d_pts;
     sa.n = n;
-    sa.filt = d.filt.as<uint4>();
+    sa.filt = d.filt.as<uint2>();
     sa.rec = d.rec.p;
     sa.n_edges = (uint32_t)n_edges;
     sa.bbox_keys = d.bbox.as<unsigned long long>();

@@ -73,13 +73,16 @@ __global__ void __launch_bounds__(256) prep_bbox_kernel(const double* __restrict
 
 // One thread per vertex v: if (v, v+1) is an edge of the same ring, write its
 // filter pair and exact record at edge index e = v - ring(v).
-//   C1/C2 filter: {(-q(ylo) mod 2^15) << 1 in both 16-bit halves,
-//                  ((q(yhi) - q(ylo)) << 1) + 2 in both halves, q(ylo), q(yhi)} (15-bit keys)
-//   Robust filter: {fkey(ylo), fkey(yhi), 0, 0} (32-bit keys)
+// The filter array is tile-blocked: for edge tile t (kEdgeTile edges) the
+// block filt[t*2*kEdgeTile ...] holds kEdgeTile key ranges (warp-level test)
+// followed by kEdgeTile per-point filter words, so one bulk copy stages both.
+//   C1/C2: range {q(ylo), q(yhi)}; word {(-q(ylo) mod 2^15) << 1 in both 16-bit
+//          halves, ((q(yhi) - q(ylo)) << 1) + 2 in both halves} (15-bit keys)
+//   Robust: range = word = {fkey(ylo), fkey(yhi)} (32-bit keys)
 template <int MODE>
 __global__ void __launch_bounds__(256) prep_edges_kernel(
     const double* __restrict__ vx, const double* __restrict__ vy, const uint64_t* __restrict__ ring_off,
-    uint32_t n_rings, uint64_t n_verts, uint4* __restrict__ filt, EdgeRec* __restrict__ rec,
+    uint32_t n_rings, uint64_t n_verts, uint2* __restrict__ filt, EdgeRec* __restrict__ rec,
     unsigned long long* __restrict__ bbox_keys) {
     const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -95,6 +98,7 @@ __global__ void __launch_bounds__(256) prep_edges_kernel(
         const uint32_t r = ring_of(ring_off, n_rings, v);
         if (v + 1 >= ring_off[r + 1]) continue; // last (closing) vertex of its ring
         const uint64_t e = v - r;
+        const uint64_t fb = (e / kEdgeTile) * (2 * kEdgeTile) + e % kEdgeTile; // tile-blocked filter index
         const double ax = vx[v], ay = vy[v], bx = vx[v + 1], by = vy[v + 1];
         EdgeRec er;
 #pragma unroll
@@ -111,7 +115,9 @@ __global__ void __launch_bounds__(256) prep_edges_kernel(
             er.d[5] = __dadd_rn(__dmul_rn(abx, abx), __dmul_rn(aby, aby));
             er.d[6] = ylo;
             er.d[7] = yhi;
-            filt[e] = make_uint4((uint32_t)fkey(ylo), (uint32_t)fkey(yhi), 0u, 0u);
+            const uint2 w = make_uint2((uint32_t)fkey(ylo), (uint32_t)fkey(yhi));
+            filt[fb] = w;
+            filt[fb + kEdgeTile] = w;
         } else {
             if (MODE == kC1) {
                 double nx = __dsub_rn(by, ay), ny = __dsub_rn(ax, bx);
@@ -135,7 +141,8 @@ __global__ void __launch_bounds__(256) prep_edges_kernel(
             // threshold + 1 in both halves: candidate iff min(d_lo, d_hi) < ((khi - klo) << 1) + 2
             // (<= 65534 since keys are <= 32766), see lane_candidate (pip_single.cu)
             const uint32_t thr1 = ((khi - klo) << 1) + 2u;
-            filt[e] = make_uint4(neg | (neg << 16), thr1 | (thr1 << 16), klo, khi); // .z/.w: warp-level test
+            filt[fb] = make_uint2(klo, khi);
+            filt[fb + kEdgeTile] = make_uint2(neg | (neg << 16), thr1 | (thr1 << 16));
         }
         rec[e] = er;
     }
@@ -246,6 +253,8 @@ int sm_count(int dev) {
 }
 
 } // namespace
+
+size_t filt_words(uint64_t n_edges) { return ((n_edges + kEdgeTile - 1) / kEdgeTile + 1) * 2 * kEdgeTile; }
 
 size_t edge_rec_bytes() { return sizeof(EdgeRec); }
 

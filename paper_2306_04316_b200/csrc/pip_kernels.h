@@ -15,7 +15,7 @@ struct PrepArgs {
     const uint64_t* ring_off;
     uint32_t n_rings;
     uint64_t n_verts;
-    uint4* filt;                  // n_edges filter words (see prep_edges_kernel)
+    uint2* filt;                  // filter words, tile-blocked (see prep_edges_kernel)
     void* rec;                    // n_edges EdgeRec (edge_rec_bytes() each)
     unsigned long long* bbox_keys; // 4 monotone keys: min x, min y, ~max x, ~max y; [4..5] 16-bit key map
     uint32_t* zero_words;          // output bit planes to clear (inside ++ aux, contiguous)
@@ -27,7 +27,7 @@ struct SingleArgs {
     int mode;
     const double* pts;
     uint64_t n;
-    const uint4* filt;
+    const uint2* filt;
     const void* rec;
     uint32_t n_edges;
     const unsigned long long* bbox_keys;
@@ -55,6 +55,8 @@ struct CsrArgs {
 };
 
 size_t edge_rec_bytes();
+constexpr int kEdgeTile = 256; // edges per filter block (= pip_single.cu's shared-memory stage)
+size_t filt_words(uint64_t n_edges); // uint2 entries of the tile-blocked filter array
 size_t csr_meta_bytes(uint64_t n_polys);
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st, int dev, uint64_t* launches);
 cudaError_t launch_single(const SingleArgs& a, cudaStream_t st, int dev, uint64_t* launches);

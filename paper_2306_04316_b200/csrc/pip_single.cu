@@ -45,8 +45,10 @@ constexpr int kTile = 256;  // edges per shared-memory stage (multiple of 2: 16-
 
 struct __align__(128) TileStage {
     EdgeRec rec[kTile];
-    uint4 filt[kTile];
+    uint2 wkr[kTile];  // key range per edge (warp-level test)   } one bulk copy:
+    uint2 filt[kTile]; // per-point filter word                   } the tile-blocked block
 };
+static_assert(kTile == kEdgeTile, "the stage holds one filter block");
 
 // C1 keeps only the polygon-local fp32 coordinates of its points in shared
 // memory (the fp32 side test; the rare exact fallbacks re-read the binary64
@@ -81,15 +83,15 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
 
 // One elected thread: load tile [t0, t0+nt) of the edge arrays into stage s.
 template <class Shared>
-__device__ __forceinline__ void issue_tile(Shared& sh, int s, const uint4* filt, const EdgeRec* rec,
+__device__ __forceinline__ void issue_tile(Shared& sh, int s, const uint2* filt, const EdgeRec* rec,
                                            uint32_t t0, uint32_t nt) {
-    const unsigned fb = nt * 16u;
+    const unsigned fb = 2u * kTile * 8u; // the whole block of ranges + words (t0 is tile-aligned)
     const unsigned rb = nt * (unsigned)sizeof(EdgeRec);
     const unsigned bar = smem_u32(&sh.full[s]);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(fb + rb) : "memory");
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(sh.st[s].filt)),
-                 "l"(filt + t0), "r"(fb), "r"(bar)
+                     smem_u32(sh.st[s].wkr)),
+                 "l"(filt + 2ull * t0), "r"(fb), "r"(bar)
                  : "memory");
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                      smem_u32(sh.st[s].rec)),
@@ -250,7 +252,7 @@ __device__ __forceinline__ void slow_generic(const double2* my_pts, const Keys<M
 
 template <int MODE>
 __global__ void __launch_bounds__(kTPB, MODE == kC1 ? 3 : 2) pip_tile_kernel(const double2* __restrict__ pts, uint64_t n,
-                                                        const uint4* __restrict__ filt,
+                                                        const uint2* __restrict__ filt,
                                                         const EdgeRec* __restrict__ rec, uint32_t n_edges,
                                                         uint32_t edges_per_chunk,
                                                         const unsigned long long* __restrict__ bbox_keys,
@@ -374,9 +376,9 @@ __global__ void __launch_bounds__(kTPB, MODE == kC1 ? 3 : 2) pip_tile_kernel(con
     }
     // may any active point of the warp straddle edge f?  (exact: the keys are
     // monotone; the per-point filter and the slow path then decide per point)
-    auto warp_may = [&](const uint4& f) {
-        if constexpr (MODE == kRobust) return (int)f.x <= wka_max && (int)f.y >= wkb_min;
-        else return f.z <= wkey_hi && f.w >= wkey_lo;
+    auto warp_may = [&](uint32_t lo, uint32_t hi) {
+        if constexpr (MODE == kRobust) return ((int)lo <= wka_max) & ((int)hi >= wkb_min);
+        else return (lo <= wkey_hi) & (hi >= wkey_lo);
     };
 
     uint32_t par = 0, auxm = 0;
@@ -390,15 +392,16 @@ __global__ void __launch_bounds__(kTPB, MODE == kC1 ? 3 : 2) pip_tile_kernel(con
             for (uint32_t e0 = 0; e0 < nt; e0 += 4) {
                 // warp-level interval test of 4 edges (warp-uniform: the key
                 // ranges of the warp's points against each edge's key range)
-                const uint4 f0 = T.filt[e0], f1 = T.filt[e0 + 1], f2 = T.filt[e0 + 2], f3 = T.filt[e0 + 3];
-                if (!(warp_may(f0) || warp_may(f1) || warp_may(f2) || warp_may(f3))) continue;
+                const uint4 r01 = *reinterpret_cast<const uint4*>(&T.wkr[e0]);
+                const uint4 r23 = *reinterpret_cast<const uint4*>(&T.wkr[e0 + 2]);
+                if (!(warp_may(r01.x, r01.y) | warp_may(r01.z, r01.w) | warp_may(r23.x, r23.y) |
+                      warp_may(r23.z, r23.w)))
+                    continue;
                 // per-point filter of the 4 edges, then one warp-wide OR says
                 // which of them need the slow path
                 bool c[4];
-                c[0] = lane_candidate<MODE>(K, make_uint2(f0.x, f0.y));
-                c[1] = lane_candidate<MODE>(K, make_uint2(f1.x, f1.y));
-                c[2] = lane_candidate<MODE>(K, make_uint2(f2.x, f2.y));
-                c[3] = lane_candidate<MODE>(K, make_uint2(f3.x, f3.y));
+#pragma unroll
+                for (int u = 0; u < 4; ++u) c[u] = lane_candidate<MODE>(K, T.filt[e0 + u]);
                 // common case: no candidate in the warp for any of the 4 edges
                 if (!__any_sync(0xffffffffu, c[0] | c[1] | c[2] | c[3])) continue;
                 uint32_t bits = 0;
@@ -409,7 +412,7 @@ __global__ void __launch_bounds__(kTPB, MODE == kC1 ? 3 : 2) pip_tile_kernel(con
                 while (todo) {
                     const uint32_t e = e0 + (__ffs(todo) - 1);
                     todo &= todo - 1;
-                    const uint2 f = make_uint2(T.filt[e].x, T.filt[e].y);
+                    const uint2 f = T.filt[e];
                     // ---- slow path: exact binary64 test for the candidate points ----
                     if constexpr (MODE == kC1)
                         slow_c1(sh.pts + wloc + lane, pts + cta_base + wloc + lane, K, act, nonloc, f, T.rec[e], par,
