@@ -389,21 +389,15 @@ __global__ void __launch_bounds__(kTPB, MODE == kC1 ? 3 : 2) pip_tile_kernel(con
         mbar_wait(&sh.full[s], (q >> 1) & 1);
         const TileStage& T = sh.st[s];
         if (warp_live) {
-            for (uint32_t e0 = 0; e0 < nt; e0 += 4) {
-                // warp-level interval test of 4 edges (warp-uniform: the key
-                // ranges of the warp's points against each edge's key range)
-                const uint4 r01 = *reinterpret_cast<const uint4*>(&T.wkr[e0]);
-                const uint4 r23 = *reinterpret_cast<const uint4*>(&T.wkr[e0 + 2]);
-                if (!(warp_may(r01.x, r01.y) | warp_may(r01.z, r01.w) | warp_may(r23.x, r23.y) |
-                      warp_may(r23.z, r23.w)))
-                    continue;
+            // process one group of 4 edges that passed the warp-level test
+            auto group = [&](uint32_t e0) {
                 // per-point filter of the 4 edges, then one warp-wide OR says
                 // which of them need the slow path
                 bool c[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) c[u] = lane_candidate<MODE>(K, T.filt[e0 + u]);
                 // common case: no candidate in the warp for any of the 4 edges
-                if (!__any_sync(0xffffffffu, c[0] | c[1] | c[2] | c[3])) continue;
+                if (!__any_sync(0xffffffffu, c[0] | c[1] | c[2] | c[3])) return;
                 uint32_t bits = 0;
 #pragma unroll
                 for (int u = 0; u < 4; ++u) bits |= (uint32_t)c[u] << u;
@@ -420,6 +414,25 @@ __global__ void __launch_bounds__(kTPB, MODE == kC1 ? 3 : 2) pip_tile_kernel(con
                     else
                         slow_generic<MODE>(sh.pts + wloc + lane, K, act, f, T.rec[e], tol, tol2, par, auxm);
                 }
+            };
+            // warp-level interval test (warp-uniform: the key range of the warp's
+            // points against each edge's key range), 8 edges per step with the
+            // loads of both halves issued together; the stage's shared address is
+            // formed once per tile
+            const unsigned wkr_s = smem_u32(T.wkr);
+            for (uint32_t e0 = 0; e0 < nt; e0 += 8) {
+                uint4 r[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(r[j].x), "=r"(r[j].y), "=r"(r[j].z), "=r"(r[j].w)
+                                 : "r"(wkr_s + (e0 + 2 * j) * 8u));
+                const bool pa = warp_may(r[0].x, r[0].y) | warp_may(r[0].z, r[0].w) | warp_may(r[1].x, r[1].y) |
+                                warp_may(r[1].z, r[1].w);
+                const bool pb = warp_may(r[2].x, r[2].y) | warp_may(r[2].z, r[2].w) | warp_may(r[3].x, r[3].y) |
+                                warp_may(r[3].z, r[3].w);
+                if (pa) group(e0);
+                if (pb && e0 + 4 < nt) group(e0 + 4);
             }
         }
         __syncthreads(); // stage s fully consumed
