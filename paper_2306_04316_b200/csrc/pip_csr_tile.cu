@@ -106,18 +106,22 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
         slow = act;
         band = act; // every candidate edge of every point
     } else if (fast) {
-        uint32_t fpar = 0, t0 = 0xffffffffu, t1 = 0xffffffffu;
-        float m0 = 1.f, m1 = 1.f;
+        // per record and point: x = q - q_hi < 0 and y = q - (q_lo + 1) >= 0 iff
+        // q_lo < q < q_hi (a sure straddle); s' = s + B (B folded into the
+        // record's offset) has its sign bit set iff the side test counts, so the
+        // sign bit of x & ~y & s' toggles the parity; +0 <= s' <= 2B is a band hit
+        int acc0 = 0, acc1 = 0;
+        uint32_t t0 = 0xffffffffu, t1 = 0xffffffffu, u0 = 0xffffffffu, u1 = 0xffffffffu;
         auto rec = [&](uint32_t i) {
             const int4 f = ws.rec[i];
             const float2 g = ws.rec2[i];
             const float nxf = __int_as_float(f.w);
             const float s0 = fmaf(lx[0], nxf, fmaf(ly[0], g.x, g.y));
             const float s1 = fmaf(lx[1], nxf, fmaf(ly[1], g.x, g.y));
-            fast_toggle(fpar, 1u, (unsigned)(qy[0] - f.x), (unsigned)f.y, s0);
-            fast_toggle(fpar, 2u, (unsigned)(qy[1] - f.x), (unsigned)f.y, s1);
-            m0 = fminf(m0, fabsf(s0)); // band hits
-            m1 = fminf(m1, fabsf(s1));
+            acc0 ^= (qy[0] - f.y) & ~(qy[0] - f.x) & __float_as_int(s0);
+            acc1 ^= (qy[1] - f.y) & ~(qy[1] - f.x) & __float_as_int(s1);
+            u0 = min(u0, __float_as_uint(s0)); // band hits
+            u1 = min(u1, __float_as_uint(s1));
             t0 = min(t0, (unsigned)(qy[0] - f.z)); // ties: 0 iff q(p.y) == q(vertex)
             t1 = min(t1, (unsigned)(qy[1] - f.z));
         };
@@ -129,7 +133,9 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
 #pragma unroll
             for (int k = 0; k < 4; ++k) rec(min(i + k, last));
         }
-        band = ((uint32_t)(m0 <= kFastBand) | ((uint32_t)(m1 <= kFastBand) << 1)) & act;
+        constexpr uint32_t k2B = 0x36000000u; // bits of 2^-19 = 2 * kFastBand
+        const uint32_t fpar = ((uint32_t)acc0 >> 31) | (((uint32_t)acc1 >> 31) << 1);
+        band = ((uint32_t)(u0 <= k2B) | ((uint32_t)(u1 <= k2B) << 1)) & act;
         const uint32_t tie = ((uint32_t)(t0 == 0u) | ((uint32_t)(t1 == 0u) << 1)) & act;
         slow |= band | tie;
         // decided contributions (ties never toggle fpar); points with a band hit
@@ -163,19 +169,19 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
             if (sh && w + 1 < (uint32_t)(kWV / 32)) ends |= ws.ring_end[w + 1] << (32 - sh);
             const uint32_t real = ~ends & (n == 32 ? 0xffffffffu : ((1u << n) - 1u));
             uint32_t cm0 = 0u, cm1 = 0u;
-            if (cand_mode) { // q_lo <= q <= q_hi (a superset when q_hi == q_lo)
+            // record: f.x = q_lo + 1, f.y = q_hi
+            if (cand_mode) { // q_lo <= q <= q_hi
                 for (int u = n - 1; u >= 0; --u) {
                     const int2 f = *reinterpret_cast<const int2*>(&ws.rec[i0 + u]);
-                    const unsigned r = (unsigned)f.y + 1u;
+                    const unsigned r = (unsigned)(f.y - f.x + 1);
                     cm0 = (cm0 << 1) | (uint32_t)((unsigned)(qy1[0] - f.x) <= r);
                     cm1 = (cm1 << 1) | (uint32_t)((unsigned)(qy1[1] - f.x) <= r);
                 }
-            } else { // ties only: q == q_lo (d == -1) or q == q_hi (d == f.y)
+            } else { // ties only: q == q_lo or q == q_hi
                 for (int u = n - 1; u >= 0; --u) {
                     const int2 f = *reinterpret_cast<const int2*>(&ws.rec[i0 + u]);
-                    const unsigned d0 = (unsigned)(qy[0] - f.x), d1 = (unsigned)(qy[1] - f.x);
-                    cm0 = (cm0 << 1) | (uint32_t)(d0 == 0xffffffffu || d0 == (unsigned)f.y);
-                    cm1 = (cm1 << 1) | (uint32_t)(d1 == 0xffffffffu || d1 == (unsigned)f.y);
+                    cm0 = (cm0 << 1) | (uint32_t)(qy1[0] == f.x || qy[0] == f.y);
+                    cm1 = (cm1 << 1) | (uint32_t)(qy1[1] == f.x || qy[1] == f.y);
                 }
             }
             // points whose key filter is not exact: every edge
@@ -348,8 +354,10 @@ __global__ void __launch_bounds__(kBThreads, 8) pip_csr_tile_kernel(
                     const int qlo = min(qa, qb), qhi = max(qa, qb);
                     const double Nx = __dmul_rn(nx, sy), Ny = __dmul_rn(ny, sx);
                     const double cd = __dadd_rn(__dmul_rn(axl, Nx), __dmul_rn(ayl, Ny));
-                    f = make_int4(qlo + 1, max(qhi - qlo - 1, 0), qa, __float_as_int(__double2float_rn(Nx)));
-                    gg = make_float2(__double2float_rn(Ny), __double2float_rn(-cd));
+                    f = make_int4(qlo + 1, qhi, qa, __float_as_int(__double2float_rn(Nx)));
+                    // offset c + B (see classify_item): the extra fp32 rounding (<= 2 * 2^-24)
+                    // keeps the error at 15.1 * 2^-24 < B
+                    gg = make_float2(__double2float_rn(Ny), __double2float_rn(__dadd_rn(-cd, (double)kFastBand)));
                 }
                 ws.rec[i] = f;
                 ws.rec2[i] = gg;
