@@ -307,7 +307,9 @@ def run_ours(args, rank, world, local_rank):
     # ---- roofline of the dominant kernel (rank 0's device) -----------------------------
     per_item_ms = np.array(kern_ms, dtype=np.float64).reshape(args.steps, len(items)).mean(0)
     csr = items[0].csr is not None
-    if csr:
+    # configs 3 (and 2 at n <= ~25) are HBM-bound, configs 1, 2, 4
+    # and 5 (~35 edges per point) FP64-bound
+    if args.workload == "c3":
         bytes_launch = sum(i.bytes for i in items) / len(items)
         achieved = bytes_launch / (per_item_ms.mean() / 1e3) / 1e9
         peak_src = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
