@@ -89,6 +89,7 @@ __device__ __forceinline__ uint32_t qkey15(double y, const QMap& m) {
 // side scaled by sx*sy, so |s| > kLocalBand = 2^-20 decides its sign.
 struct LocalMap {
     double x0, y0, sx, sy;
+    bool c2ok; // C2 also needs max(|x|) * sx <= 2^20 (its reference error is ~u * |x|)
 };
 constexpr float kLocalBand = 0x1p-20f;
 
@@ -105,6 +106,8 @@ __device__ __forceinline__ LocalMap local_map_from_bbox(const unsigned long long
     const bool ok = W >= 0x1p-300 && W <= 0x1p300 && H >= 0x1p-300 && H <= 0x1p300;
     m.sx = ok ? pow2_inv_above(W) : 0.0;
     m.sy = ok ? pow2_inv_above(H) : 0.0;
+    const double mx = fmax(fabs(m.x0), fabs(dkey_inv(~bbox_keys[2])));
+    m.c2ok = ok && __dmul_rn(mx, m.sx) <= 0x1p20;
     return m;
 }
 
@@ -122,6 +125,28 @@ __device__ __forceinline__ float3 local_side_record(const LocalMap& m, double ax
     // c + kLocalBand: the kernel's s' = s + B is then <= -0 (sign bit) for a sure
     // count and in [+0, 2B] for a band hit; the extra fp32 rounding of c + B
     // (<= 2 * 2^-24) keeps the total error at 15.1 * 2^-24 < B
+    return make_float3(__double2float_rn(Nx), __double2float_rn(Ny),
+                       __double2float_rn(__dadd_rn(-cd, (double)kLocalBand)));
+}
+
+// C2 (geometry.hpp:216-224): count iff x > p.x with x the reference's rounded
+// intercept.  With X* = a.x + (p.y - a.y) * dx / dy (the rounded dx, dy),
+// |x - X*| <= u*|a.x| + 4.03u*|dx| for a sure straddle (0 < lambda < 1), and
+// (X* - p.x) * dy = -C with C = (p - a) x (dx, dy); so the local fp32 value of
+// C * sign(dy), with N = sign(dy) * (dy * s_y, -dx * s_x), has the error of
+// §3.4 plus at most u * (max|x| * s_x + 4.03) <= 2^-33 after scaling when
+// max|x| * s_x <= 2^20: it is certified by the same band, and the count is
+// its sign bit (s' = s + B as for C1).  NaN record when not usable.
+__device__ __forceinline__ float3 local_side_record_c2(const LocalMap& m, double ax, double ay, double bx, double by,
+                                                       double dx, double dy) {
+    const double axl = __dmul_rn(__dsub_rn(ax, m.x0), m.sx), ayl = __dmul_rn(__dsub_rn(ay, m.y0), m.sy);
+    const double bxl = __dmul_rn(__dsub_rn(bx, m.x0), m.sx), byl = __dmul_rn(__dsub_rn(by, m.y0), m.sy);
+    const bool ok = m.c2ok && dy != 0.0 && axl >= 0.0 && axl < 1.0 && ayl >= 0.0 && ayl < 1.0 && bxl >= 0.0 &&
+                    bxl < 1.0 && byl >= 0.0 && byl < 1.0;
+    if (!ok) return make_float3(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
+    const double sg = dy > 0.0 ? 1.0 : -1.0;
+    const double Nx = __dmul_rn(__dmul_rn(dy, m.sy), sg), Ny = __dmul_rn(__dmul_rn(-dx, m.sx), sg);
+    const double cd = __dadd_rn(__dmul_rn(axl, Nx), __dmul_rn(ayl, Ny));
     return make_float3(__double2float_rn(Nx), __double2float_rn(Ny),
                        __double2float_rn(__dadd_rn(-cd, (double)kLocalBand)));
 }

@@ -135,6 +135,10 @@ __global__ void __launch_bounds__(256) prep_edges_kernel(
             } else {
                 er.d[3] = __dsub_rn(bx, ax);
                 er.d[4] = __dsub_rn(by, ay);
+                // fp32 side-test record of the intercept sign (d[5] = {Nx, Ny}, d[6] = {c + B, 0})
+                const float3 fr = local_side_record_c2(lm, ax, ay, bx, by, er.d[3], er.d[4]);
+                er.d[5] = __hiloint2double(__float_as_int(fr.y), __float_as_int(fr.x));
+                er.d[6] = __hiloint2double(0, __float_as_int(fr.z));
             }
             const uint32_t klo = qkey15(ylo, qm), khi = qkey15(yhi, qm);
             const uint32_t neg = ((0x8000u - klo) & 0x7fffu) << 1; // -q(ylo) mod 2^15, guard bit clear

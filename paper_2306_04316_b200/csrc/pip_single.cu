@@ -50,12 +50,12 @@ struct __align__(128) TileStage {
 };
 static_assert(kTile == kEdgeTile, "the stage holds one filter block");
 
-// C1 keeps only the polygon-local fp32 coordinates of its points in shared
-// memory (the fp32 side test; the rare exact fallbacks re-read the binary64
-// point from global memory / L2); C2 and Robust keep the binary64 points.
+// C1 and C2 keep only the polygon-local fp32 coordinates of their points in
+// shared memory (the fp32 side test; the rare exact fallbacks re-read the
+// binary64 point from global memory / L2); Robust keeps the binary64 points.
 template <int MODE>
 struct SingleShared {
-    using PointT = std::conditional_t<MODE == kC1, float2, double2>;
+    using PointT = std::conditional_t<MODE == kRobust, double2, float2>;
     PointT pts[kTPB * kK]; // this CTA's points (bucketed order)
     TileStage st[2];
     unsigned long long full[2];
@@ -221,6 +221,65 @@ __device__ __forceinline__ void slow_c1(const float2* my_l, const double2* __res
     par ^= hit & cm;
 }
 
+// C2 slow path (geometry.hpp:216-224) for one candidate edge: sure straddles
+// decide the intercept sign with the certified fp32 test (local_side_record_c2);
+// key ties, band hits and points without local coordinates run the
+// reference's expression (division included, DegenerateEdge -> Error).
+__device__ __forceinline__ void slow_c2(const float2* my_l, const double2* __restrict__ my_g, const Keys<kC2>& K,
+                                        uint32_t act, uint32_t nonloc, uint2 f, const EdgeRec& r, uint32_t& par,
+                                        uint32_t& auxm, uint32_t wkey_lo, uint32_t wkey_hi) {
+    const uint32_t rng = ((f.y & 0xffffu) - 2u) >> 1;
+    const uint32_t klo = (0x8000u - ((f.x & 0xffffu) >> 1)) & 0x7fffu;
+    uint32_t cm = act, tm = 0;
+    if (!(klo < wkey_lo && wkey_hi < klo + rng)) {
+        cm = 0;
+#pragma unroll
+        for (int k = 0; k < kK; ++k) {
+            const uint32_t d = K.diff(k, f.x);
+            cm |= (uint32_t)(d <= rng) << k;
+            tm |= (uint32_t)(d == 0u || d == rng) << k;
+        }
+        cm &= act;
+        tm &= cm;
+    }
+    const uint32_t sure = cm & ~tm;
+    const float nxf = __int_as_float(__double2loint(r.d[5])), nyf = __int_as_float(__double2hiint(r.d[5]));
+    const float cf = __int_as_float(__double2loint(r.d[6])); // c + B
+    constexpr uint32_t k2B = 0x36000000u;                   // bits of 2^-19 = 2 * kLocalBand
+    uint32_t hit = 0, umin = 0xffffffffu;
+#pragma unroll
+    for (int k = kK - 1; k >= 0; --k) {
+        const float2 l = my_l[k * 32];
+        const uint32_t u = __float_as_uint(fmaf(l.x, nxf, fmaf(l.y, nyf, cf)));
+        hit = (hit << 1) | (u >> 31);
+        umin = min(umin, u);
+    }
+    uint32_t und = nonloc | ((nxf == nxf) ? 0u : 0xffffu);
+    if (umin <= k2B) {
+#pragma unroll
+        for (int k = 0; k < kK; ++k) {
+            const float2 l = my_l[k * 32];
+            und |= (uint32_t)(__float_as_uint(fmaf(l.x, nxf, fmaf(l.y, nyf, cf))) <= k2B) << k;
+        }
+    }
+    und &= sure;
+    par ^= hit & sure & ~und;
+    const uint32_t ex = und | tm; // binary64: band hits / no local coordinates (sure) and key ties
+    if (__any_sync(0xffffffffu, ex != 0)) {
+#pragma unroll 1
+        for (int k = 0; k < kK; ++k) {
+            if (ex >> k & 1u) {
+                const double2 p = my_g[k * 32];
+                int cnt = 0;
+                bool err = false;
+                exact_c2(p.x, p.y, r, cnt, err, (und >> k) & 1u);
+                par ^= (uint32_t)(cnt & 1) << k;
+                auxm |= (uint32_t)err << k;
+            }
+        }
+    }
+}
+
 // C2 / Robust slow path: per point, only for candidates (division is costly).
 template <int MODE>
 __device__ __forceinline__ void slow_generic(const double2* my_pts, const Keys<MODE>& K, uint32_t act, uint2 f,
@@ -251,7 +310,7 @@ __device__ __forceinline__ void slow_generic(const double2* my_pts, const Keys<M
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kTPB, MODE == kC1 ? 3 : 2) pip_tile_kernel(const double2* __restrict__ pts, uint64_t n,
+__global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3) pip_tile_kernel(const double2* __restrict__ pts, uint64_t n,
                                                         const uint2* __restrict__ filt,
                                                         const EdgeRec* __restrict__ rec, uint32_t n_edges,
                                                         uint32_t edges_per_chunk,
@@ -280,7 +339,7 @@ __global__ void __launch_bounds__(kTPB, MODE == kC1 ? 3 : 2) pip_tile_kernel(con
     __syncthreads();
     const uint32_t n_tiles = (e_end - e_begin + kTile - 1) / kTile;
     if (tid == 0) {
-        if constexpr (MODE != kC1) { // C1 reads its points directly (they become fp32 local coordinates)
+        if constexpr (MODE == kRobust) { // C1/C2 read their points directly (they become fp32 local coordinates)
             const unsigned pb = cta_n * 16u, bar = smem_u32(&sh.pbar);
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(pb) : "memory");
             asm volatile(
@@ -302,9 +361,9 @@ __global__ void __launch_bounds__(kTPB, MODE == kC1 ? 3 : 2) pip_tile_kernel(con
         maxy = dkey_inv(~bbox_keys[3]);
     }
     const uint32_t wloc = (uint32_t)warp * 32 * kK; // this warp's first point within the CTA
-    if constexpr (MODE != kC1) mbar_wait(&sh.pbar, 0);
+    if constexpr (MODE == kRobust) mbar_wait(&sh.pbar, 0);
     LocalMap lm{};
-    if constexpr (MODE == kC1) {
+    if constexpr (MODE != kRobust) {
         lm.x0 = dkey_inv(bbox_keys[0]);
         lm.y0 = dkey_inv(bbox_keys[1]);
         lm.sx = reinterpret_cast<const double*>(bbox_keys)[6];
@@ -318,14 +377,14 @@ __global__ void __launch_bounds__(kTPB, MODE == kC1 ? 3 : 2) pip_tile_kernel(con
         const uint32_t li = wloc + k * 32 + lane;
         bool a = li < cta_n;
         double2 p = make_double2(0.0, 0.0);
-        if constexpr (MODE == kC1) {
+        if constexpr (MODE != kRobust) {
             if (a) p = pts[cta_base + li];
             if ((k & 3) == 3) asm volatile("" ::: "memory"); // at most 4 point loads in flight (registers)
         } else {
             if (a) p = sh.pts[li];
         }
         if (a && prefilter) a = p.x >= minx && p.x <= maxx && p.y >= miny && p.y <= maxy; // batch.hpp:39-41
-        if constexpr (MODE == kC1) {
+        if constexpr (MODE != kRobust) {
             // polygon-local fp32 coordinates; NaN outside the bbox / without a map (-> exact side test)
             const double lxd = __dmul_rn(__dsub_rn(p.x, lm.x0), lm.sx), lyd = __dmul_rn(__dsub_rn(p.y, lm.y0), lm.sy);
             const bool ok = lm.sx != 0.0 && lxd >= 0.0 && lxd < 1.0 && lyd >= 0.0 && lyd < 1.0;
@@ -411,6 +470,9 @@ __global__ void __launch_bounds__(kTPB, MODE == kC1 ? 3 : 2) pip_tile_kernel(con
                     if constexpr (MODE == kC1)
                         slow_c1(sh.pts + wloc + lane, pts + cta_base + wloc + lane, K, act, nonloc, f, T.rec[e], par,
                                 wkey_lo, wkey_hi);
+                    else if constexpr (MODE == kC2)
+                        slow_c2(sh.pts + wloc + lane, pts + cta_base + wloc + lane, K, act, nonloc, f, T.rec[e], par,
+                                auxm, wkey_lo, wkey_hi);
                     else
                         slow_generic<MODE>(sh.pts + wloc + lane, K, act, f, T.rec[e], tol, tol2, par, auxm);
                 }
