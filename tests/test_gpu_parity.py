@@ -498,7 +498,7 @@ def test_single_fast_side_band(engine):
     deltas = (1e-16, 1e-12, 1e-9, 2e-7, 4e-7, 1e-6, 3e-6, 1e-4)
     ring = [(5.0 + 0.0004 * np.cos(t), 0.5 + 0.0003 * np.sin(t)) for t in np.linspace(0, 2 * np.pi, 41)[:-1]]
     far = [(1.0e6 + 1.5 * np.cos(t), 0.5 + 1.2 * np.sin(t)) for t in np.linspace(0, 2 * np.pi, 23)[:-1]]
-    far2 = [(1.0e6 + 0.4 * np.cos(t), 0.5 + 0.3 * np.sin(t)) for t in np.linspace(0, 2 * np.pi, 23)[:-1]]
+    far2 = [(1.0e6 + 0.2 * np.cos(t), 0.5 + 0.15 * np.sin(t)) for t in np.linspace(0, 2 * np.pi, 23)[:-1]]
     # C2's fp32 test is gated on max|x| / W <= 2^20: `far` passes the gate, `far2` does not
     polys = [W.star_polygon(300, seed=12), Polygon.from_rings([ring + [ring[0]]]),
              Polygon.from_rings([far + [far[0]]]), Polygon.from_rings([far2 + [far2[0]]])]
