@@ -145,6 +145,7 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
     pa.rec = d.rec.p;
     pa.bbox_keys = d.bbox.as<unsigned long long>();
     pa.stats = d_stats;
+    pa.tol = tol;
     // inside and aux are zeroed separately (they need not be contiguous)
     pa.zero_words = d_inside;
     pa.n_zero_words = nwords;

@@ -344,8 +344,6 @@ __global__ void __launch_bounds__(kCsrThreads, MODE == kC1 ? 3 : 4) pip_csr_warp
                             rr.d[3] = q.x;
                             rr.d[4] = q.y;
                             rr.d[5] = MODE == kRobust ? es.len2[i] : 0.0;
-                            rr.d[6] = rr.d[2] < a.y ? rr.d[2] : a.y;
-                            rr.d[7] = a.y < rr.d[2] ? rr.d[2] : a.y;
                             int cnt = 0;
                             bool ax = false;
                             if (MODE == kRobust) exact_robust(px[j], py[j], tol, tol2, rr, cnt, ax);

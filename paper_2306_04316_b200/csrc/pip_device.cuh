@@ -181,8 +181,9 @@ __device__ __forceinline__ void exact_c2(double px, double py, const EdgeRec& r,
 // Robust exact test (geometry.hpp:245-270); `bnd` marks on_boundary.
 __device__ __forceinline__ void exact_robust(double px, double py, double tol, double tol2,
                                              const EdgeRec& r, int& cnt, bool& bnd) {
-    const double ax = r.d[0], ay = r.d[1], by = r.d[2], abx = r.d[3], aby = r.d[4], len2 = r.d[5],
-                 ylo = r.d[6], yhi = r.d[7];
+    const double ax = r.d[0], ay = r.d[1], by = r.d[2], abx = r.d[3], aby = r.d[4], len2 = r.d[5];
+    const double ylo = by < ay ? by : ay; // std::min(a.y, b.y)
+    const double yhi = ay < by ? by : ay; // std::max(a.y, b.y)
     if (__dadd_rn(py, tol) < ylo || __dsub_rn(py, tol) > yhi) return;
     const double apx = __dsub_rn(px, ax);
     const double apy = __dsub_rn(py, ay);

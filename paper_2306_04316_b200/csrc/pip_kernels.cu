@@ -83,7 +83,7 @@ template <int MODE>
 __global__ void __launch_bounds__(256) prep_edges_kernel(
     const double* __restrict__ vx, const double* __restrict__ vy, const uint64_t* __restrict__ ring_off,
     uint32_t n_rings, uint64_t n_verts, uint2* __restrict__ filt, EdgeRec* __restrict__ rec,
-    unsigned long long* __restrict__ bbox_keys) {
+    unsigned long long* __restrict__ bbox_keys, double tol) {
     const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const QMap qm = qmap_from_bbox(bbox_keys);
@@ -113,8 +113,14 @@ __global__ void __launch_bounds__(256) prep_edges_kernel(
             er.d[3] = abx;
             er.d[4] = aby;
             er.d[5] = __dadd_rn(__dmul_rn(abx, abx), __dmul_rn(aby, aby));
-            er.d[6] = ylo;
-            er.d[7] = yhi;
+            // fp32 record of the intercept sign (as C2: same expression), valid only
+            // while tol is far below the polygon's size (then a decided sign also
+            // rules out the boundary): d[6] = {Nx, Ny}, d[7] = {c + B, 0}
+            LocalMap lr = lm;
+            lr.c2ok = lm.c2ok && tol >= 0.0 && __dmul_rn(__dmul_rn(tol, 2.0), fmax(lm.sx, lm.sy)) <= 0x1p-30;
+            const float3 fr = local_side_record_c2(lr, ax, ay, bx, by, abx, aby);
+            er.d[6] = __hiloint2double(__float_as_int(fr.y), __float_as_int(fr.x));
+            er.d[7] = __hiloint2double(0, __float_as_int(fr.z));
             const uint2 w = make_uint2((uint32_t)fkey(ylo), (uint32_t)fkey(yhi));
             filt[fb] = w;
             filt[fb + kEdgeTile] = w;
@@ -279,15 +285,15 @@ cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st, int dev, uint64_t* l
     switch (a.mode) {
     case kC1:
         prep_edges_kernel<kC1><<<blocks, 256, 0, st>>>(a.vx, a.vy, a.ring_off, a.n_rings, a.n_verts, a.filt,
-                                                       reinterpret_cast<EdgeRec*>(a.rec), a.bbox_keys);
+                                                       reinterpret_cast<EdgeRec*>(a.rec), a.bbox_keys, a.tol);
         break;
     case kC2:
         prep_edges_kernel<kC2><<<blocks, 256, 0, st>>>(a.vx, a.vy, a.ring_off, a.n_rings, a.n_verts, a.filt,
-                                                       reinterpret_cast<EdgeRec*>(a.rec), a.bbox_keys);
+                                                       reinterpret_cast<EdgeRec*>(a.rec), a.bbox_keys, a.tol);
         break;
     default:
         prep_edges_kernel<kRobust><<<blocks, 256, 0, st>>>(a.vx, a.vy, a.ring_off, a.n_rings, a.n_verts, a.filt,
-                                                           reinterpret_cast<EdgeRec*>(a.rec), a.bbox_keys);
+                                                           reinterpret_cast<EdgeRec*>(a.rec), a.bbox_keys, a.tol);
         break;
     }
     *launches += 2;

@@ -21,6 +21,7 @@ struct PrepArgs {
     uint32_t* zero_words;          // output bit planes to clear (inside ++ aux, contiguous)
     uint64_t n_zero_words;
     unsigned long long* stats;     // 4 counters to clear
+    double tol;                    // Robust boundary tolerance (gates its fp32 side records)
 };
 
 struct SingleArgs {

@@ -50,12 +50,12 @@ struct __align__(128) TileStage {
 };
 static_assert(kTile == kEdgeTile, "the stage holds one filter block");
 
-// C1 and C2 keep only the polygon-local fp32 coordinates of their points in
-// shared memory (the fp32 side test; the rare exact fallbacks re-read the
-// binary64 point from global memory / L2); Robust keeps the binary64 points.
+// Every mode keeps only the polygon-local fp32 coordinates of its points in
+// shared memory (the certified fp32 side / intercept test); the binary64
+// fallbacks re-read the point from global memory (L2).
 template <int MODE>
 struct SingleShared {
-    using PointT = std::conditional_t<MODE == kRobust, double2, float2>;
+    using PointT = float2;
     PointT pts[kTPB * kK]; // this CTA's points (bucketed order)
     TileStage st[2];
     unsigned long long full[2];
@@ -280,31 +280,63 @@ __device__ __forceinline__ void slow_c2(const float2* my_l, const double2* __res
     }
 }
 
-// C2 / Robust slow path: per point, only for candidates (division is costly).
-template <int MODE>
-__device__ __forceinline__ void slow_generic(const double2* my_pts, const Keys<MODE>& K, uint32_t act, uint2 f,
-                                             const EdgeRec& r, double tol, double tol2, uint32_t& par,
-                                             uint32_t& auxm) {
+// Robust slow path (geometry.hpp:237-273) for one candidate edge.  Keys of
+// p.y + tol and p.y - tol strictly inside the edge's key range imply
+// y_lo < p.y - tol and p.y + tol < y_hi: no band reject, and exactly one of
+// upward / downward holds; the crossing is then C2's intercept sign (the
+// reference evaluates the same expression), certified in fp32, and a decided
+// sign also rules out the boundary when tol <= 2^-30 * min(W, H) (the record
+// is NaN otherwise): the point's distance to the edge's line is then at least
+// ~29 tol.  Everything else runs the reference's expression.
+__device__ __forceinline__ void slow_robust(const float2* my_l, const double2* __restrict__ my_g,
+                                            const Keys<kRobust>& K, uint32_t act, uint32_t nonloc, uint2 f,
+                                            const EdgeRec& r, double tol, double tol2, uint32_t& par, uint32_t& auxm,
+                                            int wka_max, int wkb_min) {
+    const int flo = (int)f.x, fhi = (int)f.y;
+    uint32_t cm = act, sure = act;
+    if (!(flo < wkb_min && wka_max < fhi)) {
+        cm = sure = 0;
 #pragma unroll
-    for (int k = 0; k < kK; ++k) {
-        bool c;
-        bool sure = false;
-        if constexpr (MODE == kRobust) {
-            c = (K.ka[k] >= (int)f.x) & (K.kb[k] <= (int)f.y);
-        } else {
-            const uint32_t d = K.diff(k, f.x), rng = ((f.y & 0xffffu) - 2u) >> 1;
-            c = d <= rng && (act >> k & 1u);
-            sure = d != 0u && d != rng; // key order strict on both sides
+        for (int k = 0; k < kK; ++k) {
+            cm |= (uint32_t)(K.ka[k] >= flo && K.kb[k] <= fhi) << k;
+            sure |= (uint32_t)(flo < K.kb[k] && K.ka[k] < fhi) << k;
         }
-        if (!__any_sync(0xffffffffu, c)) continue;
-        if (c) {
-            const double2 p = my_pts[k * 32];
-            int cnt = 0;
-            bool ax = false;
-            if (MODE == kC2) exact_c2(p.x, p.y, r, cnt, ax, sure);
-            else exact_robust(p.x, p.y, tol, tol2, r, cnt, ax);
-            par ^= (uint32_t)(cnt & 1) << k;
-            auxm |= (uint32_t)ax << k;
+        cm &= act;
+        sure &= cm;
+    }
+    const float nxf = __int_as_float(__double2loint(r.d[6])), nyf = __int_as_float(__double2hiint(r.d[6]));
+    const float cf = __int_as_float(__double2loint(r.d[7])); // c + B
+    constexpr uint32_t k2B = 0x36000000u;                   // bits of 2^-19 = 2 * kLocalBand
+    uint32_t hit = 0, umin = 0xffffffffu;
+#pragma unroll
+    for (int k = kK - 1; k >= 0; --k) {
+        const float2 l = my_l[k * 32];
+        const uint32_t u = __float_as_uint(fmaf(l.x, nxf, fmaf(l.y, nyf, cf)));
+        hit = (hit << 1) | (u >> 31);
+        umin = min(umin, u);
+    }
+    uint32_t und = nonloc | ((nxf == nxf) ? 0u : 0xffffu);
+    if (umin <= k2B) {
+#pragma unroll
+        for (int k = 0; k < kK; ++k) {
+            const float2 l = my_l[k * 32];
+            und |= (uint32_t)(__float_as_uint(fmaf(l.x, nxf, fmaf(l.y, nyf, cf))) <= k2B) << k;
+        }
+    }
+    und &= sure;
+    par ^= hit & sure & ~und;
+    const uint32_t ex = und | (cm & ~sure);
+    if (__any_sync(0xffffffffu, ex != 0)) {
+#pragma unroll 1
+        for (int k = 0; k < kK; ++k) {
+            if (ex >> k & 1u) {
+                const double2 p = my_g[k * 32];
+                int cnt = 0;
+                bool bnd = false;
+                exact_robust(p.x, p.y, tol, tol2, r, cnt, bnd);
+                par ^= (uint32_t)(cnt & 1) << k;
+                auxm |= (uint32_t)bnd << k;
+            }
         }
     }
 }
@@ -339,15 +371,6 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3) pip_tile_kernel
     __syncthreads();
     const uint32_t n_tiles = (e_end - e_begin + kTile - 1) / kTile;
     if (tid == 0) {
-        if constexpr (MODE == kRobust) { // C1/C2 read their points directly (they become fp32 local coordinates)
-            const unsigned pb = cta_n * 16u, bar = smem_u32(&sh.pbar);
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(pb) : "memory");
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                    smem_u32(sh.pts)),
-                "l"(pts + cta_base), "r"(pb), "r"(bar)
-                : "memory");
-        }
         for (uint32_t q = 0; q < 2 && q < n_tiles; ++q)
             issue_tile(sh, (int)q, filt, rec, e_begin + q * kTile, min((uint32_t)kTile, e_end - e_begin - q * kTile));
     }
@@ -361,9 +384,8 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3) pip_tile_kernel
         maxy = dkey_inv(~bbox_keys[3]);
     }
     const uint32_t wloc = (uint32_t)warp * 32 * kK; // this warp's first point within the CTA
-    if constexpr (MODE == kRobust) mbar_wait(&sh.pbar, 0);
     LocalMap lm{};
-    if constexpr (MODE != kRobust) {
+    {
         lm.x0 = dkey_inv(bbox_keys[0]);
         lm.y0 = dkey_inv(bbox_keys[1]);
         lm.sx = reinterpret_cast<const double*>(bbox_keys)[6];
@@ -377,14 +399,12 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3) pip_tile_kernel
         const uint32_t li = wloc + k * 32 + lane;
         bool a = li < cta_n;
         double2 p = make_double2(0.0, 0.0);
-        if constexpr (MODE != kRobust) {
+        {
             if (a) p = pts[cta_base + li];
             if ((k & 3) == 3) asm volatile("" ::: "memory"); // at most 4 point loads in flight (registers)
-        } else {
-            if (a) p = sh.pts[li];
         }
         if (a && prefilter) a = p.x >= minx && p.x <= maxx && p.y >= miny && p.y <= maxy; // batch.hpp:39-41
-        if constexpr (MODE != kRobust) {
+        {
             // polygon-local fp32 coordinates; NaN outside the bbox / without a map (-> exact side test)
             const double lxd = __dmul_rn(__dsub_rn(p.x, lm.x0), lm.sx), lyd = __dmul_rn(__dsub_rn(p.y, lm.y0), lm.sy);
             const bool ok = lm.sx != 0.0 && lxd >= 0.0 && lxd < 1.0 && lyd >= 0.0 && lyd < 1.0;
@@ -474,7 +494,8 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3) pip_tile_kernel
                         slow_c2(sh.pts + wloc + lane, pts + cta_base + wloc + lane, K, act, nonloc, f, T.rec[e], par,
                                 auxm, wkey_lo, wkey_hi);
                     else
-                        slow_generic<MODE>(sh.pts + wloc + lane, K, act, f, T.rec[e], tol, tol2, par, auxm);
+                        slow_robust(sh.pts + wloc + lane, pts + cta_base + wloc + lane, K, act, nonloc, f, T.rec[e],
+                                    tol, tol2, par, auxm, wka_max, wkb_min);
                 }
             };
             // warp-level interval test (warp-uniform: the key range of the warp's

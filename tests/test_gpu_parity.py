@@ -513,3 +513,17 @@ def test_single_fast_side_band(engine):
                     check_single(xy, poly, mode, engine.classify(xy, poly, mode, prefilter=False), prefilter=False)
             finally:
                 engine.set_bucketing(-1)
+
+
+def test_robust_tolerances(engine):
+    """Robust mode's fp32 records are valid only while tol <= 2^-30 * min(W, H):
+    tolerances on both sides of that gate (0, the default 1e-12, 1e-9, 1e-6, 1e-2)
+    on a star polygon (W ~ 2) with near-edge points, against the reference."""
+    poly = W.star_polygon(200, seed=14)
+    s = _near_edge_points(_single_as_csr(poly, np.zeros((1, 2))), (1e-16, 1e-12, 1e-9, 1e-7, 1e-6, 1e-3))
+    xy = s.xy
+    for tol in (0.0, 1e-12, 1e-9, 1e-6, 1e-2):
+        got = engine.classify(xy, poly, CrossingMode.Robust, boundary_tol=tol)
+        want_v, want_s = oracle.ref_classify(xy, poly.vx, poly.vy, poly.ring_off, 2, tol=tol)
+        assert np.array_equal(got.verdicts, want_v), (tol, int((got.verdicts != want_v).sum()))
+        assert np.array_equal(got.stats, want_s)
