@@ -1,0 +1,24 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out/ev6
+O=gpurun_out/ev6
+nvidia-smi > $O/nvidia-smi.txt 2>&1; lscpu > $O/lscpu.txt 2>&1
+timeout 1200 python -m pytest tests -m gpu -q --timeout 900 > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
+timeout 900 python bench.py > $O/bench_default.json 2> $O/bench_default.err
+for w in c1 c4 c3 c5; do timeout 900 python bench.py --workload $w --steps 5 --warmup 3 > $O/bench_$w.json 2> $O/bench_$w.err; done
+timeout 900 python bench.py --impl reference > $O/bench_reference.json 2> $O/bench_reference.err
+timeout 600 python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > $O/plain_bench.log 2>&1 && \
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_default.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > $O/ncu_launch.log 2>&1
+timeout 600 python bench.py --workload c1 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > $O/plain_c1b.log 2>&1 && \
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c1.csv python bench.py --workload c1 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > $O/ncu_launch_c1.log 2>&1
+timeout 300 python tools/prof_kernel.py --workload c2 --n 1000000 --points 1000000 --reps 2 > $O/plain_c2.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:pip_tile -s 1 -c 1 -o $O/full_sweep_n1e6 python tools/prof_kernel.py --workload c2 --n 1000000 --points 1000000 --reps 2 > $O/ncu_full_sweep.log 2>&1
+timeout 300 python tools/prof_kernel.py --workload c4 --points 10000000 --reps 2 > $O/plain_c4.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:pip_tile -s 1 -c 1 -o $O/full_c4 python tools/prof_kernel.py --workload c4 --points 10000000 --reps 2 > $O/ncu_full_c4.log 2>&1
+timeout 300 python tools/prof_kernel.py --workload c3 --polys 1000000 --reps 2 > $O/plain_c3.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:pip_csr_tile -s 1 -c 1 -o $O/full_c3 python tools/prof_kernel.py --workload c3 --polys 1000000 --reps 2 > $O/ncu_full_c3.log 2>&1
+timeout 300 python tools/prof_kernel.py --workload c5 --polys 100000 --reps 2 > $O/plain_c5.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:pip_csr_tile -s 1 -c 1 -o $O/full_c5 python tools/prof_kernel.py --workload c5 --polys 100000 --reps 2 > $O/ncu_full_c5.log 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c3.csv python bench.py --workload c3 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > $O/ncu_launch_c3.log 2>&1
+
+for m in 1 2; do timeout 900 python bench.py --mode $m --steps 3 --warmup 3 > gpurun_out/ev6/bench_sweep_mode$m.json 2> gpurun_out/ev6/bench_sweep_mode$m.err; done
+echo done
