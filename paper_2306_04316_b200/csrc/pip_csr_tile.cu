@@ -128,8 +128,13 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
         // four records per iteration; reads past the polygon's last record
         // re-read it (the final vertex's sentinel: no toggle, no band hit, a
         // repeated tie check), so no remainder loop is needed
-        const uint32_t last = e1 - 1u;
-        for (uint32_t i = e0; i < e0 + (tp.nloop & 0x7fffffffu); i += 4) {
+        const uint32_t last = e1 - 1u, stop = e0 + (tp.nloop & 0x7fffffffu);
+        uint32_t i = e0;
+        for (; i + 4 <= stop; i += 4) { // whole groups: consecutive records, fixed offsets
+#pragma unroll
+            for (int k = 0; k < 4; ++k) rec(i + k);
+        }
+        if (i < stop) { // the remainder, clamped
 #pragma unroll
             for (int k = 0; k < 4; ++k) rec(min(i + k, last));
         }
