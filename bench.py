@@ -518,7 +518,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--bucket", type=int, default=None, choices=[-1, 0, 1], help="y-bucketing: auto/off/on")
     args = ap.parse_args()
-    args.warmup = max(args.warmup, 1)
+    args.warmup = max(args.warmup, 3)  # timing rule: at least 3 untimed warm-up steps (reported as run)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
