@@ -51,12 +51,12 @@ __device__ __forceinline__ BinMap make_map(const unsigned long long* bbox_keys, 
 
 // Atomic-free (in global memory) counting sort over P CTAs:
 //   count    CTA b histograms its contiguous chunk of points in shared memory
-//            and writes the counts to blk[b][bin];
-//   colscan  per bin, an exclusive prefix over the CTAs (blk[b][bin] becomes
-//            CTA b's offset inside the bin) and the bin total;
+//            and writes the counts to blk[bin][b] (bin-major);
+//   colscan  a warp per bin: exclusive prefix over the CTAs (blk[bin][b]
+//            becomes CTA b's offset inside the bin) and the bin total;
 //   scan     exclusive scan of the bin totals -> bin base (and n_in);
 //   scatter  CTA b re-reads its chunk and places each point at base[bin] +
-//            blk[b][bin] + (shared-memory cursor), no global atomics.
+//            blk[bin][b] + (shared-memory cursor), no global atomics.
 __global__ void __launch_bounds__(1024) bucket_count_kernel(const double2* __restrict__ pts, uint64_t n,
                                                             uint64_t chunk,
                                                             const unsigned long long* __restrict__ bbox_keys,
@@ -71,34 +71,32 @@ __global__ void __launch_bounds__(1024) bucket_count_kernel(const double2* __res
         atomicAdd(&h[m.bin(p.x, p.y)], 1u);
     }
     __syncthreads();
-    uint32_t* row = blk + (uint64_t)blockIdx.x * (kBuckets + 1);
-    for (int j = threadIdx.x; j <= kBuckets; j += blockDim.x) row[j] = h[j];
+    // bin-major: blk[bin * n_blk + block], so the per-bin scan over blocks reads contiguous memory
+    for (int j = threadIdx.x; j <= kBuckets; j += blockDim.x) blk[(uint64_t)j * gridDim.x + blockIdx.x] = h[j];
 }
 
-__global__ void __launch_bounds__(128) bucket_colscan_kernel(uint32_t* __restrict__ blk, int n_blk,
+// Per bin (one warp each): exclusive scan over the blocks of blk[bin][*]
+// (contiguous) -> each block's offset inside the bin; hist[bin] = bin total.
+__global__ void __launch_bounds__(256) bucket_colscan_kernel(uint32_t* __restrict__ blk, int n_blk,
                                                              uint32_t* __restrict__ hist) {
-    const int bin = blockIdx.x * blockDim.x + threadIdx.x;
+    const int bin = (int)((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
     if (bin > kBuckets) return;
+    uint32_t* col = blk + (uint64_t)bin * n_blk;
     uint32_t run = 0;
-    // eight rows per step: the loads are independent, so their latencies overlap
-    int b = 0;
-    for (; b + 8 <= n_blk; b += 8) {
-        uint32_t v[8];
+    for (int b0 = 0; b0 < n_blk; b0 += 32) {
+        const int b = b0 + lane;
+        const uint32_t v = b < n_blk ? col[b] : 0u;
+        uint32_t incl = v;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = blk[(uint64_t)(b + u) * (kBuckets + 1) + bin];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            blk[(uint64_t)(b + u) * (kBuckets + 1) + bin] = run;
-            run += v[u];
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
         }
+        if (b < n_blk) col[b] = run + incl - v;
+        run += __shfl_sync(0xffffffffu, incl, 31);
     }
-    for (; b < n_blk; ++b) {
-        uint32_t* p = blk + (uint64_t)b * (kBuckets + 1) + bin;
-        const uint32_t v = *p;
-        *p = run;
-        run += v;
-    }
-    hist[bin] = run;
+    if (lane == 0) hist[bin] = run;
 }
 
 // Exclusive scan of the kBuckets+1 counts (one CTA of 1024 threads): every
@@ -159,8 +157,7 @@ __global__ void __launch_bounds__(1024) bucket_scatter_kernel(const double2* __r
                                                               double2* __restrict__ sorted_pts,
                                                               uint32_t* __restrict__ sorted_idx) {
     __shared__ uint32_t cur[kBuckets + 1];
-    const uint32_t* row = blk + (uint64_t)blockIdx.x * (kBuckets + 1);
-    for (int j = threadIdx.x; j <= kBuckets; j += blockDim.x) cur[j] = base[j] + row[j];
+    for (int j = threadIdx.x; j <= kBuckets; j += blockDim.x) cur[j] = base[j] + blk[(uint64_t)j * gridDim.x + blockIdx.x];
     __syncthreads();
     const BinMap m = make_map(bbox_keys, prefilter);
     const uint64_t lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
@@ -207,7 +204,7 @@ cudaError_t launch_bucket(const BucketArgs& a, cudaStream_t st, int dev, uint64_
     const int n_blk = a.n_blk;
     const uint64_t chunk = (a.n + n_blk - 1) / n_blk;
     bucket_count_kernel<<<n_blk, 1024, 0, st>>>(p, a.n, chunk, a.bbox_keys, a.prefilter, a.blk);
-    bucket_colscan_kernel<<<(kBuckets + 1 + 127) / 128, 128, 0, st>>>(a.blk, n_blk, a.hist);
+    bucket_colscan_kernel<<<(kBuckets + 1 + 7) / 8, 256, 0, st>>>(a.blk, n_blk, a.hist);
     bucket_scan_kernel<<<1, 1024, 0, st>>>(a.hist);
     bucket_scatter_kernel<<<n_blk, 1024, 0, st>>>(p, a.n, chunk, a.bbox_keys, a.prefilter, a.blk, a.hist,
                                                   reinterpret_cast<double2*>(a.sorted_pts), a.sorted_idx);
