@@ -57,6 +57,13 @@ def ref():
         lib.ref_classify_csr.argtypes = [_vp, _vp, C.c_uint64, _vp, _vp, _vp, _vp, C.c_int, C.c_double, C.c_uint64,
                                          _vp, _vp]
         lib.ref_default_worker_count.restype = C.c_uint64
+        if hasattr(lib, "ref_parse_double"):
+            lib.ref_parse_double.argtypes = [C.c_char_p, C.c_uint64, C.POINTER(C.c_double)]
+            lib.ref_parse_double.restype = C.c_int
+            lib.ref_read_points_csv.argtypes = [C.c_char_p, C.c_char_p, C.c_uint64, C.c_char_p, C.c_uint64, C.c_int,
+                                                C.c_char, C.c_int, _vp, C.c_uint64, _vp, _vp, _vp, C.c_char_p,
+                                                C.c_uint64]
+            lib.ref_read_points_csv.restype = C.c_int
         _ref = lib
     return _ref
 
@@ -179,3 +186,33 @@ def port_count_crossings(xy, vx, vy, mode):
     err = np.zeros(n, np.uint8)
     port().orc_count_crossings(_p(xy), n, _p(vx), _p(vy), len(vx), int(mode), _p(counts), _p(err))
     return counts, err
+
+
+# ---- reference CSV reader / number parser (io.hpp; ref_io_shim.cpp) -----------------------
+
+def ref_parse_double(cell: bytes):
+    """(ok, value) of the reference's detail::parse_double (io.hpp:116-124)."""
+    lib = ref()
+    out = C.c_double(0.0)
+    ok = lib.ref_parse_double(C.c_char_p(cell), C.c_uint64(len(cell)), C.byref(out))
+    return bool(ok), out.value
+
+
+def ref_read_points_csv(path, x=1, y=2, has_header=True, delim=",", lenient=False, cap=None):
+    """The reference's read_points_csv (io.hpp:148-225) -> dict(kind, points, skipped, row, msg);
+    x / y: column name (str) or index (int); kind 0 = ok, 1 CsvParseError, 2 ColumnMissing,
+    3 FileNotFound, 4 IoError, 5 invalid_argument."""
+    lib = ref()
+    if cap is None:
+        cap = os.path.getsize(path) // 2 + 16 if os.path.exists(path) else 16
+    out = np.empty((cap, 2), np.float64)
+    n, sk, row = C.c_uint64(0), C.c_uint64(0), C.c_uint64(0)
+    msg = C.create_string_buffer(1024)
+    xs = x.encode() if isinstance(x, str) else None
+    ys = y.encode() if isinstance(y, str) else None
+    k = lib.ref_read_points_csv(str(path).encode(), xs, 0 if xs else int(x), ys, 0 if ys else int(y),
+                                int(bool(has_header)), delim.encode(), int(bool(lenient)),
+                                out.ctypes.data_as(C.c_void_p), C.c_uint64(cap), C.byref(n), C.byref(sk),
+                                C.byref(row), msg, C.c_uint64(1024))
+    return {"kind": k, "points": out[:min(n.value, cap)].copy(), "skipped": sk.value, "row": row.value,
+            "msg": msg.value.decode(errors="replace")}

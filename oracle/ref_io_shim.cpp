@@ -1,0 +1,78 @@
+// TEST INFRASTRUCTURE — NOT PRODUCT CODE.
+//
+// C-ABI shim around the *unmodified* reference CSV reader and number parser
+// (proj/include/polycast/io.hpp: detail::parse_double :116-124,
+// read_points_csv :148-225), included from /root/reference at build time.
+// Checker for the GPU CSV reader (paper_2306_04316_b200/csrc/pip_csv.cu) in
+// tests/ and the CPU baseline of bench.py's csv workload; never the product.
+#include <polycast/io.hpp>
+
+#include <cstdint>
+#include <cstring>
+#include <string>
+
+using namespace polycast;
+
+extern "C" {
+
+// 1 if the reference parses [s, s+n) as a finite double (its value in *out)
+int ref_parse_double(const char* s, uint64_t n, double* out) {
+    double v = 0.0;
+    const bool ok = detail::parse_double(std::string_view(s, n), v);
+    if (ok) *out = v;
+    return ok ? 1 : 0;
+}
+
+// read_points_csv; kind: 0 ok, 1 CsvParseError, 2 ColumnMissing, 3 FileNotFound,
+// 4 IoError, 5 std::invalid_argument, 6 other.  x_name / y_name NULL: use the index.
+int ref_read_points_csv(const char* path, const char* x_name, uint64_t x_idx, const char* y_name, uint64_t y_idx,
+                        int has_header, char delim, int lenient, double* out_xy, uint64_t cap, uint64_t* n_points,
+                        uint64_t* skipped, uint64_t* err_row, char* msg, uint64_t msg_cap) {
+    PointsFileSpec spec;
+    spec.path = path;
+    if (x_name) spec.x_column = std::string(x_name);
+    else spec.x_column = std::size_t(x_idx);
+    if (y_name) spec.y_column = std::string(y_name);
+    else spec.y_column = std::size_t(y_idx);
+    spec.has_header = has_header != 0;
+    spec.delimiter = delim;
+    spec.lenient = lenient != 0;
+    auto put = [&](const char* w) {
+        if (msg && msg_cap) {
+            std::strncpy(msg, w, msg_cap - 1);
+            msg[msg_cap - 1] = 0;
+        }
+    };
+    *n_points = *skipped = *err_row = 0;
+    try {
+        const CsvPoints r = read_points_csv(spec);
+        *n_points = r.batch.size();
+        *skipped = r.skipped_rows;
+        for (std::size_t i = 0; i < r.batch.size() && i < cap; ++i) {
+            out_xy[2 * i] = r.batch.points[i].x;
+            out_xy[2 * i + 1] = r.batch.points[i].y;
+        }
+        return 0;
+    } catch (const CsvParseError& e) {
+        *err_row = e.row;
+        put(e.what());
+        return 1;
+    } catch (const ColumnMissing& e) {
+        put(e.what());
+        return 2;
+    } catch (const FileNotFound& e) {
+        put(e.what());
+        return 3;
+    } catch (const IoError& e) {
+        put(e.what());
+        return 4;
+    } catch (const std::invalid_argument& e) {
+        put(e.what());
+        return 5;
+    } catch (const std::exception& e) {
+        put(e.what());
+        return 6;
+    }
+}
+
+} // extern "C"

@@ -46,6 +46,7 @@ struct DevState {
     DevBuf bucket_scratch, sorted_pts, sorted_idx, bucket_blk; // y-bucketing (pip_sort.cu)
     DevBuf csr_meta;                                          // per-polygon records (pip_csr.cu)
     DevBuf cmp_blk, cmp_pts, cmp_idx, cmp_v, cmp_out;         // prefilter / scatter (pip_compact.cu)
+    DevBuf csv_text, csv_ends, csv_status, csv_xy, csv_out;   // CSV reader (pip_csv.cu)
     unsigned long long* h_stats = nullptr; // pinned 4 x u64
     // profiling: one event pair per main-kernel launch since the last take
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
@@ -669,6 +670,73 @@ int pc_scatter_verdicts_dev(pc_ctx* c, int dev_index, void* stream, const uint64
         check(c, pcd::launch_scatter_verdicts(reinterpret_cast<const unsigned long long*>(d_idx), d_inbox_verdicts,
                                               n_inbox, n_total, d_out, d_bad, st, d.dev, &c->launches),
               "scatter kernel");
+    });
+}
+
+int pc_parse_points_csv(pc_ctx* c, const char* text, uint64_t len, uint64_t first_data_line, uint32_t x_col,
+                        uint32_t y_col, char delim, double* out_xy, uint64_t cap_points, uint64_t* n_points,
+                        uint64_t* n_bad, uint64_t* first_bad_line, uint32_t* first_bad_kind) {
+    return guarded(c, [&] {
+        if (!n_points || !n_bad || !first_bad_line || !first_bad_kind) invalid(c, "null outputs");
+        *first_bad_kind = 0;
+        if (x_col == y_col) invalid(c, "read_points_csv: x and y columns must differ");
+        *n_points = *n_bad = 0;
+        *first_bad_line = ~0ull;
+        if (len == 0) return;
+        if (!text) invalid(c, "null text");
+        DevState& d = c->devs[0];
+        check(c, cudaSetDevice(d.dev), "cudaSetDevice");
+        cudaStream_t st = d.stream;
+        h2d(c, d.csv_text, text, len, st, "upload text");
+        const char* dt = d.csv_text.as<char>();
+        const int nb = pcd::csv_blocks(len, d.dev);
+        check(c, d.cmp_blk.ensure((size_t)(nb + 1) * 8 + 8), "alloc scan scratch");
+        unsigned long long* blk = d.cmp_blk.as<unsigned long long>();
+        // newline count bounds the line count: allocate for the worst case of the
+        // text (one line per byte would be len + 1)
+        unsigned long long n_nl = 0;
+        check(c, d.csv_ends.ensure((len + 1) * 8), "alloc line ends");
+        check(c, pcd::launch_csv_lines(dt, len, nb, blk, d.csv_ends.as<unsigned long long>(), st, &c->launches),
+              "csv line kernels");
+        check(c, cudaMemcpyAsync(&n_nl, blk + nb, 8, cudaMemcpyDeviceToHost, st), "download line count");
+        check(c, cudaStreamSynchronize(st), "csv lines");
+        const uint64_t n_lines = n_nl + (text[len - 1] != '\n' ? 1 : 0);
+        check(c, d.csv_status.ensure(n_lines + 16), "alloc row status");
+        check(c, d.csv_xy.ensure(n_lines * 16 + 16), "alloc rows");
+        check(c, d.csv_out.ensure(n_lines * 16 + 16), "alloc points");
+        unsigned long long* first_bad = blk + nb + 1;
+        check(c, cudaMemsetAsync(first_bad, 0xff, 8, st), "init first bad");
+        check(c, pcd::launch_csv_rows(dt, len, d.csv_ends.as<unsigned long long>(), n_lines, first_data_line, x_col,
+                                      y_col, delim, d.csv_status.as<uint8_t>(), d.csv_xy.as<double>(), first_bad, st,
+                                      &c->launches),
+              "csv row kernel");
+        unsigned long long fb = ~0ull;
+        check(c, cudaMemcpyAsync(&fb, first_bad, 8, cudaMemcpyDeviceToHost, st), "download first bad");
+        const int nb2 = pcd::csv_blocks(n_lines, d.dev);
+        check(c, d.cmp_idx.ensure((size_t)(nb2 + 1) * 8), "alloc scan scratch");
+        unsigned long long* blk2 = d.cmp_idx.as<unsigned long long>();
+        check(c, pcd::launch_csv_compact(d.csv_status.as<uint8_t>(), d.csv_xy.as<double>(), n_lines, nb2, blk2,
+                                         d.csv_out.as<double>(), st, &c->launches),
+              "csv compaction kernels");
+        unsigned long long n_ok = 0;
+        check(c, cudaMemcpyAsync(&n_ok, blk2 + nb2, 8, cudaMemcpyDeviceToHost, st), "download row count");
+        check(c, cudaStreamSynchronize(st), "csv rows");
+        *first_bad_line = fb;
+        *n_points = n_ok;
+        if (fb != ~0ull) { // count the bad rows (host-side, from the statuses)
+            std::vector<uint8_t> stv(n_lines);
+            check(c, cudaMemcpy(stv.data(), d.csv_status.p, n_lines, cudaMemcpyDeviceToHost), "download statuses");
+            uint64_t bad = 0;
+            for (uint8_t v : stv) bad += v >= 2;
+            *n_bad = bad;
+            *first_bad_kind = stv[fb];
+        }
+        if (n_ok > cap_points) invalid(c, "read_points_csv: output capacity too small (n_points holds the need)");
+        if (n_ok) {
+            if (!out_xy) invalid(c, "null out_xy");
+            check(c, cudaMemcpyAsync(out_xy, d.csv_out.p, n_ok * 16, cudaMemcpyDeviceToHost, st), "download points");
+            check(c, cudaStreamSynchronize(st), "csv points");
+        }
     });
 }
 

@@ -14,6 +14,7 @@
 #include <string>
 #include <vector>
 
+#include <polycast/io.hpp>
 #include <polycast/polycast.hpp>
 
 using namespace polycast;
@@ -67,6 +68,9 @@ Polygon random_polygon(std::mt19937_64& g, std::size_t n) {
 using RefClassify = int (*)(const double*, uint64_t, const double*, const double*, const uint64_t*, uint32_t, int,
                             double, uint64_t, uint8_t*, uint64_t*);
 RefClassify g_ref = nullptr;
+using RefReadCsv = int (*)(const char*, const char*, uint64_t, const char*, uint64_t, int, char, int, double*, uint64_t,
+                           uint64_t*, uint64_t*, uint64_t*, char*, uint64_t);
+RefReadCsv g_ref_csv = nullptr;
 
 void kats() {
     const Ring sq = square();
@@ -245,16 +249,135 @@ void prefilter_scatter() {
     }
 }
 
+// read_points_csv (io.hpp:148-225) against the unmodified reference on
+// generated files: number formats, quotes, spaces, CRLF, empty lines, BOM +
+// named columns, delimiters, short rows, bad cells; strict and lenient.
+std::string rand_cell(std::mt19937_64& g) {
+    char b[64];
+    const double v = uni(g, -1e3, 1e3) * std::pow(10.0, (double)((int)(g() % 40) - 20));
+    switch (g() % 16) {
+    case 0: return "abc";
+    case 1: return "";
+    case 2: return " " + std::to_string(v) + "\t";
+    case 3: std::snprintf(b, sizeof b, "\"%.17g\"", v); return b;
+    case 4: return "+1.5";
+    case 5: return "1e999";
+    case 6: return "nan";
+    case 7: std::snprintf(b, sizeof b, "%.3e", v); return b;
+    case 8: return "1e-400";
+    case 9: return "-0";
+    default: std::snprintf(b, sizeof b, "%.17g", v); return b;
+    }
+}
+
+void csv_vs_reference() {
+    if (!g_ref_csv) {
+        std::printf("note: reference CSV reader not available; skipped\n");
+        return;
+    }
+    std::mt19937_64 g(23);
+    int compared = 0;
+    for (int trial = 0; trial < 60; ++trial) {
+        const char delim = "x,;\t"[1 + trial % 3];
+        const bool header = trial % 4 != 3, lenient = trial % 2, crlf = trial % 5 == 0, bom = trial % 7 == 1;
+        std::string text;
+        if (header) text += std::string(bom ? "\xEF\xBB\xBF" : "") + "id" + delim + "lon" + delim + "\"lat\"" + (crlf ? "\r\n" : "\n");
+        const int rows = 1 + (int)(g() % 300);
+        const bool clean = trial % 3 == 0; // clean files: no bad rows (strict mode succeeds)
+        for (int r = 0; r < rows; ++r) {
+            if (g() % 23 == 0) text += crlf ? "\r\n" : "\n"; // empty line
+            char b[64];
+            std::snprintf(b, sizeof b, "%d", r);
+            std::string row = b;
+            const int ncells = clean ? 3 : (int)(g() % 4) + 1;
+            for (int c = 1; c < ncells; ++c) {
+                std::string cell;
+                if (clean) {
+                    std::snprintf(b, sizeof b, "%.17g", uni(g, -180, 180));
+                    cell = b;
+                } else {
+                    cell = rand_cell(g);
+                }
+                row += delim + cell;
+            }
+            text += row + (crlf ? "\r\n" : "\n");
+        }
+        if (trial % 6 == 2 && !text.empty()) text.pop_back(); // no final newline
+        const std::string path = "/tmp/pc_csv_test_" + std::to_string(trial) + ".csv";
+        FILE* f = std::fopen(path.c_str(), "wb");
+        std::fwrite(text.data(), 1, text.size(), f);
+        std::fclose(f);
+        PointsFileSpec spec;
+        spec.path = path;
+        spec.delimiter = delim;
+        spec.has_header = header;
+        spec.lenient = lenient;
+        const bool named = header && trial % 2 == 0;
+        if (named) {
+            spec.x_column = std::string("lon");
+            spec.y_column = std::string("lat");
+        } else {
+            spec.x_column = std::size_t(1);
+            spec.y_column = std::size_t(2);
+        }
+        std::vector<double> ref(2 * (rows + 4));
+        uint64_t rn = 0, rs = 0, rrow = 0;
+        char msg[512] = {0};
+        const int rk = g_ref_csv(path.c_str(), named ? "lon" : nullptr, 1, named ? "lat" : nullptr, 2, header, delim,
+                                 lenient, ref.data(), rows + 4, &rn, &rs, &rrow, msg, sizeof msg);
+        int k = 0;
+        std::string what;
+        CsvPoints got;
+        try {
+            got = read_points_csv(spec);
+        } catch (const CsvParseError& e) {
+            k = 1;
+            what = e.what();
+            CHECK(e.row == rrow);
+        } catch (const ColumnMissing& e) {
+            k = 2;
+            what = e.what();
+        } catch (const IoError& e) {
+            k = 4;
+            what = e.what();
+        }
+        CHECK(k == rk);
+        if (k != rk || (k && what != msg)) std::fprintf(stderr, "trial %d: kind %d vs %d, '%s' vs '%s'\n", trial, k, rk, what.c_str(), msg);
+        if (k == 0 && rk == 0) {
+            bool ok = got.batch.size() == rn && got.skipped_rows == rs;
+            for (std::size_t i = 0; ok && i < rn; ++i)
+                ok = std::memcmp(&got.batch.points[i].x, &ref[2 * i], 8) == 0 &&
+                     std::memcmp(&got.batch.points[i].y, &ref[2 * i + 1], 8) == 0;
+            CHECK(ok);
+        } else {
+            CHECK(what == msg);
+        }
+        ++compared;
+        std::remove(path.c_str());
+    }
+    // the reference's own error cases
+    CHECK_THROWS(read_points_csv(PointsFileSpec{"/nonexistent/file.csv"}), FileNotFound);
+    PointsFileSpec same;
+    same.path = "/nonexistent/file.csv";
+    same.y_column = std::size_t(0);
+    CHECK_THROWS(read_points_csv(same), std::invalid_argument);
+    std::printf("csv: %d files compared against the reference reader\n", compared);
+}
+
 } // namespace
 
 int main(int argc, char** argv) {
     const char* ref_path = argc > 1 ? argv[1] : "oracle/_ref/libpolycast_ref.so";
-    if (void* h = dlopen(ref_path, RTLD_NOW)) g_ref = reinterpret_cast<RefClassify>(dlsym(h, "ref_classify"));
+    if (void* h = dlopen(ref_path, RTLD_NOW)) {
+        g_ref = reinterpret_cast<RefClassify>(dlsym(h, "ref_classify"));
+        g_ref_csv = reinterpret_cast<RefReadCsv>(dlsym(h, "ref_read_points_csv"));
+    }
     else std::printf("note: reference shim not found at %s; reference cross-check skipped\n", ref_path);
     try {
         kats();
         randomized();
         prefilter_scatter();
+        csv_vs_reference();
     } catch (const std::exception& e) {
         std::fprintf(stderr, "FAIL: uncaught exception: %s\n", e.what());
         return 100;

@@ -1,0 +1,175 @@
+"""Points-CSV ingest: the GPU reader behind
+pc_parse_points_csv / polycast::read_points_csv against the reference's
+read_points_csv and detail::parse_double (proj/include/polycast/io.hpp:111-119,
+148-225), compiled unmodified into oracle/_ref.
+
+CPU: the device number parser compiled as host code vs std::from_chars
+(tests/cpp/parse_test, ~2M strings) and the reference parser's own semantics.
+GPU: cell-by-cell parity with the reference parser, whole files (header,
+CRLF, empty lines, short rows, bad cells, no final newline) in lenient mode
+vs the reference reader, and the 17-significant-digit round trip of 2^20
+random doubles (bit-exact)."""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CPP = os.path.join(ROOT, "tests", "cpp")
+
+needs_ref = pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built")
+
+
+def test_device_parser_vs_from_chars():
+    subprocess.run(["make", "-s", "-C", CPP, os.path.join(CPP, "parse_test")], check=True)
+    r = subprocess.run([os.path.join(CPP, "parse_test")], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:]
+    assert " 0 mismatches" in r.stdout
+
+
+@needs_ref
+@pytest.mark.parametrize("cell,ok,val", [
+    (b"1.5", True, 1.5), (b" 2.25\t", True, 2.25), (b'"-3"', True, -3.0), (b"+1", False, None),
+    (b"1e400", False, None), (b"1e-400", False, None), (b"nan", False, None), (b"inf", False, None),
+    (b"", False, None), (b'""', False, None), (b"1,5", False, None), (b"4.9e-324", True, 5e-324),
+    (b"0x10", False, None), (b"-0", True, -0.0), (b"1.", True, 1.0), (b".5", True, 0.5)])
+def test_reference_parse_double_semantics(cell, ok, val):
+    """Pins the reference semantics the GPU parser follows (io.hpp:111-119)."""
+    got_ok, got = oracle.ref_parse_double(cell)
+    assert got_ok == ok
+    if ok:
+        assert np.float64(got).tobytes() == np.float64(val).tobytes()
+
+
+def _cells(rng, n):
+    """A mix of well-formed numbers in many formats and malformed cells."""
+    u = rng.integers(0, 2 ** 63, n, dtype=np.uint64) | (rng.integers(0, 2, n, dtype=np.uint64) << np.uint64(63))
+    d = u.view(np.float64)
+    out = []
+    fmts = ["%.17g", "%.16g", "%.6e", "%.25g", "%.3f", "%.20e"]
+    bad = [b"abc", b"", b"+1.5", b"1e999", b"nan", b"-inf", b"1e-400", b"1..2", b"--1", b"1e", b" ", b'"', b"0x1p3"]
+    for i in range(n):
+        k = int(rng.integers(0, 12))
+        v = d[i]
+        if not np.isfinite(v):
+            v = float(rng.standard_normal())
+        if k < 6:
+            s = (fmts[k] % v).encode()
+        elif k == 6:
+            s = bad[int(rng.integers(0, len(bad)))]
+        elif k == 7:
+            s = b'"' + (b"%.17g" % v) + b'"'
+        elif k == 8:
+            s = b" \t" + (b"%.9g" % (rng.standard_normal() * 10.0 ** rng.integers(-30, 30))) + b"\t "
+        elif k == 9:  # long digit strings
+            s = "".join(map(str, rng.integers(0, 10, int(rng.integers(18, 60))))).encode()
+            s = s[:5] + b"." + s[5:] + b"e" + str(int(rng.integers(-330, 300))).encode()
+        elif k == 10:  # subnormal / boundary magnitudes
+            s = b"%.17g" % (float(rng.random()) * 10.0 ** float(rng.integers(-325, -300)))
+        else:
+            s = b"%d" % int(rng.integers(-(2 ** 62), 2 ** 62))
+        out.append(s)
+    return out
+
+
+@needs_ref
+@pytest.mark.gpu
+def test_cells_match_reference_parser(engine):
+    rng = np.random.default_rng(5)
+    cells = _cells(rng, 60_000)
+    # one cell per row in column 1 (x), a fixed good y in column 2
+    text = b"id,x,y\n" + b"".join(b"%d,%s,0.5\n" % (i, c) for i, c in enumerate(cells))
+    ref = [oracle.ref_parse_double(c) for c in cells]
+    xy, n_bad, first_bad, kind = engine.parse_points_csv(text, 1, 1, 2, ",")
+    want = np.array([v for ok, v in ref if ok], np.float64)
+    assert n_bad == sum(1 for ok, _ in ref if not ok)
+    assert len(xy) == len(want)
+    assert xy[:, 0].tobytes() == want.tobytes()
+    assert np.all(xy[:, 1] == 0.5)
+    bad_rows = [i for i, (ok, _) in enumerate(ref) if not ok]
+    if bad_rows:
+        assert first_bad == bad_rows[0] + 1 and kind == 3
+
+
+def _rand_file(rng, path, delim, header, crlf, final_nl, rows):
+    eol = b"\r\n" if crlf else b"\n"
+    d = delim.encode()
+    lines = []
+    if header:
+        lines.append(b"id" + d + b"lon" + d + b"lat")
+    for r in range(rows):
+        if rng.random() < 0.03:
+            lines.append(b"")
+        nc = int(rng.integers(1, 5)) if rng.random() < 0.2 else 3
+        cells = [b"%d" % r]
+        for c in range(1, nc):
+            p = rng.random()
+            if p < 0.05:
+                cells.append(b"bad")
+            elif p < 0.08:
+                cells.append(b"")
+            else:
+                cells.append(b"%.17g" % (rng.uniform(-180, 180)))
+        lines.append(d.join(cells))
+    text = eol.join(lines) + (eol if final_nl else b"")
+    with open(path, "wb") as f:
+        f.write(text)
+    return text
+
+
+@needs_ref
+@pytest.mark.gpu
+@pytest.mark.parametrize("trial", range(8))
+def test_files_match_reference_reader(engine, tmp_path, trial):
+    """Lenient read: same points (bitwise) and skipped count as the reference;
+    the first bad line is the reference's strict-mode error row."""
+    rng = np.random.default_rng(100 + trial)
+    delim = ",;\t,"[trial % 4]
+    header = trial % 3 != 2
+    path = tmp_path / f"p{trial}.csv"
+    rows = [0, 1, 7, 500, 3000, 20000, 64, 100_000][trial]
+    text = _rand_file(rng, path, delim, header, crlf=trial % 2 == 1, final_nl=trial % 4 != 3, rows=rows)
+    ref = oracle.ref_read_points_csv(str(path), 1, 2, has_header=header, delim=delim, lenient=True)
+    assert ref["kind"] == 0, ref["msg"]
+    first_data_line = 0
+    if header:  # the header is the first line (no leading empty lines here)
+        first_data_line = 1
+    xy, n_bad, first_bad, kind = engine.parse_points_csv(text, first_data_line, 1, 2, delim)
+    assert n_bad == ref["skipped"]
+    assert xy.shape == ref["points"].shape
+    assert xy.tobytes() == ref["points"].tobytes()
+    strict = oracle.ref_read_points_csv(str(path), 1, 2, has_header=header, delim=delim, lenient=False)
+    if strict["kind"] == 1:
+        lines = text.split(b"\n")
+        data_row = sum(1 for ln in lines[first_data_line:first_bad + 1] if ln.rstrip(b"\r"))
+        assert data_row == strict["row"]
+        assert ("row has only" in strict["msg"]) == (kind == 2)
+    else:
+        assert first_bad is None
+
+
+@pytest.mark.gpu
+def test_round_trip_17_digits(engine):
+    """%.17g of any finite double parses back to the same bits (2^20 rows)."""
+    rng = np.random.default_rng(9)
+    u = rng.integers(0, 2 ** 64, (1 << 20, 2), dtype=np.uint64)
+    v = u.view(np.float64).copy()
+    v[~np.isfinite(v)] = 1.0
+    text = "\n".join("%.17g,%.17g" % (a, b) for a, b in v).encode()
+    xy, n_bad, first_bad, _ = engine.parse_points_csv(text, 0, 0, 1, ",")
+    assert n_bad == 0 and first_bad is None
+    assert xy.tobytes() == v.tobytes()
+
+
+@pytest.mark.gpu
+def test_empty_and_degenerate_texts(engine):
+    assert engine.parse_points_csv(b"", 0, 0, 1)[0].shape == (0, 2)
+    xy, n_bad, fb, _ = engine.parse_points_csv(b"\n\r\n\n", 0, 0, 1)
+    assert len(xy) == 0 and n_bad == 0 and fb is None
+    xy, n_bad, fb, kind = engine.parse_points_csv(b"1,2\n3\n4,5", 0, 0, 1)
+    assert xy.tolist() == [[1.0, 2.0], [4.0, 5.0]] and n_bad == 1 and fb == 1 and kind == 2
+    xy, n_bad, fb, kind = engine.parse_points_csv(b"1,x\r\n", 0, 0, 1)
+    assert len(xy) == 0 and n_bad == 1 and fb == 0 and kind == 4
