@@ -144,20 +144,29 @@ int pc_scatter_verdicts_dev(pc_ctx* ctx, int dev_index, void* stream, const uint
 
 /* The data-row loop of read_points_csv (io.hpp:148-225) on GPU 0 of the
  * context: text[len] is the file's bytes; lines split at '\n' (a trailing
- * '\r' is removed, empty lines skipped); lines before first_data_line (the
- * header and the empty lines before it) are not data rows.  Each data row is
- * split at `delim` and cells x_col / y_col are parsed as the reference's
- * parse_double does (one pair of surrounding quotes and spaces/tabs stripped,
- * then a correctly rounded, finite binary64).  Good rows are written to
- * out_xy in file order, *n_points of them; *n_bad counts the rows that have
- * too few cells or a cell that is not a finite number (the rows lenient mode
- * skips), and *first_bad_line is the 0-based line index of the first such row
- * (UINT64_MAX if none) -- strict mode reports it -- with *first_bad_kind =
- * 2 (too few cells), 3 (x cell) or 4 (y cell).  If cap_points < *n_points,
- * nothing is copied and PC_EINVAL is returned with *n_points set. */
-int pc_parse_points_csv(pc_ctx* ctx, const char* text, uint64_t len, uint64_t first_data_line, uint32_t x_col,
+ * '\r' is removed, empty lines skipped); lines starting before byte
+ * data_start (the header and the empty lines before it) are not data rows.
+ * Each data row is split at `delim` and cells x_col / y_col are parsed as the
+ * reference's parse_double does (one pair of surrounding quotes and
+ * spaces/tabs stripped, then a correctly rounded, finite binary64).  Good rows
+ * are written to out_xy in file order, *n_points of them; *n_bad counts the
+ * rows that have too few cells or a cell that is not a finite number (the rows
+ * lenient mode skips), *first_bad_offset is the byte offset of the first such
+ * row's line (UINT64_MAX if none) -- strict mode reports it -- with
+ * *first_bad_kind = 2 (too few cells), 3 (x cell) or 4 (y cell).  If
+ * cap_points < *n_points, nothing is copied and PC_EINVAL is returned with
+ * *n_points set.  x_col == y_col is PC_EINVAL (io.hpp:149-156). */
+int pc_parse_points_csv(pc_ctx* ctx, const char* text, uint64_t len, uint64_t data_start, uint32_t x_col,
                         uint32_t y_col, char delim, double* out_xy, uint64_t cap_points, uint64_t* n_points,
-                        uint64_t* n_bad, uint64_t* first_bad_line, uint32_t* first_bad_kind);
+                        uint64_t* n_bad, uint64_t* first_bad_offset, uint32_t* first_bad_kind);
+
+/* Device-pointer variant (not synchronised): d_text in device memory, points
+ * to d_out_xy (at most cap_points written); d_result = 4 x u64 in device
+ * memory: [0] good rows (may exceed cap_points), [1] bad rows, [2] first bad
+ * row as (line offset << 3 | kind) or UINT64_MAX, [3] scratch.  One kernel. */
+int pc_parse_points_csv_dev(pc_ctx* ctx, int dev_index, void* stream, const char* d_text, uint64_t len,
+                            uint64_t data_start, uint32_t x_col, uint32_t y_col, char delim, double* d_out_xy,
+                            uint64_t cap_points, uint64_t* d_result);
 
 /* Number of GPU kernels the last call on this context launched (all devices). */
 uint64_t pc_last_launch_count(const pc_ctx* ctx);

@@ -7,6 +7,7 @@
 // / Boundary outcomes come back as bit planes + verdict bytes + BatchStats.
 #include "../../include/polycast_cuda.h"
 #include "pip_kernels.h"
+#include "host_stage.h"
 
 #include <cuda_runtime.h>
 
@@ -46,8 +47,9 @@ struct DevState {
     DevBuf bucket_scratch, sorted_pts, sorted_idx, bucket_blk; // y-bucketing (pip_sort.cu)
     DevBuf csr_meta;                                          // per-polygon records (pip_csr.cu)
     DevBuf cmp_blk, cmp_pts, cmp_idx, cmp_v, cmp_out;         // prefilter / scatter (pip_compact.cu)
-    DevBuf csv_text, csv_ends, csv_status, csv_xy, csv_out;   // CSV reader (pip_csv.cu)
+    DevBuf csv_text, csv_state, csv_res, csv_out;             // CSV reader (pip_csv.cu)
     unsigned long long* h_stats = nullptr; // pinned 4 x u64
+    pch::Stager* stager = nullptr;         // pageable host copies (host_stage.h), made on first use
     // profiling: one event pair per main-kernel launch since the last take
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
     size_t ev_used = 0;
@@ -232,9 +234,20 @@ void enqueue_csr(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts, u
           "finalize kernel");
 }
 
-void h2d(pc_ctx* c, DevBuf& b, const void* src, size_t bytes, cudaStream_t st, const char* what) {
+pch::Stager& stager(DevState& d) {
+    if (!d.stager) d.stager = new pch::Stager();
+    return *d.stager;
+}
+
+// upload (pageable sources of >= 4 MiB go through the pinned staging chunks)
+void h2d(pc_ctx* c, DevState& d, DevBuf& b, const void* src, size_t bytes, cudaStream_t st, const char* what) {
     check(c, b.ensure(std::max<size_t>(bytes, 16)), what);
-    if (bytes) check(c, cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, st), what);
+    if (bytes) check(c, stager(d).h2d(b.p, src, bytes, st), what);
+}
+
+// download after the work queued on st; complete on return
+void d2h(pc_ctx* c, DevState& d, void* dst, const void* src, size_t bytes, cudaStream_t st, const char* what) {
+    if (bytes) check(c, stager(d).d2h(dst, src, bytes, st), what);
 }
 
 // OR `nbits` bits from src (bit 0 = point `bit_off` of the destination) into dst.
@@ -307,9 +320,11 @@ void pc_destroy(pc_ctx* c) {
         cudaStreamSynchronize(d.stream);
         for (DevBuf* b : {&d.pts, &d.vx, &d.vy, &d.ring_off, &d.pt_off, &d.poly_ring_off, &d.filt, &d.rec, &d.bbox,
                           &d.bits, &d.verdicts, &d.stats, &d.counts, &d.degen, &d.bucket_scratch, &d.sorted_pts,
-                          &d.sorted_idx, &d.bucket_blk})
+                          &d.sorted_idx, &d.bucket_blk, &d.csr_meta, &d.cmp_blk, &d.cmp_pts, &d.cmp_idx, &d.cmp_v,
+                          &d.cmp_out, &d.csv_text, &d.csv_state, &d.csv_res, &d.csv_out})
             b->release();
         if (d.h_stats) cudaFreeHost(d.h_stats);
+        delete d.stager;
         for (auto& e : d.evs) {
             cudaEventDestroy(e.first);
             cudaEventDestroy(e.second);
@@ -420,10 +435,10 @@ int pc_classify(pc_ctx* c, const double* pts_xy, uint64_t n, const double* vx, c
             const uint64_t m = parts[i].hi - parts[i].lo, nwords = (m + 31) / 32;
             check(c, cudaSetDevice(d.dev), "cudaSetDevice");
             cudaStream_t st = d.stream;
-            h2d(c, d.pts, pts_xy + 2 * parts[i].lo, m * 16, st, "upload points");
-            h2d(c, d.vx, vx, n_verts * 8, st, "upload vx");
-            h2d(c, d.vy, vy, n_verts * 8, st, "upload vy");
-            h2d(c, d.ring_off, ring_off, (n_rings + 1) * 8ull, st, "upload ring_off");
+            h2d(c, d, d.pts, pts_xy + 2 * parts[i].lo, m * 16, st, "upload points");
+            h2d(c, d, d.vx, vx, n_verts * 8, st, "upload vx");
+            h2d(c, d, d.vy, vy, n_verts * 8, st, "upload vy");
+            h2d(c, d, d.ring_off, ring_off, (n_rings + 1) * 8ull, st, "upload ring_off");
             check(c, d.bits.ensure(2 * nwords * 4), "alloc bit planes");
             check(c, d.stats.ensure(4 * 8), "alloc stats");
             uint8_t* dv = nullptr;
@@ -497,12 +512,12 @@ int pc_classify_csr(pc_ctx* c, const double* pts_xy, const uint64_t* pt_off, uin
             cudaStream_t st = d.stream;
             const uint64_t r0 = poly_ring_off[p0], r1 = poly_ring_off[p1];
             const uint64_t v0 = r1 > r0 ? ring_off[r0] : 0, v1 = r1 > r0 ? ring_off[r1] : 0;
-            h2d(c, d.pts, pts_xy + 2 * (s - P0), m * 16, st, "upload points");
-            h2d(c, d.pt_off, pt_off + p0, (p1 - p0 + 1) * 8, st, "upload pt_off");
-            h2d(c, d.poly_ring_off, poly_ring_off + p0, (p1 - p0 + 1) * 8, st, "upload poly_ring_off");
-            h2d(c, d.ring_off, ring_off + r0, (r1 - r0 + 1) * 8, st, "upload ring_off");
-            h2d(c, d.vx, vx + v0, (v1 - v0) * 8, st, "upload vx");
-            h2d(c, d.vy, vy + v0, (v1 - v0) * 8, st, "upload vy");
+            h2d(c, d, d.pts, pts_xy + 2 * (s - P0), m * 16, st, "upload points");
+            h2d(c, d, d.pt_off, pt_off + p0, (p1 - p0 + 1) * 8, st, "upload pt_off");
+            h2d(c, d, d.poly_ring_off, poly_ring_off + p0, (p1 - p0 + 1) * 8, st, "upload poly_ring_off");
+            h2d(c, d, d.ring_off, ring_off + r0, (r1 - r0 + 1) * 8, st, "upload ring_off");
+            h2d(c, d, d.vx, vx + v0, (v1 - v0) * 8, st, "upload vx");
+            h2d(c, d, d.vy, vy + v0, (v1 - v0) * 8, st, "upload vy");
             check(c, d.bits.ensure(2 * nwords * 4), "alloc bit planes");
             check(c, d.stats.ensure(32), "alloc stats");
             uint8_t* dv = nullptr;
@@ -548,9 +563,9 @@ int pc_count_crossings(pc_ctx* c, const double* pts_xy, uint64_t n, const double
         DevState& d = c->devs[0];
         check(c, cudaSetDevice(d.dev), "cudaSetDevice");
         cudaStream_t st = d.stream;
-        h2d(c, d.pts, pts_xy, n * 16, st, "upload points");
-        h2d(c, d.vx, vx, nv * 8, st, "upload vx");
-        h2d(c, d.vy, vy, nv * 8, st, "upload vy");
+        h2d(c, d, d.pts, pts_xy, n * 16, st, "upload points");
+        h2d(c, d, d.vx, vx, nv * 8, st, "upload vx");
+        h2d(c, d, d.vy, vy, nv * 8, st, "upload vy");
         check(c, d.counts.ensure(n * 8), "alloc counts");
         check(c, d.degen.ensure(n), "alloc flags");
         check(c, pcd::launch_count(d.pts.as<double>(), n, d.vx.as<double>(), d.vy.as<double>(), nv, mode,
@@ -592,7 +607,7 @@ int pc_prefilter_bbox(pc_ctx* c, const double* pts_xy, uint64_t n, const double 
         DevState& d = c->devs[0];
         check(c, cudaSetDevice(d.dev), "cudaSetDevice");
         cudaStream_t st = d.stream;
-        h2d(c, d.cmp_pts, pts_xy, n * 16, st, "upload points");
+        h2d(c, d, d.cmp_pts, pts_xy, n * 16, st, "upload points");
         check(c, d.cmp_out.ensure(n * 16), "alloc compacted points");
         check(c, d.cmp_idx.ensure(n * 8), "alloc indices");
         const unsigned long long* cnt = enqueue_prefilter(c, d, st, d.cmp_pts.as<double>(), n, box,
@@ -601,9 +616,8 @@ int pc_prefilter_bbox(pc_ctx* c, const double* pts_xy, uint64_t n, const double 
         check(c, cudaMemcpyAsync(&k, cnt, 8, cudaMemcpyDeviceToHost, st), "download count");
         check(c, cudaStreamSynchronize(st), "prefilter");
         if (k) {
-            check(c, cudaMemcpyAsync(out_xy, d.cmp_out.p, k * 16, cudaMemcpyDeviceToHost, st), "download points");
-            check(c, cudaMemcpyAsync(out_idx, d.cmp_idx.p, k * 8, cudaMemcpyDeviceToHost, st), "download indices");
-            check(c, cudaStreamSynchronize(st), "prefilter");
+            d2h(c, d, out_xy, d.cmp_out.p, k * 16, st, "download points");
+            d2h(c, d, out_idx, d.cmp_idx.p, k * 8, st, "download indices");
         }
         *n_inside = k;
     });
@@ -618,8 +632,8 @@ int pc_scatter_verdicts(pc_ctx* c, const uint64_t* idx, const uint8_t* inbox_ver
         DevState& d = c->devs[0];
         check(c, cudaSetDevice(d.dev), "cudaSetDevice");
         cudaStream_t st = d.stream;
-        h2d(c, d.cmp_idx, idx, n_inbox * 8, st, "upload indices");
-        h2d(c, d.cmp_v, inbox_verdicts, n_inbox, st, "upload verdicts");
+        h2d(c, d, d.cmp_idx, idx, n_inbox * 8, st, "upload indices");
+        h2d(c, d, d.cmp_v, inbox_verdicts, n_inbox, st, "upload verdicts");
         const size_t off = (n_total + 7) & ~7ull; // the out-of-range flag after the verdicts
         check(c, d.cmp_out.ensure(off + 16), "alloc verdicts");
         uint8_t* o = d.cmp_out.as<uint8_t>();
@@ -630,7 +644,7 @@ int pc_scatter_verdicts(pc_ctx* c, const uint64_t* idx, const uint8_t* inbox_ver
               "scatter kernel");
         unsigned b = 0;
         check(c, cudaMemcpyAsync(&b, bad, 4, cudaMemcpyDeviceToHost, st), "download flag");
-        check(c, cudaMemcpyAsync(out, o, n_total, cudaMemcpyDeviceToHost, st), "download verdicts");
+        d2h(c, d, out, o, n_total, st, "download verdicts");
         check(c, cudaStreamSynchronize(st), "scatter_verdicts");
         if (b) invalid(c, "scatter_verdicts: original index out of range");
     });
@@ -673,70 +687,67 @@ int pc_scatter_verdicts_dev(pc_ctx* c, int dev_index, void* stream, const uint64
     });
 }
 
-int pc_parse_points_csv(pc_ctx* c, const char* text, uint64_t len, uint64_t first_data_line, uint32_t x_col,
+int pc_parse_points_csv(pc_ctx* c, const char* text, uint64_t len, uint64_t data_start, uint32_t x_col,
                         uint32_t y_col, char delim, double* out_xy, uint64_t cap_points, uint64_t* n_points,
-                        uint64_t* n_bad, uint64_t* first_bad_line, uint32_t* first_bad_kind) {
+                        uint64_t* n_bad, uint64_t* first_bad_offset, uint32_t* first_bad_kind) {
     return guarded(c, [&] {
-        if (!n_points || !n_bad || !first_bad_line || !first_bad_kind) invalid(c, "null outputs");
+        if (!n_points || !n_bad || !first_bad_offset || !first_bad_kind) invalid(c, "null outputs");
         *first_bad_kind = 0;
-        if (x_col == y_col) invalid(c, "read_points_csv: x and y columns must differ");
         *n_points = *n_bad = 0;
-        *first_bad_line = ~0ull;
+        *first_bad_offset = ~0ull;
+        if (x_col == y_col) invalid(c, "read_points_csv: x and y columns must differ");
         if (len == 0) return;
         if (!text) invalid(c, "null text");
         DevState& d = c->devs[0];
         check(c, cudaSetDevice(d.dev), "cudaSetDevice");
         cudaStream_t st = d.stream;
-        h2d(c, d.csv_text, text, len, st, "upload text");
-        const char* dt = d.csv_text.as<char>();
-        const int nb = pcd::csv_blocks(len, d.dev);
-        check(c, d.cmp_blk.ensure((size_t)(nb + 1) * 8 + 8), "alloc scan scratch");
-        unsigned long long* blk = d.cmp_blk.as<unsigned long long>();
-        // newline count bounds the line count: allocate for the worst case of the
-        // text (one line per byte would be len + 1)
-        unsigned long long n_nl = 0;
-        check(c, d.csv_ends.ensure((len + 1) * 8), "alloc line ends");
-        check(c, pcd::launch_csv_lines(dt, len, nb, blk, d.csv_ends.as<unsigned long long>(), st, &c->launches),
-              "csv line kernels");
-        check(c, cudaMemcpyAsync(&n_nl, blk + nb, 8, cudaMemcpyDeviceToHost, st), "download line count");
-        check(c, cudaStreamSynchronize(st), "csv lines");
-        const uint64_t n_lines = n_nl + (text[len - 1] != '\n' ? 1 : 0);
-        check(c, d.csv_status.ensure(n_lines + 16), "alloc row status");
-        check(c, d.csv_xy.ensure(n_lines * 16 + 16), "alloc rows");
-        check(c, d.csv_out.ensure(n_lines * 16 + 16), "alloc points");
-        unsigned long long* first_bad = blk + nb + 1;
-        check(c, cudaMemsetAsync(first_bad, 0xff, 8, st), "init first bad");
-        check(c, pcd::launch_csv_rows(dt, len, d.csv_ends.as<unsigned long long>(), n_lines, first_data_line, x_col,
-                                      y_col, delim, d.csv_status.as<uint8_t>(), d.csv_xy.as<double>(), first_bad, st,
-                                      &c->launches),
-              "csv row kernel");
-        unsigned long long fb = ~0ull;
-        check(c, cudaMemcpyAsync(&fb, first_bad, 8, cudaMemcpyDeviceToHost, st), "download first bad");
-        const int nb2 = pcd::csv_blocks(n_lines, d.dev);
-        check(c, d.cmp_idx.ensure((size_t)(nb2 + 1) * 8), "alloc scan scratch");
-        unsigned long long* blk2 = d.cmp_idx.as<unsigned long long>();
-        check(c, pcd::launch_csv_compact(d.csv_status.as<uint8_t>(), d.csv_xy.as<double>(), n_lines, nb2, blk2,
-                                         d.csv_out.as<double>(), st, &c->launches),
-              "csv compaction kernels");
-        unsigned long long n_ok = 0;
-        check(c, cudaMemcpyAsync(&n_ok, blk2 + nb2, 8, cudaMemcpyDeviceToHost, st), "download row count");
-        check(c, cudaStreamSynchronize(st), "csv rows");
-        *first_bad_line = fb;
+        h2d(c, d, d.csv_text, text, len, st, "upload text");
+        check(c, d.csv_state.ensure(pcd::csv_scratch_bytes(len)), "alloc csv scratch");
+        // a good row spans >= 4 bytes ("d,d\n") except the file's last: (len + 1) / 4 bounds the rows
+        const uint64_t dev_cap = std::min<uint64_t>(cap_points, (len + 1) / 4 + 1);
+        check(c, d.csv_out.ensure(std::max<uint64_t>(dev_cap, 1) * 16), "alloc points");
+        check(c, d.csv_res.ensure(4 * 8), "alloc results");
+        unsigned long long* res = d.csv_res.as<unsigned long long>();
+        mark_begin(c, d, st);
+        check(c, pcd::launch_csv_points(d.csv_text.as<char>(), len, data_start, x_col, y_col, delim,
+                                        d.csv_out.as<double>(), dev_cap, d.csv_state.p,
+                                        res, st, &c->launches),
+              "csv kernel");
+        mark_end(c, d, st);
+        check(c, cudaMemcpyAsync(d.h_stats, res, 32, cudaMemcpyDeviceToHost, st), "download counts");
+        check(c, cudaStreamSynchronize(st), "csv");
+        const uint64_t n_ok = d.h_stats[0], fb = d.h_stats[2];
         *n_points = n_ok;
-        if (fb != ~0ull) { // count the bad rows (host-side, from the statuses)
-            std::vector<uint8_t> stv(n_lines);
-            check(c, cudaMemcpy(stv.data(), d.csv_status.p, n_lines, cudaMemcpyDeviceToHost), "download statuses");
-            uint64_t bad = 0;
-            for (uint8_t v : stv) bad += v >= 2;
-            *n_bad = bad;
-            *first_bad_kind = stv[fb];
+        *n_bad = d.h_stats[1];
+        if (fb != ~0ull) {
+            *first_bad_offset = fb >> 3;
+            *first_bad_kind = (uint32_t)(fb & 7);
         }
         if (n_ok > cap_points) invalid(c, "read_points_csv: output capacity too small (n_points holds the need)");
         if (n_ok) {
             if (!out_xy) invalid(c, "null out_xy");
-            check(c, cudaMemcpyAsync(out_xy, d.csv_out.p, n_ok * 16, cudaMemcpyDeviceToHost, st), "download points");
-            check(c, cudaStreamSynchronize(st), "csv points");
+            d2h(c, d, out_xy, d.csv_out.p, n_ok * 16, st, "download points");
         }
+    });
+}
+
+int pc_parse_points_csv_dev(pc_ctx* c, int dev_index, void* stream, const char* d_text, uint64_t len,
+                            uint64_t data_start, uint32_t x_col, uint32_t y_col, char delim, double* d_out_xy,
+                            uint64_t cap_points, uint64_t* d_result) {
+    return guarded(c, [&] {
+        if (dev_index < 0 || dev_index >= (int)c->devs.size()) invalid(c, "bad device index");
+        if (x_col == y_col) invalid(c, "read_points_csv: x and y columns must differ");
+        if (!d_result || (len && !d_text) || (cap_points && !d_out_xy)) invalid(c, "null arrays");
+        DevState& d = c->devs[dev_index];
+        check(c, cudaSetDevice(d.dev), "cudaSetDevice");
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d.stream;
+        check(c, d.csv_state.ensure(pcd::csv_scratch_bytes(len)), "alloc csv scratch");
+        mark_begin(c, d, st);
+        check(c, pcd::launch_csv_points(d_text, len, data_start, x_col, y_col, delim, d_out_xy, cap_points,
+                                        d.csv_state.p,
+                                        reinterpret_cast<unsigned long long*>(d_result), st, &c->launches),
+              "csv kernel");
+        mark_end(c, d, st);
     });
 }
 

@@ -81,15 +81,15 @@ cudaError_t launch_prefilter(const double* pts, uint64_t n, const double box[4],
 cudaError_t launch_scatter_verdicts(const unsigned long long* idx, const uint8_t* v, uint64_t n_in, uint64_t n_total,
                                     uint8_t* out, unsigned* bad, cudaStream_t st, int dev, uint64_t* launches);
 
-// GPU points-CSV reader (pip_csv.cu)
-int csv_blocks(uint64_t n, int dev);
-cudaError_t launch_csv_lines(const char* text, uint64_t len, int nb, unsigned long long* blk,
-                             unsigned long long* ends, cudaStream_t st, uint64_t* launches);
-cudaError_t launch_csv_rows(const char* text, uint64_t len, const unsigned long long* ends, uint64_t n_lines,
-                            uint64_t first_data_line, uint32_t x_idx, uint32_t y_idx, char delim, uint8_t* status,
-                            double* xy, unsigned long long* first_bad, cudaStream_t st, uint64_t* launches);
-cudaError_t launch_csv_compact(const uint8_t* status, const double* xy, uint64_t n_lines, int nb,
-                               unsigned long long* blk, double* out, cudaStream_t st, uint64_t* launches);
+// GPU points-CSV reader (pip_csv.cu): three launches (parse tiles, scan the
+// tile counts, emit); scratch = csv_scratch_bytes(len) bytes of device memory;
+// res = 4 words ([0] rows kept, [1] bad rows, [2] first bad row as (line start
+// offset << 3 | kind), [3] unused), reset here.
+uint64_t csv_tiles(uint64_t len);
+uint64_t csv_scratch_bytes(uint64_t len);
+cudaError_t launch_csv_points(const char* text, uint64_t len, uint64_t data_start, uint32_t x_idx, uint32_t y_idx,
+                              char delim, double* out, uint64_t cap, void* scratch, unsigned long long* res,
+                              cudaStream_t st, uint64_t* launches);
 
 // y-bucketing of the points of one polygon (pip_sort.cu): counting sort by
 // y over the outer ring's bbox into kBuckets bins; bbox-rejected points

@@ -251,6 +251,34 @@ PC_HD uint64_t exact_decide(const char* s, int n, int64_t exp10, uint64_t lo_bit
     return (lo_bits & 1u) ? lo_bits + 1 : lo_bits; // tie: to even
 }
 
+// ---- SWAR digit runs (8 or 4 ASCII bytes at once, little-endian) ---------------
+PC_HD uint64_t load_le(const char* p, int k) {
+    uint64_t v = 0;
+    for (int j = 0; j < k; ++j) v |= (uint64_t)(uint8_t)p[j] << (8 * j);
+    return v;
+}
+// every byte in '0'..'9': high nibble 3, and adding 6 does not carry out of the low nibble
+PC_HD bool all_digits8(uint64_t v) {
+    return ((v & 0xf0f0f0f0f0f0f0f0ull) | (((v + 0x0606060606060606ull) & 0xf0f0f0f0f0f0f0f0ull) >> 4)) ==
+           0x3333333333333333ull;
+}
+PC_HD bool all_digits4(uint32_t v) {
+    return ((v & 0xf0f0f0f0u) | (((v + 0x06060606u) & 0xf0f0f0f0u) >> 4)) == 0x33333333u;
+}
+// value of 8 digit bytes (first digit in the low byte): pairs, then quads, then the two halves
+PC_HD uint32_t digits8(uint64_t v) {
+    v -= 0x3030303030303030ull;
+    v = v * 10 + (v >> 8);                                  // byte 2k: 2-digit value of digits 2k, 2k+1
+    v = ((v & 0x000000ff000000ffull) * (100 + (1000000ull << 32)) +
+         ((v >> 16) & 0x000000ff000000ffull) * (1 + (10000ull << 32))) >> 32;
+    return (uint32_t)v;
+}
+PC_HD uint32_t digits4(uint32_t v) {
+    v -= 0x30303030u;
+    v = v * 10 + (v >> 8);                      // bytes 0 and 2: 2-digit values
+    return (v & 0xff) * 100 + ((v >> 16) & 0xff);
+}
+
 // Parses the whole range [s, s+n).  Returns true and *out on success.
 PC_HD bool parse_f64(const char* s, int n, double* out) {
     int i = 0;
@@ -264,6 +292,29 @@ PC_HD bool parse_f64(const char* s, int n, double* out) {
     int nsig = 0, frac = 0, ndig = 0;
     bool trunc = false, point = false;
     for (; i < n; ++i) {
+        // runs of digits inside the 19-digit window, 8 or 4 at a time (after the first significant one)
+        if (nsig > 0 && nsig <= 11 && i + 8 <= n) {
+            const uint64_t v = load_le(s + i, 8);
+            if (all_digits8(v)) {
+                w = w * 100000000ull + digits8(v);
+                nsig += 8;
+                ndig += 8;
+                if (point) frac += 8;
+                i += 7;
+                continue;
+            }
+        }
+        if (nsig > 0 && nsig <= 15 && i + 4 <= n) {
+            const uint32_t v = (uint32_t)load_le(s + i, 4);
+            if (all_digits4(v)) {
+                w = w * 10000ull + digits4(v);
+                nsig += 4;
+                ndig += 4;
+                if (point) frac += 4;
+                i += 3;
+                continue;
+            }
+        }
         const char c = s[i];
         if (c == '.') {
             if (point) break;

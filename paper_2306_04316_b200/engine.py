@@ -288,25 +288,27 @@ class Engine:
         self._check(rc, "pc_scatter_verdicts")
         return out
 
-    def parse_points_csv(self, text: bytes, first_data_line: int, x_col: int, y_col: int, delim: str = ","):
+    def parse_points_csv(self, text: bytes, data_start: int, x_col: int, y_col: int, delim: str = ","):
         """The data-row loop of read_points_csv on the GPU (pc_parse_points_csv):
-        (xy float64 (n,2) of the good rows in file order, n_bad, first_bad_line or None,
-        first_bad_kind (2 short row, 3 x cell, 4 y cell))."""
+        (xy float64 (n,2) of the good rows in file order, n_bad, byte offset of the
+        first bad row's line or None, its kind (2 short row, 3 x cell, 4 y cell))."""
         buf = np.frombuffer(text, dtype=np.uint8) if len(text) else np.zeros(1, np.uint8)
-        cap = max(16, len(text) // 8 + 16)
-        for _ in range(2):
-            out = np.empty((cap, 2), np.float64)
-            n, bad, fb, kind = C.c_uint64(0), C.c_uint64(0), C.c_uint64(0), C.c_uint32(0)
-            rc = self.lib.pc_parse_points_csv(self.ctx, _ptr(buf), len(text), int(first_data_line), int(x_col),
-                                              int(y_col), delim.encode(), _ptr(out), cap, C.byref(n), C.byref(bad),
-                                              C.byref(fb), C.byref(kind))
-            if rc == _native.PC_OK:
-                break
-            if rc != _native.PC_EINVAL or n.value <= cap:
-                self._check(rc, "pc_parse_points_csv")
-            cap = n.value
+        cap = (len(text) + 1) // 4 + 1  # a good row takes >= 4 bytes ("d,d\n") except the file's last
+        out = np.empty((cap, 2), np.float64)  # untouched pages cost nothing
+        n, bad, fb, kind = C.c_uint64(0), C.c_uint64(0), C.c_uint64(0), C.c_uint32(0)
+        rc = self.lib.pc_parse_points_csv(self.ctx, _ptr(buf), len(text), int(data_start), int(x_col), int(y_col),
+                                          delim.encode(), _ptr(out), cap, C.byref(n), C.byref(bad), C.byref(fb),
+                                          C.byref(kind))
+        self._check(rc, "pc_parse_points_csv")
         first = None if fb.value == 2 ** 64 - 1 else fb.value
-        return out[:n.value].copy(), bad.value, first, kind.value
+        return out[:n.value], bad.value, first, kind.value
+
+    def parse_points_csv_dev(self, dev_index, stream_ptr, d_text, n_bytes, data_start, x_col, y_col, delim,
+                             d_out_xy, cap_points, d_result):
+        rc = self.lib.pc_parse_points_csv_dev(self.ctx, dev_index, stream_ptr, _ptr(d_text), int(n_bytes),
+                                              int(data_start), int(x_col), int(y_col), delim.encode(),
+                                              _ptr(d_out_xy), int(cap_points), _ptr(d_result))
+        self._check(rc, "pc_parse_points_csv_dev")
 
     # ---- device-pointer API (torch tensors as HBM buffers) ------------------
     def classify_dev(self, dev_index, stream_ptr, d_xy, n, d_vx, d_vy, d_ring_off, n_rings, n_verts, mode,

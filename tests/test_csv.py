@@ -83,7 +83,7 @@ def test_cells_match_reference_parser(engine):
     # one cell per row in column 1 (x), a fixed good y in column 2
     text = b"id,x,y\n" + b"".join(b"%d,%s,0.5\n" % (i, c) for i, c in enumerate(cells))
     ref = [oracle.ref_parse_double(c) for c in cells]
-    xy, n_bad, first_bad, kind = engine.parse_points_csv(text, 1, 1, 2, ",")
+    xy, n_bad, first_bad, kind = engine.parse_points_csv(text, 7, 1, 2, ",")
     want = np.array([v for ok, v in ref if ok], np.float64)
     assert n_bad == sum(1 for ok, _ in ref if not ok)
     assert len(xy) == len(want)
@@ -91,7 +91,7 @@ def test_cells_match_reference_parser(engine):
     assert np.all(xy[:, 1] == 0.5)
     bad_rows = [i for i, (ok, _) in enumerate(ref) if not ok]
     if bad_rows:
-        assert first_bad == bad_rows[0] + 1 and kind == 3
+        assert first_bad == text.index(b"\n%d," % bad_rows[0]) + 1 and kind == 3
 
 
 def _rand_file(rng, path, delim, header, crlf, final_nl, rows):
@@ -134,17 +134,15 @@ def test_files_match_reference_reader(engine, tmp_path, trial):
     text = _rand_file(rng, path, delim, header, crlf=trial % 2 == 1, final_nl=trial % 4 != 3, rows=rows)
     ref = oracle.ref_read_points_csv(str(path), 1, 2, has_header=header, delim=delim, lenient=True)
     assert ref["kind"] == 0, ref["msg"]
-    first_data_line = 0
-    if header:  # the header is the first line (no leading empty lines here)
-        first_data_line = 1
-    xy, n_bad, first_bad, kind = engine.parse_points_csv(text, first_data_line, 1, 2, delim)
+    data_start = text.index(b"\n") + 1 if header else 0  # the header is the first line
+    xy, n_bad, first_bad, kind = engine.parse_points_csv(text, data_start, 1, 2, delim)
     assert n_bad == ref["skipped"]
     assert xy.shape == ref["points"].shape
     assert xy.tobytes() == ref["points"].tobytes()
     strict = oracle.ref_read_points_csv(str(path), 1, 2, has_header=header, delim=delim, lenient=False)
     if strict["kind"] == 1:
-        lines = text.split(b"\n")
-        data_row = sum(1 for ln in lines[first_data_line:first_bad + 1] if ln.rstrip(b"\r"))
+        lines = text[data_start:first_bad].split(b"\n")[:-1]  # the lines before the bad one
+        data_row = 1 + sum(1 for ln in lines if ln.rstrip(b"\r"))
         assert data_row == strict["row"]
         assert ("row has only" in strict["msg"]) == (kind == 2)
     else:
@@ -170,6 +168,79 @@ def test_empty_and_degenerate_texts(engine):
     xy, n_bad, fb, _ = engine.parse_points_csv(b"\n\r\n\n", 0, 0, 1)
     assert len(xy) == 0 and n_bad == 0 and fb is None
     xy, n_bad, fb, kind = engine.parse_points_csv(b"1,2\n3\n4,5", 0, 0, 1)
-    assert xy.tolist() == [[1.0, 2.0], [4.0, 5.0]] and n_bad == 1 and fb == 1 and kind == 2
+    assert xy.tolist() == [[1.0, 2.0], [4.0, 5.0]] and n_bad == 1 and fb == 4 and kind == 2
     xy, n_bad, fb, kind = engine.parse_points_csv(b"1,x\r\n", 0, 0, 1)
     assert len(xy) == 0 and n_bad == 1 and fb == 0 and kind == 4
+
+
+def _tile_texts():
+    """Inputs aimed at the reader's 8 KiB tiles: lines ending on / starting at
+    tile boundaries, lines longer than a tile plus its spill, tiles of empty
+    lines, tiles of minimal rows, a header longer than a tile."""
+    T = 8192
+    out = {}
+    # '\n' exactly at byte T-1 and at T: rows of a fixed width that divides T
+    out["width16"] = b"".join(b"%07d,%07d\n" % (i, -i) for i in range(5000))  # 16-byte rows
+    out["width17"] = b"".join(b"%07d,%08d\n" % (i, i) for i in range(5000))
+    out["min_rows"] = b"1,2\n" * 9000 + b"3,4"                                 # 2048 good rows per tile
+    out["empty_tiles"] = b"5,6\n" + b"\n" * (3 * T) + b"7,8\r\n" + b"\r\n" * T + b"9,1"
+    long_cell = b" " * (3 * T) + b"2.5"
+    out["long_line"] = b"1,1\n" + long_cell + b"," + long_cell + b"\n2,2\n" + b"x" * (T - 2) + b"\n3,3"
+    out["spill_edge"] = b"a" * (T - 3) + b"\n" + b"4," + b"0" * 600 + b"7\n5,5"
+    out["no_newline"] = b"1.25,2.5"
+    rng = np.random.default_rng(3)
+    rows = []
+    for i in range(20000):
+        w = int(rng.integers(0, 40))
+        rows.append(b" " * w + b"%.17g,%.17g" % tuple(rng.standard_normal(2)))
+    out["ragged"] = b"\n".join(rows)
+    return out
+
+
+@needs_ref
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", list(_tile_texts()))
+def test_tile_boundaries_match_reference_reader(engine, tmp_path, name):
+    text = _tile_texts()[name]
+    path = tmp_path / f"{name}.csv"
+    path.write_bytes(text)
+    ref = oracle.ref_read_points_csv(str(path), 0, 1, has_header=False, lenient=True)
+    assert ref["kind"] == 0, ref["msg"]
+    xy, n_bad, first_bad, kind = engine.parse_points_csv(text, 0, 0, 1, ",")
+    assert n_bad == ref["skipped"]
+    assert xy.tobytes() == ref["points"].tobytes()
+
+
+@needs_ref
+@pytest.mark.gpu
+def test_header_longer_than_a_tile(engine, tmp_path):
+    head = b",".join(b"col%05d" % i for i in range(3000))  # ~27 KB header
+    body = b"".join(b"%d,%d\n" % (i, 2 * i) for i in range(3000))
+    text = b"\n\n" + head + b"\n" + body
+    path = tmp_path / "wide.csv"
+    path.write_bytes(text)
+    ref = oracle.ref_read_points_csv(str(path), "col00000", "col00001", has_header=True, lenient=False)
+    assert ref["kind"] == 0, ref["msg"]
+    xy, n_bad, first_bad, _ = engine.parse_points_csv(text, len(text) - len(body), 0, 1, ",")
+    assert n_bad == 0 and first_bad is None
+    assert xy.tobytes() == ref["points"].tobytes()
+
+
+@pytest.mark.gpu
+def test_device_pointer_csv_api(engine):
+    """pc_parse_points_csv_dev on an unaligned device pointer, capacity short."""
+    import torch
+    rows = b"".join(b"%d.5,%d\n" % (i, -i) for i in range(100_000))
+    buf = torch.zeros(len(rows) + 3, dtype=torch.uint8)
+    buf[3:] = torch.frombuffer(bytearray(rows), dtype=torch.uint8)
+    d_text = buf.cuda()[3:]
+    assert d_text.data_ptr() % 16 != 0
+    d_out = torch.zeros((50_000, 2), dtype=torch.float64, device="cuda")
+    d_res = torch.zeros(4, dtype=torch.int64, device="cuda")
+    engine.parse_points_csv_dev(0, None, d_text, len(rows), 0, 0, 1, ",", d_out, 50_000, d_res)
+    torch.cuda.synchronize()
+    res = d_res.cpu().numpy().view(np.uint64)
+    assert res[0] == 100_000 and res[1] == 0 and res[2] == np.uint64(2 ** 64 - 1)
+    want = np.stack([np.arange(50_000) + 0.5, -np.arange(50_000.0)], 1)
+    want[0, 1] = 0.0  # "0" parses to +0
+    assert d_out.cpu().numpy().tobytes() == want.tobytes()
