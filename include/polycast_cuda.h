@@ -168,6 +168,30 @@ int pc_parse_points_csv_dev(pc_ctx* ctx, int dev_index, void* stream, const char
                             uint64_t data_start, uint32_t x_col, uint32_t y_col, char delim, double* d_out_xy,
                             uint64_t cap_points, uint64_t* d_result);
 
+/* One row of write_results_csv (io.hpp:312-322): layout-compatible with
+ * polycast::ResultRecord (32 bytes; verdict = PC_INSIDE .. PC_ERROR). */
+typedef struct pc_result_record {
+    uint64_t index;
+    double x;
+    double y;
+    uint8_t verdict;
+    uint8_t pad[7];
+} pc_result_record;
+
+/* The text write_results_csv (io.hpp:325-335) puts in its file, on GPU 0:
+ * "index,x,y,verdict\n" and one "index,x,y,verdict\n" row per record, x and y
+ * as printf("%.17g") prints them (byte-identical; every finite double reads
+ * back exactly), verdict as to_string(Verdict) (batch.hpp:71-79).  *len = the
+ * text's length; if cap < *len nothing is copied and PC_EINVAL is returned
+ * (18 + 80 n bytes always suffice). */
+int pc_format_results_csv(pc_ctx* ctx, const pc_result_record* recs, uint64_t n, char* out, uint64_t cap,
+                          uint64_t* len);
+
+/* Device-pointer variant (not synchronised): at most cap bytes to d_out,
+ * the full length to d_len (one u64 in device memory). */
+int pc_format_results_csv_dev(pc_ctx* ctx, int dev_index, void* stream, const pc_result_record* d_recs, uint64_t n,
+                              char* d_out, uint64_t cap, uint64_t* d_len);
+
 /* Number of GPU kernels the last call on this context launched (all devices). */
 uint64_t pc_last_launch_count(const pc_ctx* ctx);
 

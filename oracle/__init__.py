@@ -64,6 +64,9 @@ def ref():
                                                 C.c_char, C.c_int, _vp, C.c_uint64, _vp, _vp, _vp, C.c_char_p,
                                                 C.c_uint64]
             lib.ref_read_points_csv.restype = C.c_int
+        if hasattr(lib, "ref_write_results_csv"):
+            lib.ref_write_results_csv.argtypes = [C.c_char_p, _vp, _vp, _vp, C.c_uint64]
+            lib.ref_write_results_csv.restype = C.c_int
         _ref = lib
     return _ref
 
@@ -216,3 +219,11 @@ def ref_read_points_csv(path, x=1, y=2, has_header=True, delim=",", lenient=Fals
                                 C.byref(row), msg, C.c_uint64(1024))
     return {"kind": k, "points": out[:min(n.value, cap)].copy(), "skipped": sk.value, "row": row.value,
             "msg": msg.value.decode(errors="replace")}
+
+
+def ref_write_results_csv(path, index, xy, verdict):
+    """The reference's write_results_csv (io.hpp:325-335) -> 0 ok, 4 IoError, 6 other."""
+    idx = _c(index, np.uint64)
+    xy = _c(xy, np.float64)
+    v = _c(verdict, np.uint8)
+    return ref().ref_write_results_csv(str(path).encode(), _p(idx), _p(xy), _p(v), len(v))

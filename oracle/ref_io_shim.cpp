@@ -2,7 +2,8 @@
 //
 // C-ABI shim around the *unmodified* reference CSV reader and number parser
 // (proj/include/polycast/io.hpp: detail::parse_double :116-124,
-// read_points_csv :148-225), included from /root/reference at build time.
+// read_points_csv :148-225, write_results_csv :325-335), included from
+// /root/reference at build time.
 // Checker for the GPU CSV reader (paper_2306_04316_b200/csrc/pip_csv.cu) in
 // tests/ and the CPU baseline of bench.py's csv workload; never the product.
 #include <polycast/io.hpp>
@@ -10,6 +11,7 @@
 #include <cstdint>
 #include <cstring>
 #include <string>
+#include <vector>
 
 using namespace polycast;
 
@@ -71,6 +73,22 @@ int ref_read_points_csv(const char* path, const char* x_name, uint64_t x_idx, co
         return 5;
     } catch (const std::exception& e) {
         put(e.what());
+        return 6;
+    }
+}
+
+// write_results_csv of n records given as arrays; 0 ok, 4 IoError, 6 other
+int ref_write_results_csv(const char* path, const uint64_t* index, const double* xy, const uint8_t* verdict,
+                          uint64_t n) {
+    try {
+        std::vector<ResultRecord> recs(n);
+        for (uint64_t i = 0; i < n; ++i)
+            recs[i] = ResultRecord{index[i], xy[2 * i], xy[2 * i + 1], static_cast<Verdict>(verdict[i])};
+        write_results_csv(recs, path);
+        return 0;
+    } catch (const IoError&) {
+        return 4;
+    } catch (const std::exception&) {
         return 6;
     }
 }

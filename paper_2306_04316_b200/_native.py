@@ -47,6 +47,8 @@ SIGNATURES = {
                                       C.c_uint64, _vp, _vp, _vp, _vp]),
     "pc_parse_points_csv_dev": (C.c_int, [_vp, C.c_int, _vp, _vp, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32,
                                           C.c_char, _vp, C.c_uint64, _vp]),
+    "pc_format_results_csv": (C.c_int, [_vp, _vp, C.c_uint64, _vp, C.c_uint64, _vp]),
+    "pc_format_results_csv_dev": (C.c_int, [_vp, C.c_int, _vp, _vp, C.c_uint64, _vp, C.c_uint64, _vp]),
     "pc_last_launch_count": (C.c_uint64, [_vp]),
     "pc_set_profiling": (C.c_int, [_vp, C.c_int]),
     "pc_set_option": (C.c_int, [_vp, C.c_int, C.c_int64]),

@@ -48,6 +48,7 @@ struct DevState {
     DevBuf csr_meta;                                          // per-polygon records (pip_csr.cu)
     DevBuf cmp_blk, cmp_pts, cmp_idx, cmp_v, cmp_out;         // prefilter / scatter (pip_compact.cu)
     DevBuf csv_text, csv_state, csv_res, csv_out;             // CSV reader (pip_csv.cu)
+    DevBuf emit_recs, emit_scratch, emit_out;                 // results-CSV writer (pip_emit.cu)
     unsigned long long* h_stats = nullptr; // pinned 4 x u64
     pch::Stager* stager = nullptr;         // pageable host copies (host_stage.h), made on first use
     // profiling: one event pair per main-kernel launch since the last take
@@ -321,7 +322,8 @@ void pc_destroy(pc_ctx* c) {
         for (DevBuf* b : {&d.pts, &d.vx, &d.vy, &d.ring_off, &d.pt_off, &d.poly_ring_off, &d.filt, &d.rec, &d.bbox,
                           &d.bits, &d.verdicts, &d.stats, &d.counts, &d.degen, &d.bucket_scratch, &d.sorted_pts,
                           &d.sorted_idx, &d.bucket_blk, &d.csr_meta, &d.cmp_blk, &d.cmp_pts, &d.cmp_idx, &d.cmp_v,
-                          &d.cmp_out, &d.csv_text, &d.csv_state, &d.csv_res, &d.csv_out})
+                          &d.cmp_out, &d.csv_text, &d.csv_state, &d.csv_res, &d.csv_out, &d.emit_recs,
+                          &d.emit_scratch, &d.emit_out})
             b->release();
         if (d.h_stats) cudaFreeHost(d.h_stats);
         delete d.stager;
@@ -747,6 +749,53 @@ int pc_parse_points_csv_dev(pc_ctx* c, int dev_index, void* stream, const char* 
                                         d.csv_state.p,
                                         reinterpret_cast<unsigned long long*>(d_result), st, &c->launches),
               "csv kernel");
+        mark_end(c, d, st);
+    });
+}
+
+int pc_format_results_csv(pc_ctx* c, const pc_result_record* recs, uint64_t n, char* out, uint64_t cap,
+                          uint64_t* len) {
+    return guarded(c, [&] {
+        if (!len) invalid(c, "null length");
+        *len = 0;
+        if (n && !recs) invalid(c, "null records");
+        DevState& d = c->devs[0];
+        check(c, cudaSetDevice(d.dev), "cudaSetDevice");
+        cudaStream_t st = d.stream;
+        h2d(c, d, d.emit_recs, recs, n * sizeof(pc_result_record), st, "upload records");
+        check(c, d.emit_scratch.ensure(pcd::emit_scratch_bytes(n)), "alloc emit scratch");
+        const uint64_t dev_cap = pcd::emit_max_bytes(n);
+        check(c, d.emit_out.ensure(dev_cap), "alloc text");
+        check(c, d.csv_res.ensure(4 * 8), "alloc results");
+        unsigned long long* dl = d.csv_res.as<unsigned long long>();
+        mark_begin(c, d, st);
+        check(c, pcd::launch_emit_results(d.emit_recs.p, n, d.emit_out.as<char>(), dev_cap, d.emit_scratch.p, dl, st,
+                                          &c->launches),
+              "emit kernels");
+        mark_end(c, d, st);
+        check(c, cudaMemcpyAsync(d.h_stats, dl, 8, cudaMemcpyDeviceToHost, st), "download length");
+        check(c, cudaStreamSynchronize(st), "emit");
+        const uint64_t total = d.h_stats[0];
+        *len = total;
+        if (total > cap) invalid(c, "write_results_csv: output capacity too small (len holds the need)");
+        if (!out) invalid(c, "null out");
+        d2h(c, d, out, d.emit_out.p, total, st, "download text");
+    });
+}
+
+int pc_format_results_csv_dev(pc_ctx* c, int dev_index, void* stream, const pc_result_record* d_recs, uint64_t n,
+                              char* d_out, uint64_t cap, uint64_t* d_len) {
+    return guarded(c, [&] {
+        if (dev_index < 0 || dev_index >= (int)c->devs.size()) invalid(c, "bad device index");
+        if (!d_len || (n && !d_recs) || (cap && !d_out)) invalid(c, "null arrays");
+        DevState& d = c->devs[dev_index];
+        check(c, cudaSetDevice(d.dev), "cudaSetDevice");
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d.stream;
+        check(c, d.emit_scratch.ensure(pcd::emit_scratch_bytes(n)), "alloc emit scratch");
+        mark_begin(c, d, st);
+        check(c, pcd::launch_emit_results(d_recs, n, d_out, cap, d.emit_scratch.p,
+                                          reinterpret_cast<unsigned long long*>(d_len), st, &c->launches),
+              "emit kernels");
         mark_end(c, d, st);
     });
 }

@@ -91,6 +91,15 @@ cudaError_t launch_csv_points(const char* text, uint64_t len, uint64_t data_star
                               char delim, double* out, uint64_t cap, void* scratch, unsigned long long* res,
                               cudaStream_t st, uint64_t* launches);
 
+// GPU results-CSV writer (pip_emit.cu): recs = n 32-byte records
+// (pc_result_record); out gets the header and the rows (at most cap bytes
+// written), *out_len (device) the full length; scratch = emit_scratch_bytes(n).
+uint64_t emit_tiles(uint64_t n);
+uint64_t emit_scratch_bytes(uint64_t n);
+uint64_t emit_max_bytes(uint64_t n);
+cudaError_t launch_emit_results(const void* recs, uint64_t n, char* out, uint64_t cap, void* scratch,
+                                unsigned long long* out_len, cudaStream_t st, uint64_t* launches);
+
 // y-bucketing of the points of one polygon (pip_sort.cu): counting sort by
 // y over the outer ring's bbox into kBuckets bins; bbox-rejected points
 // (prefilter) go to a trailing bin that is not classified.

@@ -49,7 +49,7 @@ static const Pow5 kPow5[] = {
 static const double kPow10[23] = {1e0,  1e1,  1e2,  1e3,  1e4,  1e5,  1e6,  1e7,  1e8,  1e9,  1e10, 1e11,
                                   1e12, 1e13, 1e14, 1e15, 1e16, 1e17, 1e18, 1e19, 1e20, 1e21, 1e22};
 #endif
-constexpr int kQMin = -342, kQMax = 308;
+constexpr int kQMin = -342, kQMax = 308; // parser range; the table runs to 342 (formatter)
 constexpr int kMaxDigits = 800; // digits beyond this only act as a sticky bit in the exact comparison
 
 PC_HD uint64_t mulhi64(uint64_t a, uint64_t b) {

@@ -51,6 +51,21 @@ class DeviceError(RuntimeError):
         self.status = status
 
 
+# pc_result_record / polycast::ResultRecord (32 bytes)
+RESULT_RECORD = np.dtype({"names": ["index", "x", "y", "verdict"], "formats": [np.uint64, np.float64, np.float64,
+                                                                               np.uint8],
+                          "offsets": [0, 8, 16, 24], "itemsize": 32})
+
+
+def make_records(index, xy, verdict) -> np.ndarray:
+    """Records for format_results_csv from an index array, (n, 2) points and verdict bytes."""
+    n = len(verdict)
+    xy = np.asarray(xy, np.float64).reshape(n, 2)
+    recs = np.zeros(n, dtype=RESULT_RECORD)
+    recs["index"], recs["x"], recs["y"], recs["verdict"] = index, xy[:, 0], xy[:, 1], verdict
+    return recs
+
+
 def _ptr(a) -> int | None:
     if a is None:
         return None
@@ -302,6 +317,24 @@ class Engine:
         self._check(rc, "pc_parse_points_csv")
         first = None if fb.value == 2 ** 64 - 1 else fb.value
         return out[:n.value], bad.value, first, kind.value
+
+    def format_results_csv(self, recs: np.ndarray) -> np.ndarray:
+        """write_results_csv's text on the GPU (pc_format_results_csv) for records of
+        dtype RESULT_RECORD (see make_records): header plus one "index,x,y,verdict"
+        row per record, coordinates as printf("%.17g").  Returns the bytes (uint8)."""
+        assert recs.dtype == RESULT_RECORD and recs.flags.c_contiguous
+        n = len(recs)
+        cap = 18 + 80 * n
+        out = np.empty(cap, np.uint8)  # untouched pages past the text cost nothing
+        ln = C.c_uint64(0)
+        rc = self.lib.pc_format_results_csv(self.ctx, _ptr(recs) if n else None, n, _ptr(out), cap, C.byref(ln))
+        self._check(rc, "pc_format_results_csv")
+        return out[:ln.value]
+
+    def format_results_csv_dev(self, dev_index, stream_ptr, d_recs, n, d_out, cap, d_len):
+        rc = self.lib.pc_format_results_csv_dev(self.ctx, dev_index, stream_ptr, _ptr(d_recs), int(n), _ptr(d_out),
+                                                int(cap), _ptr(d_len))
+        self._check(rc, "pc_format_results_csv_dev")
 
     def parse_points_csv_dev(self, dev_index, stream_ptr, d_text, n_bytes, data_start, x_col, y_col, delim,
                              d_out_xy, cap_points, d_result):

@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <fstream>
 #include <numbers>
 #include <random>
 #include <string>
@@ -71,6 +72,8 @@ RefClassify g_ref = nullptr;
 using RefReadCsv = int (*)(const char*, const char*, uint64_t, const char*, uint64_t, int, char, int, double*, uint64_t,
                            uint64_t*, uint64_t*, uint64_t*, char*, uint64_t);
 RefReadCsv g_ref_csv = nullptr;
+using RefWriteResults = int (*)(const char*, const uint64_t*, const double*, const uint8_t*, uint64_t);
+RefWriteResults g_ref_write = nullptr;
 
 void kats() {
     const Ring sq = square();
@@ -364,6 +367,94 @@ void csv_vs_reference() {
     std::printf("csv: %d files compared against the reference reader\n", compared);
 }
 
+std::string slurp(const std::string& path) {
+    std::ifstream in(path, std::ios::binary);
+    return std::string((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+}
+
+// io_test.cpp:197-225 (results round-trip bitwise) re-expressed, plus the
+// written bytes against the reference's writer and awkward doubles
+void results_csv() {
+    std::mt19937_64 rng(99);
+    std::vector<ResultRecord> records;
+    for (std::size_t i = 0; i < 10000; ++i) {
+        const double x = (static_cast<double>(rng()) / 1e3) * (rng() % 2 ? 1 : -1e-7);
+        const double y = static_cast<double>(rng() >> 11) * 0x1.0p-53;
+        records.push_back({i, x, y, static_cast<Verdict>(rng() % 4)});
+    }
+    // awkward values: signed zeros, subnormals, extremes, powers of ten, huge indices
+    const double odd[] = {0.0, -0.0, 5e-324, -2.2250738585072014e-308, 1.7976931348623157e308, 1e-5, 1e16, 1e17,
+                          0.1, 123456789012345678.0, -1e-300, 9.999999999999999e22};
+    for (double v : odd) records.push_back({~std::size_t(0) - records.size(), v, -v, Verdict::Boundary});
+    for (int k = 0; k < 20000; ++k) { // random bit patterns
+        uint64_t a = rng(), b = rng();
+        double x, y;
+        std::memcpy(&x, &a, 8);
+        std::memcpy(&y, &b, 8);
+        if (!std::isfinite(x)) x = 1.5;
+        if (!std::isfinite(y)) y = -2.5;
+        records.push_back({rng(), x, y, static_cast<Verdict>(rng() % 4)});
+    }
+    const std::string out = "/tmp/pc_results_test.csv", ref = "/tmp/pc_results_ref.csv";
+    write_results_csv(records, out);
+    const std::vector<ResultRecord> back = read_results_csv(out);
+    CHECK(back.size() == records.size());
+    bool same = back.size() == records.size();
+    for (std::size_t i = 0; same && i < records.size(); ++i)
+        same = back[i].index == records[i].index && std::memcmp(&back[i].x, &records[i].x, 8) == 0 &&
+               std::memcmp(&back[i].y, &records[i].y, 8) == 0 && back[i].verdict == records[i].verdict;
+    CHECK(same);
+    // coordinates also survive re-reading through the points reader
+    PointsFileSpec spec;
+    spec.path = out;
+    spec.x_column = std::string("x");
+    spec.y_column = std::string("y");
+    const CsvPoints pts = read_points_csv(spec);
+    CHECK(pts.batch.size() == records.size());
+    bool same_pts = pts.batch.size() == records.size();
+    for (std::size_t i = 0; same_pts && i < records.size(); ++i)
+        same_pts = pts.batch.points[i].x == records[i].x && pts.batch.points[i].y == records[i].y;
+    CHECK(same_pts);
+    // byte-identical to the reference's writer
+    if (g_ref_write) {
+        std::vector<uint64_t> idx(records.size());
+        std::vector<double> xy(2 * records.size());
+        std::vector<uint8_t> v(records.size());
+        for (std::size_t i = 0; i < records.size(); ++i) {
+            idx[i] = records[i].index;
+            xy[2 * i] = records[i].x;
+            xy[2 * i + 1] = records[i].y;
+            v[i] = static_cast<uint8_t>(records[i].verdict);
+        }
+        CHECK(g_ref_write(ref.c_str(), idx.data(), xy.data(), v.data(), records.size()) == 0);
+        const std::string a = slurp(out), b = slurp(ref);
+        CHECK(a == b);
+        if (a != b) {
+            std::size_t k = 0;
+            while (k < a.size() && k < b.size() && a[k] == b[k]) ++k;
+            std::fprintf(stderr, "results differ at byte %zu: '%.60s' vs '%.60s'\n", k, a.c_str() + (k > 20 ? k - 20 : 0),
+                         b.c_str() + (k > 20 ? k - 20 : 0));
+        }
+        std::printf("results: %zu records, %zu bytes, identical to the reference writer: %s\n", records.size(),
+                    a.size(), a == b ? "yes" : "NO");
+        std::remove(ref.c_str());
+    }
+    // empty batch: header only (io_test.cpp:184-194)
+    write_results_csv(std::vector<ResultRecord>{}, out);
+    CHECK(slurp(out) == "index,x,y,verdict\n");
+    CHECK(read_results_csv(out).empty());
+    // reader errors
+    {
+        std::FILE* f = std::fopen(out.c_str(), "wb");
+        std::fputs("index,x,y,verdict\n0,1,2,inside\n1,1,2,sideways\n", f);
+        std::fclose(f);
+        CHECK_THROWS(read_results_csv(out), CsvParseError);
+    }
+    CHECK_THROWS(read_results_csv("/nonexistent/results.csv"), FileNotFound);
+    CHECK_THROWS(write_results_csv(records, "/nonexistent/dir/results.csv"), IoError);
+    std::remove(out.c_str());
+}
+
 } // namespace
 
 int main(int argc, char** argv) {
@@ -371,6 +462,7 @@ int main(int argc, char** argv) {
     if (void* h = dlopen(ref_path, RTLD_NOW)) {
         g_ref = reinterpret_cast<RefClassify>(dlsym(h, "ref_classify"));
         g_ref_csv = reinterpret_cast<RefReadCsv>(dlsym(h, "ref_read_points_csv"));
+        g_ref_write = reinterpret_cast<RefWriteResults>(dlsym(h, "ref_write_results_csv"));
     }
     else std::printf("note: reference shim not found at %s; reference cross-check skipped\n", ref_path);
     try {
@@ -378,6 +470,7 @@ int main(int argc, char** argv) {
         randomized();
         prefilter_scatter();
         csv_vs_reference();
+        results_csv();
     } catch (const std::exception& e) {
         std::fprintf(stderr, "FAIL: uncaught exception: %s\n", e.what());
         return 100;

@@ -30,6 +30,14 @@ def test_device_parser_vs_from_chars():
     assert " 0 mismatches" in r.stdout
 
 
+def test_device_formatter_vs_printf():
+    """The GPU writer's %.17g formatter, compiled as host code, vs glibc snprintf (4.4M values)."""
+    subprocess.run(["make", "-s", "-C", CPP, os.path.join(CPP, "format_test")], check=True)
+    r = subprocess.run([os.path.join(CPP, "format_test")], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:]
+    assert " 0 mismatches" in r.stdout
+
+
 @needs_ref
 @pytest.mark.parametrize("cell,ok,val", [
     (b"1.5", True, 1.5), (b" 2.25\t", True, 2.25), (b'"-3"', True, -3.0), (b"+1", False, None),
@@ -244,3 +252,51 @@ def test_device_pointer_csv_api(engine):
     want = np.stack([np.arange(50_000) + 0.5, -np.arange(50_000.0)], 1)
     want[0, 1] = 0.0  # "0" parses to +0
     assert d_out.cpu().numpy().tobytes() == want.tobytes()
+
+
+def _records(rng, n):
+    u = rng.integers(0, 2 ** 64, (n, 2), dtype=np.uint64)
+    xy = u.view(np.float64).copy()
+    xy[~np.isfinite(xy)] = 0.25
+    k = n // 4  # coordinates and the io_test magnitudes too
+    xy[:k, 0] = rng.uniform(-180, 180, k)
+    xy[:k, 1] = rng.uniform(-90, 90, k)
+    xy[k:2 * k, 0] = rng.integers(0, 2 ** 63, k).astype(np.float64) / 1e3 * -1e-7
+    if n >= 8:
+        xy[2 * k:2 * k + 4] = [[0.0, -0.0], [5e-324, 1e17], [1e-5, 123456789012345678.0],
+                               [-1e-300, 1.7976931348623157e308]]
+    index = rng.integers(0, 2 ** 64, n, dtype=np.uint64)
+    index[: n // 2] = np.arange(n // 2)
+    verdict = rng.integers(0, 4, n).astype(np.uint8)
+    return index, xy, verdict
+
+
+@needs_ref
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [0, 1, 255, 256, 257, 100_000])
+def test_results_text_matches_reference_writer(engine, tmp_path, n):
+    """write_results_csv's bytes: the GPU writer vs the reference's own file."""
+    rng = np.random.default_rng(n + 1)
+    index, xy, verdict = _records(rng, n)
+    from paper_2306_04316_b200.engine import make_records
+    got = engine.format_results_csv(make_records(index, xy, verdict)).tobytes()
+    path = tmp_path / "ref.csv"
+    assert oracle.ref_write_results_csv(path, index, xy, verdict) == 0
+    want = path.read_bytes()
+    assert got == want
+    names = [b"inside", b"outside", b"boundary", b"error"]
+    py = b"index,x,y,verdict\n" + b"".join(b"%d,%s,%s,%s\n" % (int(i), (b"%.17g" % a), (b"%.17g" % b), names[v])
+                                           for i, (a, b), v in zip(index, xy.tolist(), verdict))
+    assert got == py
+
+
+@pytest.mark.gpu
+def test_results_round_trip_through_points_reader(engine):
+    """17 significant digits round-trip: format on the GPU, parse on the GPU, same bits (2^20 rows)."""
+    rng = np.random.default_rng(12)
+    index, xy, verdict = _records(rng, 1 << 20)
+    from paper_2306_04316_b200.engine import make_records
+    text = engine.format_results_csv(make_records(index, xy, verdict)).tobytes()
+    back, n_bad, fb, _ = engine.parse_points_csv(text, len(b"index,x,y,verdict\n"), 1, 2, ",")
+    assert n_bad == 0 and fb is None
+    assert back.tobytes() == xy.tobytes()

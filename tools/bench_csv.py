@@ -154,6 +154,76 @@ def main():
                     "d2h_bytes_per_step": 16 * args.rows + 32, "seconds": e2e},
             "gpu_launches": 3, "cpu_baseline": cpu, "kernel_ms_all": ms}
     print(json.dumps(line), flush=True)
+
+    # ---- results-CSV writer (write_results_csv): the parsed points as records
+    from paper_2306_04316_b200.engine import RESULT_RECORD
+    rng = np.random.default_rng(5)
+    n = args.rows
+    recs = np.zeros(n, dtype=RESULT_RECORD)
+    recs["index"] = np.arange(n)
+    recs["x"], recs["y"] = want[:, 0], want[:, 1]
+    recs["verdict"] = rng.integers(0, 4, n).astype(np.uint8)
+    d_recs = torch.from_numpy(recs.view(np.uint8)).to(dev)
+    cap = 18 + 80 * n
+    d_txt = torch.empty(cap, dtype=torch.uint8, device=dev)
+    d_len = torch.zeros(1, dtype=torch.int64, device=dev)
+
+    def emit():
+        eng.format_results_csv_dev(0, sp, d_recs, n, d_txt, cap, d_len)
+
+    for _ in range(3):
+        emit()
+    torch.cuda.synchronize()
+    out_len = int(d_len.item())
+    eng.set_profiling(True)
+    eng.profile_take(0)
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        emit()
+        stream.synchronize()
+    ems = eng.profile_take(0)
+    eng.set_profiling(False)
+    emit_ms = float(np.median(ems))
+    host_text = eng.format_results_csv(recs)  # records in host memory, as write_results_csv gets them
+    assert len(host_text) == out_len
+    ee = []
+    for _ in range(max(3, args.steps // 2)):
+        t = time.perf_counter()
+        eng.format_results_csv(recs)
+        ee.append(time.perf_counter() - t)
+    e2e_emit = float(np.median(ee))
+    cpu2 = None
+    if not args.no_cpu_baseline:
+        import oracle
+        if oracle.ref_available():
+            k = min(args.cpu_rows, n)
+            with tempfile.NamedTemporaryFile(suffix=".csv", delete=False) as f:
+                path = f.name
+            t = time.perf_counter()
+            rc = oracle.ref_write_results_csv(path, recs["index"][:k], want[:k], recs["verdict"][:k])
+            cs = time.perf_counter() - t
+            ref_bytes = open(path, "rb").read()
+            os.unlink(path)
+            assert rc == 0
+            gpu_k = eng.format_results_csv(np.ascontiguousarray(recs[:k])).tobytes()
+            assert gpu_k == ref_bytes, "parity: GPU text differs from the reference writer"
+            cpu2 = {"value": k / cs, "unit": "rows/s", "cores": 1, "kind": "reference",
+                    "sample": f"reference write_results_csv of the first {k} records (to a file in /tmp, page "
+                              f"cache), 1 timed run; byte-identical to the GPU text"}
+    alg2 = 32 * n + out_len
+    ach2 = alg2 / (emit_ms * 1e-3) / 1e9
+    line2 = {"metric": "csv_emit_rows_per_s", "value": n / (emit_ms * 1e-3), "unit": "rows/s", "n_gpus": 1,
+             "steps": args.steps, "warmup": 3, "ms_per_step": emit_ms, "higher_is_better": True, "dtype": "f64",
+             "data": "synthetic",
+             "config": {"workload": f"write_results_csv text of {n} records ({out_len} bytes), the parsed points, "
+                                    f"random verdicts", "l2": "256 MiB buffer written between timed launches"},
+             "roofline": {"bound": "hbm", "achieved": ach2, "peak": peak, "unit": "GB/s", "frac": ach2 / peak,
+                          "traffic": None, "algorithmic_bytes": alg2},
+             "e2e": {"value": n / e2e_emit, "unit": "rows/s", "h2d_bytes_per_step": 32 * n,
+                     "d2h_bytes_per_step": out_len, "seconds": e2e_emit},
+             "gpu_launches": 3, "cpu_baseline": cpu2, "kernel_ms_all": ems}
+    print(json.dumps(line2), flush=True)
     eng.close()
 
 
