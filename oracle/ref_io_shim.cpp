@@ -2,8 +2,8 @@
 //
 // C-ABI shim around the *unmodified* reference CSV reader and number parser
 // (proj/include/polycast/io.hpp: detail::parse_double :116-124,
-// read_points_csv :148-225, write_results_csv :325-335), included from
-// /root/reference at build time.
+// read_points_csv :148-225, read_polygon_geojson :280-309, write_results_csv
+// :325-335), included from /root/reference at build time.
 // Checker for the GPU CSV reader (paper_2306_04316_b200/csrc/pip_csv.cu) in
 // tests/ and the CPU baseline of bench.py's csv workload; never the product.
 #include <polycast/io.hpp>
@@ -89,6 +89,56 @@ int ref_write_results_csv(const char* path, const uint64_t* index, const double*
     } catch (const IoError&) {
         return 4;
     } catch (const std::exception&) {
+        return 6;
+    }
+}
+
+// read_polygon_geojson; kind: 0 ok, 1 GeoJsonError, 2 UnsupportedGeometry, 3 RingTooShort,
+// 4 FileNotFound, 5 IoError, 6 other std::exception.  Rings: ring_sizes[k] vertices each
+// (closing vertex included), all vertices in out_xy.
+int ref_read_polygon_geojson(const char* path, double* out_xy, uint64_t cap_verts, uint64_t* ring_sizes,
+                             uint64_t cap_rings, uint64_t* n_rings, uint64_t* n_verts, char* msg, uint64_t msg_cap) {
+    auto put = [&](const char* w) {
+        if (msg && msg_cap) {
+            std::strncpy(msg, w, msg_cap - 1);
+            msg[msg_cap - 1] = 0;
+        }
+    };
+    *n_rings = *n_verts = 0;
+    try {
+        const Polygon poly = read_polygon_geojson(path);
+        uint64_t v = 0, r = 0;
+        for (const Ring& ring : poly.rings()) {
+            if (r < cap_rings) ring_sizes[r] = ring.size();
+            ++r;
+            for (const Point2& q : ring.vertices()) {
+                if (v < cap_verts) {
+                    out_xy[2 * v] = q.x;
+                    out_xy[2 * v + 1] = q.y;
+                }
+                ++v;
+            }
+        }
+        *n_rings = r;
+        *n_verts = v;
+        return 0;
+    } catch (const RingTooShort& e) {
+        put(e.what());
+        return 3;
+    } catch (const UnsupportedGeometry& e) {
+        put(e.what());
+        return 2;
+    } catch (const GeoJsonError& e) {
+        put(e.what());
+        return 1;
+    } catch (const FileNotFound& e) {
+        put(e.what());
+        return 4;
+    } catch (const IoError& e) {
+        put(e.what());
+        return 5;
+    } catch (const std::exception& e) {
+        put(e.what());
         return 6;
     }
 }

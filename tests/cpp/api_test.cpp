@@ -455,6 +455,79 @@ void results_csv() {
     std::remove(out.c_str());
 }
 
+// read_polygons_geojson (extension) feeding classify_batch_many: a
+// FeatureCollection of random polygons with holes, written with %.17g, reads
+// back bit-exactly and classifies like per-polygon classify_batch
+void geojson_to_csr() {
+    std::mt19937_64 g(31);
+    std::vector<Polygon> polys;
+    std::string doc = R"({"type":"FeatureCollection","features":[)";
+    char b[64];
+    auto ring_json = [&](const Ring& r) {
+        std::string s = "[";
+        for (std::size_t i = 0; i < r.size(); ++i) {
+            std::snprintf(b, sizeof b, "%s[%.17g,%.17g]", i ? "," : "", r[i].x, r[i].y);
+            s += b;
+        }
+        return s + "]";
+    };
+    for (int k = 0; k < 60; ++k) {
+        const Polygon base = random_polygon(g, 5 + g() % 60);
+        std::vector<Ring> holes;
+        if (k % 3 == 0) { // a small square hole around the polygon's first vertex's midpoint to its centroid
+            const Point2 v = base.outer()[0];
+            const double h = 1e-3;
+            holes.emplace_back(std::vector<Point2>{Point2(v.x * 0.5 - h, v.y * 0.5 - h), Point2(v.x * 0.5 + h, v.y * 0.5 - h),
+                                                   Point2(v.x * 0.5 + h, v.y * 0.5 + h), Point2(v.x * 0.5 - h, v.y * 0.5 + h),
+                                                   Point2(v.x * 0.5 - h, v.y * 0.5 - h)});
+        }
+        Ring outer(std::vector<Point2>(base.outer().vertices().begin(), base.outer().vertices().end()));
+        const Polygon poly(outer, holes);
+        std::string coords = ring_json(poly.outer());
+        for (const Ring& hr : poly.holes()) coords += "," + ring_json(hr);
+        doc += std::string(k ? "," : "") + R"({"type":"Feature","properties":{"id":)" + std::to_string(k) +
+               R"(},"geometry":{"type":"Polygon","coordinates":[)" + coords + "]}}";
+        polys.push_back(poly);
+    }
+    doc += "]}";
+    const std::string path = "/tmp/pc_geojson_csr.json";
+    FILE* f = std::fopen(path.c_str(), "wb");
+    std::fwrite(doc.data(), 1, doc.size(), f);
+    std::fclose(f);
+    const std::vector<Polygon> back = read_polygons_geojson(path);
+    CHECK(back.size() == polys.size());
+    bool same = back.size() == polys.size();
+    for (std::size_t i = 0; same && i < polys.size(); ++i) {
+        same = back[i].rings().size() == polys[i].rings().size();
+        for (std::size_t r = 0; same && r < polys[i].rings().size(); ++r) {
+            const Ring &a = back[i].rings()[r], &c = polys[i].rings()[r];
+            same = a.size() == c.size() &&
+                   std::memcmp(a.vertices().data(), c.vertices().data(), a.size() * sizeof(Point2)) == 0;
+        }
+    }
+    CHECK(same);
+    CHECK(read_polygon_geojson(path).outer().size() == polys[0].outer().size()); // the first feature
+    std::vector<PointBatch> batches(polys.size());
+    for (std::size_t i = 0; i < polys.size(); ++i) {
+        const BBox bb = bbox_of(polys[i]);
+        for (int j = 0; j < 300; ++j)
+            batches[i].points.emplace_back(uni(g, bb.min_x - 1, bb.max_x + 1), uni(g, bb.min_y - 1, bb.max_y + 1));
+    }
+    for (CrossingMode m : {CrossingMode::C1, CrossingMode::C2, CrossingMode::Robust}) {
+        const BatchResult all = classify_batch_many(batches, polys, m);
+        std::size_t at = 0;
+        bool eq = true;
+        for (std::size_t i = 0; i < polys.size(); ++i) {
+            const BatchResult one = classify_batch(batches[i], polys[i], m);
+            for (std::size_t j = 0; j < one.verdicts.size(); ++j) eq = eq && all.verdicts[at + j] == one.verdicts[j];
+            at += one.verdicts.size();
+        }
+        CHECK(eq);
+    }
+    std::remove(path.c_str());
+    std::printf("geojson: %zu polygons read back bit-exactly and classified through the CSR path\n", back.size());
+}
+
 } // namespace
 
 int main(int argc, char** argv) {
@@ -471,6 +544,7 @@ int main(int argc, char** argv) {
         prefilter_scatter();
         csv_vs_reference();
         results_csv();
+        geojson_to_csr();
     } catch (const std::exception& e) {
         std::fprintf(stderr, "FAIL: uncaught exception: %s\n", e.what());
         return 100;
