@@ -127,8 +127,11 @@ PC_HD uint64_t round192(const uint64_t z[3], int top, int f) {
     return ((uint64_t)(e2 + 1023) << 52) | (mant & ((1ull << 52) - 1));
 }
 
-// Rounding of w * M * 2^(e5 - 127 + q) where M = {mhi, mlo} (a 128-bit value)
-PC_HD uint64_t round_product(uint64_t w, uint64_t mhi, uint64_t mlo, int e5, int q) {
+// Rounding of w * M * 2^(e5 - 127 + q) where M = {mhi, mlo} (a 128-bit value).
+// With near_half != nullptr, also reports whether the bits below the
+// rounding position are within 2^64 units of one half: then w * (M + 1) --
+// the product's upper bound when M is a truncation -- may round differently.
+PC_HD uint64_t round_product(uint64_t w, uint64_t mhi, uint64_t mlo, int e5, int q, bool* near_half = nullptr) {
     const int lz = clz64(w);
     const uint64_t wn = w << lz;
     // Z = wn * (mhi * 2^64 + mlo), 192 bits
@@ -139,7 +142,33 @@ PC_HD uint64_t round_product(uint64_t w, uint64_t mhi, uint64_t mlo, int e5, int
     z[1] = p1 + p2;
     z[2] = p3 + (z[1] < p1 ? 1u : 0u);
     const int top = (z[2] >> 63) ? 191 : 190;
-    return round192(z, top, e5 - 127 + q - lz);
+    const int f = e5 - 127 + q - lz;
+    if (near_half) {
+        // the rounding position of round192: bits below `drop` are rounded off
+        const int e2 = top + f;
+        int drop = top - 52;
+        if (e2 < -1022) drop += -1022 - e2;
+        if (drop <= 66 || drop > 192) {
+            *near_half = true; // the error window reaches the half bit: decide exactly
+        } else {
+            // bits [64, drop - 1): z[1] whole, then z[2] below bit drop - 1 - 128 (if drop - 1 > 128)
+            const int hb = drop - 1;
+            const bool half = bit192(z, hb);
+            uint64_t m1 = z[1], m2 = 0, full2 = 0;
+            if (hb > 128) {
+                full2 = (hb - 128 >= 64) ? ~0ull : ((1ull << (hb - 128)) - 1ull);
+                m2 = z[2] & full2;
+            } else { // hb in (66, 128]: only z[1] bits [0, hb - 64)
+                const uint64_t k = (1ull << (hb - 64)) - 1ull;
+                m1 &= k;
+                full2 = 0;
+                *near_half = half ? (m1 == 0) : (m1 == k);
+                return round192(z, top, f);
+            }
+            *near_half = half ? (m1 == 0 && m2 == 0) : (m1 == ~0ull && m2 == full2);
+        }
+    }
+    return round192(z, top, f);
 }
 
 // ---- exact comparison (rare path) ------------------------------------------
@@ -365,27 +394,35 @@ PC_HD bool parse_f64(const char* s, int n, double* out) {
     if (q > kQMax) return false; // overflow
     const Pow5& P = kPow5[q - kQMin];
     const bool exact5 = q >= 0 && q <= 55;
-    const uint64_t lo = round_product(w, P.hi, P.lo, P.e, (int)q);
-    // upper bound of the scaled value: (w + 1 if digits were dropped) * (M + 1 unless exact) - 1
-    const uint64_t wu = trunc ? w + 1 : w;
-    uint64_t mhi = P.hi, mlo = P.lo;
-    uint64_t hi;
-    if (!exact5 || trunc) {
-        if (!exact5 && ++mlo == 0) ++mhi;
-        // (wu * M') is an exclusive upper bound; rounding of (wu * M' - 1) -- the
-        // product minus one ulp of the 192-bit value -- is approximated by the
-        // rounding of wu * M' itself, which can only make the bounds disagree
-        // (then the exact path decides)
-        hi = round_product(wu, mhi, mlo, P.e, (int)q);
-    } else {
-        hi = lo;
-    }
     uint64_t bits;
-    if (lo == hi) {
-        bits = lo;
+    if (!trunc) {
+        // w is exact: the scaled value lies in [w M, w (M + 1)) (M exact for 0 <= q <= 55);
+        // one product decides unless its rounded-off bits sit within w of one half
+        bool near = false;
+        const uint64_t r = round_product(w, P.hi, P.lo, P.e, (int)q, exact5 ? nullptr : &near);
+        if (!near) {
+            bits = r;
+        } else {
+            if (r == ~0ull) return false; // overflow even from below
+            // candidates r - 1 / r when z rounded up (half bit set), r / r + 1 otherwise:
+            // decide between the two around the half
+            bits = exact_decide(s + start, mant_end - start, exp10, r);
+            const uint64_t b2 = r ? exact_decide(s + start, mant_end - start, exp10, r - 1) : r;
+            bits = (b2 == r - 1 && r) ? b2 : bits;
+        }
     } else {
-        if (lo == ~0ull) return false; // even the lower bound overflows
-        bits = exact_decide(s + start, mant_end - start, exp10, lo);
+        const uint64_t lo = round_product(w, P.hi, P.lo, P.e, (int)q);
+        // upper bound: (w + 1) (M + 1 unless exact); rounding of that product stands in
+        // for the rounding of the exclusive bound (can only make the bounds disagree)
+        uint64_t mhi = P.hi, mlo = P.lo;
+        if (!exact5 && ++mlo == 0) ++mhi;
+        const uint64_t hi = round_product(w + 1, mhi, mlo, P.e, (int)q);
+        if (lo == hi) {
+            bits = lo;
+        } else {
+            if (lo == ~0ull) return false; // even the lower bound overflows
+            bits = exact_decide(s + start, mant_end - start, exp10, lo);
+        }
     }
     if (bits == 0 || bits >= (0x7ffull << 52)) return false; // rounded to zero / overflow
     *out = bits_to_double(bits | sign);
