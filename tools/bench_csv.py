@@ -116,6 +116,10 @@ def main():
     if os.path.exists(pp):
         peaks = json.load(open(pp))
     peak = peaks.get("hbm_gbs", 7672.0)
+    traffic = {}  # DRAM bytes per launch from the last committed ncu --set full capture
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tf):
+        traffic = json.load(open(tf))
     alg = len(text) + 16 * args.rows
     achieved = alg / (kern_ms * 1e-3) / 1e9
 
@@ -147,7 +151,7 @@ def main():
             "config": {"workload": f"points CSV id,lon,lat: {args.rows} rows, %.17g coordinates, "
                                    f"{len(text)} bytes", "l2": "256 MiB buffer written between timed launches"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": (traffic.get("csv_parse") or {}).get("dram_bytes_per_launch"),
                          "algorithmic_bytes": alg, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else
                          "B200_PROFILING.md fallback"},
             "e2e": {"value": args.rows / e2e, "unit": "rows/s", "h2d_bytes_per_step": len(text),
@@ -219,7 +223,7 @@ def main():
              "config": {"workload": f"write_results_csv text of {n} records ({out_len} bytes), the parsed points, "
                                     f"random verdicts", "l2": "256 MiB buffer written between timed launches"},
              "roofline": {"bound": "hbm", "achieved": ach2, "peak": peak, "unit": "GB/s", "frac": ach2 / peak,
-                          "traffic": None, "algorithmic_bytes": alg2},
+                          "traffic": (traffic.get("csv_emit") or {}).get("dram_bytes_per_launch"), "algorithmic_bytes": alg2},
              "e2e": {"value": n / e2e_emit, "unit": "rows/s", "h2d_bytes_per_step": 32 * n,
                      "d2h_bytes_per_step": out_len, "seconds": e2e_emit},
              "gpu_launches": 3, "cpu_baseline": cpu2, "kernel_ms_all": ems}
