@@ -409,21 +409,18 @@ size_t csr_meta_bytes(uint64_t n_polys) {
 
 cudaError_t launch_csr(const CsrArgs& a, cudaStream_t st, int dev, uint64_t* launches) {
     if (a.n_polys == 0) return cudaSuccess;
-    switch (a.mode) {
-    case kC1: {
-        // tiles of small polygons in the tile kernel; tiles whose vertices do not
-        // fit its shared memory are deferred to the warp-per-polygon kernel
-        uint32_t* list = reinterpret_cast<uint32_t*>(static_cast<char*>(a.meta) + (size_t)a.n_polys * sizeof(PolyMeta));
-        uint32_t* count = list + a.n_polys;
-        cudaError_t e = cudaMemsetAsync(count, 0, sizeof(uint32_t), st);
-        if (e != cudaSuccess) return e;
-        e = launch_csr_tile(a, list, count, st, dev, launches);
-        if (e != cudaSuccess) return e;
-        return launch_warp<kC1>(a, list, count, st, dev, launches);
-    }
-    case kC2: return launch_warp<kC2>(a, nullptr, nullptr, st, dev, launches);
-    default: return launch_warp<kRobust>(a, nullptr, nullptr, st, dev, launches);
-    }
+    if (a.mode == kRobust) return launch_warp<kRobust>(a, nullptr, nullptr, st, dev, launches);
+    // C1 / C2: small polygons in the tile kernel (pip_csr_tile.cu); polygons whose
+    // vertices do not fit its shared-memory slice are deferred to the
+    // warp-per-polygon kernel
+    uint32_t* list = reinterpret_cast<uint32_t*>(static_cast<char*>(a.meta) + (size_t)a.n_polys * sizeof(PolyMeta));
+    uint32_t* count = list + a.n_polys;
+    cudaError_t e = cudaMemsetAsync(count, 0, sizeof(uint32_t), st);
+    if (e != cudaSuccess) return e;
+    e = launch_csr_tile(a, list, count, st, dev, launches);
+    if (e != cudaSuccess) return e;
+    return a.mode == kC1 ? launch_warp<kC1>(a, list, count, st, dev, launches)
+                         : launch_warp<kC2>(a, list, count, st, dev, launches);
 }
 
 } // namespace pcd

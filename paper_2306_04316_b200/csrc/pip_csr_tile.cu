@@ -1,5 +1,6 @@
-// CSR batch kernel for C1 (the paper's side-of-normal test, configs 3 and 5):
-// many small polygons, each with its own contiguous run of query points.
+// CSR batch kernel for C1 (the paper's side-of-normal test, configs 3 and 5)
+// and C2 (parametric crossing): many small polygons, each with its own
+// contiguous run of query points.
 //
 // Every warp works on its own: it takes a group of 32 consecutive polygons
 // (lane = polygon), resolves their point / vertex / ring ranges, and then
@@ -21,9 +22,12 @@
 // afterwards by the warp-per-polygon kernel (pip_csr.cu), which streams
 // edges in chunks.
 //
-// Reference semantics per polygon: classify_batch(points_i, poly_i, C1)
+// Reference semantics per polygon: classify_batch(points_i, poly_i, mode)
 // (batch.hpp:184-230) -> bbox short-circuit (batch.hpp:200) -> contains
-// (geometry.hpp:281-300) -> count_crossings_c1 over every ring.
+// (geometry.hpp:281-300) -> count_crossings_c1 / _c2 over every ring; a C2
+// DegenerateEdge (a horizontal edge on the ray) makes the point Error (aux
+// plane).  C2 uses the same fast pass with the intercept-side record of
+// pip_device.cuh local_side_record_c2 (gate: max|x| * s_x <= 2^20).
 #include "pip_kernels.h"
 
 #include <cuda_runtime.h>
@@ -76,9 +80,11 @@ __device__ __forceinline__ bool is_ring_end(const WarpSmem& ws, uint32_t i) {
 // walk_all (warp-uniform): skip the fp32 pass and walk every candidate edge in
 // binary64 -- cheaper when most points tie vertex keys anyway (returns the
 // number of undecided points so the caller can pick the mode adaptively).
+template <int MODE>
 __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t cc, const double2 (&qc)[2],
                                              int lane, const double2* __restrict__ pts,
-                                             uint32_t* __restrict__ inside_bits, bool walk_all) {
+                                             uint32_t* __restrict__ inside_bits, uint32_t* __restrict__ aux_bits,
+                                             bool walk_all) {
     const BPoly& tp = ws.bp[j];
     const uint32_t np = tp.np, e0 = tp.e0, e1 = tp.e1;
     const double bx0 = tp.bx0, by0 = tp.by0, bx1 = tp.bx1, by1 = tp.by1;
@@ -101,7 +107,7 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
         qok |= (uint32_t)(a && fast && fabs(q.y) >= 0x1p-400) << k;
     }
     if (!__any_sync(kFull, act != 0)) return 0;
-    uint32_t par = 0, slow = act & ~qok, band = 0;
+    uint32_t par = 0, slow = act & ~qok, band = 0, err = 0;
     if (fast && walk_all) {
         slow = act;
         band = act; // every candidate edge of every point
@@ -202,31 +208,48 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
                     m &= m - 1;
                     const double2 a = ws.vert[i], b = ws.vert[i + 1];
                     if (__dmul_rn(__dsub_rn(a.y, py[k]), __dsub_rn(b.y, py[k])) <= 0.0) {
-                        double nx = __dsub_rn(b.y, a.y), ny = __dsub_rn(a.x, b.x);
-                        if (nx < 0.0) {
-                            nx = -nx;
-                            ny = -ny;
+                        if (MODE == kC1) { // count_crossings_c1 (geometry.hpp:189-200)
+                            double nx = __dsub_rn(b.y, a.y), ny = __dsub_rn(a.x, b.x);
+                            if (nx < 0.0) {
+                                nx = -nx;
+                                ny = -ny;
+                            }
+                            const double side =
+                                __dadd_rn(__dmul_rn(__dsub_rn(px[k], a.x), nx), __dmul_rn(__dsub_rn(py[k], a.y), ny));
+                            if (side <= 0.0) par ^= 1u << k;
+                        } else { // count_crossings_c2 (geometry.hpp:216-224)
+                            const double dy = __dsub_rn(b.y, a.y);
+                            if (dy == 0.0) {
+                                err |= 1u << k; // DegenerateEdge
+                            } else {
+                                const double lambda = __ddiv_rn(__dsub_rn(py[k], a.y), dy);
+                                const double x = __dadd_rn(a.x, __dmul_rn(lambda, __dsub_rn(b.x, a.x)));
+                                if (x > px[k]) par ^= 1u << k;
+                            }
                         }
-                        const double side =
-                            __dadd_rn(__dmul_rn(__dsub_rn(px[k], a.x), nx), __dmul_rn(__dsub_rn(py[k], a.y), ny));
-                        if (side <= 0.0) par ^= 1u << k;
                     }
                 }
             }
         }
     }
-    const uint32_t b0 = __ballot_sync(kFull, act & par & 1u);
-    const uint32_t b1 = __ballot_sync(kFull, (act & par) >> 1 & 1u);
+    const uint32_t b0 = __ballot_sync(kFull, act & par & ~err & 1u);
+    const uint32_t b1 = __ballot_sync(kFull, (act & par & ~err) >> 1 & 1u);
     if (lane < 2) or_bits(inside_bits, tp.s + cc + 32 * lane, lane ? b1 : b0);
+    if (MODE == kC2 && __any_sync(kFull, err != 0)) {
+        const uint32_t e0 = __ballot_sync(kFull, act & err & 1u);
+        const uint32_t e1 = __ballot_sync(kFull, (act & err) >> 1 & 1u);
+        if (lane < 2) or_bits(aux_bits, tp.s + cc + 32 * lane, lane ? e1 : e0);
+    }
     return __popc(__ballot_sync(kFull, slow & 1u)) + __popc(__ballot_sync(kFull, slow >> 1 & 1u));
 }
 
+template <int MODE>
 __global__ void __launch_bounds__(kBThreads, 8) pip_csr_tile_kernel(
     const double2* __restrict__ pts, const unsigned long long* __restrict__ pt_off, unsigned long long n_polys,
     const double* __restrict__ vx, const double* __restrict__ vy, const unsigned long long* __restrict__ ring_off,
     const unsigned long long* __restrict__ poly_ring_off, unsigned long long pt_base, unsigned long long ring_base,
-    unsigned long long vert_base, uint32_t* __restrict__ inside_bits, uint32_t* __restrict__ defer_list,
-    uint32_t* __restrict__ defer_count) {
+    unsigned long long vert_base, uint32_t* __restrict__ inside_bits, uint32_t* __restrict__ aux_bits,
+    uint32_t* __restrict__ defer_list, uint32_t* __restrict__ defer_count) {
     __shared__ WarpSmem smem[kBWarps];
     const int lane = threadIdx.x & 31;
     WarpSmem& ws = smem[threadIdx.x >> 5];
@@ -324,9 +347,11 @@ __global__ void __launch_bounds__(kBThreads, 8) pip_csr_tile_kernel(
                 b.bx1 = bx1;
                 b.by1 = by1;
                 const double W = __dsub_rn(bx1, bx0), H = __dsub_rn(by1, by0);
-                const bool fast = W >= 0x1p-300 && W <= 0x1p300 && H >= 0x1p-300 && H <= 0x1p300;
+                bool fast = W >= 0x1p-300 && W <= 0x1p300 && H >= 0x1p-300 && H <= 0x1p300;
                 b.sx = fast ? pow2_below_inv(W) : 1.0;
                 b.sy = fast ? pow2_below_inv(H) : 1.0;
+                // C2: the reference's intercept rounding scales with |x| (pip_device.cuh local_side_record_c2)
+                if (MODE == kC2) fast = fast && __dmul_rn(fmax(fabs(bx0), fabs(bx1)), b.sx) <= 0x1p20;
                 b.s = ws.gs[lane];
                 b.np = ws.gnp[lane];
                 b.e0 = excl;
@@ -350,14 +375,22 @@ __global__ void __launch_bounds__(kBThreads, 8) pip_csr_tile_kernel(
                 if (!is_ring_end(ws, i)) {
                     const double2 b = ws.vert[i + 1];
                     const int qb = __double2int_rz(__dmul_rn(__dmul_rn(__dsub_rn(b.y, by0), sy), 0x1p30));
-                    // the reference's normal (geometry.hpp:190-195)
-                    double nx = __dsub_rn(b.y, a.y), ny = __dsub_rn(a.x, b.x);
-                    if (nx < 0.0) {
-                        nx = -nx;
-                        ny = -ny;
+                    double Nx, Ny;
+                    if (MODE == kC1) { // the reference's normal (geometry.hpp:190-195)
+                        double nx = __dsub_rn(b.y, a.y), ny = __dsub_rn(a.x, b.x);
+                        if (nx < 0.0) {
+                            nx = -nx;
+                            ny = -ny;
+                        }
+                        Nx = __dmul_rn(nx, sy);
+                        Ny = __dmul_rn(ny, sx);
+                    } else { // C2: sign(dy) * (dy, -dx): the count is the sign of C * sign(dy) < 0
+                        const double dy = __dsub_rn(b.y, a.y), dx = __dsub_rn(b.x, a.x);
+                        const double sg = dy > 0.0 ? 1.0 : -1.0;
+                        Nx = __dmul_rn(__dmul_rn(dy, sy), sg);
+                        Ny = __dmul_rn(__dmul_rn(-dx, sx), sg);
                     }
                     const int qlo = min(qa, qb), qhi = max(qa, qb);
-                    const double Nx = __dmul_rn(nx, sy), Ny = __dmul_rn(ny, sx);
                     const double cd = __dadd_rn(__dmul_rn(axl, Nx), __dmul_rn(ayl, Ny));
                     f = make_int4(qlo + 1, qhi, qa, __float_as_int(__double2float_rn(Nx)));
                     // offset c + B (see classify_item): the extra fp32 rounding (<= 2 * 2^-24)
@@ -391,7 +424,7 @@ __global__ void __launch_bounds__(kBThreads, 8) pip_csr_tile_kernel(
                     ++j;
                 }
                 if (j < nb) load(j, c, qn0, qn1);
-                const int ns = classify_item(ws, cj, cc, qc, lane, pts, inside_bits, walk_left > 0);
+                const int ns = classify_item<MODE>(ws, cj, cc, qc, lane, pts, inside_bits, aux_bits, walk_left > 0);
                 // mode choice: after an fp32 pass that left >= 1/4 of the points
                 // undecided, walk everything for the next 16 steps, then probe again
                 if (walk_left > 0) --walk_left;
@@ -411,22 +444,33 @@ int sms(int dev) {
 
 } // namespace
 
-cudaError_t launch_csr_tile(const CsrArgs& a, uint32_t* list, uint32_t* count, cudaStream_t st, int dev,
-                            uint64_t* launches) {
-    if (a.n_polys > 0xffffffffull) return cudaErrorInvalidValue; // 32-bit deferred-polygon list
+namespace {
+
+template <int MODE>
+cudaError_t launch_tile(const CsrArgs& a, uint32_t* list, uint32_t* count, cudaStream_t st, int dev,
+                        uint64_t* launches) {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pip_csr_tile_kernel, kBThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pip_csr_tile_kernel<MODE>, kBThreads, 0);
     per_sm = std::max(per_sm, 1);
     const uint64_t ngroups = (a.n_polys + 31) / 32;
     const uint64_t want = (ngroups + kBWarps - 1) / kBWarps;
     const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)sms(dev) * per_sm));
-    pip_csr_tile_kernel<<<grid, kBThreads, 0, st>>>(
+    pip_csr_tile_kernel<MODE><<<grid, kBThreads, 0, st>>>(
         reinterpret_cast<const double2*>(a.pts), reinterpret_cast<const unsigned long long*>(a.pt_off), a.n_polys,
         a.vx, a.vy, reinterpret_cast<const unsigned long long*>(a.ring_off),
         reinterpret_cast<const unsigned long long*>(a.poly_ring_off), a.pt_base, a.ring_base, a.vert_base,
-        a.inside_bits, list, count);
+        a.inside_bits, a.aux_bits, list, count);
     ++*launches;
     return cudaGetLastError();
+}
+
+} // namespace
+
+cudaError_t launch_csr_tile(const CsrArgs& a, uint32_t* list, uint32_t* count, cudaStream_t st, int dev,
+                            uint64_t* launches) {
+    if (a.n_polys > 0xffffffffull) return cudaErrorInvalidValue; // 32-bit deferred-polygon list
+    if (a.mode == kC2) return launch_tile<kC2>(a, list, count, st, dev, launches);
+    return launch_tile<kC1>(a, list, count, st, dev, launches);
 }
 
 } // namespace pcd

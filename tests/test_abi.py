@@ -45,7 +45,7 @@ def test_no_fma_in_c1_kernels():
     correctly rounded __ddiv_rn sequence, which contains DFMA internally)."""
     sass = subprocess.run(["cuobjdump", "-sass", _native.CUDA_LIB], capture_output=True, text=True).stdout
     funcs = re.split(r"\n\s*Function : ", sass)
-    c1 = [f for f in funcs if re.match(r"\S*(pip_tile_kernelILi0E|pip_csr_warp_kernelILi0E|pip_csr_tile_kernel|count_kernelILi0E)", f)]
+    c1 = [f for f in funcs if re.match(r"\S*(pip_tile_kernelILi0E|pip_csr_warp_kernelILi0E|pip_csr_tile_kernelILi0E|count_kernelILi0E)", f)]
     assert len(c1) >= 3
     for f in c1:
         assert "DFMA" not in f

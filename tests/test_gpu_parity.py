@@ -435,6 +435,11 @@ def test_csr_fast_path_gates(engine):
     ys = np.array([0.0, -0.0, 1e-320, -1e-320, 1e-310, -1e-310, 2e-310, 1e-130, 1e-121, 3e-121, -3e-121])
     exy = np.stack([np.repeat(np.linspace(-1.2, 1.2, 13), len(ys)), np.tile(ys, 13)], 1)
     parts.append(_single_as_csr(pe, np.concatenate([exy, rng.uniform(-1.2, 1.2, (500, 2))])))
+    # footprints moved along x: |x| * s_x below / above the C2 fast-path gate (2^20)
+    for shift in (100.0, 3000.0):
+        fp = _near_edge_points(W.footprints(60, seed=int(shift)), (1e-12, 1e-9, 1e-6))
+        parts.append(CsrSet(np.ascontiguousarray(fp.xy + [shift, 0.0]), fp.pt_off, fp.vx + shift, fp.vy, fp.ring_off,
+                            fp.poly_ring_off))
     s = _concat_csr(parts)
     for mode in MODES:
         got = engine.classify_csr(s, mode)
