@@ -409,8 +409,7 @@ size_t csr_meta_bytes(uint64_t n_polys) {
 
 cudaError_t launch_csr(const CsrArgs& a, cudaStream_t st, int dev, uint64_t* launches) {
     if (a.n_polys == 0) return cudaSuccess;
-    if (a.mode == kRobust) return launch_warp<kRobust>(a, nullptr, nullptr, st, dev, launches);
-    // C1 / C2: small polygons in the tile kernel (pip_csr_tile.cu); polygons whose
+    // small polygons in the tile kernel (pip_csr_tile.cu); polygons whose
     // vertices do not fit its shared-memory slice are deferred to the
     // warp-per-polygon kernel
     uint32_t* list = reinterpret_cast<uint32_t*>(static_cast<char*>(a.meta) + (size_t)a.n_polys * sizeof(PolyMeta));
@@ -419,8 +418,9 @@ cudaError_t launch_csr(const CsrArgs& a, cudaStream_t st, int dev, uint64_t* lau
     if (e != cudaSuccess) return e;
     e = launch_csr_tile(a, list, count, st, dev, launches);
     if (e != cudaSuccess) return e;
-    return a.mode == kC1 ? launch_warp<kC1>(a, list, count, st, dev, launches)
-                         : launch_warp<kC2>(a, list, count, st, dev, launches);
+    if (a.mode == kC1) return launch_warp<kC1>(a, list, count, st, dev, launches);
+    if (a.mode == kC2) return launch_warp<kC2>(a, list, count, st, dev, launches);
+    return launch_warp<kRobust>(a, list, count, st, dev, launches);
 }
 
 } // namespace pcd

@@ -84,14 +84,14 @@ template <int MODE>
 __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t cc, const double2 (&qc)[2],
                                              int lane, const double2* __restrict__ pts,
                                              uint32_t* __restrict__ inside_bits, uint32_t* __restrict__ aux_bits,
-                                             bool walk_all) {
+                                             double tol, double tol2, bool walk_all) {
     const BPoly& tp = ws.bp[j];
     const uint32_t np = tp.np, e0 = tp.e0, e1 = tp.e1;
     const double bx0 = tp.bx0, by0 = tp.by0, bx1 = tp.bx1, by1 = tp.by1;
     const double sx = tp.sx, sy = tp.sy;
     const bool fast = tp.nloop >> 31;
     float lx[2], ly[2];
-    int qy[2];
+    int qy[2], qm[2], qp[2]; // keys of p.y; Robust: of RN(p.y - tol), RN(p.y + tol) (else = qy)
     uint32_t act = 0, qok = 0;
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
@@ -103,6 +103,12 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
         lx[k] = __double2float_rn(__dmul_rn(__dsub_rn(q.x, bx0), sx));
         ly[k] = __double2float_rn(yl);
         qy[k] = __double2int_rz(__dmul_rn(yl, 0x1p30)); // = trunc((y - o_y) * s_y * 2^30): exact scaling
+        if (MODE == kRobust) { // the band reject's own rounded values (geometry.hpp:248)
+            qm[k] = __double2int_rz(__dmul_rn(__dmul_rn(__dsub_rn(__dsub_rn(q.y, tol), by0), sy), 0x1p30));
+            qp[k] = __double2int_rz(__dmul_rn(__dmul_rn(__dsub_rn(__dadd_rn(q.y, tol), by0), sy), 0x1p30));
+        } else {
+            qm[k] = qp[k] = qy[k];
+        }
         // the key filters are exact only for |p.y| >= 2^-400 (pip_csr_common.cuh)
         qok |= (uint32_t)(a && fast && fabs(q.y) >= 0x1p-400) << k;
     }
@@ -124,12 +130,12 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
             const float nxf = __int_as_float(f.w);
             const float s0 = fmaf(lx[0], nxf, fmaf(ly[0], g.x, g.y));
             const float s1 = fmaf(lx[1], nxf, fmaf(ly[1], g.x, g.y));
-            acc0 ^= (qy[0] - f.y) & ~(qy[0] - f.x) & __float_as_int(s0);
-            acc1 ^= (qy[1] - f.y) & ~(qy[1] - f.x) & __float_as_int(s1);
+            acc0 ^= (qp[0] - f.y) & ~(qm[0] - f.x) & __float_as_int(s0);
+            acc1 ^= (qp[1] - f.y) & ~(qm[1] - f.x) & __float_as_int(s1);
             u0 = min(u0, __float_as_uint(s0)); // band hits
             u1 = min(u1, __float_as_uint(s1));
-            t0 = min(t0, (unsigned)(qy[0] - f.z)); // ties: 0 iff q(p.y) == q(vertex)
-            t1 = min(t1, (unsigned)(qy[1] - f.z));
+            t0 = min(t0, (unsigned)(f.z - qm[0])); // ties: a vertex key in [qm, qp]
+            t1 = min(t1, (unsigned)(f.z - qm[1]));
         };
         // four records per iteration; reads past the polygon's last record
         // re-read it (the final vertex's sentinel: no toggle, no band hit, a
@@ -147,7 +153,8 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
         constexpr uint32_t k2B = 0x36000000u; // bits of 2^-19 = 2 * kFastBand
         const uint32_t fpar = ((uint32_t)acc0 >> 31) | (((uint32_t)acc1 >> 31) << 1);
         band = ((uint32_t)(u0 <= k2B) | ((uint32_t)(u1 <= k2B) << 1)) & act;
-        const uint32_t tie = ((uint32_t)(t0 == 0u) | ((uint32_t)(t1 == 0u) << 1)) & act;
+        const uint32_t tie =
+            ((uint32_t)(t0 <= (unsigned)(qp[0] - qm[0])) | ((uint32_t)(t1 <= (unsigned)(qp[1] - qm[1])) << 1)) & act;
         slow |= band | tie;
         // decided contributions (ties never toggle fpar); points with a band hit
         // redo every candidate edge
@@ -170,7 +177,7 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
         // one selection rule per warp: if any point has a band hit, every
         // undecided point redoes all its candidate edges (and drops fpar)
         const bool cand_mode = __any_sync(kFull, band != 0);
-        if (cand_mode) par &= ~slow;
+        if (cand_mode || MODE == kRobust) par &= ~slow; // Robust: a slow point redoes every candidate edge
         const int qy1[2] = {qy[0] + 1, qy[1] + 1};
         for (uint32_t i0 = e0; i0 < e1; i0 += 32) {
             const int n = (int)min(32u, e1 - i0);
@@ -181,7 +188,13 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
             const uint32_t real = ~ends & (n == 32 ? 0xffffffffu : ((1u << n) - 1u));
             uint32_t cm0 = 0u, cm1 = 0u;
             // record: f.x = q_lo + 1, f.y = q_hi
-            if (cand_mode) { // q_lo <= q <= q_hi
+            if (MODE == kRobust) { // edges the band reject may keep: q_lo <= q(RN(p.y + tol)), q(RN(p.y - tol)) <= q_hi
+                for (int u = n - 1; u >= 0; --u) {
+                    const int2 f = *reinterpret_cast<const int2*>(&ws.rec[i0 + u]);
+                    cm0 = (cm0 << 1) | (uint32_t)(((qp[0] + 1 - f.x) | (f.y - qm[0])) >= 0);
+                    cm1 = (cm1 << 1) | (uint32_t)(((qp[1] + 1 - f.x) | (f.y - qm[1])) >= 0);
+                }
+            } else if (cand_mode) { // q_lo <= q <= q_hi
                 for (int u = n - 1; u >= 0; --u) {
                     const int2 f = *reinterpret_cast<const int2*>(&ws.rec[i0 + u]);
                     const unsigned r = (unsigned)(f.y - f.x + 1);
@@ -207,7 +220,14 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
                     const uint32_t i = i0 + __ffs(m) - 1;
                     m &= m - 1;
                     const double2 a = ws.vert[i], b = ws.vert[i + 1];
-                    if (__dmul_rn(__dsub_rn(a.y, py[k]), __dsub_rn(b.y, py[k])) <= 0.0) {
+                    if (MODE == kRobust) { // robust_ray_crossings (geometry.hpp:242-270), literally
+                        int c = 0;
+                        bool bnd = false;
+                        double f_prev = 0.0; // unused by the Robust step
+                        raw_edge<kRobust>(px[k], py[k], tol, tol2, a.x, a.y, b.x, b.y, f_prev, c, bnd);
+                        if (c) par ^= 1u << k;
+                        if (bnd) err |= 1u << k; // Boundary
+                    } else if (__dmul_rn(__dsub_rn(a.y, py[k]), __dsub_rn(b.y, py[k])) <= 0.0) {
                         if (MODE == kC1) { // count_crossings_c1 (geometry.hpp:189-200)
                             double nx = __dsub_rn(b.y, a.y), ny = __dsub_rn(a.x, b.x);
                             if (nx < 0.0) {
@@ -235,7 +255,7 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
     const uint32_t b0 = __ballot_sync(kFull, act & par & ~err & 1u);
     const uint32_t b1 = __ballot_sync(kFull, (act & par & ~err) >> 1 & 1u);
     if (lane < 2) or_bits(inside_bits, tp.s + cc + 32 * lane, lane ? b1 : b0);
-    if (MODE == kC2 && __any_sync(kFull, err != 0)) {
+    if (MODE != kC1 && __any_sync(kFull, err != 0)) { // C2: Error (DegenerateEdge), Robust: Boundary
         const uint32_t e0 = __ballot_sync(kFull, act & err & 1u);
         const uint32_t e1 = __ballot_sync(kFull, (act & err) >> 1 & 1u);
         if (lane < 2) or_bits(aux_bits, tp.s + cc + 32 * lane, lane ? e1 : e0);
@@ -248,8 +268,8 @@ __global__ void __launch_bounds__(kBThreads, 8) pip_csr_tile_kernel(
     const double2* __restrict__ pts, const unsigned long long* __restrict__ pt_off, unsigned long long n_polys,
     const double* __restrict__ vx, const double* __restrict__ vy, const unsigned long long* __restrict__ ring_off,
     const unsigned long long* __restrict__ poly_ring_off, unsigned long long pt_base, unsigned long long ring_base,
-    unsigned long long vert_base, uint32_t* __restrict__ inside_bits, uint32_t* __restrict__ aux_bits,
-    uint32_t* __restrict__ defer_list, uint32_t* __restrict__ defer_count) {
+    unsigned long long vert_base, double tol, double tol2, uint32_t* __restrict__ inside_bits,
+    uint32_t* __restrict__ aux_bits, uint32_t* __restrict__ defer_list, uint32_t* __restrict__ defer_count) {
     __shared__ WarpSmem smem[kBWarps];
     const int lane = threadIdx.x & 31;
     WarpSmem& ws = smem[threadIdx.x >> 5];
@@ -350,8 +370,14 @@ __global__ void __launch_bounds__(kBThreads, 8) pip_csr_tile_kernel(
                 bool fast = W >= 0x1p-300 && W <= 0x1p300 && H >= 0x1p-300 && H <= 0x1p300;
                 b.sx = fast ? pow2_below_inv(W) : 1.0;
                 b.sy = fast ? pow2_below_inv(H) : 1.0;
-                // C2: the reference's intercept rounding scales with |x| (pip_device.cuh local_side_record_c2)
-                if (MODE == kC2) fast = fast && __dmul_rn(fmax(fabs(bx0), fabs(bx1)), b.sx) <= 0x1p20;
+                // C2 / Robust: the reference's intercept rounding scales with |x|
+                // (pip_device.cuh local_side_record_c2)
+                if (MODE != kC1) fast = fast && __dmul_rn(fmax(fabs(bx0), fabs(bx1)), b.sx) <= 0x1p20;
+                // Robust: a decided sign must also rule out the boundary -- the point is
+                // then >= 0.64 * 2^-24 / max(s_x, s_y) from the edge's line,
+                // >= 2.5 tol under this gate
+                if (MODE == kRobust)
+                    fast = fast && tol >= 0.0 && __dmul_rn(__dmul_rn(tol, 2.0), fmax(b.sx, b.sy)) <= 0x1p-25;
                 b.s = ws.gs[lane];
                 b.np = ws.gnp[lane];
                 b.e0 = excl;
@@ -424,7 +450,8 @@ __global__ void __launch_bounds__(kBThreads, 8) pip_csr_tile_kernel(
                     ++j;
                 }
                 if (j < nb) load(j, c, qn0, qn1);
-                const int ns = classify_item<MODE>(ws, cj, cc, qc, lane, pts, inside_bits, aux_bits, walk_left > 0);
+                const int ns =
+                    classify_item<MODE>(ws, cj, cc, qc, lane, pts, inside_bits, aux_bits, tol, tol2, walk_left > 0);
                 // mode choice: after an fp32 pass that left >= 1/4 of the points
                 // undecided, walk everything for the next 16 steps, then probe again
                 if (walk_left > 0) --walk_left;
@@ -459,7 +486,7 @@ cudaError_t launch_tile(const CsrArgs& a, uint32_t* list, uint32_t* count, cudaS
         reinterpret_cast<const double2*>(a.pts), reinterpret_cast<const unsigned long long*>(a.pt_off), a.n_polys,
         a.vx, a.vy, reinterpret_cast<const unsigned long long*>(a.ring_off),
         reinterpret_cast<const unsigned long long*>(a.poly_ring_off), a.pt_base, a.ring_base, a.vert_base,
-        a.inside_bits, a.aux_bits, list, count);
+        a.tol, a.tol2, a.inside_bits, a.aux_bits, list, count);
     ++*launches;
     return cudaGetLastError();
 }
@@ -470,6 +497,7 @@ cudaError_t launch_csr_tile(const CsrArgs& a, uint32_t* list, uint32_t* count, c
                             uint64_t* launches) {
     if (a.n_polys > 0xffffffffull) return cudaErrorInvalidValue; // 32-bit deferred-polygon list
     if (a.mode == kC2) return launch_tile<kC2>(a, list, count, st, dev, launches);
+    if (a.mode == kRobust) return launch_tile<kRobust>(a, list, count, st, dev, launches);
     return launch_tile<kC1>(a, list, count, st, dev, launches);
 }
 

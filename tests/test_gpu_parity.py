@@ -532,3 +532,23 @@ def test_robust_tolerances(engine):
         want_v, want_s = oracle.ref_classify(xy, poly.vx, poly.vy, poly.ring_off, 2, tol=tol)
         assert np.array_equal(got.verdicts, want_v), (tol, int((got.verdicts != want_v).sum()))
         assert np.array_equal(got.stats, want_s)
+
+
+def test_csr_robust_tolerances(engine):
+    """CSR Robust fast path (pip_csr_tile.cu): keys of RN(p.y -+ tol) and the C2
+    record, gated by tol * 2 * max(s_x, s_y) <= 2^-25.  Footprints (~1e-4 deg) and
+    integer-grid polygons with points at distances around each tol from every edge
+    (0.5, 0.99, 1.01, 2 tol) plus the usual band deltas; tolerances on both sides
+    of the gate, against the C restatement (pinned to the reference)."""
+    base_fp = W.footprints(150, seed=51)
+    base_gr = W.degenerate(60, seed=52, allow_dups=False)
+    for tol in (0.0, 1e-12, 1e-10, 1e-8, 1e-6, 1e-3):
+        parts = []
+        for base, size in ((base_fp, 3e-4), (base_gr, 30.0)):
+            rel = tuple(f * tol / size for f in (0.5, 0.99, 1.01, 2.0)) if tol > 0 else ()
+            parts.append(_near_edge_points(base, rel + (1e-13, 1e-9, 1e-6)))
+        s = _concat_csr(parts)
+        got = engine.classify_csr(s, CrossingMode.Robust, boundary_tol=tol)
+        want_v, want_s = oracle.port_classify_csr(s, CrossingMode.Robust, tol=tol, threads=THREADS)
+        assert np.array_equal(got.verdicts, want_v), (tol, int((got.verdicts != want_v).sum()))
+        assert np.array_equal(got.stats, want_s)
