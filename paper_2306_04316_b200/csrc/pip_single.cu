@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstddef>
 #include <climits>
 #include <type_traits>
 
@@ -64,6 +65,21 @@ struct SingleShared {
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+// explicit shared-memory loads from a 32-bit shared address (kept in a
+// register by the caller, see the edge loop)
+__device__ __forceinline__ uint2 lds_u2(unsigned a) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ EdgeRec lds_rec(unsigned a) {
+    EdgeRec r;
+#pragma unroll
+    for (int i = 0; i < 8; i += 2)
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r.d[i]), "=d"(r.d[i + 1]) : "r"(a + 8u * i));
+    return r;
 }
 
 __device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
@@ -468,13 +484,19 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3) pip_tile_kernel
         mbar_wait(&sh.full[s], (q >> 1) & 1);
         const TileStage& T = sh.st[s];
         if (warp_live) {
+            // the stage's shared address, opaque to the compiler: kept in a
+            // register instead of being re-derived from the CTA's shared window
+            // base on every step of the edge loop
+            unsigned st_s = smem_u32(&T);
+            asm volatile("" : "+r"(st_s));
+            const unsigned filt_s = st_s + (unsigned)offsetof(TileStage, filt);
             // process one group of 4 edges that passed the warp-level test
             auto group = [&](uint32_t e0) {
                 // per-point filter of the 4 edges, then one warp-wide OR says
                 // which of them need the slow path
                 bool c[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) c[u] = lane_candidate<MODE>(K, T.filt[e0 + u]);
+                for (int u = 0; u < 4; ++u) c[u] = lane_candidate<MODE>(K, lds_u2(filt_s + 8u * (e0 + u)));
                 // common case: no candidate in the warp for any of the 4 edges
                 if (!__any_sync(0xffffffffu, c[0] | c[1] | c[2] | c[3])) return;
                 uint32_t bits = 0;
@@ -485,16 +507,17 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3) pip_tile_kernel
                 while (todo) {
                     const uint32_t e = e0 + (__ffs(todo) - 1);
                     todo &= todo - 1;
-                    const uint2 f = T.filt[e];
+                    const uint2 f = lds_u2(filt_s + 8u * e);
+                    const EdgeRec rec_e = lds_rec(st_s + (unsigned)sizeof(EdgeRec) * e);
                     // ---- slow path: exact binary64 test for the candidate points ----
                     if constexpr (MODE == kC1)
-                        slow_c1(sh.pts + wloc + lane, pts + cta_base + wloc + lane, K, act, nonloc, f, T.rec[e], par,
+                        slow_c1(sh.pts + wloc + lane, pts + cta_base + wloc + lane, K, act, nonloc, f, rec_e, par,
                                 wkey_lo, wkey_hi);
                     else if constexpr (MODE == kC2)
-                        slow_c2(sh.pts + wloc + lane, pts + cta_base + wloc + lane, K, act, nonloc, f, T.rec[e], par,
+                        slow_c2(sh.pts + wloc + lane, pts + cta_base + wloc + lane, K, act, nonloc, f, rec_e, par,
                                 auxm, wkey_lo, wkey_hi);
                     else
-                        slow_robust(sh.pts + wloc + lane, pts + cta_base + wloc + lane, K, act, nonloc, f, T.rec[e],
+                        slow_robust(sh.pts + wloc + lane, pts + cta_base + wloc + lane, K, act, nonloc, f, rec_e,
                                     tol, tol2, par, auxm, wka_max, wkb_min);
                 }
             };
@@ -502,7 +525,7 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3) pip_tile_kernel
             // points against each edge's key range), 8 edges per step with the
             // loads of both halves issued together; the stage's shared address is
             // formed once per tile
-            const unsigned wkr_s = smem_u32(T.wkr);
+            const unsigned wkr_s = st_s + (unsigned)offsetof(TileStage, wkr);
             for (uint32_t e0 = 0; e0 < nt; e0 += 8) {
                 uint4 r[4];
 #pragma unroll
