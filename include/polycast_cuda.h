@@ -199,6 +199,10 @@ uint64_t pc_last_launch_count(const pc_ctx* ctx);
  *  PC_OPT_BUCKET_POINTS: -1 auto (default), 0 off, 1 on — y-bucket the points of
  *  a single-polygon call before classifying, for SIMT coherence (pip_sort.cu). */
 #define PC_OPT_BUCKET_POINTS 1
+/*  PC_OPT_TREE: -1 auto (default), 0 off, 1 on — C1 single polygons: count a
+ *  point's crossings through a segment tree over the vertices' y-order
+ *  (pip_tree.cu) instead of scanning the edges. */
+#define PC_OPT_TREE 2
 int pc_set_option(pc_ctx* ctx, int option, int64_t value);
 
 /* Measurement hooks (bench.py).  With profiling on, every call records a pair

@@ -49,6 +49,7 @@ struct DevState {
     DevBuf cmp_blk, cmp_pts, cmp_idx, cmp_v, cmp_out;         // prefilter / scatter (pip_compact.cu)
     DevBuf csv_text, csv_state, csv_res, csv_out;             // CSV reader (pip_csv.cu)
     DevBuf emit_recs, emit_scratch, emit_out;                 // results-CSV writer (pip_emit.cu)
+    DevBuf tree;                                              // segment tree + fallback (pip_tree.cu)
     unsigned long long* h_stats = nullptr; // pinned 4 x u64
     pch::Stager* stager = nullptr;         // pageable host copies (host_stage.h), made on first use
     // profiling: one event pair per main-kernel launch since the last take
@@ -65,6 +66,7 @@ struct pc_ctx {
     uint64_t launches = 0;
     bool profiling = false;
     int64_t bucket_mode = -1; // PC_OPT_BUCKET_POINTS: -1 auto, 0 off, 1 on
+    int64_t tree_mode = -1;   // PC_OPT_TREE: -1 auto, 0 off, 1 on
 };
 
 namespace {
@@ -155,7 +157,8 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
     pa.n_zero_words = nwords;
     check(c, pcd::launch_prep(pa, st, d.dev, &c->launches), "prep kernel");
     check(c, cudaMemsetAsync(d_aux, 0, nwords * 4, st), "clear aux plane");
-    const bool bucket = n < 0xffffffffull &&
+    const bool tree = mode == 0 /* C1 */ && c->tree_mode != 0 && pcd::tree_eligible(n_verts, n, c->tree_mode == 1);
+    const bool bucket = !tree && n < 0xffffffffull &&
                         (c->bucket_mode == 1 || (c->bucket_mode < 0 && n_edges >= 64 && n >= 4096));
     pcd::SingleArgs sa{};
     sa.mode = mode;
@@ -189,6 +192,29 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
         sa.inside_bits = hist + hist_words;
         sa.aux_bits = hist + hist_words + nwords;
         sa.n_dev = hist + pcd::kBuckets + 1;
+    }
+    if (tree) { // segment-tree counts; key-tie / off-map points through the scan kernel
+        pcd::TreeArgs ta{};
+        ta.pts = d_pts;
+        ta.n = n;
+        ta.prefilter = prefilter;
+        ta.vx = d_vx;
+        ta.vy = d_vy;
+        ta.ring_off = d_ring_off;
+        ta.n_rings = n_rings;
+        ta.n_verts = n_verts;
+        ta.n_edges = n_edges;
+        ta.rec = d.rec.p;
+        ta.bbox_keys = d.bbox.as<unsigned long long>();
+        ta.inside_bits = d_inside;
+        ta.single = sa;
+        check(c, d.tree.ensure(pcd::tree_scratch_bytes(n_verts, n_edges, n)), "alloc segment tree");
+        mark_begin(c, d, st);
+        check(c, pcd::launch_tree(ta, d.tree.p, st, d.dev, &c->launches), "segment-tree kernels");
+        mark_end(c, d, st);
+        check(c, pcd::launch_finalize(n, d_inside, d_aux, d_verdicts, mode, d_stats, st, d.dev, &c->launches),
+              "finalize kernel");
+        return;
     }
     mark_begin(c, d, st);
     check(c, pcd::launch_single(sa, st, d.dev, &c->launches), "classify kernel");
@@ -323,7 +349,7 @@ void pc_destroy(pc_ctx* c) {
                           &d.bits, &d.verdicts, &d.stats, &d.counts, &d.degen, &d.bucket_scratch, &d.sorted_pts,
                           &d.sorted_idx, &d.bucket_blk, &d.csr_meta, &d.cmp_blk, &d.cmp_pts, &d.cmp_idx, &d.cmp_v,
                           &d.cmp_out, &d.csv_text, &d.csv_state, &d.csv_res, &d.csv_out, &d.emit_recs,
-                          &d.emit_scratch, &d.emit_out})
+                          &d.emit_scratch, &d.emit_out, &d.tree})
             b->release();
         if (d.h_stats) cudaFreeHost(d.h_stats);
         delete d.stager;
@@ -345,6 +371,10 @@ int pc_set_option(pc_ctx* c, int option, int64_t value) {
     std::lock_guard<std::mutex> lk(c->mu);
     if (option == PC_OPT_BUCKET_POINTS && value >= -1 && value <= 1) {
         c->bucket_mode = value;
+        return PC_OK;
+    }
+    if (option == PC_OPT_TREE && value >= -1 && value <= 1) {
+        c->tree_mode = value;
         return PC_OK;
     }
     c->err = "unknown option or value";

@@ -91,6 +91,28 @@ cudaError_t launch_csv_points(const char* text, uint64_t len, uint64_t data_star
                               char delim, double* out, uint64_t cap, void* scratch, unsigned long long* res,
                               cudaStream_t st, uint64_t* launches);
 
+// Segment-tree C1 path for one large polygon (pip_tree.cu): builds the tree
+// from the prepared polygon (prep_edges_kernel's records and map), counts the
+// clean points' crossings and sends the rest through launch_single(single);
+// writes every word of inside_bits.
+struct TreeArgs {
+    const double* pts;
+    uint64_t n;
+    int prefilter;
+    const double* vx;
+    const double* vy;
+    const uint64_t* ring_off;
+    uint32_t n_rings;
+    uint64_t n_verts, n_edges;
+    const void* rec;
+    const unsigned long long* bbox_keys;
+    uint32_t* inside_bits;
+    SingleArgs single; // the prepared scan-kernel arguments (for the fallback points)
+};
+bool tree_eligible(uint64_t n_verts, uint64_t n_pts, bool forced);
+size_t tree_scratch_bytes(uint64_t n_verts, uint64_t n_edges, uint64_t n_pts);
+cudaError_t launch_tree(const TreeArgs& a, void* scratch, cudaStream_t st, int dev, uint64_t* launches);
+
 // GPU results-CSV writer (pip_emit.cu): recs = n 32-byte records
 // (pc_result_record); out gets the header and the rows (at most cap bytes
 // written), *out_len (device) the full length; scratch = emit_scratch_bytes(n).

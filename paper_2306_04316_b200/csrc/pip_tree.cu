@@ -1,0 +1,529 @@
+// Segment-tree crossing count for one large polygon in C1 mode (the paper's
+// side-of-normal test; reference count_crossings_c1, geometry.hpp:182-203,
+// over every ring, contains :281-300).
+//
+// The scan kernel (pip_single.cu) tests every edge whose y-range holds a
+// point; for a spiky polygon ~5% of all (point, edge) pairs truly straddle and
+// each needs a side test.  Here a point's count comes from O(log^2 n)
+// comparisons instead:
+//
+//   keys      q(y) = trunc(RN(RN(y - o_y) s_y) 2^30) on the polygon-local map of
+//             DESIGN.md §3.4 (monotone); V = the sorted distinct vertex keys.
+//             A point whose key is not a vertex key ("clean") straddles edge e
+//             iff q_lo(e) < q < q_hi(e) -- exactly the reference's
+//             f_prev * f_next <= 0 (§3.4, |p.y| >= 2^-400);
+//   tree      leaves = the open key intervals (V_j, V_j+1); edge e is stored
+//             at the O(log n) canonical nodes of its leaf range.  The edges
+//             of a node span the node's whole key range, so for a simple
+//             polygon they never cross inside it and are totally ordered in x;
+//             each node's list is sorted by x at the range's middle;
+//   verify    consecutive edges of a node must stay ordered (within 2^-30
+//             local, far inside the fp32 test's band) at both ends of the
+//             range, else the node is flagged and queried by a linear scan
+//             (non-simple input);
+//   query     thread per clean point: walk leaf -> root; per node count the
+//             edges right of the point (the reference counts iff
+//             (p - a).n <= 0 with n_x >= 0, i.e. the edge lies right of p):
+//             a binary search with the certified fp32 side test of §3.4 as the
+//             comparator (the reference's binary64 expression when the
+//             fp32 value is inside the band), then a scan from the boundary
+//             in both directions over the edges the fp32 test cannot decide,
+//             stopping at the first decided one.  Decided (|s| > B) edges are
+//             farther than ~2^-24 local from the point, far beyond the
+//             rounding of the order, so only undecided edges can be out of
+//             order with respect to the point and all of them are evaluated.
+//   fallback  points with a key tie, |p.y| < 2^-400 or outside the local map
+//             are compacted and classified by the scan kernel.
+#include "pip_kernels.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
+#include <cub/device/device_select.cuh>
+
+#include "pip_device.cuh"
+
+namespace pcd {
+
+namespace {
+
+constexpr float kBand = 0x1p-20f;
+constexpr uint32_t k2BBits = 0x36000000u; // bits of 2^-19 = 2 kBand
+
+struct Map {
+    double x0, y0, sx, sy;
+};
+
+__device__ __forceinline__ Map map_of(const unsigned long long* bbox_keys) {
+    Map m;
+    m.x0 = dkey_inv(bbox_keys[0]);
+    m.y0 = dkey_inv(bbox_keys[1]);
+    m.sx = reinterpret_cast<const double*>(bbox_keys)[6];
+    m.sy = reinterpret_cast<const double*>(bbox_keys)[7];
+    return m;
+}
+
+// 30-bit key of y on the local map (valid for y in the bbox; clamped otherwise)
+__device__ __forceinline__ uint32_t key30(double y, const Map& m) {
+    double t = __dmul_rn(__dmul_rn(__dsub_rn(y, m.y0), m.sy), 0x1p30);
+    t = t > 0.0 ? t : 0.0;
+    t = t < 0x1p31 ? t : 0x1p31;
+    return (uint32_t)t;
+}
+
+// number of keys < v (lower_bound) / <= v (upper_bound) in V[0, m)
+__device__ __forceinline__ uint32_t lower_bound(const uint32_t* __restrict__ V, uint32_t m, uint32_t v) {
+    uint32_t lo = 0, hi = m;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(V + mid) < v) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+__device__ __forceinline__ uint32_t upper_bound(const uint32_t* __restrict__ V, uint32_t m, uint32_t v) {
+    uint32_t lo = 0, hi = m;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(V + mid) <= v) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// ring of vertex v (ring_off[r] <= v < ring_off[r+1])
+__device__ __forceinline__ uint32_t ring_of(const unsigned long long* __restrict__ ring_off, uint32_t n_rings,
+                                            unsigned long long v) {
+    uint32_t lo = 0, hi = n_rings;
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (ring_off[mid] <= v) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void vkey_kernel(const double* __restrict__ vy, uint64_t nv, const unsigned long long* __restrict__ bbox_keys,
+                            uint32_t* __restrict__ vk) {
+    const Map m = map_of(bbox_keys);
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nv; v += (uint64_t)gridDim.x * blockDim.x)
+        vk[v] = key30(vy[v], m);
+}
+
+// canonical nodes of leaf range [lo, hi) in a tree of L leaves (node ids 1 ..
+// 2L-1), level by level from the leaves: at most a left and a right node per
+// level.  Warp-collective (all lanes call it; inactive lanes pass lo == hi) so
+// lanes that emit the same node share one atomic: f(node, rank, leader_count)
+// gets the lane's rank among the lanes emitting that node and, for the
+// lowest such lane, their number (0 for the others).
+template <class F>
+__device__ __forceinline__ void canonical_warp(uint32_t lo, uint32_t hi, uint32_t L, F f) {
+    const unsigned lane = threadIdx.x & 31;
+    uint32_t l = lo + L, r = hi + L;
+    while (__any_sync(0xffffffffu, l < r)) {
+        uint32_t nodes[2] = {0u, 0u};
+        if (l < r) {
+            if (l & 1u) nodes[0] = l++;
+            if (r & 1u) nodes[1] = --r;
+            l >>= 1;
+            r >>= 1;
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const uint32_t nd = nodes[k];
+            const uint32_t same = __match_any_sync(0xffffffffu, nd);
+            if (nd) {
+                const uint32_t rank = __popc(same & ((1u << lane) - 1u));
+                f(nd, rank, rank == 0 ? (uint32_t)__popc(same) : 0u, same);
+            }
+        }
+    }
+}
+
+// count (fill == false) or fill (fill == true) the node lists
+template <bool kFill>
+__global__ void edges_kernel(const double* __restrict__ vx, const double* __restrict__ vy,
+                             const unsigned long long* __restrict__ ring_off, uint32_t n_rings, uint64_t nv,
+                             const unsigned long long* __restrict__ bbox_keys, const uint32_t* __restrict__ V,
+                             const uint32_t* __restrict__ m_dev, uint32_t L, uint32_t* __restrict__ cnt,
+                             const uint32_t* __restrict__ off, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                             uint32_t* __restrict__ node_of) {
+    const Map mp = map_of(bbox_keys);
+    const uint32_t m = *m_dev;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    // whole warps iterate together (canonical_warp is warp-collective)
+    for (uint64_t v0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) & ~31ull; v0 < nv; v0 += stride) {
+        const uint64_t v = v0 + (threadIdx.x & 31);
+        uint32_t lo = 0, hi = 0, e = 0;
+        double axl = 0, ayl = 0, slope = 0;
+        if (v < nv) {
+            const uint32_t r = ring_of(ring_off, n_rings, v);
+            if (v + 1 < ring_off[r + 1]) { // a ring's last vertex starts no edge
+                e = (uint32_t)(v - r);
+                const double ay = vy[v], by = vy[v + 1];
+                const uint32_t qa = key30(ay, mp), qb = key30(by, mp);
+                lo = lower_bound(V, m, min(qa, qb));
+                hi = lower_bound(V, m, max(qa, qb));
+                if (hi < lo) hi = lo; // (cannot happen: keys are monotone)
+                if (kFill && hi > lo) { // local endpoints for the x order at each node's middle
+                    const double ax = vx[v], bx = vx[v + 1];
+                    axl = __dmul_rn(__dsub_rn(ax, mp.x0), mp.sx);
+                    ayl = __dmul_rn(__dsub_rn(ay, mp.y0), mp.sy);
+                    const double bxl = __dmul_rn(__dsub_rn(bx, mp.x0), mp.sx);
+                    const double byl = __dmul_rn(__dsub_rn(by, mp.y0), mp.sy);
+                    slope = __ddiv_rn(__dsub_rn(bxl, axl), __dsub_rn(byl, ayl));
+                }
+            }
+        }
+        // flat in key space (hi == lo): never a sure straddle, stored nowhere
+        if (!kFill) {
+            canonical_warp(lo, hi, L, [&](uint32_t nd, uint32_t, uint32_t lead, uint32_t) {
+                if (lead) atomicAdd(&cnt[nd], lead);
+            });
+        } else {
+            canonical_warp(lo, hi, L, [&](uint32_t nd, uint32_t rank, uint32_t lead, uint32_t same) {
+                uint32_t base = 0;
+                if (lead) base = atomicAdd(&cnt[nd], lead);
+                base = __shfl_sync(same, base, __ffs(same) - 1);
+                const int d = 31 - __clz(nd);
+                const uint32_t span = L >> d, a = (nd - (1u << d)) * span, b = a + span;
+                const double ym = ((double)V[a] + (double)V[min(b, m - 1)]) * 0x1p-31; // middle, local units
+                // x at the middle as 32-bit fixed point: two edges the key misorders are
+                // within 2^-32 there, hence within 2^-31 over the whole range (the
+                // difference of two non-crossing segments is linear and keeps its sign)
+                double xm = __dmul_rn(__dadd_rn(axl, __dmul_rn(__dsub_rn(ym, ayl), slope)), 0x1p32);
+                xm = xm > 0.0 ? xm : 0.0;
+                xm = xm < 4294967295.0 ? xm : 4294967295.0;
+                const uint32_t key = (uint32_t)xm;
+                const uint32_t slot = off[nd] + base + rank;
+                keys[slot] = key;
+                vals[slot] = e;
+                node_of[slot] = nd;
+            });
+        }
+    }
+}
+
+// x of edge e (local units) at local height y, from its exact vertices
+__device__ __forceinline__ double edge_x(const EdgeRec* __restrict__ rec, const double* __restrict__ vx, uint32_t e,
+                                         double y, const Map& mp) {
+    const EdgeRec& r = rec[e];
+    // C1 record: d[0] = ax, d[1] = ay, d[2] = by, d[3] = nx, d[4] = ny with n = +-(dy, -dx)
+    const double axl = __dmul_rn(__dsub_rn(r.d[0], mp.x0), mp.sx), ayl = __dmul_rn(__dsub_rn(r.d[1], mp.y0), mp.sy);
+    const double byl = __dmul_rn(__dsub_rn(r.d[2], mp.y0), mp.sy);
+    // dx / dy = -ny / nx (the flip cancels); local: dxl / dyl = (dx sx) / (dy sy)
+    const double dxdy = __ddiv_rn(__dmul_rn(-r.d[4], mp.sx), __dmul_rn(r.d[3], mp.sy));
+    (void)byl;
+    (void)vx;
+    return __dadd_rn(axl, __dmul_rn(__dsub_rn(y, ayl), dxdy));
+}
+
+__global__ void verify_kernel(const uint32_t* __restrict__ vals, const uint32_t* __restrict__ node_of,
+                              const uint32_t* __restrict__ off, uint32_t L, const uint32_t* __restrict__ V,
+                              const uint32_t* __restrict__ m_dev, const EdgeRec* __restrict__ rec,
+                              const unsigned long long* __restrict__ bbox_keys, uint8_t* __restrict__ flag) {
+    const Map mp = map_of(bbox_keys);
+    const uint32_t m = *m_dev, total = off[2 * L];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i + 1 < total; i += gridDim.x * blockDim.x) {
+        const uint32_t nd = node_of[i];
+        if (node_of[i + 1] != nd) continue;
+        const int d = 31 - __clz(nd);
+        const uint32_t span = L >> d, a = (nd - (1u << d)) * span, b = min(a + span, m - 1);
+        const double y0 = (double)V[a] * 0x1p-30, y1 = (double)V[b] * 0x1p-30;
+        const uint32_t e0 = vals[i], e1 = vals[i + 1];
+        const bool bad = edge_x(rec, nullptr, e0, y0, mp) > __dadd_rn(edge_x(rec, nullptr, e1, y0, mp), 0x1p-30) ||
+                         edge_x(rec, nullptr, e0, y1, mp) > __dadd_rn(edge_x(rec, nullptr, e1, y1, mp), 0x1p-30);
+        if (bad) flag[nd] = 1;
+    }
+}
+
+// F: the reference's C1 count decision for a sure straddle, from a packed node
+// entry {Nx, Ny, c + B, edge}: 1 counted, 0 not; *certain: decided by the fp32
+// test (else the binary64 expression of the edge's record ran)
+__device__ __forceinline__ int decide(const float4 pk, const EdgeRec* __restrict__ rec, float lx, float ly, double px,
+                                      double py, bool* certain) {
+    const float s = fmaf(lx, pk.x, fmaf(ly, pk.y, pk.z)); // s' = s + B
+    const uint32_t u = __float_as_uint(s);
+    if (s == s && u > k2BBits) { // sign bit set (count) or s' > 2B (no count)
+        *certain = true;
+        return (int)(u >> 31);
+    }
+    *certain = false;
+    int cnt = 0;
+    exact_c1(px, py, rec[__float_as_uint(pk.w)], cnt, true); // keys proved the straddle (geometry.hpp:189-200)
+    return cnt;
+}
+
+// edges of one node list that the point counts
+__device__ __forceinline__ uint32_t node_count(const float4* __restrict__ packed, uint32_t o, uint32_t k, bool linear,
+                                               const EdgeRec* __restrict__ rec, float lx, float ly, double px,
+                                               double py) {
+    bool cert;
+    const float4* P = packed + o;
+    if (linear) { // non-simple input: every edge
+        uint32_t c = 0;
+        for (uint32_t i = 0; i < k; ++i) c += decide(__ldg(P + i), rec, lx, ly, px, py, &cert);
+        return c;
+    }
+    // lists run left to right: not counted, then counted.  b = first counted
+    uint32_t lo = 0, hi = k;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (decide(__ldg(P + mid), rec, lx, ly, px, py, &cert)) hi = mid;
+        else lo = mid + 1;
+    }
+    const uint32_t b = lo;
+    uint32_t c = k - b; // [b, k) counted, corrected below
+    // right of b: undecided edges may be "not counted" after all
+    for (uint32_t i = b; i < k; ++i) {
+        const int f = decide(__ldg(P + i), rec, lx, ly, px, py, &cert);
+        if (cert && f) break;
+        c -= (uint32_t)(1 - f);
+    }
+    // left of b: undecided edges may be counted
+    for (uint32_t i = b; i-- > 0;) {
+        const int f = decide(__ldg(P + i), rec, lx, ly, px, py, &cert);
+        if (cert && !f) break;
+        c += (uint32_t)f;
+    }
+    return c;
+}
+
+// node entries -> {Nx, Ny, c + B, edge} (the C1 fp32 record of pip_kernels.cu prep_edges_kernel)
+__global__ void pack_kernel(const uint32_t* __restrict__ vals, const uint32_t* __restrict__ off, uint32_t L,
+                            const EdgeRec* __restrict__ rec, float4* __restrict__ packed) {
+    const uint32_t total = off[2 * L];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const uint32_t e = vals[i];
+        const double d5 = rec[e].d[5], d6 = rec[e].d[6];
+        packed[i] = make_float4(__int_as_float(__double2loint(d5)), __int_as_float(__double2hiint(d5)),
+                                __int_as_float(__double2loint(d6)), __uint_as_float(e));
+    }
+}
+
+__global__ void __launch_bounds__(256) query_kernel(const double2* __restrict__ pts, uint64_t n, int prefilter,
+                                                    const unsigned long long* __restrict__ bbox_keys,
+                                                    const uint32_t* __restrict__ V, const uint32_t* __restrict__ m_dev,
+                                                    uint32_t L, const uint32_t* __restrict__ off,
+                                                    const float4* __restrict__ packed, const uint8_t* __restrict__ flag,
+                                                    const EdgeRec* __restrict__ rec, uint32_t* __restrict__ inside_bits,
+                                                    uint32_t* __restrict__ fb_idx, uint32_t* __restrict__ fb_count) {
+    const Map mp = map_of(bbox_keys);
+    const uint32_t m = *m_dev;
+    const double minx = dkey_inv(bbox_keys[0]), miny = dkey_inv(bbox_keys[1]);
+    const double maxx = dkey_inv(~bbox_keys[2]), maxy = dkey_inv(~bbox_keys[3]);
+    const int lane = threadIdx.x & 31;
+    const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t wi = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; wi * 32 < n; wi += warps) {
+        const uint64_t i = wi * 32 + lane;
+        bool in = false, fb = false;
+        if (i < n) {
+            const double2 p = pts[i];
+            bool act = true;
+            if (prefilter) act = p.x >= minx && p.x <= maxx && p.y >= miny && p.y <= maxy; // batch.hpp:39-41
+            if (act) {
+                const double lxd = __dmul_rn(__dsub_rn(p.x, mp.x0), mp.sx);
+                const double lyd = __dmul_rn(__dsub_rn(p.y, mp.y0), mp.sy);
+                const bool ok = mp.sx != 0.0 && lxd >= 0.0 && lxd < 1.0 && lyd >= 0.0 && lyd < 1.0 &&
+                                fabs(p.y) >= 0x1p-400;
+                if (!ok) {
+                    fb = true;
+                } else {
+                    const uint32_t q = (uint32_t)__dmul_rn(lyd, 0x1p30);
+                    const uint32_t j = upper_bound(V, m, q); // keys <= q
+                    if (j > 0 && __ldg(V + j - 1) == q) {
+                        fb = true; // a vertex key: the exact straddle products decide
+                    } else if (j > 0 && j < m) {
+                        const float lx = __double2float_rn(lxd), ly = __double2float_rn(lyd);
+                        uint32_t c = 0;
+                        for (uint32_t nd = L + j - 1; nd; nd >>= 1) {
+                            const uint32_t o = __ldg(off + nd), k = __ldg(off + nd + 1) - o;
+                            if (k) c += node_count(packed, o, k, __ldg(flag + nd) != 0, rec, lx, ly, p.x, p.y);
+                        }
+                        in = c & 1u;
+                    }
+                }
+            }
+        }
+        const uint32_t w = __ballot_sync(0xffffffffu, in);
+        const uint32_t fbm = __ballot_sync(0xffffffffu, fb);
+        if (lane == 0) inside_bits[wi] = w;
+        if (fbm) {
+            uint32_t pos = 0;
+            if (lane == 0) pos = atomicAdd(fb_count, (uint32_t)__popc(fbm));
+            pos = __shfl_sync(0xffffffffu, pos, 0);
+            if (fb) fb_idx[pos + __popc(fbm & ((1u << lane) - 1u))] = (uint32_t)i;
+        }
+    }
+}
+
+__global__ void gather_kernel(const double2* __restrict__ pts, const uint32_t* __restrict__ idx,
+                              const uint32_t* __restrict__ count, double2* __restrict__ out) {
+    const uint32_t n = *count;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) out[k] = pts[idx[k]];
+}
+
+__global__ void scatter_kernel(const uint32_t* __restrict__ idx, const uint32_t* __restrict__ count,
+                               const uint32_t* __restrict__ bits, uint32_t* __restrict__ inside_bits) {
+    const uint32_t n = *count;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+        if ((bits[k >> 5] >> (k & 31)) & 1u) {
+            const uint32_t i = idx[k];
+            atomicOr(&inside_bits[i >> 5], 1u << (i & 31));
+        }
+}
+
+int sms(int dev) {
+    int v = 148;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+}
+
+uint32_t tree_leaves(uint64_t nv) {
+    uint32_t L = 1;
+    while (L < nv) L <<= 1;
+    return L;
+}
+
+struct Layout {
+    uint64_t nv, ne, L, emax;
+    size_t o_vk, o_V, o_m, o_cnt, o_off, o_keys, o_vals, o_keys2, o_vals2, o_node, o_packed, o_flag, o_fbidx, o_fbcnt,
+        o_fbpts, o_fbbits, o_tmp, tmp_bytes, total;
+};
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+Layout layout(uint64_t nv, uint64_t ne, uint64_t n_pts) {
+    Layout l{};
+    l.nv = nv;
+    l.ne = ne;
+    l.L = tree_leaves(std::max<uint64_t>(nv, 2));
+    const int depth = 63 - __builtin_clzll(l.L);
+    l.emax = std::max<uint64_t>(ne * 2ull * (depth + 1), nv);
+    // CUB temporary storage: the largest of the four primitives
+    size_t t1 = 0, t2 = 0, t3 = 0, t4 = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, t1, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)nv, 0, 32);
+    cub::DeviceSelect::Unique(nullptr, t2, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)nv);
+    cub::DeviceScan::ExclusiveSum(nullptr, t3, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)(2 * l.L + 1));
+    cub::DeviceSegmentedSort::SortPairs(nullptr, t4, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                        (uint32_t*)nullptr, (int)l.emax, (int)(2 * l.L), (uint32_t*)nullptr,
+                                        (uint32_t*)nullptr);
+    l.tmp_bytes = std::max({t1, t2, t3, t4, (size_t)256});
+    size_t o = 0;
+    auto put = [&](size_t bytes) {
+        const size_t at = o;
+        o = align256(o + bytes);
+        return at;
+    };
+    l.o_vk = put(nv * 4);
+    l.o_V = put(nv * 4);
+    l.o_m = put(16);
+    l.o_cnt = put((2 * l.L + 1) * 4);
+    l.o_off = put((2 * l.L + 1) * 4);
+    l.o_keys = put(l.emax * 4);
+    l.o_vals = put(l.emax * 4);
+    l.o_keys2 = put(l.emax * 4);
+    l.o_vals2 = put(l.emax * 4);
+    l.o_node = put(l.emax * 4);
+    l.o_packed = put(l.emax * 16);
+    l.o_flag = put(2 * l.L);
+    l.o_fbidx = put(n_pts * 4 + 4);
+    l.o_fbcnt = put(16);
+    l.o_fbpts = put(n_pts * 16 + 16);
+    l.o_fbbits = put(((n_pts + 31) / 32) * 4 + 4);
+    l.o_tmp = put(l.tmp_bytes);
+    l.total = o;
+    return l;
+}
+
+} // namespace
+
+bool tree_eligible(uint64_t n_verts, uint64_t n_pts, bool forced) {
+    // 32-bit node lists and point indices; (auto) big enough to pay for the build
+    if (n_verts < 4 || n_verts >= (1ull << 24) || n_pts == 0 || n_pts >= 0xffffffffull) return false;
+    return forced || (n_verts >= 4096 && n_pts >= 16384);
+}
+
+size_t tree_scratch_bytes(uint64_t n_verts, uint64_t n_edges, uint64_t n_pts) {
+    return layout(n_verts, n_edges, n_pts).total;
+}
+
+cudaError_t launch_tree(const TreeArgs& a, void* scratch, cudaStream_t st, int dev, uint64_t* launches) {
+    const Layout l = layout(a.n_verts, a.n_edges, a.n);
+    char* s = static_cast<char*>(scratch);
+    uint32_t* vk = reinterpret_cast<uint32_t*>(s + l.o_vk);
+    uint32_t* V = reinterpret_cast<uint32_t*>(s + l.o_V);
+    uint32_t* m_dev = reinterpret_cast<uint32_t*>(s + l.o_m);
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(s + l.o_cnt);
+    uint32_t* off = reinterpret_cast<uint32_t*>(s + l.o_off);
+    uint32_t* keys = reinterpret_cast<uint32_t*>(s + l.o_keys);
+    uint32_t* vals = reinterpret_cast<uint32_t*>(s + l.o_vals);
+    uint32_t* keys2 = reinterpret_cast<uint32_t*>(s + l.o_keys2);
+    uint32_t* vals2 = reinterpret_cast<uint32_t*>(s + l.o_vals2);
+    uint32_t* node_of = reinterpret_cast<uint32_t*>(s + l.o_node);
+    float4* packed = reinterpret_cast<float4*>(s + l.o_packed);
+    uint8_t* flag = reinterpret_cast<uint8_t*>(s + l.o_flag);
+    uint32_t* fb_idx = reinterpret_cast<uint32_t*>(s + l.o_fbidx);
+    uint32_t* fb_cnt = reinterpret_cast<uint32_t*>(s + l.o_fbcnt);
+    double* fb_pts = reinterpret_cast<double*>(s + l.o_fbpts);
+    uint32_t* fb_bits = reinterpret_cast<uint32_t*>(s + l.o_fbbits);
+    void* tmp = s + l.o_tmp;
+    size_t tmp_bytes = l.tmp_bytes;
+    const uint32_t L = (uint32_t)l.L;
+    const int grid = sms(dev) * 8;
+    const EdgeRec* rec = static_cast<const EdgeRec*>(a.rec);
+    const unsigned long long* ro = reinterpret_cast<const unsigned long long*>(a.ring_off);
+    cudaError_t e;
+#define PC_TRY(x)                                                                                                      \
+    if ((e = (x)) != cudaSuccess) return e
+    // ---- build ----
+    vkey_kernel<<<grid, 256, 0, st>>>(a.vy, a.n_verts, a.bbox_keys, vk);
+    PC_TRY(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, vk, keys, (int)a.n_verts, 0, 32, st));
+    tmp_bytes = l.tmp_bytes;
+    PC_TRY(cub::DeviceSelect::Unique(tmp, tmp_bytes, keys, V, m_dev, (int)a.n_verts, st));
+    PC_TRY(cudaMemsetAsync(cnt, 0, (2 * l.L + 1) * 4, st));
+    PC_TRY(cudaMemsetAsync(flag, 0, 2 * l.L, st));
+    edges_kernel<false><<<grid, 256, 0, st>>>(a.vx, a.vy, ro, a.n_rings, a.n_verts, a.bbox_keys, V, m_dev, L, cnt,
+                                              nullptr, nullptr, nullptr, nullptr);
+    tmp_bytes = l.tmp_bytes;
+    PC_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, off, (int)(2 * l.L + 1), st));
+    PC_TRY(cudaMemsetAsync(cnt, 0, (2 * l.L + 1) * 4, st));
+    edges_kernel<true><<<grid, 256, 0, st>>>(a.vx, a.vy, ro, a.n_rings, a.n_verts, a.bbox_keys, V, m_dev, L, cnt, off,
+                                             keys, vals, node_of);
+    tmp_bytes = l.tmp_bytes;
+    PC_TRY(cub::DeviceSegmentedSort::SortPairs(tmp, tmp_bytes, keys, keys2, vals, vals2, (int)l.emax, (int)(2 * l.L),
+                                               off, off + 1, st));
+    verify_kernel<<<grid, 256, 0, st>>>(vals2, node_of, off, L, V, m_dev, rec, a.bbox_keys, flag);
+    pack_kernel<<<grid, 256, 0, st>>>(vals2, off, L, rec, packed);
+    // ---- query ----
+    PC_TRY(cudaMemsetAsync(fb_cnt, 0, 4, st));
+    const unsigned qgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((a.n + 255) / 256, (uint64_t)grid * 4));
+    query_kernel<<<qgrid, 256, 0, st>>>(reinterpret_cast<const double2*>(a.pts), a.n, a.prefilter, a.bbox_keys, V,
+                                        m_dev, L, off, packed, flag, rec, a.inside_bits, fb_idx, fb_cnt);
+    *launches += 10;
+    // ---- fallback points through the scan kernel, its grid sized for their number ----
+    uint32_t n_fb = 0;
+    PC_TRY(cudaMemcpyAsync(&n_fb, fb_cnt, 4, cudaMemcpyDeviceToHost, st));
+    PC_TRY(cudaStreamSynchronize(st));
+    if (n_fb) {
+        gather_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const double2*>(a.pts), fb_idx, fb_cnt,
+                                            reinterpret_cast<double2*>(fb_pts));
+        PC_TRY(cudaMemsetAsync(fb_bits, 0, ((n_fb + 31) / 32) * 4, st));
+        SingleArgs sa = a.single;
+        sa.pts = fb_pts;
+        sa.n = n_fb;
+        sa.n_dev = nullptr;
+        sa.prefilter = 0; // gathered points were active
+        sa.inside_bits = fb_bits;
+        PC_TRY(launch_single(sa, st, dev, launches));
+        scatter_kernel<<<grid, 256, 0, st>>>(fb_idx, fb_cnt, fb_bits, a.inside_bits);
+        *launches += 2;
+    }
+#undef PC_TRY
+    return cudaGetLastError();
+}
+
+} // namespace pcd

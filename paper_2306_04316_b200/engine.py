@@ -198,6 +198,11 @@ class Engine:
         """-1 auto, 0 off, 1 on (PC_OPT_BUCKET_POINTS); never changes results."""
         self.set_option(1, mode)
 
+    def set_tree(self, mode: int):
+        """-1 auto, 0 off, 1 on (PC_OPT_TREE): the segment-tree C1 path for single
+        polygons; never changes results."""
+        self.set_option(2, mode)
+
     def set_profiling(self, on: bool = True):
         self._check(self.lib.pc_set_profiling(self.ctx, int(bool(on))), "pc_set_profiling")
 

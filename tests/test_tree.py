@@ -1,0 +1,96 @@
+"""Segment-tree C1 path for single polygons (pip_tree.cu, PC_OPT_TREE) against
+the reference, bit-exact: forced on for every input shape (stars of many
+sizes, the adversarial cases, points on vertices / vertex y-levels / edges,
+overlapping holes and self-intersecting rings -- the verified-order fallback --,
+no bbox prefilter), and on vs off on the sweep's large polygons."""
+import numpy as np
+import pytest
+
+import adversarial
+import oracle
+from paper_2306_04316_b200 import workloads as W
+from paper_2306_04316_b200.engine import Polygon
+
+pytestmark = pytest.mark.gpu
+THREADS = 16
+
+
+def _check(engine, xy, poly, prefilter=True, source=None):
+    got = engine.classify(xy, poly, 0, prefilter=prefilter)
+    if source is None:
+        source = "reference" if prefilter and oracle.ref_available() else "port"
+    if source == "reference":
+        want_v, want_s = oracle.ref_classify(xy, poly.vx, poly.vy, poly.ring_off, 0)
+    else:
+        want_v, want_s = oracle.port_classify(xy, poly.vx, poly.vy, poly.ring_off, 0, prefilter=prefilter,
+                                              threads=THREADS)
+    assert np.array_equal(got.verdicts, want_v), f"{int((got.verdicts != want_v).sum())} of {len(xy)} differ"
+    assert np.array_equal(got.stats, want_s)
+
+
+@pytest.fixture
+def tree_on(engine):
+    engine.set_tree(1)
+    yield engine
+    engine.set_tree(-1)
+
+
+@pytest.mark.parametrize("n", [10, 100, 1000, 20_000])
+def test_stars(tree_on, n):
+    poly = W.star_polygon(n, seed=n)
+    xy = W.uniform_points(60_000, W.bounds(poly), n + 1)
+    _check(tree_on, xy, poly)
+    _check(tree_on, xy, poly, prefilter=False)
+
+
+def test_adversarial_cases(tree_on):
+    for name, poly, xy in adversarial.cases():
+        src = "port" if name == adversarial.cases()[-1][0] else None  # duplicate vertices: the C restatement
+        _check(tree_on, np.ascontiguousarray(xy), poly, source=src)
+
+
+def test_points_on_vertices_levels_and_edges(tree_on):
+    poly = W.star_polygon(5000, seed=7)
+    rng = np.random.default_rng(8)
+    vx, vy = poly.vx, poly.vy
+    k = rng.integers(0, len(vx) - 1, 4000)
+    t = rng.random(4000)
+    on_edge = np.stack([vx[k] + t * (vx[k + 1] - vx[k]), vy[k] + t * (vy[k + 1] - vy[k])], 1)
+    levels = np.stack([rng.uniform(-1, 1, 4000), vy[k]], 1)              # exactly on vertex y-levels
+    near = levels + np.stack([np.zeros(4000), rng.choice([-1, 1], 4000) * np.spacing(np.abs(levels[:, 1]))], 1)
+    verts = np.stack([vx, vy], 1)
+    xy = np.ascontiguousarray(np.concatenate([on_edge, levels, near, verts, W.uniform_points(20_000, W.bounds(poly), 9)]))
+    _check(tree_on, xy, poly)
+
+
+def test_overlapping_holes_and_self_intersections(tree_on):
+    rng = np.random.default_rng(12)
+    rings = [np.stack([np.cos(t) * 100, np.sin(t) * 100], 1) for t in [np.linspace(0, 2 * np.pi, 3001)]]
+    rings[0][-1] = rings[0][0]
+    for _ in range(120):  # overlapping square holes: edges cross inside node ranges
+        cx, cy = rng.uniform(-60, 60, 2)
+        rings.append(np.array([(cx, cy), (cx + 9, cy), (cx + 9, cy + 9), (cx, cy + 9), (cx, cy)]))
+    holed = Polygon.from_rings(rings)
+    _check(tree_on, W.uniform_points(100_000, (-110, -110, 110, 110), 13), holed)
+    # a random-order ring: thousands of crossings
+    p = rng.uniform(-1, 1, (2000, 2))
+    p = np.concatenate([p, p[:1]])
+    tangled = Polygon.from_rings([p])
+    _check(tree_on, W.uniform_points(50_000, (-1, -1, 1, 1), 14), tangled)
+
+
+@pytest.mark.parametrize("n", [100_000, 1_000_000])
+def test_sweep_tree_vs_scan(engine, n):
+    """Auto mode on the sweep's big polygons: tree and scan paths agree on all
+    1e6 points, and a seeded subsample agrees with the reference."""
+    poly, xy = W.config2(n)
+    engine.set_tree(1)
+    a = engine.classify(xy, poly, 0)
+    engine.set_tree(0)
+    b = engine.classify(xy, poly, 0)
+    engine.set_tree(-1)
+    assert np.array_equal(a.verdicts, b.verdicts)
+    idx = np.random.default_rng(n).choice(len(xy), 3000, replace=False)
+    sub = np.ascontiguousarray(xy[idx])
+    want_v, _ = oracle.ref_classify(sub, poly.vx, poly.vy, poly.ring_off, 0)
+    assert np.array_equal(a.verdicts[idx], want_v)
