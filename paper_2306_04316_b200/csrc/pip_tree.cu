@@ -366,6 +366,37 @@ __global__ void gather_kernel(const double2* __restrict__ pts, const uint32_t* _
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) out[k] = pts[idx[k]];
 }
 
+// the fallback points (few) against every edge, the reference's literal C1 step
+// (geometry.hpp:189-200: straddle product, then the side of the flipped
+// normal); block (chunk of kFbEdges edges, group of 256 points), parity bits
+// XOR-combined across chunks
+constexpr int kFbEdges = 256;
+__global__ void __launch_bounds__(256) fallback_kernel(const double2* __restrict__ pts, const uint32_t* __restrict__ idx,
+                                                       const uint32_t* __restrict__ count, const EdgeRec* __restrict__ rec,
+                                                       uint32_t n_edges, uint32_t* __restrict__ bits) {
+    __shared__ double sa[5][kFbEdges];
+    const uint32_t e0 = blockIdx.x * kFbEdges, ne = min((uint32_t)kFbEdges, n_edges - e0);
+    for (uint32_t i = threadIdx.x; i < ne; i += blockDim.x) {
+        const EdgeRec& r = rec[e0 + i];
+#pragma unroll
+        for (int f = 0; f < 5; ++f) sa[f][i] = r.d[f];
+    }
+    __syncthreads();
+    const uint32_t n = *count, k = blockIdx.y * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const double2 p = pts[idx[k]];
+    uint32_t par = 0;
+    for (uint32_t i = 0; i < ne; ++i) {
+        const double ay = sa[1][i], by = sa[2][i];
+        if (__dmul_rn(__dsub_rn(ay, p.y), __dsub_rn(by, p.y)) <= 0.0) {
+            const double side = __dadd_rn(__dmul_rn(__dsub_rn(p.x, sa[0][i]), sa[3][i]),
+                                          __dmul_rn(__dsub_rn(p.y, ay), sa[4][i]));
+            par ^= side <= 0.0;
+        }
+    }
+    if (par) atomicXor(&bits[k >> 5], 1u << (k & 31));
+}
+
 __global__ void scatter_kernel(const uint32_t* __restrict__ idx, const uint32_t* __restrict__ count,
                                const uint32_t* __restrict__ bits, uint32_t* __restrict__ inside_bits) {
     const uint32_t n = *count;
@@ -443,7 +474,7 @@ Layout layout(uint64_t nv, uint64_t ne, uint64_t n_pts) {
 
 bool tree_eligible(uint64_t n_verts, uint64_t n_pts, bool forced) {
     // 32-bit node lists and point indices; (auto) big enough to pay for the build
-    if (n_verts < 4 || n_verts >= (1ull << 24) || n_pts == 0 || n_pts >= 0xffffffffull) return false;
+    if (n_verts < 4 || n_verts > (1ull << 22) || n_pts == 0 || n_pts >= 0xffffffffull) return false;
     return forced || (n_verts >= 4096 && n_pts >= 16384);
 }
 
@@ -509,18 +540,26 @@ cudaError_t launch_tree(const TreeArgs& a, void* scratch, cudaStream_t st, int d
     PC_TRY(cudaMemcpyAsync(&n_fb, fb_cnt, 4, cudaMemcpyDeviceToHost, st));
     PC_TRY(cudaStreamSynchronize(st));
     if (n_fb) {
-        gather_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const double2*>(a.pts), fb_idx, fb_cnt,
-                                            reinterpret_cast<double2*>(fb_pts));
         PC_TRY(cudaMemsetAsync(fb_bits, 0, ((n_fb + 31) / 32) * 4, st));
-        SingleArgs sa = a.single;
-        sa.pts = fb_pts;
-        sa.n = n_fb;
-        sa.n_dev = nullptr;
-        sa.prefilter = 0; // gathered points were active
-        sa.inside_bits = fb_bits;
-        PC_TRY(launch_single(sa, st, dev, launches));
+        if ((double)n_fb * (double)a.n_edges <= 2e10) { // few points: every edge, literally
+            const dim3 fgrid((unsigned)((a.n_edges + kFbEdges - 1) / kFbEdges), (unsigned)((n_fb + 255) / 256));
+            fallback_kernel<<<fgrid, 256, 0, st>>>(reinterpret_cast<const double2*>(a.pts), fb_idx, fb_cnt, rec,
+                                                   (uint32_t)a.n_edges, fb_bits);
+            ++*launches;
+        } else { // many: the scan kernel (its filters), grid sized for their number
+            gather_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const double2*>(a.pts), fb_idx, fb_cnt,
+                                                reinterpret_cast<double2*>(fb_pts));
+            SingleArgs sa = a.single;
+            sa.pts = fb_pts;
+            sa.n = n_fb;
+            sa.n_dev = nullptr;
+            sa.prefilter = 0; // gathered points were active
+            sa.inside_bits = fb_bits;
+            PC_TRY(launch_single(sa, st, dev, launches));
+            ++*launches;
+        }
         scatter_kernel<<<grid, 256, 0, st>>>(fb_idx, fb_cnt, fb_bits, a.inside_bits);
-        *launches += 2;
+        ++*launches;
     }
 #undef PC_TRY
     return cudaGetLastError();
