@@ -341,7 +341,8 @@ def run_ours(args, rank, world, local_rank):
     traffic = None
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tf) and args.mode == 0:
-        ent = json.load(open(tf)).get({"c2_sweep": "sweep_n1e6"}.get(args.workload, args.workload))
+        # C1 sweep / c4 run the segment tree: its query kernel's capture; c1 the scan kernel
+        ent = json.load(open(tf)).get({"c2_sweep": "tree_query"}.get(args.workload, args.workload))
         if ent:
             traffic = ent["dram_bytes_per_launch"]
             roof["traffic_source"] = ent["source"]

@@ -20,12 +20,14 @@ ap.add_argument("--polys", type=int, default=200_000)
 ap.add_argument("--mode", type=int, default=0)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--bucket", type=int, default=-1)
+ap.add_argument("--tree", type=int, default=-1, help="PC_OPT_TREE: -1 auto, 0 scan kernel, 1 segment tree")
 a = ap.parse_args()
 
 dev = torch.device("cuda:0")
 torch.cuda.set_stream(torch.cuda.Stream())
 eng = Engine(devices=[0])
 eng.set_bucketing(a.bucket)
+eng.set_tree(a.tree)
 st = torch.cuda.current_stream().cuda_stream
 
 
