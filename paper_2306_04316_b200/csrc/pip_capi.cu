@@ -157,7 +157,7 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
     pa.n_zero_words = nwords;
     check(c, pcd::launch_prep(pa, st, d.dev, &c->launches), "prep kernel");
     check(c, cudaMemsetAsync(d_aux, 0, nwords * 4, st), "clear aux plane");
-    const bool tree = mode == 0 /* C1 */ && c->tree_mode != 0 && pcd::tree_eligible(n_verts, n, c->tree_mode == 1);
+    const bool tree = (mode == 0 || mode == 1) /* C1, C2 */ && c->tree_mode != 0 && pcd::tree_eligible(n_verts, n, c->tree_mode == 1);
     const bool bucket = !tree && n < 0xffffffffull &&
                         (c->bucket_mode == 1 || (c->bucket_mode < 0 && n_edges >= 64 && n >= 4096));
     pcd::SingleArgs sa{};
@@ -195,6 +195,7 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
     }
     if (tree) { // segment-tree counts; key-tie / off-map points through the scan kernel
         pcd::TreeArgs ta{};
+        ta.mode = mode;
         ta.pts = d_pts;
         ta.n = n;
         ta.prefilter = prefilter;
@@ -207,6 +208,7 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
         ta.rec = d.rec.p;
         ta.bbox_keys = d.bbox.as<unsigned long long>();
         ta.inside_bits = d_inside;
+        ta.aux_bits = d_aux;
         ta.single = sa;
         check(c, d.tree.ensure(pcd::tree_scratch_bytes(n_verts, n_edges, n)), "alloc segment tree");
         mark_begin(c, d, st);

@@ -96,6 +96,7 @@ cudaError_t launch_csv_points(const char* text, uint64_t len, uint64_t data_star
 // clean points' crossings and sends the rest through launch_single(single);
 // writes every word of inside_bits.
 struct TreeArgs {
+    int mode; // kC1 or kC2
     const double* pts;
     uint64_t n;
     int prefilter;
@@ -107,7 +108,8 @@ struct TreeArgs {
     const void* rec;
     const unsigned long long* bbox_keys;
     uint32_t* inside_bits;
-    SingleArgs single; // the prepared scan-kernel arguments (for the fallback points)
+    uint32_t* aux_bits; // C2: DegenerateEdge (zeroed by the caller)
+    SingleArgs single;  // the prepared scan-kernel arguments (for the fallback points)
 };
 bool tree_eligible(uint64_t n_verts, uint64_t n_pts, bool forced);
 size_t tree_scratch_bytes(uint64_t n_verts, uint64_t n_edges, uint64_t n_pts);

@@ -1,6 +1,8 @@
 // Segment-tree crossing count for one large polygon in C1 mode (the paper's
 // side-of-normal test; reference count_crossings_c1, geometry.hpp:182-203,
-// over every ring, contains :281-300).
+// over every ring, contains :281-300) and C2 (count_crossings_c2 :208-229: the
+// same straddle, the intercept-side record of pip_device.cuh, DegenerateEdge
+// on the fallback points' horizontal edges -> aux plane).
 //
 // The scan kernel (pip_single.cu) tests every edge whose y-range holds a
 // point; for a spiky polygon ~5% of all (point, edge) pairs truly straddle and
@@ -207,20 +209,19 @@ __global__ void edges_kernel(const double* __restrict__ vx, const double* __rest
     }
 }
 
-// x of edge e (local units) at local height y, from its exact vertices
-__device__ __forceinline__ double edge_x(const EdgeRec* __restrict__ rec, const double* __restrict__ vx, uint32_t e,
-                                         double y, const Map& mp) {
+// x of edge e (local units) at local height y, from its record's exact values
+template <int MODE>
+__device__ __forceinline__ double edge_x(const EdgeRec* __restrict__ rec, uint32_t e, double y, const Map& mp) {
     const EdgeRec& r = rec[e];
-    // C1 record: d[0] = ax, d[1] = ay, d[2] = by, d[3] = nx, d[4] = ny with n = +-(dy, -dx)
+    // d[0] = ax, d[1] = ay; C1: d[3], d[4] = nx, ny with n = +-(dy, -dx) -> dx / dy = -ny / nx;
+    // C2: d[3], d[4] = dx, dy
     const double axl = __dmul_rn(__dsub_rn(r.d[0], mp.x0), mp.sx), ayl = __dmul_rn(__dsub_rn(r.d[1], mp.y0), mp.sy);
-    const double byl = __dmul_rn(__dsub_rn(r.d[2], mp.y0), mp.sy);
-    // dx / dy = -ny / nx (the flip cancels); local: dxl / dyl = (dx sx) / (dy sy)
-    const double dxdy = __ddiv_rn(__dmul_rn(-r.d[4], mp.sx), __dmul_rn(r.d[3], mp.sy));
-    (void)byl;
-    (void)vx;
-    return __dadd_rn(axl, __dmul_rn(__dsub_rn(y, ayl), dxdy));
+    const double dxl = MODE == kC1 ? __dmul_rn(-r.d[4], mp.sx) : __dmul_rn(r.d[3], mp.sx);
+    const double dyl = MODE == kC1 ? __dmul_rn(r.d[3], mp.sy) : __dmul_rn(r.d[4], mp.sy);
+    return __dadd_rn(axl, __dmul_rn(__dsub_rn(y, ayl), __ddiv_rn(dxl, dyl)));
 }
 
+template <int MODE>
 __global__ void verify_kernel(const uint32_t* __restrict__ vals, const uint32_t* __restrict__ node_of,
                               const uint32_t* __restrict__ off, uint32_t L, const uint32_t* __restrict__ V,
                               const uint32_t* __restrict__ m_dev, const EdgeRec* __restrict__ rec,
@@ -234,8 +235,8 @@ __global__ void verify_kernel(const uint32_t* __restrict__ vals, const uint32_t*
         const uint32_t span = L >> d, a = (nd - (1u << d)) * span, b = min(a + span, m - 1);
         const double y0 = (double)V[a] * 0x1p-30, y1 = (double)V[b] * 0x1p-30;
         const uint32_t e0 = vals[i], e1 = vals[i + 1];
-        const bool bad = edge_x(rec, nullptr, e0, y0, mp) > __dadd_rn(edge_x(rec, nullptr, e1, y0, mp), 0x1p-30) ||
-                         edge_x(rec, nullptr, e0, y1, mp) > __dadd_rn(edge_x(rec, nullptr, e1, y1, mp), 0x1p-30);
+        const bool bad = edge_x<MODE>(rec, e0, y0, mp) > __dadd_rn(edge_x<MODE>(rec, e1, y0, mp), 0x1p-30) ||
+                         edge_x<MODE>(rec, e0, y1, mp) > __dadd_rn(edge_x<MODE>(rec, e1, y1, mp), 0x1p-30);
         if (bad) flag[nd] = 1;
     }
 }
@@ -243,6 +244,7 @@ __global__ void verify_kernel(const uint32_t* __restrict__ vals, const uint32_t*
 // F: the reference's C1 count decision for a sure straddle, from a packed node
 // entry {Nx, Ny, c + B, edge}: 1 counted, 0 not; *certain: decided by the fp32
 // test (else the binary64 expression of the edge's record ran)
+template <int MODE>
 __device__ __forceinline__ int decide(const float4 pk, const EdgeRec* __restrict__ rec, float lx, float ly, double px,
                                       double py, bool* certain) {
     const float s = fmaf(lx, pk.x, fmaf(ly, pk.y, pk.z)); // s' = s + B
@@ -253,11 +255,17 @@ __device__ __forceinline__ int decide(const float4 pk, const EdgeRec* __restrict
     }
     *certain = false;
     int cnt = 0;
-    exact_c1(px, py, rec[__float_as_uint(pk.w)], cnt, true); // keys proved the straddle (geometry.hpp:189-200)
+    if (MODE == kC1) {
+        exact_c1(px, py, rec[__float_as_uint(pk.w)], cnt, true); // keys proved the straddle (geometry.hpp:189-200)
+    } else {
+        bool err = false; // a sure straddle has dy != 0: no DegenerateEdge
+        exact_c2(px, py, rec[__float_as_uint(pk.w)], cnt, err, true); // geometry.hpp:214-226
+    }
     return cnt;
 }
 
 // edges of one node list that the point counts
+template <int MODE>
 __device__ __forceinline__ uint32_t node_count(const float4* __restrict__ packed, uint32_t o, uint32_t k, bool linear,
                                                const EdgeRec* __restrict__ rec, float lx, float ly, double px,
                                                double py) {
@@ -265,27 +273,27 @@ __device__ __forceinline__ uint32_t node_count(const float4* __restrict__ packed
     const float4* P = packed + o;
     if (linear) { // non-simple input: every edge
         uint32_t c = 0;
-        for (uint32_t i = 0; i < k; ++i) c += decide(__ldg(P + i), rec, lx, ly, px, py, &cert);
+        for (uint32_t i = 0; i < k; ++i) c += decide<MODE>(__ldg(P + i), rec, lx, ly, px, py, &cert);
         return c;
     }
     // lists run left to right: not counted, then counted.  b = first counted
     uint32_t lo = 0, hi = k;
     while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
-        if (decide(__ldg(P + mid), rec, lx, ly, px, py, &cert)) hi = mid;
+        if (decide<MODE>(__ldg(P + mid), rec, lx, ly, px, py, &cert)) hi = mid;
         else lo = mid + 1;
     }
     const uint32_t b = lo;
     uint32_t c = k - b; // [b, k) counted, corrected below
     // right of b: undecided edges may be "not counted" after all
     for (uint32_t i = b; i < k; ++i) {
-        const int f = decide(__ldg(P + i), rec, lx, ly, px, py, &cert);
+        const int f = decide<MODE>(__ldg(P + i), rec, lx, ly, px, py, &cert);
         if (cert && f) break;
         c -= (uint32_t)(1 - f);
     }
     // left of b: undecided edges may be counted
     for (uint32_t i = b; i-- > 0;) {
-        const int f = decide(__ldg(P + i), rec, lx, ly, px, py, &cert);
+        const int f = decide<MODE>(__ldg(P + i), rec, lx, ly, px, py, &cert);
         if (cert && !f) break;
         c += (uint32_t)f;
     }
@@ -304,6 +312,7 @@ __global__ void pack_kernel(const uint32_t* __restrict__ vals, const uint32_t* _
     }
 }
 
+template <int MODE>
 __global__ void __launch_bounds__(256) query_kernel(const double2* __restrict__ pts, uint64_t n, int prefilter,
                                                     const unsigned long long* __restrict__ bbox_keys,
                                                     const uint32_t* __restrict__ V, const uint32_t* __restrict__ m_dev,
@@ -341,7 +350,7 @@ __global__ void __launch_bounds__(256) query_kernel(const double2* __restrict__ 
                         uint32_t c = 0;
                         for (uint32_t nd = L + j - 1; nd; nd >>= 1) {
                             const uint32_t o = __ldg(off + nd), k = __ldg(off + nd + 1) - o;
-                            if (k) c += node_count(packed, o, k, __ldg(flag + nd) != 0, rec, lx, ly, p.x, p.y);
+                            if (k) c += node_count<MODE>(packed, o, k, __ldg(flag + nd) != 0, rec, lx, ly, p.x, p.y);
                         }
                         in = c & 1u;
                     }
@@ -371,9 +380,11 @@ __global__ void gather_kernel(const double2* __restrict__ pts, const uint32_t* _
 // normal); block (chunk of kFbEdges edges, group of 256 points), parity bits
 // XOR-combined across chunks
 constexpr int kFbEdges = 256;
+template <int MODE>
 __global__ void __launch_bounds__(256) fallback_kernel(const double2* __restrict__ pts, const uint32_t* __restrict__ idx,
                                                        const uint32_t* __restrict__ count, const EdgeRec* __restrict__ rec,
-                                                       uint32_t n_edges, uint32_t* __restrict__ bits) {
+                                                       uint32_t n_edges, uint32_t* __restrict__ bits,
+                                                       uint32_t* __restrict__ ebits) {
     __shared__ double sa[5][kFbEdges];
     const uint32_t e0 = blockIdx.x * kFbEdges, ne = min((uint32_t)kFbEdges, n_edges - e0);
     for (uint32_t i = threadIdx.x; i < ne; i += blockDim.x) {
@@ -385,26 +396,38 @@ __global__ void __launch_bounds__(256) fallback_kernel(const double2* __restrict
     const uint32_t n = *count, k = blockIdx.y * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const double2 p = pts[idx[k]];
-    uint32_t par = 0;
+    uint32_t par = 0, err = 0;
     for (uint32_t i = 0; i < ne; ++i) {
-        const double ay = sa[1][i], by = sa[2][i];
+        const double ax = sa[0][i], ay = sa[1][i], by = sa[2][i];
         if (__dmul_rn(__dsub_rn(ay, p.y), __dsub_rn(by, p.y)) <= 0.0) {
-            const double side = __dadd_rn(__dmul_rn(__dsub_rn(p.x, sa[0][i]), sa[3][i]),
-                                          __dmul_rn(__dsub_rn(p.y, ay), sa[4][i]));
-            par ^= side <= 0.0;
+            if (MODE == kC1) { // geometry.hpp:189-200 (record: nx, ny)
+                const double side =
+                    __dadd_rn(__dmul_rn(__dsub_rn(p.x, ax), sa[3][i]), __dmul_rn(__dsub_rn(p.y, ay), sa[4][i]));
+                par ^= side <= 0.0;
+            } else { // geometry.hpp:214-226 (record: dx, dy)
+                const double dy = sa[4][i];
+                if (dy == 0.0) {
+                    err = 1; // DegenerateEdge
+                } else {
+                    const double x = __dadd_rn(ax, __dmul_rn(__ddiv_rn(__dsub_rn(p.y, ay), dy), sa[3][i]));
+                    par ^= x > p.x;
+                }
+            }
         }
     }
     if (par) atomicXor(&bits[k >> 5], 1u << (k & 31));
+    if (err) atomicOr(&ebits[k >> 5], 1u << (k & 31));
 }
 
 __global__ void scatter_kernel(const uint32_t* __restrict__ idx, const uint32_t* __restrict__ count,
-                               const uint32_t* __restrict__ bits, uint32_t* __restrict__ inside_bits) {
+                               const uint32_t* __restrict__ bits, const uint32_t* __restrict__ ebits,
+                               uint32_t* __restrict__ inside_bits, uint32_t* __restrict__ aux_bits) {
     const uint32_t n = *count;
-    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
-        if ((bits[k >> 5] >> (k & 31)) & 1u) {
-            const uint32_t i = idx[k];
-            atomicOr(&inside_bits[i >> 5], 1u << (i & 31));
-        }
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const uint32_t i = idx[k], b = 1u << (i & 31);
+        if ((bits[k >> 5] >> (k & 31)) & 1u) atomicOr(&inside_bits[i >> 5], b);
+        if ((ebits[k >> 5] >> (k & 31)) & 1u) atomicOr(&aux_bits[i >> 5], b);
+    }
 }
 
 int sms(int dev) {
@@ -422,7 +445,7 @@ uint32_t tree_leaves(uint64_t nv) {
 struct Layout {
     uint64_t nv, ne, L, emax;
     size_t o_vk, o_V, o_m, o_cnt, o_off, o_keys, o_vals, o_keys2, o_vals2, o_node, o_packed, o_flag, o_fbidx, o_fbcnt,
-        o_fbpts, o_fbbits, o_tmp, tmp_bytes, total;
+        o_fbpts, o_fbbits, o_fbebits, o_tmp, tmp_bytes, total;
 };
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -465,6 +488,7 @@ Layout layout(uint64_t nv, uint64_t ne, uint64_t n_pts) {
     l.o_fbcnt = put(16);
     l.o_fbpts = put(n_pts * 16 + 16);
     l.o_fbbits = put(((n_pts + 31) / 32) * 4 + 4);
+    l.o_fbebits = put(((n_pts + 31) / 32) * 4 + 4);
     l.o_tmp = put(l.tmp_bytes);
     l.total = o;
     return l;
@@ -501,6 +525,7 @@ cudaError_t launch_tree(const TreeArgs& a, void* scratch, cudaStream_t st, int d
     uint32_t* fb_cnt = reinterpret_cast<uint32_t*>(s + l.o_fbcnt);
     double* fb_pts = reinterpret_cast<double*>(s + l.o_fbpts);
     uint32_t* fb_bits = reinterpret_cast<uint32_t*>(s + l.o_fbbits);
+    uint32_t* fb_ebits = reinterpret_cast<uint32_t*>(s + l.o_fbebits);
     void* tmp = s + l.o_tmp;
     size_t tmp_bytes = l.tmp_bytes;
     const uint32_t L = (uint32_t)l.L;
@@ -527,13 +552,18 @@ cudaError_t launch_tree(const TreeArgs& a, void* scratch, cudaStream_t st, int d
     tmp_bytes = l.tmp_bytes;
     PC_TRY(cub::DeviceSegmentedSort::SortPairs(tmp, tmp_bytes, keys, keys2, vals, vals2, (int)l.emax, (int)(2 * l.L),
                                                off, off + 1, st));
-    verify_kernel<<<grid, 256, 0, st>>>(vals2, node_of, off, L, V, m_dev, rec, a.bbox_keys, flag);
+    if (a.mode == kC1) verify_kernel<kC1><<<grid, 256, 0, st>>>(vals2, node_of, off, L, V, m_dev, rec, a.bbox_keys, flag);
+    else verify_kernel<kC2><<<grid, 256, 0, st>>>(vals2, node_of, off, L, V, m_dev, rec, a.bbox_keys, flag);
     pack_kernel<<<grid, 256, 0, st>>>(vals2, off, L, rec, packed);
     // ---- query ----
     PC_TRY(cudaMemsetAsync(fb_cnt, 0, 4, st));
     const unsigned qgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((a.n + 255) / 256, (uint64_t)grid * 4));
-    query_kernel<<<qgrid, 256, 0, st>>>(reinterpret_cast<const double2*>(a.pts), a.n, a.prefilter, a.bbox_keys, V,
-                                        m_dev, L, off, packed, flag, rec, a.inside_bits, fb_idx, fb_cnt);
+    if (a.mode == kC1)
+        query_kernel<kC1><<<qgrid, 256, 0, st>>>(reinterpret_cast<const double2*>(a.pts), a.n, a.prefilter, a.bbox_keys,
+                                                 V, m_dev, L, off, packed, flag, rec, a.inside_bits, fb_idx, fb_cnt);
+    else
+        query_kernel<kC2><<<qgrid, 256, 0, st>>>(reinterpret_cast<const double2*>(a.pts), a.n, a.prefilter, a.bbox_keys,
+                                                 V, m_dev, L, off, packed, flag, rec, a.inside_bits, fb_idx, fb_cnt);
     *launches += 10;
     // ---- fallback points through the scan kernel, its grid sized for their number ----
     uint32_t n_fb = 0;
@@ -541,10 +571,15 @@ cudaError_t launch_tree(const TreeArgs& a, void* scratch, cudaStream_t st, int d
     PC_TRY(cudaStreamSynchronize(st));
     if (n_fb) {
         PC_TRY(cudaMemsetAsync(fb_bits, 0, ((n_fb + 31) / 32) * 4, st));
+        PC_TRY(cudaMemsetAsync(fb_ebits, 0, ((n_fb + 31) / 32) * 4, st));
         if ((double)n_fb * (double)a.n_edges <= 2e10) { // few points: every edge, literally
             const dim3 fgrid((unsigned)((a.n_edges + kFbEdges - 1) / kFbEdges), (unsigned)((n_fb + 255) / 256));
-            fallback_kernel<<<fgrid, 256, 0, st>>>(reinterpret_cast<const double2*>(a.pts), fb_idx, fb_cnt, rec,
-                                                   (uint32_t)a.n_edges, fb_bits);
+            if (a.mode == kC1)
+                fallback_kernel<kC1><<<fgrid, 256, 0, st>>>(reinterpret_cast<const double2*>(a.pts), fb_idx, fb_cnt,
+                                                            rec, (uint32_t)a.n_edges, fb_bits, fb_ebits);
+            else
+                fallback_kernel<kC2><<<fgrid, 256, 0, st>>>(reinterpret_cast<const double2*>(a.pts), fb_idx, fb_cnt,
+                                                            rec, (uint32_t)a.n_edges, fb_bits, fb_ebits);
             ++*launches;
         } else { // many: the scan kernel (its filters), grid sized for their number
             gather_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const double2*>(a.pts), fb_idx, fb_cnt,
@@ -555,10 +590,11 @@ cudaError_t launch_tree(const TreeArgs& a, void* scratch, cudaStream_t st, int d
             sa.n_dev = nullptr;
             sa.prefilter = 0; // gathered points were active
             sa.inside_bits = fb_bits;
+            sa.aux_bits = fb_ebits;
             PC_TRY(launch_single(sa, st, dev, launches));
             ++*launches;
         }
-        scatter_kernel<<<grid, 256, 0, st>>>(fb_idx, fb_cnt, fb_bits, a.inside_bits);
+        scatter_kernel<<<grid, 256, 0, st>>>(fb_idx, fb_cnt, fb_bits, fb_ebits, a.inside_bits, a.aux_bits);
         ++*launches;
     }
 #undef PC_TRY

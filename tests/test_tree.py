@@ -1,4 +1,4 @@
-"""Segment-tree C1 path for single polygons (pip_tree.cu, PC_OPT_TREE) against
+"""Segment-tree C1 / C2 path for single polygons (pip_tree.cu, PC_OPT_TREE) against
 the reference, bit-exact: forced on for every input shape (stars of many
 sizes, the adversarial cases, points on vertices / vertex y-levels / edges,
 overlapping holes and self-intersecting rings -- the verified-order fallback --,
@@ -15,14 +15,22 @@ pytestmark = pytest.mark.gpu
 THREADS = 16
 
 
-def _check(engine, xy, poly, prefilter=True, source=None):
-    got = engine.classify(xy, poly, 0, prefilter=prefilter)
+MODES = (0, 1)  # C1, C2 (the tree's modes)
+
+
+def _check(engine, xy, poly, prefilter=True, source=None, modes=MODES):
+    for mode in modes:
+        _check1(engine, xy, poly, mode, prefilter, source)
+
+
+def _check1(engine, xy, poly, mode, prefilter, source):
+    got = engine.classify(xy, poly, mode, prefilter=prefilter)
     if source is None:
         source = "reference" if prefilter and oracle.ref_available() else "port"
     if source == "reference":
-        want_v, want_s = oracle.ref_classify(xy, poly.vx, poly.vy, poly.ring_off, 0)
+        want_v, want_s = oracle.ref_classify(xy, poly.vx, poly.vy, poly.ring_off, mode)
     else:
-        want_v, want_s = oracle.port_classify(xy, poly.vx, poly.vy, poly.ring_off, 0, prefilter=prefilter,
+        want_v, want_s = oracle.port_classify(xy, poly.vx, poly.vy, poly.ring_off, mode, prefilter=prefilter,
                                               threads=THREADS)
     assert np.array_equal(got.verdicts, want_v), f"{int((got.verdicts != want_v).sum())} of {len(xy)} differ"
     assert np.array_equal(got.stats, want_s)
@@ -84,13 +92,14 @@ def test_sweep_tree_vs_scan(engine, n):
     """Auto mode on the sweep's big polygons: tree and scan paths agree on all
     1e6 points, and a seeded subsample agrees with the reference."""
     poly, xy = W.config2(n)
-    engine.set_tree(1)
-    a = engine.classify(xy, poly, 0)
-    engine.set_tree(0)
-    b = engine.classify(xy, poly, 0)
-    engine.set_tree(-1)
-    assert np.array_equal(a.verdicts, b.verdicts)
-    idx = np.random.default_rng(n).choice(len(xy), 3000, replace=False)
-    sub = np.ascontiguousarray(xy[idx])
-    want_v, _ = oracle.ref_classify(sub, poly.vx, poly.vy, poly.ring_off, 0)
-    assert np.array_equal(a.verdicts[idx], want_v)
+    for mode in MODES:
+        engine.set_tree(1)
+        a = engine.classify(xy, poly, mode)
+        engine.set_tree(0)
+        b = engine.classify(xy, poly, mode)
+        engine.set_tree(-1)
+        assert np.array_equal(a.verdicts, b.verdicts)
+        idx = np.random.default_rng(n).choice(len(xy), 3000, replace=False)
+        sub = np.ascontiguousarray(xy[idx])
+        want_v, _ = oracle.ref_classify(sub, poly.vx, poly.vy, poly.ring_off, mode)
+        assert np.array_equal(a.verdicts[idx], want_v)
