@@ -103,3 +103,40 @@ def test_sweep_tree_vs_scan(engine, n):
         sub = np.ascontiguousarray(xy[idx])
         want_v, _ = oracle.ref_classify(sub, poly.vx, poly.vy, poly.ring_off, mode)
         assert np.array_equal(a.verdicts[idx], want_v)
+
+
+def test_fuzz_random_polygons(tree_on):
+    """200 random polygons (simple stars, random-order rings, grids with holes,
+    integer coordinates for exact ties), each with points on its vertices, its
+    vertex y-levels, edge midpoints and uniform points, forced through the tree."""
+    rng = np.random.default_rng(77)
+    for t in range(200):
+        kind = t % 4
+        n = int(rng.integers(4, 60))
+        if kind == 0:  # star
+            ang = np.sort(rng.uniform(0, 2 * np.pi, n))
+            r = rng.uniform(0.3, 1.0, n)
+            ring = np.stack([r * np.cos(ang), r * np.sin(ang)], 1)
+        elif kind == 1:  # random order: self-intersecting
+            ring = rng.uniform(-1, 1, (n, 2))
+        elif kind == 2:  # integer grid (horizontal edges, ties everywhere)
+            ring = rng.integers(-5, 6, (n, 2)).astype(np.float64)
+            keep = np.concatenate([[True], np.any(ring[1:] != ring[:-1], axis=1)])
+            ring = ring[keep]
+            if len(ring) < 3 or np.all(ring[0] == ring[-1]):
+                continue
+        else:  # tiny extent far from the origin
+            ang = np.sort(rng.uniform(0, 2 * np.pi, n))
+            ring = np.stack([1e3 + 1e-6 * np.cos(ang), -7.5 + 1e-6 * np.sin(ang)], 1)
+        ring = np.concatenate([ring, ring[:1]])
+        rings = [ring]
+        if kind == 2 and t % 8 == 2:
+            rings.append(np.array([[0., 0.], [1., 0.], [1., 1.], [0., 1.], [0., 0.]]))
+        poly = Polygon.from_rings(rings)
+        vx, vy = poly.vx, poly.vy
+        x0, x1, y0, y1 = vx.min(), vx.max(), vy.min(), vy.max()
+        pts = [np.stack([vx, vy], 1), np.stack([(vx[:-1] + vx[1:]) / 2, (vy[:-1] + vy[1:]) / 2], 1),
+               np.stack([rng.uniform(x0, x1, len(vy)), vy], 1),
+               np.stack([rng.uniform(x0, x1, 300), rng.uniform(y0, y1, 300)], 1)]
+        xy = np.ascontiguousarray(np.concatenate(pts))
+        _check(tree_on, xy, poly, source="port")
