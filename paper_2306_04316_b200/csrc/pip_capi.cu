@@ -158,7 +158,7 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
     check(c, pcd::launch_prep(pa, st, d.dev, &c->launches), "prep kernel");
     check(c, cudaMemsetAsync(d_aux, 0, nwords * 4, st), "clear aux plane");
     const bool tree = (mode == 0 || mode == 1) /* C1, C2 */ && c->tree_mode != 0 && pcd::tree_eligible(n_verts, n, c->tree_mode == 1);
-    const bool bucket = !tree && n < 0xffffffffull &&
+    const bool bucket = n < 0xffffffffull &&
                         (c->bucket_mode == 1 || (c->bucket_mode < 0 && n_edges >= 64 && n >= 4096));
     pcd::SingleArgs sa{};
     sa.mode = mode;
@@ -194,11 +194,13 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
         sa.n_dev = hist + pcd::kBuckets + 1;
     }
     if (tree) { // segment-tree counts; key-tie / off-map points through the scan kernel
+        // (y-bucketed points: a warp's queries walk nearby leaves, sharing nodes)
         pcd::TreeArgs ta{};
         ta.mode = mode;
-        ta.pts = d_pts;
+        ta.pts = sa.pts;
         ta.n = n;
-        ta.prefilter = prefilter;
+        ta.n_dev = sa.n_dev;
+        ta.prefilter = sa.prefilter;
         ta.vx = d_vx;
         ta.vy = d_vy;
         ta.ring_off = d_ring_off;
@@ -207,13 +209,18 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
         ta.n_edges = n_edges;
         ta.rec = d.rec.p;
         ta.bbox_keys = d.bbox.as<unsigned long long>();
-        ta.inside_bits = d_inside;
-        ta.aux_bits = d_aux;
+        ta.inside_bits = sa.inside_bits;
+        ta.aux_bits = sa.aux_bits;
         ta.single = sa;
+        ta.single.n_dev = nullptr;
         check(c, d.tree.ensure(pcd::tree_scratch_bytes(n_verts, n_edges, n)), "alloc segment tree");
         mark_begin(c, d, st);
         check(c, pcd::launch_tree(ta, d.tree.p, st, d.dev, &c->launches), "segment-tree kernels");
         mark_end(c, d, st);
+        if (bucket)
+            check(c, pcd::launch_unbucket(n, sa.n_dev, d.sorted_idx.as<uint32_t>(), sa.inside_bits, sa.aux_bits,
+                                          d_inside, d_aux, st, d.dev, &c->launches),
+                  "unbucket kernel");
         check(c, pcd::launch_finalize(n, d_inside, d_aux, d_verdicts, mode, d_stats, st, d.dev, &c->launches),
               "finalize kernel");
         return;

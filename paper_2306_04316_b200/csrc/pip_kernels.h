@@ -99,6 +99,7 @@ struct TreeArgs {
     int mode; // kC1 or kC2
     const double* pts;
     uint64_t n;
+    const uint32_t* n_dev; // optional device-side point count (y-bucketed input)
     int prefilter;
     const double* vx;
     const double* vy;

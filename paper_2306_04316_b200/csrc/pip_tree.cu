@@ -319,7 +319,9 @@ __global__ void __launch_bounds__(256) query_kernel(const double2* __restrict__ 
                                                     uint32_t L, const uint32_t* __restrict__ off,
                                                     const float4* __restrict__ packed, const uint8_t* __restrict__ flag,
                                                     const EdgeRec* __restrict__ rec, uint32_t* __restrict__ inside_bits,
-                                                    uint32_t* __restrict__ fb_idx, uint32_t* __restrict__ fb_count) {
+                                                    uint32_t* __restrict__ fb_idx, uint32_t* __restrict__ fb_count,
+                                                    const uint32_t* __restrict__ n_dev) {
+    if (n_dev) n = min(n, (uint64_t)*n_dev); // y-bucketed input: the in-box prefix
     const Map mp = map_of(bbox_keys);
     const uint32_t m = *m_dev;
     const double minx = dkey_inv(bbox_keys[0]), miny = dkey_inv(bbox_keys[1]);
@@ -560,10 +562,12 @@ cudaError_t launch_tree(const TreeArgs& a, void* scratch, cudaStream_t st, int d
     const unsigned qgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((a.n + 255) / 256, (uint64_t)grid * 4));
     if (a.mode == kC1)
         query_kernel<kC1><<<qgrid, 256, 0, st>>>(reinterpret_cast<const double2*>(a.pts), a.n, a.prefilter, a.bbox_keys,
-                                                 V, m_dev, L, off, packed, flag, rec, a.inside_bits, fb_idx, fb_cnt);
+                                                 V, m_dev, L, off, packed, flag, rec, a.inside_bits, fb_idx, fb_cnt,
+                                                 a.n_dev);
     else
         query_kernel<kC2><<<qgrid, 256, 0, st>>>(reinterpret_cast<const double2*>(a.pts), a.n, a.prefilter, a.bbox_keys,
-                                                 V, m_dev, L, off, packed, flag, rec, a.inside_bits, fb_idx, fb_cnt);
+                                                 V, m_dev, L, off, packed, flag, rec, a.inside_bits, fb_idx, fb_cnt,
+                                                 a.n_dev);
     *launches += 10;
     // ---- fallback points through the scan kernel, its grid sized for their number ----
     uint32_t n_fb = 0;
