@@ -152,7 +152,7 @@ __global__ void edges_kernel(const double* __restrict__ vx, const double* __rest
                              const unsigned long long* __restrict__ bbox_keys, const uint32_t* __restrict__ V,
                              const uint32_t* __restrict__ m_dev, uint32_t L, uint32_t* __restrict__ cnt,
                              const uint32_t* __restrict__ off, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                             uint32_t* __restrict__ node_of) {
+                             uint32_t* __restrict__ node_of, double4* __restrict__ line) {
     const Map mp = map_of(bbox_keys);
     const uint32_t m = *m_dev;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -177,6 +177,7 @@ __global__ void edges_kernel(const double* __restrict__ vx, const double* __rest
                     const double bxl = __dmul_rn(__dsub_rn(bx, mp.x0), mp.sx);
                     const double byl = __dmul_rn(__dsub_rn(by, mp.y0), mp.sy);
                     slope = __ddiv_rn(__dsub_rn(bxl, axl), __dsub_rn(byl, ayl));
+                    line[e] = make_double4(axl, ayl, slope, 0.0); // x(y) = axl + (y - ayl) slope, local units
                 }
             }
         }
@@ -209,35 +210,29 @@ __global__ void edges_kernel(const double* __restrict__ vx, const double* __rest
     }
 }
 
-// x of edge e (local units) at local height y, from its record's exact values
-template <int MODE>
-__device__ __forceinline__ double edge_x(const EdgeRec* __restrict__ rec, uint32_t e, double y, const Map& mp) {
-    const EdgeRec& r = rec[e];
-    // d[0] = ax, d[1] = ay; C1: d[3], d[4] = nx, ny with n = +-(dy, -dx) -> dx / dy = -ny / nx;
-    // C2: d[3], d[4] = dx, dy
-    const double axl = __dmul_rn(__dsub_rn(r.d[0], mp.x0), mp.sx), ayl = __dmul_rn(__dsub_rn(r.d[1], mp.y0), mp.sy);
-    const double dxl = MODE == kC1 ? __dmul_rn(-r.d[4], mp.sx) : __dmul_rn(r.d[3], mp.sx);
-    const double dyl = MODE == kC1 ? __dmul_rn(r.d[3], mp.sy) : __dmul_rn(r.d[4], mp.sy);
-    return __dadd_rn(axl, __dmul_rn(__dsub_rn(y, ayl), __ddiv_rn(dxl, dyl)));
-}
-
-template <int MODE>
-__global__ void verify_kernel(const uint32_t* __restrict__ vals, const uint32_t* __restrict__ node_of,
-                              const uint32_t* __restrict__ off, uint32_t L, const uint32_t* __restrict__ V,
-                              const uint32_t* __restrict__ m_dev, const EdgeRec* __restrict__ rec,
-                              const unsigned long long* __restrict__ bbox_keys, uint8_t* __restrict__ flag) {
-    const Map mp = map_of(bbox_keys);
+// per entry: its packed record {Nx, Ny, c + B, edge} (the fp32 record of
+// pip_kernels.cu prep_edges_kernel), and the order check against the next
+// entry of the same node at both ends of the node's key range (x from the
+// edge's local line; a violation beyond 2^-30 flags the node)
+__global__ void verify_pack_kernel(const uint32_t* __restrict__ vals, const uint32_t* __restrict__ node_of,
+                                   const uint32_t* __restrict__ off, uint32_t L, const uint32_t* __restrict__ V,
+                                   const uint32_t* __restrict__ m_dev, const EdgeRec* __restrict__ rec,
+                                   const double4* __restrict__ line, float4* __restrict__ packed,
+                                   uint8_t* __restrict__ flag) {
     const uint32_t m = *m_dev, total = off[2 * L];
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i + 1 < total; i += gridDim.x * blockDim.x) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const uint32_t e0 = vals[i];
+        const double d5 = rec[e0].d[5], d6 = rec[e0].d[6];
+        packed[i] = make_float4(__int_as_float(__double2loint(d5)), __int_as_float(__double2hiint(d5)),
+                                __int_as_float(__double2loint(d6)), __uint_as_float(e0));
         const uint32_t nd = node_of[i];
-        if (node_of[i + 1] != nd) continue;
+        if (i + 1 >= total || node_of[i + 1] != nd) continue;
         const int d = 31 - __clz(nd);
         const uint32_t span = L >> d, a = (nd - (1u << d)) * span, b = min(a + span, m - 1);
         const double y0 = (double)V[a] * 0x1p-30, y1 = (double)V[b] * 0x1p-30;
-        const uint32_t e0 = vals[i], e1 = vals[i + 1];
-        const bool bad = edge_x<MODE>(rec, e0, y0, mp) > __dadd_rn(edge_x<MODE>(rec, e1, y0, mp), 0x1p-30) ||
-                         edge_x<MODE>(rec, e0, y1, mp) > __dadd_rn(edge_x<MODE>(rec, e1, y1, mp), 0x1p-30);
-        if (bad) flag[nd] = 1;
+        const double4 l0 = line[e0], l1 = line[vals[i + 1]];
+        auto x = [](const double4& l, double y) { return __dadd_rn(l.x, __dmul_rn(__dsub_rn(y, l.y), l.z)); };
+        if (x(l0, y0) > __dadd_rn(x(l1, y0), 0x1p-30) || x(l0, y1) > __dadd_rn(x(l1, y1), 0x1p-30)) flag[nd] = 1;
     }
 }
 
@@ -298,18 +293,6 @@ __device__ __forceinline__ uint32_t node_count(const float4* __restrict__ packed
         c += (uint32_t)f;
     }
     return c;
-}
-
-// node entries -> {Nx, Ny, c + B, edge} (the C1 fp32 record of pip_kernels.cu prep_edges_kernel)
-__global__ void pack_kernel(const uint32_t* __restrict__ vals, const uint32_t* __restrict__ off, uint32_t L,
-                            const EdgeRec* __restrict__ rec, float4* __restrict__ packed) {
-    const uint32_t total = off[2 * L];
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-        const uint32_t e = vals[i];
-        const double d5 = rec[e].d[5], d6 = rec[e].d[6];
-        packed[i] = make_float4(__int_as_float(__double2loint(d5)), __int_as_float(__double2hiint(d5)),
-                                __int_as_float(__double2loint(d6)), __uint_as_float(e));
-    }
 }
 
 template <int MODE>
@@ -447,7 +430,7 @@ uint32_t tree_leaves(uint64_t nv) {
 struct Layout {
     uint64_t nv, ne, L, emax;
     size_t o_vk, o_V, o_m, o_cnt, o_off, o_keys, o_vals, o_keys2, o_vals2, o_node, o_packed, o_flag, o_fbidx, o_fbcnt,
-        o_fbpts, o_fbbits, o_fbebits, o_tmp, tmp_bytes, total;
+        o_fbpts, o_fbbits, o_fbebits, o_line, o_tmp, tmp_bytes, total;
 };
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -491,6 +474,7 @@ Layout layout(uint64_t nv, uint64_t ne, uint64_t n_pts) {
     l.o_fbpts = put(n_pts * 16 + 16);
     l.o_fbbits = put(((n_pts + 31) / 32) * 4 + 4);
     l.o_fbebits = put(((n_pts + 31) / 32) * 4 + 4);
+    l.o_line = put(std::max<uint64_t>(ne, 1) * 32);
     l.o_tmp = put(l.tmp_bytes);
     l.total = o;
     return l;
@@ -528,6 +512,7 @@ cudaError_t launch_tree(const TreeArgs& a, void* scratch, cudaStream_t st, int d
     double* fb_pts = reinterpret_cast<double*>(s + l.o_fbpts);
     uint32_t* fb_bits = reinterpret_cast<uint32_t*>(s + l.o_fbbits);
     uint32_t* fb_ebits = reinterpret_cast<uint32_t*>(s + l.o_fbebits);
+    double4* line = reinterpret_cast<double4*>(s + l.o_line);
     void* tmp = s + l.o_tmp;
     size_t tmp_bytes = l.tmp_bytes;
     const uint32_t L = (uint32_t)l.L;
@@ -545,18 +530,16 @@ cudaError_t launch_tree(const TreeArgs& a, void* scratch, cudaStream_t st, int d
     PC_TRY(cudaMemsetAsync(cnt, 0, (2 * l.L + 1) * 4, st));
     PC_TRY(cudaMemsetAsync(flag, 0, 2 * l.L, st));
     edges_kernel<false><<<grid, 256, 0, st>>>(a.vx, a.vy, ro, a.n_rings, a.n_verts, a.bbox_keys, V, m_dev, L, cnt,
-                                              nullptr, nullptr, nullptr, nullptr);
+                                              nullptr, nullptr, nullptr, nullptr, nullptr);
     tmp_bytes = l.tmp_bytes;
     PC_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, off, (int)(2 * l.L + 1), st));
     PC_TRY(cudaMemsetAsync(cnt, 0, (2 * l.L + 1) * 4, st));
     edges_kernel<true><<<grid, 256, 0, st>>>(a.vx, a.vy, ro, a.n_rings, a.n_verts, a.bbox_keys, V, m_dev, L, cnt, off,
-                                             keys, vals, node_of);
+                                             keys, vals, node_of, line);
     tmp_bytes = l.tmp_bytes;
     PC_TRY(cub::DeviceSegmentedSort::SortPairs(tmp, tmp_bytes, keys, keys2, vals, vals2, (int)l.emax, (int)(2 * l.L),
                                                off, off + 1, st));
-    if (a.mode == kC1) verify_kernel<kC1><<<grid, 256, 0, st>>>(vals2, node_of, off, L, V, m_dev, rec, a.bbox_keys, flag);
-    else verify_kernel<kC2><<<grid, 256, 0, st>>>(vals2, node_of, off, L, V, m_dev, rec, a.bbox_keys, flag);
-    pack_kernel<<<grid, 256, 0, st>>>(vals2, off, L, rec, packed);
+    verify_pack_kernel<<<grid, 256, 0, st>>>(vals2, node_of, off, L, V, m_dev, rec, line, packed, flag);
     // ---- query ----
     PC_TRY(cudaMemsetAsync(fb_cnt, 0, 4, st));
     const unsigned qgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((a.n + 255) / 256, (uint64_t)grid * 4));
