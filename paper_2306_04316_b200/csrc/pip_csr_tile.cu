@@ -58,8 +58,12 @@ struct BPoly {
 
 struct WarpSmem {
     double2 vert[kWV];
-    int4 rec[kWV];    // (qlo+1, max(qhi-qlo-1,0), q(a), Nx) -- see pip_csr_common.cuh
-    float2 rec2[kWV]; // (Ny, c)
+    // C1 / C2: rec = (K(a), Nx, Ny, c + B) with K the packed 14-bit key of the
+    //          vertex (see classify_item), rec2 = (q_lo + 1, q_hi) on 30-bit keys
+    //          (the exact path's candidate test);
+    // Robust:  rec = (q_lo + 1, q_hi, q(a), Nx), rec2 = (Ny, c + B)
+    int4 rec[kWV];
+    int2 rec2[kWV];
     BPoly bp[32];
     unsigned long long v0s[32]; // first vertex (shard-local) of batch polygon k
     uint32_t off[32];           // batch offset of batch polygon k's first vertex
@@ -102,21 +106,73 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
         const double yl = __dmul_rn(__dsub_rn(q.y, by0), sy);
         lx[k] = __double2float_rn(__dmul_rn(__dsub_rn(q.x, bx0), sx));
         ly[k] = __double2float_rn(yl);
-        qy[k] = __double2int_rz(__dmul_rn(yl, 0x1p30)); // = trunc((y - o_y) * s_y * 2^30): exact scaling
         if (MODE == kRobust) { // the band reject's own rounded values (geometry.hpp:248)
+            qy[k] = __double2int_rz(__dmul_rn(yl, 0x1p30)); // = trunc((y - o_y) * s_y * 2^30): exact scaling
             qm[k] = __double2int_rz(__dmul_rn(__dmul_rn(__dsub_rn(__dsub_rn(q.y, tol), by0), sy), 0x1p30));
             qp[k] = __double2int_rz(__dmul_rn(__dmul_rn(__dsub_rn(__dadd_rn(q.y, tol), by0), sy), 0x1p30));
         } else {
-            qm[k] = qp[k] = qy[k];
+            qy[k] = qm[k] = qp[k] = 0; // C1 / C2: the 30-bit key is formed on the exact path only
         }
-        // the key filters are exact only for |p.y| >= 2^-400 (pip_csr_common.cuh)
-        qok |= (uint32_t)(a && fast && fabs(q.y) >= 0x1p-400) << k;
+        // the key filters are exact only for |p.y| >= 2^-400 (pip_csr_common.cuh);
+        // bit 30 of nloop: the whole closed bbox is clear of that range
+        qok |= (uint32_t)(a && fast && ((tp.nloop >> 30 & 1u) || fabs(q.y) >= 0x1p-400)) << k;
     }
     if (!__any_sync(kFull, act != 0)) return 0;
     uint32_t par = 0, slow = act & ~qok, band = 0, err = 0;
     if (fast && walk_all) {
         slow = act;
         band = act; // every candidate edge of every point
+    } else if (fast && MODE != kRobust) {
+        // Packed pass, both points of the lane in one 32-bit word per quantity.
+        // Keys: k(y) = bits 8..21 of RN32(RN32(y_local) * 0.5 + 1) -- a monotone
+        // 14-bit function of y, the same for points and vertices.  Q holds
+        // (k0 << 1 | 1) and (k1 << 1 | 1) in its halves, K(v) holds k(v) << 1 in
+        // both; in d = Q - K the half of point j has its sign bit (15 / 31) set
+        // iff k_j < k(v) (the low half's borrow only clears the high half's guard
+        // bit), and the half is 0 or 1 iff k_j == k(v) (a tie).  With no tie,
+        // edge a -> b surely straddles iff the sign bits of d(a) and d(b) differ
+        // (strict: k(a) < k < k(b) => a.y < p.y < b.y), and surely does not iff
+        // they agree (both ends strictly above / below; the product cannot
+        // underflow since |p.y| >= 2^-400).  The side test's s' = s + B as in the
+        // Robust branch below; its high halves of both points are packed into P
+        // (sign bits 15 / 31), so (d(a) ^ d(b)) & P toggles the parity bits.
+        // A point with a tie or a band hit (P half <= 0x3600, i.e. 0 <= s' <
+        // 2B (1 + 2^-7)) is decided by the exact path instead.
+        const uint32_t t0 = __float_as_uint(fmaf(ly[0], 0.5f, 1.0f)), t1 = __float_as_uint(fmaf(ly[1], 0.5f, 1.0f));
+        const uint32_t Q = ((t0 >> 7) & 0x7ffeu) | ((t1 << 9) & 0x7ffe0000u) | 0x00010001u;
+        uint32_t acc = 0u, tm = 0xffffffffu, bm = 0xffffffffu;
+        uint32_t dprev = Q - (uint32_t)ws.rec[e0].x, pprev = 0u;
+        auto step2 = [&](uint32_t i, uint32_t j) { // records i, j (consecutive, or clamped repeats)
+            const int4 fi = ws.rec[i], fj = ws.rec[j];
+            const uint32_t di = Q - (uint32_t)fi.x, dj = Q - (uint32_t)fj.x;
+            const uint32_t pi = __byte_perm(__float_as_uint(fmaf(lx[0], __int_as_float(fi.y), fmaf(ly[0], __int_as_float(fi.z), __int_as_float(fi.w)))),
+                                            __float_as_uint(fmaf(lx[1], __int_as_float(fi.y), fmaf(ly[1], __int_as_float(fi.z), __int_as_float(fi.w)))), 0x7632);
+            const uint32_t pj = __byte_perm(__float_as_uint(fmaf(lx[0], __int_as_float(fj.y), fmaf(ly[0], __int_as_float(fj.z), __int_as_float(fj.w)))),
+                                            __float_as_uint(fmaf(lx[1], __int_as_float(fj.y), fmaf(ly[1], __int_as_float(fj.z), __int_as_float(fj.w)))), 0x7632);
+            acc ^= ((dprev ^ di) & pprev) ^ ((di ^ dj) & pi);
+            tm = __vimin3_u16x2(tm, di, dj);
+            bm = __vimin3_u16x2(bm, pi, pj);
+            dprev = dj;
+            pprev = pj;
+        };
+        // every stored vertex of the polygon (a ring's last vertex carries the
+        // no-toggle sentinel record); reads past the end re-read the last record
+        // (d ^ d = 0: no toggle, the same tie / band values)
+        const uint32_t last = e1 - 1u;
+        uint32_t i = e0;
+        for (; i + 4 <= e1; i += 4) {
+            step2(i, i + 1);
+            step2(i + 2, i + 3);
+        }
+        if (i < e1) {
+            step2(i, min(i + 1, last));
+            step2(min(i + 2, last), min(i + 3, last));
+        }
+        const uint32_t fpar = (acc >> 15 & 1u) | (acc >> 30 & 2u);
+        band = ((uint32_t)((bm & 0xffffu) <= 0x3600u) | ((uint32_t)((bm >> 16) <= 0x3600u) << 1) |
+                (uint32_t)((tm & 0xffffu) <= 1u) | ((uint32_t)((tm >> 16) <= 1u) << 1)) & act;
+        slow |= band;
+        par = fpar & qok & ~band;
     } else if (fast) {
         // per record and point: x = q - q_hi < 0 and y = q - (q_lo + 1) >= 0 iff
         // q_lo < q < q_hi (a sure straddle); s' = s + B (B folded into the
@@ -126,7 +182,7 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
         uint32_t t0 = 0xffffffffu, t1 = 0xffffffffu, u0 = 0xffffffffu, u1 = 0xffffffffu;
         auto rec = [&](uint32_t i) {
             const int4 f = ws.rec[i];
-            const float2 g = ws.rec2[i];
+            const float2 g = make_float2(__int_as_float(ws.rec2[i].x), __int_as_float(ws.rec2[i].y));
             const float nxf = __int_as_float(f.w);
             const float s0 = fmaf(lx[0], nxf, fmaf(ly[0], g.x, g.y));
             const float s1 = fmaf(lx[1], nxf, fmaf(ly[1], g.x, g.y));
@@ -140,7 +196,7 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
         // four records per iteration; reads past the polygon's last record
         // re-read it (the final vertex's sentinel: no toggle, no band hit, a
         // repeated tie check), so no remainder loop is needed
-        const uint32_t last = e1 - 1u, stop = e0 + (tp.nloop & 0x7fffffffu);
+        const uint32_t last = e1 - 1u, stop = e0 + (tp.nloop & 0x3fffffffu);
         uint32_t i = e0;
         for (; i + 4 <= stop; i += 4) { // whole groups: consecutive records, fixed offsets
 #pragma unroll
@@ -176,8 +232,12 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
         }
         // one selection rule per warp: if any point has a band hit, every
         // undecided point redoes all its candidate edges (and drops fpar)
-        const bool cand_mode = __any_sync(kFull, band != 0);
-        if (cand_mode || MODE == kRobust) par &= ~slow; // Robust: a slow point redoes every candidate edge
+        // a slow point redoes every candidate edge (C1 / C2: 30-bit keys formed here)
+        par &= ~slow;
+        if (MODE != kRobust) {
+#pragma unroll
+            for (int k = 0; k < 2; ++k) qy[k] = __double2int_rz(__dmul_rn(__dmul_rn(__dsub_rn(py[k], by0), sy), 0x1p30));
+        }
         const int qy1[2] = {qy[0] + 1, qy[1] + 1};
         for (uint32_t i0 = e0; i0 < e1; i0 += 32) {
             const int n = (int)min(32u, e1 - i0);
@@ -194,18 +254,12 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
                     cm0 = (cm0 << 1) | (uint32_t)(((qp[0] + 1 - f.x) | (f.y - qm[0])) >= 0);
                     cm1 = (cm1 << 1) | (uint32_t)(((qp[1] + 1 - f.x) | (f.y - qm[1])) >= 0);
                 }
-            } else if (cand_mode) { // q_lo <= q <= q_hi
+            } else { // C1 / C2: q_lo <= q <= q_hi (rec2 = (q_lo + 1, q_hi))
                 for (int u = n - 1; u >= 0; --u) {
-                    const int2 f = *reinterpret_cast<const int2*>(&ws.rec[i0 + u]);
+                    const int2 f = ws.rec2[i0 + u];
                     const unsigned r = (unsigned)(f.y - f.x + 1);
                     cm0 = (cm0 << 1) | (uint32_t)((unsigned)(qy1[0] - f.x) <= r);
                     cm1 = (cm1 << 1) | (uint32_t)((unsigned)(qy1[1] - f.x) <= r);
-                }
-            } else { // ties only: q == q_lo or q == q_hi
-                for (int u = n - 1; u >= 0; --u) {
-                    const int2 f = *reinterpret_cast<const int2*>(&ws.rec[i0 + u]);
-                    cm0 = (cm0 << 1) | (uint32_t)(qy1[0] == f.x || qy[0] == f.y);
-                    cm1 = (cm1 << 1) | (uint32_t)(qy1[1] == f.x || qy[1] == f.y);
                 }
             }
             // points whose key filter is not exact: every edge
@@ -384,7 +438,7 @@ __global__ void __launch_bounds__(kBThreads, 8) pip_csr_tile_kernel(
                 b.e1 = excl + nv;
                 const double2 vf = ws.vert[excl], vl = ws.vert[excl + nv - 1];
                 b.nloop = (ws.gnr[lane] == 1 && nv > 1 && vf.x == vl.x && vf.y == vl.y ? nv - 1 : nv) |
-                          ((uint32_t)fast << 31);
+                          ((uint32_t)fast << 31) | ((uint32_t)(by0 >= 0x1p-400 || by1 <= -0x1p-400) << 30);
             }
             __syncwarp();
             // ---- 3. fast-path record per edge -----------------------------------
@@ -396,8 +450,12 @@ __global__ void __launch_bounds__(kBThreads, 8) pip_csr_tile_kernel(
                 const double axl = __dmul_rn(__dsub_rn(a.x, bx0), sx), ayl = __dmul_rn(__dsub_rn(a.y, by0), sy);
                 const int qa = __double2int_rz(__dmul_rn(ayl, 0x1p30));
                 if (!(axl >= 0.0 && axl < 1.0 && ayl >= 0.0 && ayl < 1.0)) atomicAnd(&ws.bp[o].nloop, 0x7fffffffu); // a hole poking out
-                int4 f = make_int4(kFastSentinelLo, 0, qa, 0);
-                float2 gg = make_float2(0.f, 1.f);
+                // C1 / C2: the packed 14-bit key of the vertex (classify_item)
+                const uint32_t kt = (__float_as_uint(fmaf(__double2float_rn(ayl), 0.5f, 1.0f)) >> 8) & 0x3fffu;
+                const int kv = (int)((kt << 1) | (kt << 17));
+                int4 f = MODE == kRobust ? make_int4(kFastSentinelLo, 0, qa, 0)
+                                         : make_int4(kv, 0, 0, __float_as_int(1.f));
+                int2 gg = MODE == kRobust ? make_int2(0, __float_as_int(1.f)) : make_int2(kFastSentinelLo, 0);
                 if (!is_ring_end(ws, i)) {
                     const double2 b = ws.vert[i + 1];
                     const int qb = __double2int_rz(__dmul_rn(__dmul_rn(__dsub_rn(b.y, by0), sy), 0x1p30));
@@ -418,10 +476,17 @@ __global__ void __launch_bounds__(kBThreads, 8) pip_csr_tile_kernel(
                     }
                     const int qlo = min(qa, qb), qhi = max(qa, qb);
                     const double cd = __dadd_rn(__dmul_rn(axl, Nx), __dmul_rn(ayl, Ny));
-                    f = make_int4(qlo + 1, qhi, qa, __float_as_int(__double2float_rn(Nx)));
                     // offset c + B (see classify_item): the extra fp32 rounding (<= 2 * 2^-24)
                     // keeps the error at 15.1 * 2^-24 < B
-                    gg = make_float2(__double2float_rn(Ny), __double2float_rn(__dadd_rn(-cd, (double)kFastBand)));
+                    const float nxf = __double2float_rn(Nx), nyf = __double2float_rn(Ny);
+                    const float cf = __double2float_rn(__dadd_rn(-cd, (double)kFastBand));
+                    if (MODE == kRobust) {
+                        f = make_int4(qlo + 1, qhi, qa, __float_as_int(nxf));
+                        gg = make_int2(__float_as_int(nyf), __float_as_int(cf));
+                    } else {
+                        f = make_int4(kv, __float_as_int(nxf), __float_as_int(nyf), __float_as_int(cf));
+                        gg = make_int2(qlo + 1, qhi);
+                    }
                 }
                 ws.rec[i] = f;
                 ws.rec2[i] = gg;
