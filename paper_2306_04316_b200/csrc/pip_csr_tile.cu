@@ -67,7 +67,9 @@ struct WarpSmem {
     BPoly bp[32];
     unsigned long long v0s[32]; // first vertex (shard-local) of batch polygon k
     uint32_t off[32];           // batch offset of batch polygon k's first vertex
+    uint32_t nvo[32];           // outer-ring vertices of batch polygon k
     uint32_t ring_end[kWV / 32]; // bit i: batch vertex i is the last vertex of its ring
+    uint32_t starts[kWV / 32];   // bit i: batch vertex i is the first vertex of a batch polygon
     unsigned char owner[kWV];
     // the current group of 32 polygons (lane = polygon), kept here rather than
     // in registers across the batches
@@ -113,9 +115,13 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
         } else {
             qy[k] = qm[k] = qp[k] = 0; // C1 / C2: the 30-bit key is formed on the exact path only
         }
-        // the key filters are exact only for |p.y| >= 2^-400 (pip_csr_common.cuh);
-        // bit 30 of nloop: the whole closed bbox is clear of that range
-        qok |= (uint32_t)(a && fast && ((tp.nloop >> 30 & 1u) || fabs(q.y) >= 0x1p-400)) << k;
+        qok |= (uint32_t)(a && fast) << k;
+    }
+    // the key filters are exact only for |p.y| >= 2^-400 (pip_csr_common.cuh);
+    // bit 30 of nloop: the polygon's whole closed bbox is clear of that range
+    if (fast && !(tp.nloop >> 30 & 1u)) {
+        if (!(fabs(qc[0].y) >= 0x1p-400)) qok &= ~1u;
+        if (!(fabs(qc[1].y) >= 0x1p-400)) qok &= ~2u;
     }
     if (!__any_sync(kFull, act != 0)) return 0;
     uint32_t par = 0, slow = act & ~qok, band = 0, err = 0;
@@ -216,7 +222,9 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
         // redo every candidate edge
         par = fpar & qok & ~band;
     }
+    int ns = 0; // undecided points of the step (the caller's adaptive mode)
     if (__any_sync(kFull, slow != 0)) {
+        ns = __popc(__ballot_sync(kFull, slow & 1u)) + __popc(__ballot_sync(kFull, slow >> 1 & 1u));
         // exact binary64 path, count_crossings_c1 (geometry.hpp:182-203), on the
         // undecided (point, edge) pairs: a point with only key ties redoes the
         // edges whose key range it ties (q == q_lo or q == q_hi); a point with a
@@ -314,7 +322,7 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
         const uint32_t e1 = __ballot_sync(kFull, (act & err) >> 1 & 1u);
         if (lane < 2) or_bits(aux_bits, tp.s + cc + 32 * lane, lane ? e1 : e0);
     }
-    return __popc(__ballot_sync(kFull, slow & 1u)) + __popc(__ballot_sync(kFull, slow >> 1 & 1u));
+    return ns;
 }
 
 template <int MODE>
@@ -344,8 +352,9 @@ __global__ void __launch_bounds__(kBThreads, 8) pip_csr_tile_kernel(
             vend = ring_off[r1] - vert_base;
             vo1 = r1 > r0 ? ring_off[r0 + 1] - vert_base : v0;
         }
-        // no points or no rings: nothing to classify (no rings -> nothing is inside)
-        const bool work = p < n_polys && e > s && r1 > r0;
+        // no points or no rings: nothing to classify (no rings -> nothing is inside;
+        // no vertices: an empty outer ring has an empty bbox -> nothing is inside)
+        const bool work = p < n_polys && e > s && r1 > r0 && vend > v0;
         const bool big = work && vend - v0 > (unsigned long long)kWV;
         if (big) defer_list[atomicAdd(defer_count, 1u)] = (uint32_t)p;
         ws.gs[lane] = s;
@@ -372,10 +381,13 @@ __global__ void __launch_bounds__(kBThreads, 8) pip_csr_tile_kernel(
             const uint32_t excl = cum - mine;
             const int k = __popc(batch & ((1u << lane) - 1u)); // compact index of this lane's polygon
             const uint32_t total = __shfl_sync(kFull, cum, 31 - __clz(batch));
-            if (lane < kWV / 32) ws.ring_end[lane] = 0u;
+            if (lane < kWV / 32) ws.ring_end[lane] = ws.starts[lane] = 0u;
+            __syncwarp();
             if (inb) {
                 ws.off[k] = excl;
+                ws.nvo[k] = ws.gnvo[lane];
                 ws.v0s[k] = ws.gv0[lane];
+                atomicOr(&ws.starts[excl >> 5], 1u << (excl & 31)); // distinct: every batch polygon has >= 1 vertex
             }
             __syncwarp();
             if (inb) { // ring ends
@@ -394,32 +406,56 @@ __global__ void __launch_bounds__(kBThreads, 8) pip_csr_tile_kernel(
             for (int u = 0; u < kWV / 32; ++u) {
                 const uint32_t i = lane + 32 * u;
                 if (i < total) {
-                    int o = 0; // owner: the last batch polygon whose first vertex is <= i
+                    // owner: the last batch polygon whose first vertex is <= i
+                    int o = __popc(ws.starts[u] & (0xffffffffu >> (31 - lane))) - 1;
 #pragma unroll
-                    for (int step = 16; step > 0; step >>= 1)
-                        if (o + step < nb && ws.off[o + step] <= i) o += step;
+                    for (int w = 0; w < u; ++w) o += __popc(ws.starts[w]);
                     ws.owner[i] = (unsigned char)o;
                     const unsigned long long v = ws.v0s[o] + (i - ws.off[o]);
                     ws.vert[i] = make_double2(vx[v], vy[v]);
                 }
             }
             __syncwarp();
-            // ---- 2. bbox of the outer ring (lane per polygon) and scaling ------------
-            if (inb) {
+            // ---- 2. bbox of the outer ring and scaling --------------------------------
+            {
+                // 2^floor(log2(32 / nb)) lanes per polygon, each a strided part of the
+                // outer ring, then a butterfly.  The reference's std::min / std::max
+                // (batch.hpp:121-133) pick the first of equal values; the only equal
+                // but distinguishable values are +0 / -0, which compare equal in the
+                // prefilter and give the same fast-path keys and signs (a zero origin
+                // only flips the sign of exact zero local coordinates).
+                const int lg = 31 - __clz(32 / nb);
+                const int kk = lane >> lg, sub = lane & ((1 << lg) - 1);
                 double bx0 = INFINITY, by0 = INFINITY, bx1 = -INFINITY, by1 = -INFINITY;
-                const uint32_t nvo = ws.gnvo[lane];
-                for (uint32_t i = excl; i < excl + nvo; ++i) {
-                    const double2 q = ws.vert[i];
-                    bx0 = q.x < bx0 ? q.x : bx0; // std::min(min_x, v.x)
-                    by0 = q.y < by0 ? q.y : by0;
-                    bx1 = bx1 < q.x ? q.x : bx1; // std::max(max_x, v.x)
-                    by1 = by1 < q.y ? q.y : by1;
+                if (kk < nb) {
+                    const uint32_t st = ws.off[kk], en = st + ws.nvo[kk];
+                    for (uint32_t i = st + sub; i < en; i += 1u << lg) {
+                        const double2 q = ws.vert[i];
+                        bx0 = q.x < bx0 ? q.x : bx0; // std::min(min_x, v.x)
+                        by0 = q.y < by0 ? q.y : by0;
+                        bx1 = bx1 < q.x ? q.x : bx1; // std::max(max_x, v.x)
+                        by1 = by1 < q.y ? q.y : by1;
+                    }
                 }
+                for (int o = 1; o < (1 << lg); o <<= 1) {
+                    const double x0 = __shfl_xor_sync(kFull, bx0, o), y0 = __shfl_xor_sync(kFull, by0, o);
+                    const double x1 = __shfl_xor_sync(kFull, bx1, o), y1 = __shfl_xor_sync(kFull, by1, o);
+                    bx0 = x0 < bx0 ? x0 : bx0;
+                    by0 = y0 < by0 ? y0 : by0;
+                    bx1 = bx1 < x1 ? x1 : bx1;
+                    by1 = by1 < y1 ? y1 : by1;
+                }
+                if (kk < nb && sub == 0) {
+                    ws.bp[kk].bx0 = bx0;
+                    ws.bp[kk].by0 = by0;
+                    ws.bp[kk].bx1 = bx1;
+                    ws.bp[kk].by1 = by1;
+                }
+            }
+            __syncwarp();
+            if (inb) {
                 BPoly& b = ws.bp[k];
-                b.bx0 = bx0;
-                b.by0 = by0;
-                b.bx1 = bx1;
-                b.by1 = by1;
+                const double bx0 = b.bx0, by0 = b.by0, bx1 = b.bx1, by1 = b.by1;
                 const double W = __dsub_rn(bx1, bx0), H = __dsub_rn(by1, by0);
                 bool fast = W >= 0x1p-300 && W <= 0x1p300 && H >= 0x1p-300 && H <= 0x1p300;
                 b.sx = fast ? pow2_below_inv(W) : 1.0;
