@@ -58,4 +58,14 @@ __device__ __forceinline__ void or_bits(uint32_t* plane, unsigned long long g0, 
     if (sh && (bits >> (32 - sh))) atomicOr(&plane[w + 1], bits >> (32 - sh));
 }
 
+// 64 consecutive bits (lo: points g0 .. g0+31, hi: g0+32 .. g0+63; warp-uniform)
+// into a bit plane: lanes 0..2 each OR one of the (at most) three words they touch
+__device__ __forceinline__ void or_bits64(uint32_t* plane, unsigned long long g0, uint32_t lo, uint32_t hi,
+                                          int lane) {
+    const unsigned sh = (unsigned)(g0 & 31);
+    // word lane of (hi:lo) << sh
+    const uint32_t w = lane == 0 ? lo << sh : lane == 1 ? __funnelshift_l(lo, hi, sh) : (sh ? hi >> (32 - sh) : 0u);
+    if (lane < 3 && w) atomicOr(&plane[(g0 >> 5) + lane], w);
+}
+
 } // namespace pcd

@@ -119,10 +119,10 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
     }
     // the key filters are exact only for |p.y| >= 2^-400 (pip_csr_common.cuh);
     // bit 30 of nloop: the polygon's whole closed bbox is clear of that range
-    if (fast && !(tp.nloop >> 30 & 1u)) {
-        if (!(fabs(qc[0].y) >= 0x1p-400)) qok &= ~1u;
-        if (!(fabs(qc[1].y) >= 0x1p-400)) qok &= ~2u;
-    }
+    // (integer form: |y| >= 2^-400 iff the high word without its sign is >= 0x26f00000)
+    if (!(tp.nloop >> 30 & 1u))
+        qok &= (uint32_t)((__double2hiint(qc[0].y) & 0x7fffffff) >= 0x26f00000) |
+               ((uint32_t)((__double2hiint(qc[1].y) & 0x7fffffff) >= 0x26f00000) << 1);
     if (!__any_sync(kFull, act != 0)) return 0;
     uint32_t par = 0, slow = act & ~qok, band = 0, err = 0;
     if (fast && walk_all) {
@@ -147,7 +147,8 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
         const uint32_t t0 = __float_as_uint(fmaf(ly[0], 0.5f, 1.0f)), t1 = __float_as_uint(fmaf(ly[1], 0.5f, 1.0f));
         const uint32_t Q = ((t0 >> 7) & 0x7ffeu) | ((t1 << 9) & 0x7ffe0000u) | 0x00010001u;
         uint32_t acc = 0u, tm = 0xffffffffu, bm = 0xffffffffu;
-        uint32_t dprev = Q - (uint32_t)ws.rec[e0].x, pprev = 0u;
+        const uint32_t dfirst = Q - (uint32_t)ws.rec[e0].x;
+        uint32_t dprev = dfirst, pprev = 0u;
         auto step2 = [&](uint32_t i, uint32_t j) { // records i, j (consecutive, or clamped repeats)
             const int4 fi = ws.rec[i], fj = ws.rec[j];
             const uint32_t di = Q - (uint32_t)fi.x, dj = Q - (uint32_t)fj.x;
@@ -162,18 +163,21 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
             pprev = pj;
         };
         // every stored vertex of the polygon (a ring's last vertex carries the
-        // no-toggle sentinel record); reads past the end re-read the last record
-        // (d ^ d = 0: no toggle, the same tie / band values)
-        const uint32_t last = e1 - 1u;
+        // no-toggle sentinel record) -- except a closed single ring's last vertex,
+        // which repeats the first: its edge closes with d(first) below; reads past
+        // the end re-read the last record (d ^ d = 0: no toggle, the same tie /
+        // band values)
+        const uint32_t stop = e0 + (tp.nloop & 0x3fffffffu), last = stop - 1u;
         uint32_t i = e0;
-        for (; i + 4 <= e1; i += 4) {
+        for (; i + 4 <= stop; i += 4) {
             step2(i, i + 1);
             step2(i + 2, i + 3);
         }
-        if (i < e1) {
+        if (i < stop) {
             step2(i, min(i + 1, last));
             step2(min(i + 2, last), min(i + 3, last));
         }
+        acc ^= (dprev ^ dfirst) & pprev; // the closing edge (a sentinel's pprev is +: no toggle)
         const uint32_t fpar = (acc >> 15 & 1u) | (acc >> 30 & 2u);
         band = ((uint32_t)((bm & 0xffffu) <= 0x3600u) | ((uint32_t)((bm >> 16) <= 0x3600u) << 1) |
                 (uint32_t)((tm & 0xffffu) <= 1u) | ((uint32_t)((tm >> 16) <= 1u) << 1)) & act;
@@ -316,11 +320,11 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
     }
     const uint32_t b0 = __ballot_sync(kFull, act & par & ~err & 1u);
     const uint32_t b1 = __ballot_sync(kFull, (act & par & ~err) >> 1 & 1u);
-    if (lane < 2) or_bits(inside_bits, tp.s + cc + 32 * lane, lane ? b1 : b0);
+    or_bits64(inside_bits, tp.s + cc, b0, b1, lane);
     if (MODE != kC1 && __any_sync(kFull, err != 0)) { // C2: Error (DegenerateEdge), Robust: Boundary
         const uint32_t e0 = __ballot_sync(kFull, act & err & 1u);
         const uint32_t e1 = __ballot_sync(kFull, (act & err) >> 1 & 1u);
-        if (lane < 2) or_bits(aux_bits, tp.s + cc + 32 * lane, lane ? e1 : e0);
+        or_bits64(aux_bits, tp.s + cc, e0, e1, lane);
     }
     return ns;
 }
@@ -535,10 +539,11 @@ __global__ void __launch_bounds__(kBThreads, 8) pip_csr_tile_kernel(
             uint32_t c = 0;
             double2 qn0, qn1;
             auto load = [&](int jj, uint32_t cc, double2& a0, double2& a1) {
-                const uint32_t n = ws.bp[jj].np;
+                // past the polygon's last point: re-read it (such lanes are inactive)
+                const uint32_t n1 = ws.bp[jj].np - 1u;
                 const double2* P = pts + ws.bp[jj].s;
-                a0 = cc + lane < n ? P[cc + lane] : make_double2(0.0, 0.0);
-                a1 = cc + 32 + lane < n ? P[cc + 32 + lane] : make_double2(0.0, 0.0);
+                a0 = P[min(cc + lane, n1)];
+                a1 = P[min(cc + 32 + lane, n1)];
             };
             load(0, 0, qn0, qn1);
             while (j < nb) {
