@@ -62,10 +62,11 @@ __device__ __forceinline__ void or_bits(uint32_t* plane, unsigned long long g0, 
 // into a bit plane: lanes 0..2 each OR one of the (at most) three words they touch
 __device__ __forceinline__ void or_bits64(uint32_t* plane, unsigned long long g0, uint32_t lo, uint32_t hi,
                                           int lane) {
-    const unsigned sh = (unsigned)(g0 & 31);
-    // word lane of (hi:lo) << sh
-    const uint32_t w = lane == 0 ? lo << sh : lane == 1 ? __funnelshift_l(lo, hi, sh) : (sh ? hi >> (32 - sh) : 0u);
-    if (lane < 3 && w) atomicOr(&plane[(g0 >> 5) + lane], w);
+    // word `lane` of (0 : hi : lo : 0) << sh, i.e. the high word of (b : a) << sh
+    // with (a, b) = (0, lo), (lo, hi), (hi, 0) for lanes 0, 1, 2
+    const uint32_t a = lane == 1 ? lo : hi, b = lane == 0 ? lo : hi;
+    const uint32_t w = __funnelshift_l(lane == 0 ? 0u : a, lane == 2 ? 0u : b, (unsigned)g0 & 31u);
+    if (lane < 3 && w) atomicOr(plane + (g0 >> 5) + lane, w);
 }
 
 } // namespace pcd

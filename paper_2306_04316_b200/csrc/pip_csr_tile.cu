@@ -330,7 +330,7 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kBThreads, 8) pip_csr_tile_kernel(
+__global__ void __launch_bounds__(kBThreads, 7) pip_csr_tile_kernel(
     const double2* __restrict__ pts, const unsigned long long* __restrict__ pt_off, unsigned long long n_polys,
     const double* __restrict__ vx, const double* __restrict__ vy, const unsigned long long* __restrict__ ring_off,
     const unsigned long long* __restrict__ poly_ring_off, unsigned long long pt_base, unsigned long long ring_base,
