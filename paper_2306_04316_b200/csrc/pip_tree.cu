@@ -9,8 +9,10 @@
 // each needs a side test.  Here a point's count comes from O(log^2 n)
 // comparisons instead:
 //
-//   keys      q(y) = trunc(RN(RN(y - o_y) s_y) 2^30) on the polygon-local map of
-//             DESIGN.md §3.4 (monotone); V = the sorted distinct vertex keys.
+//   keys      q(y) = trunc(RN(RN(y - o_y) s_y) 2^53) on the polygon-local map of
+//             DESIGN.md §3.4 (monotone, 64-bit); V = the sorted distinct vertex
+//             keys.  53 bits make a key tie (a point on a vertex's y, or within
+//             2^-53 local of it) rare even for 10^6 vertices.
 //             A point whose key is not a vertex key ("clean") straddles edge e
 //             iff q_lo(e) < q < q_hi(e) -- exactly the reference's
 //             f_prev * f_next <= 0 (§3.4, |p.y| >= 2^-400);
@@ -35,12 +37,14 @@
 //             rounding of the order, so only undecided edges can be out of
 //             order with respect to the point and all of them are evaluated.
 //   fallback  points with a key tie, |p.y| < 2^-400 or outside the local map
-//             are compacted and classified by the scan kernel.
+//             are compacted and classified literally (few) or by the scan
+//             kernel (many).
 #include "pip_kernels.h"
 
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <utility>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
@@ -68,16 +72,19 @@ __device__ __forceinline__ Map map_of(const unsigned long long* bbox_keys) {
     return m;
 }
 
-// 30-bit key of y on the local map (valid for y in the bbox; clamped otherwise)
-__device__ __forceinline__ uint32_t key30(double y, const Map& m) {
-    double t = __dmul_rn(__dmul_rn(__dsub_rn(y, m.y0), m.sy), 0x1p30);
+// 53-bit key of y on the local map (valid for y in the bbox; clamped otherwise):
+// trunc of the local y (in [0, 1)) scaled by 2^53, exact for local y >= 1/2 and
+// monotone everywhere, so a point ties a vertex key essentially only when it
+// sits on that vertex's y
+__device__ __forceinline__ uint64_t key53(double y, const Map& m) {
+    double t = __dmul_rn(__dmul_rn(__dsub_rn(y, m.y0), m.sy), 0x1p53);
     t = t > 0.0 ? t : 0.0;
-    t = t < 0x1p31 ? t : 0x1p31;
-    return (uint32_t)t;
+    t = t < 0x1.fffffffffffffp52 ? t : 0x1.fffffffffffffp52;
+    return (uint64_t)t;
 }
 
 // number of keys < v (lower_bound) / <= v (upper_bound) in V[0, m)
-__device__ __forceinline__ uint32_t lower_bound(const uint32_t* __restrict__ V, uint32_t m, uint32_t v) {
+__device__ __forceinline__ uint32_t lower_bound(const uint64_t* __restrict__ V, uint32_t m, uint64_t v) {
     uint32_t lo = 0, hi = m;
     while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
@@ -86,7 +93,7 @@ __device__ __forceinline__ uint32_t lower_bound(const uint32_t* __restrict__ V, 
     }
     return lo;
 }
-__device__ __forceinline__ uint32_t upper_bound(const uint32_t* __restrict__ V, uint32_t m, uint32_t v) {
+__device__ __forceinline__ uint32_t upper_bound(const uint64_t* __restrict__ V, uint32_t m, uint64_t v) {
     uint32_t lo = 0, hi = m;
     while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
@@ -109,10 +116,10 @@ __device__ __forceinline__ uint32_t ring_of(const unsigned long long* __restrict
 }
 
 __global__ void vkey_kernel(const double* __restrict__ vy, uint64_t nv, const unsigned long long* __restrict__ bbox_keys,
-                            uint32_t* __restrict__ vk) {
+                            uint64_t* __restrict__ vk) {
     const Map m = map_of(bbox_keys);
     for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nv; v += (uint64_t)gridDim.x * blockDim.x)
-        vk[v] = key30(vy[v], m);
+        vk[v] = key53(vy[v], m);
 }
 
 // canonical nodes of leaf range [lo, hi) in a tree of L leaves (node ids 1 ..
@@ -149,10 +156,11 @@ __device__ __forceinline__ void canonical_warp(uint32_t lo, uint32_t hi, uint32_
 template <bool kFill>
 __global__ void edges_kernel(const double* __restrict__ vx, const double* __restrict__ vy,
                              const unsigned long long* __restrict__ ring_off, uint32_t n_rings, uint64_t nv,
-                             const unsigned long long* __restrict__ bbox_keys, const uint32_t* __restrict__ V,
+                             const unsigned long long* __restrict__ bbox_keys, const uint64_t* __restrict__ V,
                              const uint32_t* __restrict__ m_dev, uint32_t L, uint32_t* __restrict__ cnt,
-                             const uint32_t* __restrict__ off, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                             uint32_t* __restrict__ node_of, double4* __restrict__ line) {
+                             const uint32_t* __restrict__ off, const uint32_t* __restrict__ khi,
+                             unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals,
+                             double4* __restrict__ line) {
     const Map mp = map_of(bbox_keys);
     const uint32_t m = *m_dev;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -166,7 +174,7 @@ __global__ void edges_kernel(const double* __restrict__ vx, const double* __rest
             if (v + 1 < ring_off[r + 1]) { // a ring's last vertex starts no edge
                 e = (uint32_t)(v - r);
                 const double ay = vy[v], by = vy[v + 1];
-                const uint32_t qa = key30(ay, mp), qb = key30(by, mp);
+                const uint64_t qa = key53(ay, mp), qb = key53(by, mp);
                 lo = lower_bound(V, m, min(qa, qb));
                 hi = lower_bound(V, m, max(qa, qb));
                 if (hi < lo) hi = lo; // (cannot happen: keys are monotone)
@@ -193,7 +201,7 @@ __global__ void edges_kernel(const double* __restrict__ vx, const double* __rest
                 base = __shfl_sync(same, base, __ffs(same) - 1);
                 const int d = 31 - __clz(nd);
                 const uint32_t span = L >> d, a = (nd - (1u << d)) * span, b = a + span;
-                const double ym = ((double)V[a] + (double)V[min(b, m - 1)]) * 0x1p-31; // middle, local units
+                const double ym = ((double)V[a] + (double)V[min(b, m - 1)]) * 0x1p-54; // middle, local units
                 // x at the middle as 32-bit fixed point: two edges the key misorders are
                 // within 2^-32 there, hence within 2^-31 over the whole range (the
                 // difference of two non-crossing segments is linear and keeps its sign)
@@ -202,9 +210,8 @@ __global__ void edges_kernel(const double* __restrict__ vx, const double* __rest
                 xm = xm < 4294967295.0 ? xm : 4294967295.0;
                 const uint32_t key = (uint32_t)xm;
                 const uint32_t slot = off[nd] + base + rank;
-                keys[slot] = key;
+                keys[slot] = (unsigned long long)khi[nd] << 32 | key; // (node or big-node rank, x)
                 vals[slot] = e;
-                node_of[slot] = nd;
             });
         }
     }
@@ -214,22 +221,24 @@ __global__ void edges_kernel(const double* __restrict__ vx, const double* __rest
 // pip_kernels.cu prep_edges_kernel), and the order check against the next
 // entry of the same node at both ends of the node's key range (x from the
 // edge's local line; a violation beyond 2^-30 flags the node)
-__global__ void verify_pack_kernel(const uint32_t* __restrict__ vals, const uint32_t* __restrict__ node_of,
-                                   const uint32_t* __restrict__ off, uint32_t L, const uint32_t* __restrict__ V,
-                                   const uint32_t* __restrict__ m_dev, const EdgeRec* __restrict__ rec,
-                                   const double4* __restrict__ line, float4* __restrict__ packed,
-                                   uint8_t* __restrict__ flag) {
-    const uint32_t m = *m_dev, total = off[2 * L];
+__global__ void verify_pack_kernel(const uint32_t* __restrict__ vals, const unsigned long long* __restrict__ keys,
+                                   const uint32_t* __restrict__ tot, const uint32_t* __restrict__ bignode, uint32_t L,
+                                   const uint64_t* __restrict__ V, const uint32_t* __restrict__ m_dev,
+                                   const EdgeRec* __restrict__ rec, const double4* __restrict__ line,
+                                   float4* __restrict__ packed, uint8_t* __restrict__ flag) {
+    const uint32_t m = *m_dev, ts = tot[0], total = tot[0] + tot[1];
+    // node of entry j: the key's high word is the node below ts, a big-node rank above
+    auto node = [&](uint32_t j) { const uint32_t h = (uint32_t)(keys[j] >> 32); return j < ts ? h : bignode[h]; };
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
         const uint32_t e0 = vals[i];
         const double d5 = rec[e0].d[5], d6 = rec[e0].d[6];
         packed[i] = make_float4(__int_as_float(__double2loint(d5)), __int_as_float(__double2hiint(d5)),
                                 __int_as_float(__double2loint(d6)), __uint_as_float(e0));
-        const uint32_t nd = node_of[i];
-        if (i + 1 >= total || node_of[i + 1] != nd) continue;
+        const uint32_t nd = node(i);
+        if (i + 1 >= total || node(i + 1) != nd) continue;
         const int d = 31 - __clz(nd);
         const uint32_t span = L >> d, a = (nd - (1u << d)) * span, b = min(a + span, m - 1);
-        const double y0 = (double)V[a] * 0x1p-30, y1 = (double)V[b] * 0x1p-30;
+        const double y0 = (double)V[a] * 0x1p-53, y1 = (double)V[b] * 0x1p-53;
         const double4 l0 = line[e0], l1 = line[vals[i + 1]];
         auto x = [](const double4& l, double y) { return __dadd_rn(l.x, __dmul_rn(__dsub_rn(y, l.y), l.z)); };
         if (x(l0, y0) > __dadd_rn(x(l1, y0), 0x1p-30) || x(l0, y1) > __dadd_rn(x(l1, y1), 0x1p-30)) flag[nd] = 1;
@@ -298,8 +307,9 @@ __device__ __forceinline__ uint32_t node_count(const float4* __restrict__ packed
 template <int MODE>
 __global__ void __launch_bounds__(256) query_kernel(const double2* __restrict__ pts, uint64_t n, int prefilter,
                                                     const unsigned long long* __restrict__ bbox_keys,
-                                                    const uint32_t* __restrict__ V, const uint32_t* __restrict__ m_dev,
+                                                    const uint64_t* __restrict__ V, const uint32_t* __restrict__ m_dev,
                                                     uint32_t L, const uint32_t* __restrict__ off,
+                                                    const uint32_t* __restrict__ cnt,
                                                     const float4* __restrict__ packed, const uint8_t* __restrict__ flag,
                                                     const EdgeRec* __restrict__ rec, uint32_t* __restrict__ inside_bits,
                                                     uint32_t* __restrict__ fb_idx, uint32_t* __restrict__ fb_count,
@@ -326,7 +336,7 @@ __global__ void __launch_bounds__(256) query_kernel(const double2* __restrict__ 
                 if (!ok) {
                     fb = true;
                 } else {
-                    const uint32_t q = (uint32_t)__dmul_rn(lyd, 0x1p30);
+                    const uint64_t q = (uint64_t)__dmul_rn(lyd, 0x1p53);
                     const uint32_t j = upper_bound(V, m, q); // keys <= q
                     if (j > 0 && __ldg(V + j - 1) == q) {
                         fb = true; // a vertex key: the exact straddle products decide
@@ -334,7 +344,7 @@ __global__ void __launch_bounds__(256) query_kernel(const double2* __restrict__ 
                         const float lx = __double2float_rn(lxd), ly = __double2float_rn(lyd);
                         uint32_t c = 0;
                         for (uint32_t nd = L + j - 1; nd; nd >>= 1) {
-                            const uint32_t o = __ldg(off + nd), k = __ldg(off + nd + 1) - o;
+                            const uint32_t o = __ldg(off + nd), k = __ldg(cnt + nd);
                             if (k) c += node_count<MODE>(packed, o, k, __ldg(flag + nd) != 0, rec, lx, ly, p.x, p.y);
                         }
                         in = c & 1u;
@@ -427,9 +437,48 @@ uint32_t tree_leaves(uint64_t nv) {
     return L;
 }
 
+// node lists of at most kSmallSeg entries are sorted by CUB's segmented sort
+// (warp-level merge sorts); the entries of bigger nodes sit after them and are
+// sorted by one device-wide radix sort on (big-node rank, x)
+constexpr uint32_t kSmallSeg = 64;
+
+__global__ void split_kernel(const uint32_t* __restrict__ cnt, uint32_t n, uint32_t* __restrict__ cs,
+                             uint32_t* __restrict__ cb, uint32_t* __restrict__ fb) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t c = cnt[i];
+        const bool big = c > kSmallSeg;
+        cs[i] = big ? 0u : c;
+        cb[i] = big ? c : 0u;
+        fb[i] = big;
+    }
+}
+
+// node offsets in the split layout, CUB segment ends (empty for big nodes), the
+// key high words and the big-node list; tot = {small entries, big entries, big nodes}
+__global__ void offsets_kernel(const uint32_t* __restrict__ cnt, uint32_t n, const uint32_t* __restrict__ os,
+                               const uint32_t* __restrict__ ob, const uint32_t* __restrict__ rb,
+                               uint32_t* __restrict__ off, uint32_t* __restrict__ seg_end, uint32_t* __restrict__ khi,
+                               uint32_t* __restrict__ bignode, uint32_t* __restrict__ tot) {
+    const uint32_t ts = os[n - 1]; // cnt[n - 1] == 0: the last exclusive sums are the totals
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t c = cnt[i];
+        const bool big = c > kSmallSeg;
+        off[i] = big ? ts + ob[i] : os[i];
+        seg_end[i] = big ? ts + ob[i] : os[i] + c;
+        khi[i] = big ? rb[i] : i;
+        if (big) bignode[rb[i]] = i;
+        if (i == 0) {
+            tot[0] = ts;
+            tot[1] = ob[n - 1];
+            tot[2] = rb[n - 1];
+        }
+    }
+}
+
 struct Layout {
     uint64_t nv, ne, L, emax;
-    size_t o_vk, o_V, o_m, o_cnt, o_off, o_keys, o_vals, o_keys2, o_vals2, o_node, o_packed, o_flag, o_fbidx, o_fbcnt,
+    size_t o_cs, o_cb, o_fb, o_os, o_ob, o_rb, o_end, o_khi, o_big, o_tot;
+    size_t o_vk, o_vs, o_V, o_m, o_cnt, o_off, o_keys, o_vals, o_keys2, o_vals2, o_packed, o_flag, o_fbidx, o_fbcnt,
         o_fbpts, o_fbbits, o_fbebits, o_line, o_tmp, tmp_bytes, total;
 };
 
@@ -444,29 +493,35 @@ Layout layout(uint64_t nv, uint64_t ne, uint64_t n_pts) {
     l.emax = std::max<uint64_t>(ne * 2ull * (depth + 1), nv);
     // CUB temporary storage: the largest of the four primitives
     size_t t1 = 0, t2 = 0, t3 = 0, t4 = 0;
-    cub::DeviceRadixSort::SortKeys(nullptr, t1, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)nv, 0, 32);
-    cub::DeviceSelect::Unique(nullptr, t2, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)nv);
+    cub::DeviceRadixSort::SortKeys(nullptr, t1, (uint64_t*)nullptr, (uint64_t*)nullptr, (int)nv, 0, 53);
+    cub::DeviceSelect::Unique(nullptr, t2, (uint64_t*)nullptr, (uint64_t*)nullptr, (uint32_t*)nullptr, (int)nv);
     cub::DeviceScan::ExclusiveSum(nullptr, t3, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)(2 * l.L + 1));
-    cub::DeviceSegmentedSort::SortPairs(nullptr, t4, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
-                                        (uint32_t*)nullptr, (int)l.emax, (int)(2 * l.L), (uint32_t*)nullptr,
-                                        (uint32_t*)nullptr);
-    l.tmp_bytes = std::max({t1, t2, t3, t4, (size_t)256});
+    cub::DeviceRadixSort::SortPairs(nullptr, t4, (unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                    (uint32_t*)nullptr, (uint32_t*)nullptr, (int)l.emax, 0, 64);
+    size_t t5 = 0;
+    cub::DeviceSegmentedSort::SortPairs(nullptr, t5, (unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                        (uint32_t*)nullptr, (uint32_t*)nullptr, (int)l.emax, (int)(2 * l.L),
+                                        (uint32_t*)nullptr, (uint32_t*)nullptr);
+    l.tmp_bytes = std::max({t1, t2, t3, t4, t5, (size_t)256});
     size_t o = 0;
     auto put = [&](size_t bytes) {
         const size_t at = o;
         o = align256(o + bytes);
         return at;
     };
-    l.o_vk = put(nv * 4);
-    l.o_V = put(nv * 4);
+    l.o_vk = put(nv * 8);
+    l.o_vs = put(nv * 8);
+    l.o_V = put(nv * 8);
     l.o_m = put(16);
     l.o_cnt = put((2 * l.L + 1) * 4);
     l.o_off = put((2 * l.L + 1) * 4);
-    l.o_keys = put(l.emax * 4);
+    for (size_t* o_split : {&l.o_cs, &l.o_cb, &l.o_fb, &l.o_os, &l.o_ob, &l.o_rb, &l.o_end, &l.o_khi, &l.o_big})
+        *o_split = put((2 * l.L + 1) * 4);
+    l.o_tot = put(16);
+    l.o_keys = put(l.emax * 8);
     l.o_vals = put(l.emax * 4);
-    l.o_keys2 = put(l.emax * 4);
+    l.o_keys2 = put(l.emax * 8);
     l.o_vals2 = put(l.emax * 4);
-    l.o_node = put(l.emax * 4);
     l.o_packed = put(l.emax * 16);
     l.o_flag = put(2 * l.L);
     l.o_fbidx = put(n_pts * 4 + 4);
@@ -495,16 +550,20 @@ size_t tree_scratch_bytes(uint64_t n_verts, uint64_t n_edges, uint64_t n_pts) {
 cudaError_t launch_tree(const TreeArgs& a, void* scratch, cudaStream_t st, int dev, uint64_t* launches) {
     const Layout l = layout(a.n_verts, a.n_edges, a.n);
     char* s = static_cast<char*>(scratch);
-    uint32_t* vk = reinterpret_cast<uint32_t*>(s + l.o_vk);
-    uint32_t* V = reinterpret_cast<uint32_t*>(s + l.o_V);
+    uint64_t* vk = reinterpret_cast<uint64_t*>(s + l.o_vk);
+    uint64_t* vs = reinterpret_cast<uint64_t*>(s + l.o_vs);
+    uint64_t* V = reinterpret_cast<uint64_t*>(s + l.o_V);
     uint32_t* m_dev = reinterpret_cast<uint32_t*>(s + l.o_m);
     uint32_t* cnt = reinterpret_cast<uint32_t*>(s + l.o_cnt);
     uint32_t* off = reinterpret_cast<uint32_t*>(s + l.o_off);
-    uint32_t* keys = reinterpret_cast<uint32_t*>(s + l.o_keys);
+    auto u32 = [&](size_t o) { return reinterpret_cast<uint32_t*>(s + o); };
+    uint32_t *cs = u32(l.o_cs), *cb = u32(l.o_cb), *fbig = u32(l.o_fb), *os = u32(l.o_os), *ob = u32(l.o_ob),
+             *rb = u32(l.o_rb), *seg_end = u32(l.o_end), *khi = u32(l.o_khi), *bignode = u32(l.o_big),
+             *tot = u32(l.o_tot);
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(s + l.o_keys);
     uint32_t* vals = reinterpret_cast<uint32_t*>(s + l.o_vals);
-    uint32_t* keys2 = reinterpret_cast<uint32_t*>(s + l.o_keys2);
+    unsigned long long* keys2 = reinterpret_cast<unsigned long long*>(s + l.o_keys2);
     uint32_t* vals2 = reinterpret_cast<uint32_t*>(s + l.o_vals2);
-    uint32_t* node_of = reinterpret_cast<uint32_t*>(s + l.o_node);
     float4* packed = reinterpret_cast<float4*>(s + l.o_packed);
     uint8_t* flag = reinterpret_cast<uint8_t*>(s + l.o_flag);
     uint32_t* fb_idx = reinterpret_cast<uint32_t*>(s + l.o_fbidx);
@@ -524,34 +583,51 @@ cudaError_t launch_tree(const TreeArgs& a, void* scratch, cudaStream_t st, int d
     if ((e = (x)) != cudaSuccess) return e
     // ---- build ----
     vkey_kernel<<<grid, 256, 0, st>>>(a.vy, a.n_verts, a.bbox_keys, vk);
-    PC_TRY(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, vk, keys, (int)a.n_verts, 0, 32, st));
+    PC_TRY(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, vk, vs, (int)a.n_verts, 0, 53, st));
     tmp_bytes = l.tmp_bytes;
-    PC_TRY(cub::DeviceSelect::Unique(tmp, tmp_bytes, keys, V, m_dev, (int)a.n_verts, st));
+    PC_TRY(cub::DeviceSelect::Unique(tmp, tmp_bytes, vs, V, m_dev, (int)a.n_verts, st));
     PC_TRY(cudaMemsetAsync(cnt, 0, (2 * l.L + 1) * 4, st));
     PC_TRY(cudaMemsetAsync(flag, 0, 2 * l.L, st));
     edges_kernel<false><<<grid, 256, 0, st>>>(a.vx, a.vy, ro, a.n_rings, a.n_verts, a.bbox_keys, V, m_dev, L, cnt,
                                               nullptr, nullptr, nullptr, nullptr, nullptr);
-    tmp_bytes = l.tmp_bytes;
-    PC_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, off, (int)(2 * l.L + 1), st));
+    const int n_nodes = (int)(2 * l.L + 1);
+    split_kernel<<<grid, 256, 0, st>>>(cnt, (uint32_t)n_nodes, cs, cb, fbig);
+    for (auto [in, out] : {std::pair{cs, os}, std::pair{cb, ob}, std::pair{fbig, rb}}) {
+        tmp_bytes = l.tmp_bytes;
+        PC_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, in, out, n_nodes, st));
+    }
+    offsets_kernel<<<grid, 256, 0, st>>>(cnt, (uint32_t)n_nodes, os, ob, rb, off, seg_end, khi, bignode, tot);
     PC_TRY(cudaMemsetAsync(cnt, 0, (2 * l.L + 1) * 4, st));
     edges_kernel<true><<<grid, 256, 0, st>>>(a.vx, a.vy, ro, a.n_rings, a.n_verts, a.bbox_keys, V, m_dev, L, cnt, off,
-                                             keys, vals, node_of, line);
-    tmp_bytes = l.tmp_bytes;
-    PC_TRY(cub::DeviceSegmentedSort::SortPairs(tmp, tmp_bytes, keys, keys2, vals, vals2, (int)l.emax, (int)(2 * l.L),
-                                               off, off + 1, st));
-    verify_pack_kernel<<<grid, 256, 0, st>>>(vals2, node_of, off, L, V, m_dev, rec, line, packed, flag);
+                                             khi, keys, vals, line);
+    // the split sizes come to the host (the sorts take them as item counts)
+    uint32_t h_tot[3] = {0, 0, 0};
+    PC_TRY(cudaMemcpyAsync(h_tot, tot, 12, cudaMemcpyDeviceToHost, st));
+    PC_TRY(cudaStreamSynchronize(st));
+    if (h_tot[0]) {
+        tmp_bytes = l.tmp_bytes;
+        PC_TRY(cub::DeviceSegmentedSort::SortPairs(tmp, tmp_bytes, keys, keys2, vals, vals2, (int)h_tot[0],
+                                                   n_nodes - 1, off, seg_end, st));
+    }
+    if (h_tot[1]) {
+        const int bits = 32 + (32 - __builtin_clz(std::max(h_tot[2], 1u)));
+        tmp_bytes = l.tmp_bytes;
+        PC_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys + h_tot[0], keys2 + h_tot[0], vals + h_tot[0],
+                                               vals2 + h_tot[0], (int)h_tot[1], 0, bits, st));
+    }
+    verify_pack_kernel<<<grid, 256, 0, st>>>(vals2, keys2, tot, bignode, L, V, m_dev, rec, line, packed, flag);
     // ---- query ----
     PC_TRY(cudaMemsetAsync(fb_cnt, 0, 4, st));
     const unsigned qgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((a.n + 255) / 256, (uint64_t)grid * 4));
     if (a.mode == kC1)
         query_kernel<kC1><<<qgrid, 256, 0, st>>>(reinterpret_cast<const double2*>(a.pts), a.n, a.prefilter, a.bbox_keys,
-                                                 V, m_dev, L, off, packed, flag, rec, a.inside_bits, fb_idx, fb_cnt,
+                                                 V, m_dev, L, off, cnt, packed, flag, rec, a.inside_bits, fb_idx, fb_cnt,
                                                  a.n_dev);
     else
         query_kernel<kC2><<<qgrid, 256, 0, st>>>(reinterpret_cast<const double2*>(a.pts), a.n, a.prefilter, a.bbox_keys,
-                                                 V, m_dev, L, off, packed, flag, rec, a.inside_bits, fb_idx, fb_cnt,
+                                                 V, m_dev, L, off, cnt, packed, flag, rec, a.inside_bits, fb_idx, fb_cnt,
                                                  a.n_dev);
-    *launches += 10;
+    *launches += 12;
     // ---- fallback points through the scan kernel, its grid sized for their number ----
     uint32_t n_fb = 0;
     PC_TRY(cudaMemcpyAsync(&n_fb, fb_cnt, 4, cudaMemcpyDeviceToHost, st));
