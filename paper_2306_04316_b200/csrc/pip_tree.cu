@@ -116,10 +116,25 @@ __device__ __forceinline__ uint32_t ring_of(const unsigned long long* __restrict
 }
 
 __global__ void vkey_kernel(const double* __restrict__ vy, uint64_t nv, const unsigned long long* __restrict__ bbox_keys,
-                            uint64_t* __restrict__ vk) {
+                            uint64_t* __restrict__ vk, uint32_t* __restrict__ vid) {
     const Map m = map_of(bbox_keys);
-    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nv; v += (uint64_t)gridDim.x * blockDim.x)
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nv; v += (uint64_t)gridDim.x * blockDim.x) {
         vk[v] = key53(vy[v], m);
+        vid[v] = (uint32_t)v;
+    }
+}
+
+// first occurrence of each key in the sorted keys (its inclusive sum is the rank + 1)
+__global__ void newkey_kernel(const uint64_t* __restrict__ vs, uint64_t nv, uint32_t* __restrict__ isnew) {
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < nv; p += (uint64_t)gridDim.x * blockDim.x)
+        isnew[p] = p == 0 || vs[p] != vs[p - 1];
+}
+
+// rank of every vertex's key among the distinct keys (= its leaf boundary index)
+__global__ void vrank_kernel(const uint32_t* __restrict__ csum, const uint32_t* __restrict__ vsid, uint64_t nv,
+                             uint32_t* __restrict__ vrank) {
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < nv; p += (uint64_t)gridDim.x * blockDim.x)
+        vrank[vsid[p]] = csum[p] - 1u;
 }
 
 // canonical nodes of leaf range [lo, hi) in a tree of L leaves (node ids 1 ..
@@ -156,8 +171,9 @@ __device__ __forceinline__ void canonical_warp(uint32_t lo, uint32_t hi, uint32_
 template <bool kFill>
 __global__ void edges_kernel(const double* __restrict__ vx, const double* __restrict__ vy,
                              const unsigned long long* __restrict__ ring_off, uint32_t n_rings, uint64_t nv,
-                             const unsigned long long* __restrict__ bbox_keys, const uint64_t* __restrict__ V,
-                             const uint32_t* __restrict__ m_dev, uint32_t L, uint32_t* __restrict__ cnt,
+                             const unsigned long long* __restrict__ bbox_keys, const uint32_t* __restrict__ vrank,
+                             const uint64_t* __restrict__ V, const uint32_t* __restrict__ m_dev, uint32_t L,
+                             uint32_t* __restrict__ cnt,
                              const uint32_t* __restrict__ off, const uint32_t* __restrict__ khi,
                              unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals,
                              double4* __restrict__ line) {
@@ -174,10 +190,10 @@ __global__ void edges_kernel(const double* __restrict__ vx, const double* __rest
             if (v + 1 < ring_off[r + 1]) { // a ring's last vertex starts no edge
                 e = (uint32_t)(v - r);
                 const double ay = vy[v], by = vy[v + 1];
-                const uint64_t qa = key53(ay, mp), qb = key53(by, mp);
-                lo = lower_bound(V, m, min(qa, qb));
-                hi = lower_bound(V, m, max(qa, qb));
-                if (hi < lo) hi = lo; // (cannot happen: keys are monotone)
+                // leaf range: the ranks of the endpoint keys among the distinct vertex keys
+                const uint32_t ra = vrank[v], rb = vrank[v + 1];
+                lo = min(ra, rb);
+                hi = max(ra, rb);
                 if (kFill && hi > lo) { // local endpoints for the x order at each node's middle
                     const double ax = vx[v], bx = vx[v + 1];
                     axl = __dmul_rn(__dsub_rn(ax, mp.x0), mp.sx);
@@ -229,19 +245,41 @@ __global__ void verify_pack_kernel(const uint32_t* __restrict__ vals, const unsi
     const uint32_t m = *m_dev, ts = tot[0], total = tot[0] + tot[1];
     // node of entry j: the key's high word is the node below ts, a big-node rank above
     auto node = [&](uint32_t j) { const uint32_t h = (uint32_t)(keys[j] >> 32); return j < ts ? h : bignode[h]; };
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-        const uint32_t e0 = vals[i];
-        const double d5 = rec[e0].d[5], d6 = rec[e0].d[6];
-        packed[i] = make_float4(__int_as_float(__double2loint(d5)), __int_as_float(__double2hiint(d5)),
-                                __int_as_float(__double2loint(d6)), __uint_as_float(e0));
-        const uint32_t nd = node(i);
-        if (i + 1 >= total || node(i + 1) != nd) continue;
-        const int d = 31 - __clz(nd);
-        const uint32_t span = L >> d, a = (nd - (1u << d)) * span, b = min(a + span, m - 1);
-        const double y0 = (double)V[a] * 0x1p-53, y1 = (double)V[b] * 0x1p-53;
-        const double4 l0 = line[e0], l1 = line[vals[i + 1]];
-        auto x = [](const double4& l, double y) { return __dadd_rn(l.x, __dmul_rn(__dsub_rn(y, l.y), l.z)); };
-        if (x(l0, y0) > __dadd_rn(x(l1, y0), 0x1p-30) || x(l0, y1) > __dadd_rn(x(l1, y1), 0x1p-30)) flag[nd] = 1;
+    auto x = [](const double4& l, double y) { return __dadd_rn(l.x, __dmul_rn(__dsub_rn(y, l.y), l.z)); };
+    const unsigned lane = threadIdx.x & 31;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    // whole warps step together: entry i + 1 is the next lane's entry, so its node
+    // and its x at this node's ends come by shuffle (lane 31 computes its own)
+    for (uint32_t i0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; i0 < total; i0 += stride) {
+        const uint32_t i = i0 + lane;
+        uint32_t nd = 0xffffffffu, e0 = 0;
+        double x0 = 0.0, x1 = 0.0, y0 = 0.0, y1 = 0.0;
+        if (i < total) {
+            e0 = vals[i];
+            const double d5 = rec[e0].d[5], d6 = rec[e0].d[6];
+            packed[i] = make_float4(__int_as_float(__double2loint(d5)), __int_as_float(__double2hiint(d5)),
+                                    __int_as_float(__double2loint(d6)), __uint_as_float(e0));
+            nd = node(i);
+            const int d = 31 - __clz(nd);
+            const uint32_t span = L >> d, a = (nd - (1u << d)) * span, b = min(a + span, m - 1);
+            y0 = (double)V[a] * 0x1p-53;
+            y1 = (double)V[b] * 0x1p-53;
+            const double4 l0 = line[e0];
+            x0 = x(l0, y0);
+            x1 = x(l0, y1);
+        }
+        uint32_t nd1 = __shfl_down_sync(0xffffffffu, nd, 1);
+        double n0 = __shfl_down_sync(0xffffffffu, x0, 1), n1 = __shfl_down_sync(0xffffffffu, x1, 1);
+        if (lane == 31 && i + 1 < total) {
+            nd1 = node(i + 1);
+            if (nd1 == nd) {
+                const double4 l1 = line[vals[i + 1]];
+                n0 = x(l1, y0);
+                n1 = x(l1, y1);
+            }
+        }
+        // consecutive entries of one node must stay ordered within 2^-30 at both ends
+        if (i + 1 < total && nd1 == nd && (x0 > __dadd_rn(n0, 0x1p-30) || x1 > __dadd_rn(n1, 0x1p-30))) flag[nd] = 1;
     }
 }
 
@@ -478,7 +516,7 @@ __global__ void offsets_kernel(const uint32_t* __restrict__ cnt, uint32_t n, con
 struct Layout {
     uint64_t nv, ne, L, emax;
     size_t o_cs, o_cb, o_fb, o_os, o_ob, o_rb, o_end, o_khi, o_big, o_tot;
-    size_t o_vk, o_vs, o_V, o_m, o_cnt, o_off, o_keys, o_vals, o_keys2, o_vals2, o_packed, o_flag, o_fbidx, o_fbcnt,
+    size_t o_vk, o_vs, o_vid, o_vsid, o_vrank, o_V, o_m, o_cnt, o_off, o_keys, o_vals, o_keys2, o_vals2, o_packed, o_flag, o_fbidx, o_fbcnt,
         o_fbpts, o_fbbits, o_fbebits, o_line, o_tmp, tmp_bytes, total;
 };
 
@@ -493,7 +531,11 @@ Layout layout(uint64_t nv, uint64_t ne, uint64_t n_pts) {
     l.emax = std::max<uint64_t>(ne * 2ull * (depth + 1), nv);
     // CUB temporary storage: the largest of the four primitives
     size_t t1 = 0, t2 = 0, t3 = 0, t4 = 0;
-    cub::DeviceRadixSort::SortKeys(nullptr, t1, (uint64_t*)nullptr, (uint64_t*)nullptr, (int)nv, 0, 53);
+    cub::DeviceRadixSort::SortPairs(nullptr, t1, (uint64_t*)nullptr, (uint64_t*)nullptr, (uint32_t*)nullptr,
+                                    (uint32_t*)nullptr, (int)nv, 0, 53);
+    size_t t6 = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, t6, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)nv);
+    t1 = std::max(t1, t6);
     cub::DeviceSelect::Unique(nullptr, t2, (uint64_t*)nullptr, (uint64_t*)nullptr, (uint32_t*)nullptr, (int)nv);
     cub::DeviceScan::ExclusiveSum(nullptr, t3, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)(2 * l.L + 1));
     cub::DeviceRadixSort::SortPairs(nullptr, t4, (unsigned long long*)nullptr, (unsigned long long*)nullptr,
@@ -511,6 +553,9 @@ Layout layout(uint64_t nv, uint64_t ne, uint64_t n_pts) {
     };
     l.o_vk = put(nv * 8);
     l.o_vs = put(nv * 8);
+    l.o_vid = put(nv * 4);
+    l.o_vsid = put(nv * 4);
+    l.o_vrank = put(nv * 4);
     l.o_V = put(nv * 8);
     l.o_m = put(16);
     l.o_cnt = put((2 * l.L + 1) * 4);
@@ -552,6 +597,9 @@ cudaError_t launch_tree(const TreeArgs& a, void* scratch, cudaStream_t st, int d
     char* s = static_cast<char*>(scratch);
     uint64_t* vk = reinterpret_cast<uint64_t*>(s + l.o_vk);
     uint64_t* vs = reinterpret_cast<uint64_t*>(s + l.o_vs);
+    uint32_t* vid = reinterpret_cast<uint32_t*>(s + l.o_vid);
+    uint32_t* vsid = reinterpret_cast<uint32_t*>(s + l.o_vsid);
+    uint32_t* vrank = reinterpret_cast<uint32_t*>(s + l.o_vrank);
     uint64_t* V = reinterpret_cast<uint64_t*>(s + l.o_V);
     uint32_t* m_dev = reinterpret_cast<uint32_t*>(s + l.o_m);
     uint32_t* cnt = reinterpret_cast<uint32_t*>(s + l.o_cnt);
@@ -582,13 +630,19 @@ cudaError_t launch_tree(const TreeArgs& a, void* scratch, cudaStream_t st, int d
 #define PC_TRY(x)                                                                                                      \
     if ((e = (x)) != cudaSuccess) return e
     // ---- build ----
-    vkey_kernel<<<grid, 256, 0, st>>>(a.vy, a.n_verts, a.bbox_keys, vk);
-    PC_TRY(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, vk, vs, (int)a.n_verts, 0, 53, st));
+    vkey_kernel<<<grid, 256, 0, st>>>(a.vy, a.n_verts, a.bbox_keys, vk, vid);
+    PC_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, vk, vs, vid, vsid, (int)a.n_verts, 0, 53, st));
     tmp_bytes = l.tmp_bytes;
     PC_TRY(cub::DeviceSelect::Unique(tmp, tmp_bytes, vs, V, m_dev, (int)a.n_verts, st));
+    // vertex ranks among the distinct keys (vid is free again: first-occurrence flags, then their sums)
+    newkey_kernel<<<grid, 256, 0, st>>>(vs, a.n_verts, vid);
+    tmp_bytes = l.tmp_bytes;
+    PC_TRY(cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, vid, vrank, (int)a.n_verts, st));
+    vrank_kernel<<<grid, 256, 0, st>>>(vrank, vsid, a.n_verts, vid);
+    uint32_t* const vr = vid;
     PC_TRY(cudaMemsetAsync(cnt, 0, (2 * l.L + 1) * 4, st));
     PC_TRY(cudaMemsetAsync(flag, 0, 2 * l.L, st));
-    edges_kernel<false><<<grid, 256, 0, st>>>(a.vx, a.vy, ro, a.n_rings, a.n_verts, a.bbox_keys, V, m_dev, L, cnt,
+    edges_kernel<false><<<grid, 256, 0, st>>>(a.vx, a.vy, ro, a.n_rings, a.n_verts, a.bbox_keys, vr, V, m_dev, L, cnt,
                                               nullptr, nullptr, nullptr, nullptr, nullptr);
     const int n_nodes = (int)(2 * l.L + 1);
     split_kernel<<<grid, 256, 0, st>>>(cnt, (uint32_t)n_nodes, cs, cb, fbig);
@@ -598,7 +652,7 @@ cudaError_t launch_tree(const TreeArgs& a, void* scratch, cudaStream_t st, int d
     }
     offsets_kernel<<<grid, 256, 0, st>>>(cnt, (uint32_t)n_nodes, os, ob, rb, off, seg_end, khi, bignode, tot);
     PC_TRY(cudaMemsetAsync(cnt, 0, (2 * l.L + 1) * 4, st));
-    edges_kernel<true><<<grid, 256, 0, st>>>(a.vx, a.vy, ro, a.n_rings, a.n_verts, a.bbox_keys, V, m_dev, L, cnt, off,
+    edges_kernel<true><<<grid, 256, 0, st>>>(a.vx, a.vy, ro, a.n_rings, a.n_verts, a.bbox_keys, vr, V, m_dev, L, cnt, off,
                                              khi, keys, vals, line);
     // the split sizes come to the host (the sorts take them as item counts)
     uint32_t h_tot[3] = {0, 0, 0};
@@ -627,7 +681,7 @@ cudaError_t launch_tree(const TreeArgs& a, void* scratch, cudaStream_t st, int d
         query_kernel<kC2><<<qgrid, 256, 0, st>>>(reinterpret_cast<const double2*>(a.pts), a.n, a.prefilter, a.bbox_keys,
                                                  V, m_dev, L, off, cnt, packed, flag, rec, a.inside_bits, fb_idx, fb_cnt,
                                                  a.n_dev);
-    *launches += 12;
+    *launches += 15;
     // ---- fallback points through the scan kernel, its grid sized for their number ----
     uint32_t n_fb = 0;
     PC_TRY(cudaMemcpyAsync(&n_fb, fb_cnt, 4, cudaMemcpyDeviceToHost, st));
