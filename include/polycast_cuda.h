@@ -206,8 +206,9 @@ uint64_t pc_last_launch_count(const pc_ctx* ctx);
 int pc_set_option(pc_ctx* ctx, int option, int64_t value);
 
 /* Measurement hooks (bench.py).  With profiling on, every call records a pair
- * of CUDA events around its main classify kernel, on the stream that kernel is
- * launched on.  pc_profile_take() waits for the pairs recorded on device
+ * of CUDA events around its main classify kernel(s), on the stream they are
+ * launched on (the segment-tree path: the build and the query, reported as one
+ * duration).  pc_profile_take() waits for the pairs recorded on device
  * `dev_index` since the previous take, writes up to `cap` kernel durations
  * (ms) to ms_out, clears them and returns how many there were. */
 int pc_set_profiling(pc_ctx* ctx, int on);

@@ -43,6 +43,8 @@ struct DevBuf {
 struct DevState {
     int dev = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t copy = nullptr; // points upload, overlapping polygon-only work on `stream` (made on first use)
+    std::vector<cudaEvent_t> up_evs; // one per uploaded chunk
     DevBuf pts, vx, vy, ring_off, pt_off, poly_ring_off, filt, rec, bbox, bits, verdicts, stats, counts, degen;
     DevBuf bucket_scratch, sorted_pts, sorted_idx, bucket_blk; // y-bucketing (pip_sort.cu)
     DevBuf csr_meta;                                          // per-polygon records (pip_csr.cu)
@@ -54,10 +56,14 @@ struct DevState {
     pch::Stager* stager = nullptr;         // pageable host copies (host_stage.h), made on first use
     // profiling: one event pair per main-kernel launch since the last take
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
+    std::vector<uint8_t> ev_cont; // pair i continues pair i - 1 (one logical measurement)
     size_t ev_used = 0;
 };
 
 } // namespace
+
+// points per upload chunk of a big single-polygon shard (128 MB)
+constexpr uint64_t kUploadChunk = 1ull << 23;
 
 struct pc_ctx {
     std::vector<DevState> devs;
@@ -111,14 +117,17 @@ void validate_rings(pc_ctx* c, const uint64_t* ring_off, uint64_t n_rings) {
         if (ring_off[r + 1] <= ring_off[r]) invalid(c, "every ring needs at least one vertex (ring_off must increase)");
 }
 
-void mark_begin(pc_ctx* c, DevState& d, cudaStream_t st) {
+// cont: this pair continues the previous one (pc_profile_take reports their sum)
+void mark_begin(pc_ctx* c, DevState& d, cudaStream_t st, bool cont = false) {
     if (!c->profiling) return;
     if (d.ev_used == d.evs.size()) {
         cudaEvent_t a, b;
         check(c, cudaEventCreate(&a), "event");
         check(c, cudaEventCreate(&b), "event");
         d.evs.emplace_back(a, b);
+        d.ev_cont.push_back(0);
     }
+    d.ev_cont[d.ev_used] = cont;
     check(c, cudaEventRecord(d.evs[d.ev_used].first, st), "event record");
 }
 
@@ -133,7 +142,12 @@ void mark_end(pc_ctx* c, DevState& d, cudaStream_t st) {
 void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts, uint64_t n, const double* d_vx,
                     const double* d_vy, const uint64_t* d_ring_off, uint32_t n_rings, uint64_t n_verts, int mode,
                     double tol, int prefilter, uint8_t* d_verdicts, uint32_t* d_inside, uint32_t* d_aux,
-                    unsigned long long* d_stats) {
+                    unsigned long long* d_stats, const cudaEvent_t* ready = nullptr, uint64_t chunk = 0) {
+    // ready (nullable): the points are still being uploaded on another stream,
+    // in chunks of `chunk` points (0: one piece), ready[k] recorded after chunk
+    // k; everything that reads only the polygon (prep, the segment-tree build)
+    // is enqueued before the first wait, so it overlaps the upload, and chunk k
+    // is classified while chunk k + 1 uploads
     const uint64_t n_edges = n_verts - n_rings;
     if (n_edges > 0xffffffffull) invalid(c, "too many edges for one polygon (>= 2^32)");
     const uint64_t nwords = (n + 31) / 32;
@@ -175,32 +189,11 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
     sa.aux_bits = d_aux;
     sa.n_dev = nullptr;
     uint32_t* hist = nullptr;
-    if (bucket) {
-        const size_t hist_words = pcd::kBuckets + 2;
-        check(c, d.bucket_scratch.ensure((hist_words + 2 * nwords) * 4), "alloc bucket scratch");
-        check(c, d.sorted_pts.ensure(n * 16), "alloc bucketed points");
-        check(c, d.sorted_idx.ensure(n * 4), "alloc bucket index");
-        hist = d.bucket_scratch.as<uint32_t>();
-        check(c, cudaMemsetAsync(hist, 0, (hist_words + 2 * nwords) * 4, st), "clear bucket scratch");
-        const int n_blk = pcd::bucket_blocks(n, d.dev);
-        check(c, d.bucket_blk.ensure((size_t)n_blk * (pcd::kBuckets + 1) * 4), "alloc bucket counts");
-        pcd::BucketArgs ba{d_pts, n, d.bbox.as<unsigned long long>(), prefilter, hist, d.sorted_pts.as<double>(),
-                           d.sorted_idx.as<uint32_t>(), d.bucket_blk.as<uint32_t>(), n_blk};
-        check(c, pcd::launch_bucket(ba, st, d.dev, &c->launches), "bucket kernels");
-        sa.pts = d.sorted_pts.as<double>();
-        sa.prefilter = 0; // rejected points were left out of the bucketed prefix
-        sa.inside_bits = hist + hist_words;
-        sa.aux_bits = hist + hist_words + nwords;
-        sa.n_dev = hist + pcd::kBuckets + 1;
-    }
-    if (tree) { // segment-tree counts; key-tie / off-map points through the scan kernel
-        // (y-bucketed points: a warp's queries walk nearby leaves, sharing nodes)
-        pcd::TreeArgs ta{};
+    pcd::TreeArgs ta{};
+    if (tree) { // segment-tree build (polygon only)
         ta.mode = mode;
-        ta.pts = sa.pts;
         ta.n = n;
-        ta.n_dev = sa.n_dev;
-        ta.prefilter = sa.prefilter;
+        ta.n_layout = chunk && chunk < n ? chunk : n; // per-chunk fallback buffers
         ta.vx = d_vx;
         ta.vy = d_vy;
         ta.ring_off = d_ring_off;
@@ -209,29 +202,65 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
         ta.n_edges = n_edges;
         ta.rec = d.rec.p;
         ta.bbox_keys = d.bbox.as<unsigned long long>();
-        ta.inside_bits = sa.inside_bits;
-        ta.aux_bits = sa.aux_bits;
-        ta.single = sa;
-        ta.single.n_dev = nullptr;
-        check(c, d.tree.ensure(pcd::tree_scratch_bytes(n_verts, n_edges, n)), "alloc segment tree");
+        check(c, d.tree.ensure(pcd::tree_scratch_bytes(n_verts, n_edges, ta.n_layout)), "alloc segment tree");
         mark_begin(c, d, st);
-        check(c, pcd::launch_tree(ta, d.tree.p, st, d.dev, &c->launches), "segment-tree kernels");
+        check(c, pcd::launch_tree_phase(ta, d.tree.p, st, d.dev, &c->launches, pcd::kTreeBuild), "segment-tree build");
         mark_end(c, d, st);
-        if (bucket)
-            check(c, pcd::launch_unbucket(n, sa.n_dev, d.sorted_idx.as<uint32_t>(), sa.inside_bits, sa.aux_bits,
-                                          d_inside, d_aux, st, d.dev, &c->launches),
-                  "unbucket kernel");
-        check(c, pcd::launch_finalize(n, d_inside, d_aux, d_verdicts, mode, d_stats, st, d.dev, &c->launches),
-              "finalize kernel");
-        return;
     }
-    mark_begin(c, d, st);
-    check(c, pcd::launch_single(sa, st, d.dev, &c->launches), "classify kernel");
-    mark_end(c, d, st);
-    if (bucket)
-        check(c, pcd::launch_unbucket(n, sa.n_dev, d.sorted_idx.as<uint32_t>(), sa.inside_bits, sa.aux_bits, d_inside,
-                                      d_aux, st, d.dev, &c->launches),
-              "unbucket kernel");
+    // the points in chunks of `chunk` (one chunk when the caller uploads them in one
+    // piece): chunk k waits for its upload event, then bucket -> classify ->
+    // unbucket on its own range of the bit planes (chunks are 32-point aligned)
+    const uint64_t cn = chunk && chunk < n ? chunk : n;
+    for (uint64_t lo = 0, k = 0; lo < n; lo += cn, ++k) {
+        const uint64_t m = std::min(cn, n - lo), mw = (m + 31) / 32;
+        if (ready) check(c, cudaStreamWaitEvent(st, ready[k], 0), "wait for the points upload");
+        pcd::SingleArgs sc = sa;
+        sc.pts = d_pts + 2 * lo;
+        sc.n = m;
+        sc.inside_bits = d_inside + lo / 32;
+        sc.aux_bits = d_aux + lo / 32;
+        if (bucket) {
+            const size_t hist_words = pcd::kBuckets + 2;
+            check(c, d.bucket_scratch.ensure((hist_words + 2 * mw) * 4), "alloc bucket scratch");
+            check(c, d.sorted_pts.ensure(m * 16), "alloc bucketed points");
+            check(c, d.sorted_idx.ensure(m * 4), "alloc bucket index");
+            hist = d.bucket_scratch.as<uint32_t>();
+            check(c, cudaMemsetAsync(hist, 0, (hist_words + 2 * mw) * 4, st), "clear bucket scratch");
+            const int n_blk = pcd::bucket_blocks(m, d.dev);
+            check(c, d.bucket_blk.ensure((size_t)n_blk * (pcd::kBuckets + 1) * 4), "alloc bucket counts");
+            pcd::BucketArgs ba{sc.pts, m, d.bbox.as<unsigned long long>(), prefilter, hist, d.sorted_pts.as<double>(),
+                               d.sorted_idx.as<uint32_t>(), d.bucket_blk.as<uint32_t>(), n_blk};
+            check(c, pcd::launch_bucket(ba, st, d.dev, &c->launches), "bucket kernels");
+            sc.pts = d.sorted_pts.as<double>();
+            sc.prefilter = 0; // rejected points were left out of the bucketed prefix
+            sc.inside_bits = hist + hist_words;
+            sc.aux_bits = hist + hist_words + mw;
+            sc.n_dev = hist + pcd::kBuckets + 1;
+        }
+        if (tree) { // segment-tree counts; key-tie / off-map points through the scan kernel
+            // (y-bucketed points: a warp's queries walk nearby leaves, sharing nodes)
+            ta.pts = sc.pts;
+            ta.n = m;
+            ta.n_dev = sc.n_dev;
+            ta.prefilter = sc.prefilter;
+            ta.inside_bits = sc.inside_bits;
+            ta.aux_bits = sc.aux_bits;
+            ta.single = sc;
+            ta.single.n_dev = nullptr;
+            mark_begin(c, d, st, true); // one measurement with the build
+            check(c, pcd::launch_tree_phase(ta, d.tree.p, st, d.dev, &c->launches, pcd::kTreeQuery),
+                  "segment-tree query");
+            mark_end(c, d, st);
+        } else {
+            mark_begin(c, d, st, k > 0);
+            check(c, pcd::launch_single(sc, st, d.dev, &c->launches), "classify kernel");
+            mark_end(c, d, st);
+        }
+        if (bucket)
+            check(c, pcd::launch_unbucket(m, sc.n_dev, d.sorted_idx.as<uint32_t>(), sc.inside_bits, sc.aux_bits,
+                                          d_inside + lo / 32, d_aux + lo / 32, st, d.dev, &c->launches),
+                  "unbucket kernel");
+    }
     check(c, pcd::launch_finalize(n, d_inside, d_aux, d_verdicts, mode, d_stats, st, d.dev, &c->launches),
           "finalize kernel");
 }
@@ -366,6 +395,8 @@ void pc_destroy(pc_ctx* c) {
             cudaEventDestroy(e.first);
             cudaEventDestroy(e.second);
         }
+        if (d.copy) cudaStreamDestroy(d.copy);
+        for (cudaEvent_t e : d.up_evs) cudaEventDestroy(e);
         cudaStreamDestroy(d.stream);
     }
     delete c;
@@ -409,6 +440,10 @@ int pc_profile_take(pc_ctx* c, int dev_index, double* ms_out, int cap) {
             cudaEventElapsedTime(&ms, d.evs[i].first, d.evs[i].second) != cudaSuccess) {
             cudaGetLastError();
             ms = -1.0f;
+        }
+        if (d.ev_cont[i] && k > 0) {
+            if (k - 1 < cap && ms_out) ms_out[k - 1] += ms;
+            continue;
         }
         if (k < cap && ms_out) ms_out[k] = ms;
         ++k;
@@ -476,10 +511,28 @@ int pc_classify(pc_ctx* c, const double* pts_xy, uint64_t n, const double* vx, c
             const uint64_t m = parts[i].hi - parts[i].lo, nwords = (m + 31) / 32;
             check(c, cudaSetDevice(d.dev), "cudaSetDevice");
             cudaStream_t st = d.stream;
-            h2d(c, d, d.pts, pts_xy + 2 * parts[i].lo, m * 16, st, "upload points");
+            // polygon first on the compute stream; the points on the copy stream, so
+            // prep and the segment-tree build run while they upload (an async
+            // copy for pinned points; pageable ones are staged by this thread)
             h2d(c, d, d.vx, vx, n_verts * 8, st, "upload vx");
             h2d(c, d, d.vy, vy, n_verts * 8, st, "upload vy");
             h2d(c, d, d.ring_off, ring_off, (n_rings + 1) * 8ull, st, "upload ring_off");
+            if (!d.copy) check(c, cudaStreamCreateWithFlags(&d.copy, cudaStreamNonBlocking), "create copy stream");
+            // big shards upload in chunks, each classified while the next one uploads
+            const uint64_t chunk = m > 2 * kUploadChunk ? kUploadChunk : 0;
+            const uint64_t nchunks = chunk ? (m + chunk - 1) / chunk : 1;
+            while (d.up_evs.size() < nchunks) {
+                cudaEvent_t ev;
+                check(c, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "create upload event");
+                d.up_evs.push_back(ev);
+            }
+            check(c, d.pts.ensure(std::max<uint64_t>(m * 16, 16)), "upload points");
+            for (uint64_t k = 0; k < nchunks; ++k) {
+                const uint64_t lo = k * (chunk ? chunk : m), cnt = std::min(chunk ? chunk : m, m - lo);
+                check(c, stager(d).h2d(d.pts.as<double>() + 2 * lo, pts_xy + 2 * (parts[i].lo + lo), cnt * 16, d.copy),
+                      "upload points");
+                check(c, cudaEventRecord(d.up_evs[k], d.copy), "record upload event");
+            }
             check(c, d.bits.ensure(2 * nwords * 4), "alloc bit planes");
             check(c, d.stats.ensure(4 * 8), "alloc stats");
             uint8_t* dv = nullptr;
@@ -491,7 +544,7 @@ int pc_classify(pc_ctx* c, const double* pts_xy, uint64_t n, const double* vx, c
             uint32_t* daux = din + nwords;
             enqueue_single(c, d, st, d.pts.as<double>(), m, d.vx.as<double>(), d.vy.as<double>(),
                            d.ring_off.as<uint64_t>(), n_rings, n_verts, mode, tol, prefilter, dv, din, daux,
-                           d.stats.as<unsigned long long>());
+                           d.stats.as<unsigned long long>(), d.up_evs.data(), chunk);
             if (inside_bits)
                 check(c, cudaMemcpyAsync(inside_bits + parts[i].lo / 32, din, nwords * 4, cudaMemcpyDeviceToHost, st),
                       "download inside plane");

@@ -99,6 +99,7 @@ struct TreeArgs {
     int mode; // kC1 or kC2
     const double* pts;
     uint64_t n;
+    uint64_t n_layout;     // points the scratch layout is sized for (>= n; 0: n) -- the same in both phases
     const uint32_t* n_dev; // optional device-side point count (y-bucketed input)
     int prefilter;
     const double* vx;
@@ -115,6 +116,11 @@ struct TreeArgs {
 bool tree_eligible(uint64_t n_verts, uint64_t n_pts, bool forced);
 size_t tree_scratch_bytes(uint64_t n_verts, uint64_t n_edges, uint64_t n_pts);
 cudaError_t launch_tree(const TreeArgs& a, void* scratch, cudaStream_t st, int dev, uint64_t* launches);
+// the two halves of launch_tree: the build (polygon only) and the query (points);
+// the query phase must follow the build phase on the same scratch
+constexpr int kTreeBuild = 1, kTreeQuery = 2;
+cudaError_t launch_tree_phase(const TreeArgs& a, void* scratch, cudaStream_t st, int dev, uint64_t* launches,
+                              int phase);
 
 // GPU results-CSV writer (pip_emit.cu): recs = n 32-byte records
 // (pc_result_record); out gets the header and the rows (at most cap bytes

@@ -593,7 +593,14 @@ size_t tree_scratch_bytes(uint64_t n_verts, uint64_t n_edges, uint64_t n_pts) {
 }
 
 cudaError_t launch_tree(const TreeArgs& a, void* scratch, cudaStream_t st, int dev, uint64_t* launches) {
-    const Layout l = layout(a.n_verts, a.n_edges, a.n);
+    const cudaError_t e = launch_tree_phase(a, scratch, st, dev, launches, kTreeBuild);
+    return e != cudaSuccess ? e : launch_tree_phase(a, scratch, st, dev, launches, kTreeQuery);
+}
+
+// kTreeBuild reads only the polygon (and the records of prep); kTreeQuery the points
+cudaError_t launch_tree_phase(const TreeArgs& a, void* scratch, cudaStream_t st, int dev, uint64_t* launches,
+                              int phase) {
+    const Layout l = layout(a.n_verts, a.n_edges, a.n_layout ? a.n_layout : a.n);
     char* s = static_cast<char*>(scratch);
     uint64_t* vk = reinterpret_cast<uint64_t*>(s + l.o_vk);
     uint64_t* vs = reinterpret_cast<uint64_t*>(s + l.o_vs);
@@ -629,6 +636,7 @@ cudaError_t launch_tree(const TreeArgs& a, void* scratch, cudaStream_t st, int d
     cudaError_t e;
 #define PC_TRY(x)                                                                                                      \
     if ((e = (x)) != cudaSuccess) return e
+    if (phase == kTreeBuild) {
     // ---- build ----
     vkey_kernel<<<grid, 256, 0, st>>>(a.vy, a.n_verts, a.bbox_keys, vk, vid);
     PC_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, vk, vs, vid, vsid, (int)a.n_verts, 0, 53, st));
@@ -670,6 +678,9 @@ cudaError_t launch_tree(const TreeArgs& a, void* scratch, cudaStream_t st, int d
                                                vals2 + h_tot[0], (int)h_tot[1], 0, bits, st));
     }
     verify_pack_kernel<<<grid, 256, 0, st>>>(vals2, keys2, tot, bignode, L, V, m_dev, rec, line, packed, flag);
+    *launches += 11;
+    return cudaGetLastError();
+    }
     // ---- query ----
     PC_TRY(cudaMemsetAsync(fb_cnt, 0, 4, st));
     const unsigned qgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((a.n + 255) / 256, (uint64_t)grid * 4));
@@ -681,7 +692,7 @@ cudaError_t launch_tree(const TreeArgs& a, void* scratch, cudaStream_t st, int d
         query_kernel<kC2><<<qgrid, 256, 0, st>>>(reinterpret_cast<const double2*>(a.pts), a.n, a.prefilter, a.bbox_keys,
                                                  V, m_dev, L, off, cnt, packed, flag, rec, a.inside_bits, fb_idx, fb_cnt,
                                                  a.n_dev);
-    *launches += 15;
+    *launches += 4;
     // ---- fallback points through the scan kernel, its grid sized for their number ----
     uint32_t n_fb = 0;
     PC_TRY(cudaMemcpyAsync(&n_fb, fb_cnt, 4, cudaMemcpyDeviceToHost, st));

@@ -235,6 +235,44 @@ def test_multi_shard_identical():
             assert np.array_equal(a.aux_bits, b.aux_bits) and np.array_equal(a.stats, b.stats)
 
 
+@pytest.mark.parametrize("n_verts", [1000, 20_000])  # scan kernel / segment tree
+def test_chunked_upload_matches_one_piece(engine, n_verts):
+    """Host-API shards above 2 x 2^23 points upload in 2^23-point chunks, each
+    classified while the next uploads (pip_capi.cu); the result must equal the
+    device-pointer call on the whole array (one piece), bit for bit, and a
+    subsample must match the reference."""
+    import torch
+    n = 2 * (1 << 23) + 12_345  # three chunks, the last one ragged
+    poly = W.star_polygon(n_verts)
+    xy = W.uniform_points(n, W.bounds(poly), 17)
+    dev = torch.device("cuda:0")
+    d_xy = torch.from_numpy(xy).to(dev)
+    d_vx, d_vy = torch.from_numpy(poly.vx).to(dev), torch.from_numpy(poly.vy).to(dev)
+    d_ro = torch.from_numpy(poly.ring_off.view(np.int64)).to(dev)
+    nw = (n + 31) // 32
+    for mode in (0, 1):
+        host = engine.classify_batch(xy, poly, mode)
+        d_in = torch.empty(nw, dtype=torch.int32, device=dev)
+        d_aux = torch.empty(nw, dtype=torch.int32, device=dev)
+        d_st = torch.empty(4, dtype=torch.int64, device=dev)
+        d_v = torch.empty(n, dtype=torch.uint8, device=dev)
+        engine.classify_dev(0, torch.cuda.current_stream().cuda_stream, d_xy, n, d_vx, d_vy, d_ro, poly.n_rings,
+                            poly.n_verts, mode, 1e-12, True, d_in, d_aux, d_st, d_v)
+        torch.cuda.synchronize()
+        assert np.array_equal(d_in.cpu().numpy().view(np.uint32), host.inside_bits)
+        assert np.array_equal(d_aux.cpu().numpy().view(np.uint32), host.aux_bits)
+        assert np.array_equal(d_v.cpu().numpy(), host.verdicts)
+        assert np.array_equal(d_st.cpu().numpy().view(np.uint64), host.stats)
+        # chunk seams and a random subsample against the reference
+        idx = np.unique(np.concatenate([np.arange(0, 64), (1 << 23) + np.arange(-64, 64),
+                                        (2 << 23) + np.arange(-64, 64), np.arange(n - 64, n),
+                                        np.random.default_rng(5).integers(0, n, 20_000)]))
+        sub = np.ascontiguousarray(xy[idx])
+        want_v, _ = (oracle.ref_classify(sub, poly.vx, poly.vy, poly.ring_off, mode) if oracle.ref_available()
+                     else oracle.port_classify(sub, poly.vx, poly.vy, poly.ring_off, mode, threads=THREADS))
+        assert np.array_equal(host.verdicts[idx], want_v)
+
+
 def test_device_pointer_api_matches_host_api(engine):
     import torch
     poly, xy = W.config2(1000, n_points=123_457)
