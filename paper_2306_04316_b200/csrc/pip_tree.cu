@@ -637,49 +637,49 @@ cudaError_t launch_tree_phase(const TreeArgs& a, void* scratch, cudaStream_t st,
 #define PC_TRY(x)                                                                                                      \
     if ((e = (x)) != cudaSuccess) return e
     if (phase == kTreeBuild) {
-    // ---- build ----
-    vkey_kernel<<<grid, 256, 0, st>>>(a.vy, a.n_verts, a.bbox_keys, vk, vid);
-    PC_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, vk, vs, vid, vsid, (int)a.n_verts, 0, 53, st));
-    tmp_bytes = l.tmp_bytes;
-    PC_TRY(cub::DeviceSelect::Unique(tmp, tmp_bytes, vs, V, m_dev, (int)a.n_verts, st));
-    // vertex ranks among the distinct keys (vid is free again: first-occurrence flags, then their sums)
-    newkey_kernel<<<grid, 256, 0, st>>>(vs, a.n_verts, vid);
-    tmp_bytes = l.tmp_bytes;
-    PC_TRY(cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, vid, vrank, (int)a.n_verts, st));
-    vrank_kernel<<<grid, 256, 0, st>>>(vrank, vsid, a.n_verts, vid);
-    uint32_t* const vr = vid;
-    PC_TRY(cudaMemsetAsync(cnt, 0, (2 * l.L + 1) * 4, st));
-    PC_TRY(cudaMemsetAsync(flag, 0, 2 * l.L, st));
-    edges_kernel<false><<<grid, 256, 0, st>>>(a.vx, a.vy, ro, a.n_rings, a.n_verts, a.bbox_keys, vr, V, m_dev, L, cnt,
-                                              nullptr, nullptr, nullptr, nullptr, nullptr);
-    const int n_nodes = (int)(2 * l.L + 1);
-    split_kernel<<<grid, 256, 0, st>>>(cnt, (uint32_t)n_nodes, cs, cb, fbig);
-    for (auto [in, out] : {std::pair{cs, os}, std::pair{cb, ob}, std::pair{fbig, rb}}) {
+        // ---- build ----
+        vkey_kernel<<<grid, 256, 0, st>>>(a.vy, a.n_verts, a.bbox_keys, vk, vid);
+        PC_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, vk, vs, vid, vsid, (int)a.n_verts, 0, 53, st));
         tmp_bytes = l.tmp_bytes;
-        PC_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, in, out, n_nodes, st));
-    }
-    offsets_kernel<<<grid, 256, 0, st>>>(cnt, (uint32_t)n_nodes, os, ob, rb, off, seg_end, khi, bignode, tot);
-    PC_TRY(cudaMemsetAsync(cnt, 0, (2 * l.L + 1) * 4, st));
-    edges_kernel<true><<<grid, 256, 0, st>>>(a.vx, a.vy, ro, a.n_rings, a.n_verts, a.bbox_keys, vr, V, m_dev, L, cnt, off,
-                                             khi, keys, vals, line);
-    // the split sizes come to the host (the sorts take them as item counts)
-    uint32_t h_tot[3] = {0, 0, 0};
-    PC_TRY(cudaMemcpyAsync(h_tot, tot, 12, cudaMemcpyDeviceToHost, st));
-    PC_TRY(cudaStreamSynchronize(st));
-    if (h_tot[0]) {
+        PC_TRY(cub::DeviceSelect::Unique(tmp, tmp_bytes, vs, V, m_dev, (int)a.n_verts, st));
+        // vertex ranks among the distinct keys (vid is free again: first-occurrence flags, then their sums)
+        newkey_kernel<<<grid, 256, 0, st>>>(vs, a.n_verts, vid);
         tmp_bytes = l.tmp_bytes;
-        PC_TRY(cub::DeviceSegmentedSort::SortPairs(tmp, tmp_bytes, keys, keys2, vals, vals2, (int)h_tot[0],
-                                                   n_nodes - 1, off, seg_end, st));
-    }
-    if (h_tot[1]) {
-        const int bits = 32 + (32 - __builtin_clz(std::max(h_tot[2], 1u)));
-        tmp_bytes = l.tmp_bytes;
-        PC_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys + h_tot[0], keys2 + h_tot[0], vals + h_tot[0],
-                                               vals2 + h_tot[0], (int)h_tot[1], 0, bits, st));
-    }
-    verify_pack_kernel<<<grid, 256, 0, st>>>(vals2, keys2, tot, bignode, L, V, m_dev, rec, line, packed, flag);
-    *launches += 11;
-    return cudaGetLastError();
+        PC_TRY(cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, vid, vrank, (int)a.n_verts, st));
+        vrank_kernel<<<grid, 256, 0, st>>>(vrank, vsid, a.n_verts, vid);
+        uint32_t* const vr = vid;
+        PC_TRY(cudaMemsetAsync(cnt, 0, (2 * l.L + 1) * 4, st));
+        PC_TRY(cudaMemsetAsync(flag, 0, 2 * l.L, st));
+        edges_kernel<false><<<grid, 256, 0, st>>>(a.vx, a.vy, ro, a.n_rings, a.n_verts, a.bbox_keys, vr, V, m_dev, L, cnt,
+                                                  nullptr, nullptr, nullptr, nullptr, nullptr);
+        const int n_nodes = (int)(2 * l.L + 1);
+        split_kernel<<<grid, 256, 0, st>>>(cnt, (uint32_t)n_nodes, cs, cb, fbig);
+        for (auto [in, out] : {std::pair{cs, os}, std::pair{cb, ob}, std::pair{fbig, rb}}) {
+            tmp_bytes = l.tmp_bytes;
+            PC_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, in, out, n_nodes, st));
+        }
+        offsets_kernel<<<grid, 256, 0, st>>>(cnt, (uint32_t)n_nodes, os, ob, rb, off, seg_end, khi, bignode, tot);
+        PC_TRY(cudaMemsetAsync(cnt, 0, (2 * l.L + 1) * 4, st));
+        edges_kernel<true><<<grid, 256, 0, st>>>(a.vx, a.vy, ro, a.n_rings, a.n_verts, a.bbox_keys, vr, V, m_dev, L, cnt, off,
+                                                 khi, keys, vals, line);
+        // the split sizes come to the host (the sorts take them as item counts)
+        uint32_t h_tot[3] = {0, 0, 0};
+        PC_TRY(cudaMemcpyAsync(h_tot, tot, 12, cudaMemcpyDeviceToHost, st));
+        PC_TRY(cudaStreamSynchronize(st));
+        if (h_tot[0]) {
+            tmp_bytes = l.tmp_bytes;
+            PC_TRY(cub::DeviceSegmentedSort::SortPairs(tmp, tmp_bytes, keys, keys2, vals, vals2, (int)h_tot[0],
+                                                       n_nodes - 1, off, seg_end, st));
+        }
+        if (h_tot[1]) {
+            const int bits = 32 + (32 - __builtin_clz(std::max(h_tot[2], 1u)));
+            tmp_bytes = l.tmp_bytes;
+            PC_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys + h_tot[0], keys2 + h_tot[0], vals + h_tot[0],
+                                                   vals2 + h_tot[0], (int)h_tot[1], 0, bits, st));
+        }
+        verify_pack_kernel<<<grid, 256, 0, st>>>(vals2, keys2, tot, bignode, L, V, m_dev, rec, line, packed, flag);
+        *launches += 11;
+        return cudaGetLastError();
     }
     // ---- query ----
     PC_TRY(cudaMemsetAsync(fb_cnt, 0, 4, st));
