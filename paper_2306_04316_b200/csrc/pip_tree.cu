@@ -45,6 +45,7 @@
 
 #include <algorithm>
 #include <utility>
+#include <cub/block/block_radix_sort.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
@@ -223,7 +224,7 @@ __global__ void edges_kernel(const double* __restrict__ vx, const double* __rest
                 // difference of two non-crossing segments is linear and keeps its sign)
                 double xm = __dmul_rn(__dadd_rn(axl, __dmul_rn(__dsub_rn(ym, ayl), slope)), 0x1p32);
                 xm = xm > 0.0 ? xm : 0.0;
-                xm = xm < 4294967295.0 ? xm : 4294967295.0;
+                xm = xm < 4294967294.0 ? xm : 4294967294.0; // below the mid-node sort's padding key
                 const uint32_t key = (uint32_t)xm;
                 const uint32_t slot = off[nd] + base + rank;
                 keys[slot] = (unsigned long long)khi[nd] << 32 | key; // (node or big-node rank, x)
@@ -242,9 +243,10 @@ __global__ void verify_pack_kernel(const uint32_t* __restrict__ vals, const unsi
                                    const uint64_t* __restrict__ V, const uint32_t* __restrict__ m_dev,
                                    const EdgeRec* __restrict__ rec, const double4* __restrict__ line,
                                    float4* __restrict__ packed, uint8_t* __restrict__ flag) {
-    const uint32_t m = *m_dev, ts = tot[0], total = tot[0] + tot[1];
-    // node of entry j: the key's high word is the node below ts, a big-node rank above
-    auto node = [&](uint32_t j) { const uint32_t h = (uint32_t)(keys[j] >> 32); return j < ts ? h : bignode[h]; };
+    const uint32_t m = *m_dev, tsm = tot[0] + tot[1], total = tsm + tot[2];
+    // node of entry j: the key's high word is the node id for small and mid nodes,
+    // the huge-node rank after them
+    auto node = [&](uint32_t j) { const uint32_t h = (uint32_t)(keys[j] >> 32); return j < tsm ? h : bignode[h]; };
     auto x = [](const double4& l, double y) { return __dadd_rn(l.x, __dmul_rn(__dsub_rn(y, l.y), l.z)); };
     const unsigned lane = threadIdx.x & 31;
     const uint32_t stride = gridDim.x * blockDim.x;
@@ -475,47 +477,95 @@ uint32_t tree_leaves(uint64_t nv) {
     return L;
 }
 
-// node lists of at most kSmallSeg entries are sorted by CUB's segmented sort
-// (warp-level merge sorts); the entries of bigger nodes sit after them and are
-// sorted by one device-wide radix sort on (big-node rank, x)
-constexpr uint32_t kSmallSeg = 64;
+// Node lists by size: at most kSmallSeg entries (CUB's segmented sort, warp-level
+// merge sorts), up to kMidSeg (one CTA each, cub::BlockRadixSort in shared
+// memory, three size classes), and bigger ("huge", a few hundred nodes near the
+// root): one device-wide radix sort on (huge-node rank, x).  The three groups
+// are laid out one after another, each node's list contiguous.
+constexpr uint32_t kSmallSeg = 64, kMidSeg = 4096;
+constexpr uint32_t kMidClass[3] = {256, 1024, 4096}; // CTA capacities of the mid classes
 
 __global__ void split_kernel(const uint32_t* __restrict__ cnt, uint32_t n, uint32_t* __restrict__ cs,
-                             uint32_t* __restrict__ cb, uint32_t* __restrict__ fb) {
+                             uint32_t* __restrict__ cm, uint32_t* __restrict__ ch, uint32_t* __restrict__ fh) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const uint32_t c = cnt[i];
-        const bool big = c > kSmallSeg;
-        cs[i] = big ? 0u : c;
-        cb[i] = big ? c : 0u;
-        fb[i] = big;
+        const bool mid = c > kSmallSeg && c <= kMidSeg, huge = c > kMidSeg;
+        cs[i] = mid || huge ? 0u : c;
+        cm[i] = mid ? c : 0u;
+        ch[i] = huge ? c : 0u;
+        fh[i] = huge;
     }
 }
 
-// node offsets in the split layout, CUB segment ends (empty for big nodes), the
-// key high words and the big-node list; tot = {small entries, big entries, big nodes}
+// node offsets, CUB segment ends (empty unless small), the key high words (node
+// id; huge: rank), the huge-node list and the mid-node lists by class;
+// tot = {small, mid, huge entries, huge nodes, mid nodes of class 0, 1, 2}
 __global__ void offsets_kernel(const uint32_t* __restrict__ cnt, uint32_t n, const uint32_t* __restrict__ os,
-                               const uint32_t* __restrict__ ob, const uint32_t* __restrict__ rb,
-                               uint32_t* __restrict__ off, uint32_t* __restrict__ seg_end, uint32_t* __restrict__ khi,
-                               uint32_t* __restrict__ bignode, uint32_t* __restrict__ tot) {
-    const uint32_t ts = os[n - 1]; // cnt[n - 1] == 0: the last exclusive sums are the totals
+                               const uint32_t* __restrict__ om, const uint32_t* __restrict__ oh,
+                               const uint32_t* __restrict__ rh, uint32_t* __restrict__ off,
+                               uint32_t* __restrict__ seg_end, uint32_t* __restrict__ khi,
+                               uint32_t* __restrict__ bignode, uint32_t* __restrict__ mlist, uint32_t mcap,
+                               uint32_t* __restrict__ tot) {
+    // cnt[n - 1] == 0: the last exclusive sums are the totals
+    const uint32_t ts = os[n - 1], tm = om[n - 1];
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const uint32_t c = cnt[i];
-        const bool big = c > kSmallSeg;
-        off[i] = big ? ts + ob[i] : os[i];
-        seg_end[i] = big ? ts + ob[i] : os[i] + c;
-        khi[i] = big ? rb[i] : i;
-        if (big) bignode[rb[i]] = i;
+        const bool mid = c > kSmallSeg && c <= kMidSeg, huge = c > kMidSeg;
+        off[i] = huge ? ts + tm + oh[i] : mid ? ts + om[i] : os[i];
+        seg_end[i] = mid || huge ? off[i] : os[i] + c;
+        khi[i] = huge ? rh[i] : i;
+        if (huge) bignode[rh[i]] = i;
+        if (mid) {
+            const int k = c <= kMidClass[0] ? 0 : c <= kMidClass[1] ? 1 : 2;
+            mlist[k * mcap + atomicAdd(&tot[4 + k], 1u)] = i;
+        }
         if (i == 0) {
             tot[0] = ts;
-            tot[1] = ob[n - 1];
-            tot[2] = rb[n - 1];
+            tot[1] = tm;
+            tot[2] = oh[n - 1];
+            tot[3] = rh[n - 1];
         }
+    }
+}
+
+// one CTA per listed mid node: its list (keys' low words = x) sorted in shared
+// memory; padding keys 0xffffffff sort last (real keys are clamped below it)
+template <int T, int I>
+__global__ void __launch_bounds__(T) node_sort_kernel(const uint32_t* __restrict__ list,
+                                                      const uint32_t* __restrict__ list_count,
+                                                      const uint32_t* __restrict__ off, const uint32_t* __restrict__ cnt,
+                                                      const unsigned long long* __restrict__ keys,
+                                                      const uint32_t* __restrict__ vals,
+                                                      unsigned long long* __restrict__ keys2,
+                                                      uint32_t* __restrict__ vals2) {
+    using BRS = cub::BlockRadixSort<uint32_t, T, I, uint32_t>;
+    __shared__ typename BRS::TempStorage tmp;
+    const uint32_t nl = *list_count;
+    for (uint32_t b = blockIdx.x; b < nl; b += gridDim.x) {
+        const uint32_t nd = list[b], o = off[nd], k = cnt[nd];
+        uint32_t kk[I], vv[I];
+#pragma unroll
+        for (int q = 0; q < I; ++q) { // striped (coalesced); equal x keys have no required order
+            const uint32_t j = q * T + threadIdx.x;
+            kk[q] = j < k ? (uint32_t)keys[o + j] : 0xffffffffu;
+            vv[q] = j < k ? vals[o + j] : 0u;
+        }
+        BRS(tmp).SortBlockedToStriped(kk, vv);
+#pragma unroll
+        for (int q = 0; q < I; ++q) {
+            const uint32_t j = q * T + threadIdx.x;
+            if (j < k) {
+                keys2[o + j] = (unsigned long long)nd << 32 | kk[q];
+                vals2[o + j] = vv[q];
+            }
+        }
+        __syncthreads(); // tmp is reused by the next node
     }
 }
 
 struct Layout {
     uint64_t nv, ne, L, emax;
-    size_t o_cs, o_cb, o_fb, o_os, o_ob, o_rb, o_end, o_khi, o_big, o_tot;
+    size_t o_cs, o_cm, o_ch, o_fh, o_os, o_om, o_oh, o_rh, o_end, o_khi, o_big, o_mlist, o_tot;
     size_t o_vk, o_vs, o_vid, o_vsid, o_vrank, o_V, o_m, o_cnt, o_off, o_keys, o_vals, o_keys2, o_vals2, o_packed, o_flag, o_fbidx, o_fbcnt,
         o_fbpts, o_fbbits, o_fbebits, o_line, o_tmp, tmp_bytes, total;
 };
@@ -560,9 +610,11 @@ Layout layout(uint64_t nv, uint64_t ne, uint64_t n_pts) {
     l.o_m = put(16);
     l.o_cnt = put((2 * l.L + 1) * 4);
     l.o_off = put((2 * l.L + 1) * 4);
-    for (size_t* o_split : {&l.o_cs, &l.o_cb, &l.o_fb, &l.o_os, &l.o_ob, &l.o_rb, &l.o_end, &l.o_khi, &l.o_big})
+    for (size_t* o_split : {&l.o_cs, &l.o_cm, &l.o_ch, &l.o_fh, &l.o_os, &l.o_om, &l.o_oh, &l.o_rh, &l.o_end,
+                            &l.o_khi, &l.o_big})
         *o_split = put((2 * l.L + 1) * 4);
-    l.o_tot = put(16);
+    l.o_mlist = put(3 * (2 * l.L + 1) * 4);
+    l.o_tot = put(32);
     l.o_keys = put(l.emax * 8);
     l.o_vals = put(l.emax * 4);
     l.o_keys2 = put(l.emax * 8);
@@ -612,9 +664,9 @@ cudaError_t launch_tree_phase(const TreeArgs& a, void* scratch, cudaStream_t st,
     uint32_t* cnt = reinterpret_cast<uint32_t*>(s + l.o_cnt);
     uint32_t* off = reinterpret_cast<uint32_t*>(s + l.o_off);
     auto u32 = [&](size_t o) { return reinterpret_cast<uint32_t*>(s + o); };
-    uint32_t *cs = u32(l.o_cs), *cb = u32(l.o_cb), *fbig = u32(l.o_fb), *os = u32(l.o_os), *ob = u32(l.o_ob),
-             *rb = u32(l.o_rb), *seg_end = u32(l.o_end), *khi = u32(l.o_khi), *bignode = u32(l.o_big),
-             *tot = u32(l.o_tot);
+    uint32_t *cs = u32(l.o_cs), *cm = u32(l.o_cm), *ch = u32(l.o_ch), *fh = u32(l.o_fh), *os = u32(l.o_os),
+             *om = u32(l.o_om), *oh = u32(l.o_oh), *rh = u32(l.o_rh), *seg_end = u32(l.o_end), *khi = u32(l.o_khi),
+             *bignode = u32(l.o_big), *mlist = u32(l.o_mlist), *tot = u32(l.o_tot);
     unsigned long long* keys = reinterpret_cast<unsigned long long*>(s + l.o_keys);
     uint32_t* vals = reinterpret_cast<uint32_t*>(s + l.o_vals);
     unsigned long long* keys2 = reinterpret_cast<unsigned long long*>(s + l.o_keys2);
@@ -653,32 +705,45 @@ cudaError_t launch_tree_phase(const TreeArgs& a, void* scratch, cudaStream_t st,
         edges_kernel<false><<<grid, 256, 0, st>>>(a.vx, a.vy, ro, a.n_rings, a.n_verts, a.bbox_keys, vr, V, m_dev, L, cnt,
                                                   nullptr, nullptr, nullptr, nullptr, nullptr);
         const int n_nodes = (int)(2 * l.L + 1);
-        split_kernel<<<grid, 256, 0, st>>>(cnt, (uint32_t)n_nodes, cs, cb, fbig);
-        for (auto [in, out] : {std::pair{cs, os}, std::pair{cb, ob}, std::pair{fbig, rb}}) {
+        split_kernel<<<grid, 256, 0, st>>>(cnt, (uint32_t)n_nodes, cs, cm, ch, fh);
+        for (auto [in, out] : {std::pair{cs, os}, std::pair{cm, om}, std::pair{ch, oh}, std::pair{fh, rh}}) {
             tmp_bytes = l.tmp_bytes;
             PC_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, in, out, n_nodes, st));
         }
-        offsets_kernel<<<grid, 256, 0, st>>>(cnt, (uint32_t)n_nodes, os, ob, rb, off, seg_end, khi, bignode, tot);
+        PC_TRY(cudaMemsetAsync(tot, 0, 32, st));
+        offsets_kernel<<<grid, 256, 0, st>>>(cnt, (uint32_t)n_nodes, os, om, oh, rh, off, seg_end, khi, bignode, mlist,
+                                             (uint32_t)n_nodes, tot);
         PC_TRY(cudaMemsetAsync(cnt, 0, (2 * l.L + 1) * 4, st));
-        edges_kernel<true><<<grid, 256, 0, st>>>(a.vx, a.vy, ro, a.n_rings, a.n_verts, a.bbox_keys, vr, V, m_dev, L, cnt, off,
-                                                 khi, keys, vals, line);
-        // the split sizes come to the host (the sorts take them as item counts)
-        uint32_t h_tot[3] = {0, 0, 0};
-        PC_TRY(cudaMemcpyAsync(h_tot, tot, 12, cudaMemcpyDeviceToHost, st));
+        edges_kernel<true><<<grid, 256, 0, st>>>(a.vx, a.vy, ro, a.n_rings, a.n_verts, a.bbox_keys, vr, V, m_dev, L, cnt,
+                                                 off, khi, keys, vals, line);
+        // the split sizes come to the host (item counts of the sorts, grid sizes)
+        uint32_t h_tot[7] = {0, 0, 0, 0, 0, 0, 0};
+        PC_TRY(cudaMemcpyAsync(h_tot, tot, 28, cudaMemcpyDeviceToHost, st));
         PC_TRY(cudaStreamSynchronize(st));
         if (h_tot[0]) {
             tmp_bytes = l.tmp_bytes;
             PC_TRY(cub::DeviceSegmentedSort::SortPairs(tmp, tmp_bytes, keys, keys2, vals, vals2, (int)h_tot[0],
                                                        n_nodes - 1, off, seg_end, st));
         }
-        if (h_tot[1]) {
-            const int bits = 32 + (32 - __builtin_clz(std::max(h_tot[2], 1u)));
+        auto mid_grid = [&](uint32_t k) { return std::max(1u, std::min(k, (uint32_t)grid * 4)); };
+        if (h_tot[4])
+            node_sort_kernel<64, 4><<<mid_grid(h_tot[4]), 64, 0, st>>>(mlist, tot + 4, off, cnt, keys, vals, keys2,
+                                                                      vals2);
+        if (h_tot[5])
+            node_sort_kernel<128, 8><<<mid_grid(h_tot[5]), 128, 0, st>>>(mlist + n_nodes, tot + 5, off, cnt, keys, vals,
+                                                                        keys2, vals2);
+        if (h_tot[6])
+            node_sort_kernel<256, 16><<<mid_grid(h_tot[6]), 256, 0, st>>>(mlist + 2 * n_nodes, tot + 6, off, cnt, keys,
+                                                                         vals, keys2, vals2);
+        if (h_tot[2]) {
+            const uint32_t o = h_tot[0] + h_tot[1];
+            const int bits = 32 + (32 - __builtin_clz(std::max(h_tot[3], 1u)));
             tmp_bytes = l.tmp_bytes;
-            PC_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys + h_tot[0], keys2 + h_tot[0], vals + h_tot[0],
-                                                   vals2 + h_tot[0], (int)h_tot[1], 0, bits, st));
+            PC_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys + o, keys2 + o, vals + o, vals2 + o,
+                                                   (int)h_tot[2], 0, bits, st));
         }
         verify_pack_kernel<<<grid, 256, 0, st>>>(vals2, keys2, tot, bignode, L, V, m_dev, rec, line, packed, flag);
-        *launches += 11;
+        *launches += 15;
         return cudaGetLastError();
     }
     // ---- query ----
