@@ -285,6 +285,13 @@ __global__ void verify_pack_kernel(const uint32_t* __restrict__ vals, const unsi
     }
 }
 
+// per node, what a query needs in one 8-byte load: {offset, count | linear << 31}
+__global__ void meta_kernel(const uint32_t* __restrict__ off, const uint32_t* __restrict__ cnt,
+                            const uint8_t* __restrict__ flag, uint32_t n, uint2* __restrict__ meta) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        meta[i] = make_uint2(off[i], cnt[i] | (uint32_t)(flag[i] != 0) << 31);
+}
+
 // F: the reference's C1 count decision for a sure straddle, from a packed node
 // entry {Nx, Ny, c + B, edge}: 1 counted, 0 not; *certain: decided by the fp32
 // test (else the binary64 expression of the edge's record ran)
@@ -348,9 +355,8 @@ template <int MODE>
 __global__ void __launch_bounds__(256) query_kernel(const double2* __restrict__ pts, uint64_t n, int prefilter,
                                                     const unsigned long long* __restrict__ bbox_keys,
                                                     const uint64_t* __restrict__ V, const uint32_t* __restrict__ m_dev,
-                                                    uint32_t L, const uint32_t* __restrict__ off,
-                                                    const uint32_t* __restrict__ cnt,
-                                                    const float4* __restrict__ packed, const uint8_t* __restrict__ flag,
+                                                    uint32_t L, const uint2* __restrict__ meta,
+                                                    const float4* __restrict__ packed,
                                                     const EdgeRec* __restrict__ rec, uint32_t* __restrict__ inside_bits,
                                                     uint32_t* __restrict__ fb_idx, uint32_t* __restrict__ fb_count,
                                                     const uint32_t* __restrict__ n_dev) {
@@ -384,8 +390,9 @@ __global__ void __launch_bounds__(256) query_kernel(const double2* __restrict__ 
                         const float lx = __double2float_rn(lxd), ly = __double2float_rn(lyd);
                         uint32_t c = 0;
                         for (uint32_t nd = L + j - 1; nd; nd >>= 1) {
-                            const uint32_t o = __ldg(off + nd), k = __ldg(cnt + nd);
-                            if (k) c += node_count<MODE>(packed, o, k, __ldg(flag + nd) != 0, rec, lx, ly, p.x, p.y);
+                            const uint2 md = __ldg(meta + nd); // {offset, count | linear << 31}
+                            const uint32_t k = md.y & 0x7fffffffu;
+                            if (k) c += node_count<MODE>(packed, md.x, k, md.y >> 31, rec, lx, ly, p.x, p.y);
                         }
                         in = c & 1u;
                     }
@@ -565,7 +572,7 @@ __global__ void __launch_bounds__(T) node_sort_kernel(const uint32_t* __restrict
 
 struct Layout {
     uint64_t nv, ne, L, emax;
-    size_t o_cs, o_cm, o_ch, o_fh, o_os, o_om, o_oh, o_rh, o_end, o_khi, o_big, o_mlist, o_tot;
+    size_t o_meta, o_cs, o_cm, o_ch, o_fh, o_os, o_om, o_oh, o_rh, o_end, o_khi, o_big, o_mlist, o_tot;
     size_t o_vk, o_vs, o_vid, o_vsid, o_vrank, o_V, o_m, o_cnt, o_off, o_keys, o_vals, o_keys2, o_vals2, o_packed, o_flag, o_fbidx, o_fbcnt,
         o_fbpts, o_fbbits, o_fbebits, o_line, o_tmp, tmp_bytes, total;
 };
@@ -621,6 +628,7 @@ Layout layout(uint64_t nv, uint64_t ne, uint64_t n_pts) {
     l.o_vals2 = put(l.emax * 4);
     l.o_packed = put(l.emax * 16);
     l.o_flag = put(2 * l.L);
+    l.o_meta = put(2 * l.L * 8);
     l.o_fbidx = put(n_pts * 4 + 4);
     l.o_fbcnt = put(16);
     l.o_fbpts = put(n_pts * 16 + 16);
@@ -673,6 +681,7 @@ cudaError_t launch_tree_phase(const TreeArgs& a, void* scratch, cudaStream_t st,
     uint32_t* vals2 = reinterpret_cast<uint32_t*>(s + l.o_vals2);
     float4* packed = reinterpret_cast<float4*>(s + l.o_packed);
     uint8_t* flag = reinterpret_cast<uint8_t*>(s + l.o_flag);
+    uint2* meta = reinterpret_cast<uint2*>(s + l.o_meta);
     uint32_t* fb_idx = reinterpret_cast<uint32_t*>(s + l.o_fbidx);
     uint32_t* fb_cnt = reinterpret_cast<uint32_t*>(s + l.o_fbcnt);
     double* fb_pts = reinterpret_cast<double*>(s + l.o_fbpts);
@@ -743,7 +752,8 @@ cudaError_t launch_tree_phase(const TreeArgs& a, void* scratch, cudaStream_t st,
                                                    (int)h_tot[2], 0, bits, st));
         }
         verify_pack_kernel<<<grid, 256, 0, st>>>(vals2, keys2, tot, bignode, L, V, m_dev, rec, line, packed, flag);
-        *launches += 15;
+        meta_kernel<<<grid, 256, 0, st>>>(off, cnt, flag, (uint32_t)(2 * l.L), meta);
+        *launches += 16;
         return cudaGetLastError();
     }
     // ---- query ----
@@ -751,11 +761,11 @@ cudaError_t launch_tree_phase(const TreeArgs& a, void* scratch, cudaStream_t st,
     const unsigned qgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((a.n + 255) / 256, (uint64_t)grid * 4));
     if (a.mode == kC1)
         query_kernel<kC1><<<qgrid, 256, 0, st>>>(reinterpret_cast<const double2*>(a.pts), a.n, a.prefilter, a.bbox_keys,
-                                                 V, m_dev, L, off, cnt, packed, flag, rec, a.inside_bits, fb_idx, fb_cnt,
+                                                 V, m_dev, L, meta, packed, rec, a.inside_bits, fb_idx, fb_cnt,
                                                  a.n_dev);
     else
         query_kernel<kC2><<<qgrid, 256, 0, st>>>(reinterpret_cast<const double2*>(a.pts), a.n, a.prefilter, a.bbox_keys,
-                                                 V, m_dev, L, off, cnt, packed, flag, rec, a.inside_bits, fb_idx, fb_cnt,
+                                                 V, m_dev, L, meta, packed, rec, a.inside_bits, fb_idx, fb_cnt,
                                                  a.n_dev);
     *launches += 4;
     // ---- fallback points through the scan kernel, its grid sized for their number ----
