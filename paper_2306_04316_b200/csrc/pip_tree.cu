@@ -234,14 +234,24 @@ __global__ void edges_kernel(const double* __restrict__ vx, const double* __rest
     }
 }
 
-// per entry: its packed record {Nx, Ny, c + B, edge} (the fp32 record of
-// pip_kernels.cu prep_edges_kernel), and the order check against the next
-// entry of the same node at both ends of the node's key range (x from the
-// edge's local line; a violation beyond 2^-30 flags the node)
+// per edge: its packed fp32 record {Nx, Ny, c + B, edge} (the record of
+// pip_kernels.cu prep_edges_kernel), 16 B instead of the 64 B EdgeRec
+__global__ void erec_kernel(const EdgeRec* __restrict__ rec, uint32_t ne, float4* __restrict__ erec) {
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += gridDim.x * blockDim.x) {
+        const double d5 = rec[e].d[5], d6 = rec[e].d[6];
+        erec[e] = make_float4(__int_as_float(__double2loint(d5)), __int_as_float(__double2hiint(d5)),
+                              __int_as_float(__double2loint(d6)), __uint_as_float(e));
+    }
+}
+
+// per entry: its packed record (erec of its edge: the query's binary search
+// probes one 16 B load per step), and the order check against the next entry
+// of the same node at both ends of the node's key range (x from the edge's
+// local line; a violation beyond 2^-30 flags the node)
 __global__ void verify_pack_kernel(const uint32_t* __restrict__ vals, const unsigned long long* __restrict__ keys,
                                    const uint32_t* __restrict__ tot, const uint32_t* __restrict__ bignode, uint32_t L,
                                    const uint64_t* __restrict__ V, const uint32_t* __restrict__ m_dev,
-                                   const EdgeRec* __restrict__ rec, const double4* __restrict__ line,
+                                   const double4* __restrict__ line, const float4* __restrict__ erec,
                                    float4* __restrict__ packed, uint8_t* __restrict__ flag) {
     const uint32_t m = *m_dev, tsm = tot[0] + tot[1], total = tsm + tot[2];
     // node of entry j: the key's high word is the node id for small and mid nodes,
@@ -258,9 +268,7 @@ __global__ void verify_pack_kernel(const uint32_t* __restrict__ vals, const unsi
         double x0 = 0.0, x1 = 0.0, y0 = 0.0, y1 = 0.0;
         if (i < total) {
             e0 = vals[i];
-            const double d5 = rec[e0].d[5], d6 = rec[e0].d[6];
-            packed[i] = make_float4(__int_as_float(__double2loint(d5)), __int_as_float(__double2hiint(d5)),
-                                    __int_as_float(__double2loint(d6)), __uint_as_float(e0));
+            packed[i] = erec[e0];
             nd = node(i);
             const int d = 31 - __clz(nd);
             const uint32_t span = L >> d, a = (nd - (1u << d)) * span, b = min(a + span, m - 1);
@@ -573,7 +581,7 @@ __global__ void __launch_bounds__(T) node_sort_kernel(const uint32_t* __restrict
 struct Layout {
     uint64_t nv, ne, L, emax;
     size_t o_meta, o_cs, o_cm, o_ch, o_fh, o_os, o_om, o_oh, o_rh, o_end, o_khi, o_big, o_mlist, o_tot;
-    size_t o_vk, o_vs, o_vid, o_vsid, o_vrank, o_V, o_m, o_cnt, o_off, o_keys, o_vals, o_keys2, o_vals2, o_packed, o_flag, o_fbidx, o_fbcnt,
+    size_t o_vk, o_vs, o_vid, o_vsid, o_vrank, o_V, o_m, o_cnt, o_off, o_keys, o_vals, o_keys2, o_vals2, o_erec, o_packed, o_flag, o_fbidx, o_fbcnt,
         o_fbpts, o_fbbits, o_fbebits, o_line, o_tmp, tmp_bytes, total;
 };
 
@@ -626,6 +634,7 @@ Layout layout(uint64_t nv, uint64_t ne, uint64_t n_pts) {
     l.o_vals = put(l.emax * 4);
     l.o_keys2 = put(l.emax * 8);
     l.o_vals2 = put(l.emax * 4);
+    l.o_erec = put(std::max<uint64_t>(ne, 1) * 16);
     l.o_packed = put(l.emax * 16);
     l.o_flag = put(2 * l.L);
     l.o_meta = put(2 * l.L * 8);
@@ -679,6 +688,7 @@ cudaError_t launch_tree_phase(const TreeArgs& a, void* scratch, cudaStream_t st,
     uint32_t* vals = reinterpret_cast<uint32_t*>(s + l.o_vals);
     unsigned long long* keys2 = reinterpret_cast<unsigned long long*>(s + l.o_keys2);
     uint32_t* vals2 = reinterpret_cast<uint32_t*>(s + l.o_vals2);
+    float4* erec = reinterpret_cast<float4*>(s + l.o_erec);
     float4* packed = reinterpret_cast<float4*>(s + l.o_packed);
     uint8_t* flag = reinterpret_cast<uint8_t*>(s + l.o_flag);
     uint2* meta = reinterpret_cast<uint2*>(s + l.o_meta);
@@ -751,9 +761,10 @@ cudaError_t launch_tree_phase(const TreeArgs& a, void* scratch, cudaStream_t st,
             PC_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys + o, keys2 + o, vals + o, vals2 + o,
                                                    (int)h_tot[2], 0, bits, st));
         }
-        verify_pack_kernel<<<grid, 256, 0, st>>>(vals2, keys2, tot, bignode, L, V, m_dev, rec, line, packed, flag);
+        erec_kernel<<<grid, 256, 0, st>>>(rec, (uint32_t)a.n_edges, erec);
+        verify_pack_kernel<<<grid, 256, 0, st>>>(vals2, keys2, tot, bignode, L, V, m_dev, line, erec, packed, flag);
         meta_kernel<<<grid, 256, 0, st>>>(off, cnt, flag, (uint32_t)(2 * l.L), meta);
-        *launches += 16;
+        *launches += 17;
         return cudaGetLastError();
     }
     // ---- query ----
