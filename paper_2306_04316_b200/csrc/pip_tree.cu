@@ -44,11 +44,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <utility>
 #include <cub/block/block_radix_sort.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
-#include <cub/device/device_segmented_sort.cuh>
 #include <cub/device/device_select.cuh>
 
 #include "pip_device.cuh"
@@ -492,13 +492,15 @@ uint32_t tree_leaves(uint64_t nv) {
     return L;
 }
 
-// Node lists by size: at most kSmallSeg entries (CUB's segmented sort, warp-level
-// merge sorts), up to kMidSeg (one CTA each, cub::BlockRadixSort in shared
-// memory, three size classes), and bigger ("huge", a few hundred nodes near the
-// root): one device-wide radix sort on (huge-node rank, x).  The three groups
-// are laid out one after another, each node's list contiguous.
-constexpr uint32_t kSmallSeg = 64, kMidSeg = 4096;
+// Node lists by size: at most kTinySeg entries (a thread each, a sorting network
+// in registers), at most kSmallSeg (a warp each, a bitonic sort over shuffles),
+// up to kMidSeg (one CTA each, cub::BlockRadixSort in shared memory, three size
+// classes), and bigger ("huge", a few hundred nodes near the root): one
+// device-wide radix sort on (huge-node rank, x).  Small, mid and huge lists are
+// laid out one after another, each node's list contiguous.
+constexpr uint32_t kTinySeg = 16, kSmallSeg = 64, kMidSeg = 4096;
 constexpr uint32_t kMidClass[3] = {256, 1024, 4096}; // CTA capacities of the mid classes
+constexpr int kClasses = 5;                          // tiny, small, mid x 3
 
 __global__ void split_kernel(const uint32_t* __restrict__ cnt, uint32_t n, uint32_t* __restrict__ cs,
                              uint32_t* __restrict__ cm, uint32_t* __restrict__ ch, uint32_t* __restrict__ fh) {
@@ -512,33 +514,133 @@ __global__ void split_kernel(const uint32_t* __restrict__ cnt, uint32_t n, uint3
     }
 }
 
-// node offsets, CUB segment ends (empty unless small), the key high words (node
-// id; huge: rank), the huge-node list and the mid-node lists by class;
-// tot = {small, mid, huge entries, huge nodes, mid nodes of class 0, 1, 2}
+// node offsets, the key high words (node id; huge: rank), the huge-node list and
+// the lists of the other non-empty nodes by size class;
+// tot = {small, mid, huge entries, huge nodes, nodes of class 0 .. 4}
 __global__ void offsets_kernel(const uint32_t* __restrict__ cnt, uint32_t n, const uint32_t* __restrict__ os,
                                const uint32_t* __restrict__ om, const uint32_t* __restrict__ oh,
                                const uint32_t* __restrict__ rh, uint32_t* __restrict__ off,
-                               uint32_t* __restrict__ seg_end, uint32_t* __restrict__ khi,
+                               uint32_t* __restrict__ khi,
                                uint32_t* __restrict__ bignode, uint32_t* __restrict__ mlist, uint32_t mcap,
                                uint32_t* __restrict__ tot) {
     // cnt[n - 1] == 0: the last exclusive sums are the totals
     const uint32_t ts = os[n - 1], tm = om[n - 1];
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const uint32_t c = cnt[i];
+    const uint32_t lane = threadIdx.x & 31;
+    // whole warps step together (the class lists are appended warp-aggregated)
+    for (uint32_t i0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; i0 < n; i0 += gridDim.x * blockDim.x) {
+        const uint32_t i = i0 + lane;
+        const uint32_t c = i < n ? cnt[i] : 0u;
         const bool mid = c > kSmallSeg && c <= kMidSeg, huge = c > kMidSeg;
-        off[i] = huge ? ts + tm + oh[i] : mid ? ts + om[i] : os[i];
-        seg_end[i] = mid || huge ? off[i] : os[i] + c;
-        khi[i] = huge ? rh[i] : i;
-        if (huge) bignode[rh[i]] = i;
-        if (mid) {
-            const int k = c <= kMidClass[0] ? 0 : c <= kMidClass[1] ? 1 : 2;
-            mlist[k * mcap + atomicAdd(&tot[4 + k], 1u)] = i;
+        if (i < n) {
+            off[i] = huge ? ts + tm + oh[i] : mid ? ts + om[i] : os[i];
+            khi[i] = huge ? rh[i] : i;
+            if (huge) bignode[rh[i]] = i;
         }
+        const int k = !c || huge ? kClasses
+                      : c <= kTinySeg ? 0 : c <= kSmallSeg ? 1 : c <= kMidClass[0] ? 2 : c <= kMidClass[1] ? 3 : 4;
+        const uint32_t peers = __match_any_sync(0xffffffffu, k);
+        const int leader = __ffs(peers) - 1;
+        uint32_t base = 0;
+        if (k < kClasses && (int)lane == leader) base = atomicAdd(&tot[4 + k], (uint32_t)__popc(peers));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (k < kClasses) mlist[k * mcap + base + __popc(peers & ((1u << lane) - 1u))] = i;
         if (i == 0) {
             tot[0] = ts;
             tot[1] = tm;
             tot[2] = oh[n - 1];
             tot[3] = rh[n - 1];
+        }
+    }
+}
+
+// one thread per listed tiny node (<= kTinySeg entries): an odd-even transposition
+// network over registers (padding keys 0xffffffff sort last)
+__global__ void tiny_sort_kernel(const uint32_t* __restrict__ list, const uint32_t* __restrict__ list_count,
+                                 const uint32_t* __restrict__ off, const uint32_t* __restrict__ cnt,
+                                 const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ vals,
+                                 unsigned long long* __restrict__ keys2, uint32_t* __restrict__ vals2) {
+    const uint32_t nl = *list_count;
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nl; t += gridDim.x * blockDim.x) {
+        const uint32_t nd = list[t], o = off[nd], k = cnt[nd];
+        uint32_t kk[kTinySeg], vv[kTinySeg];
+#pragma unroll
+        for (uint32_t q = 0; q < kTinySeg; ++q) {
+            kk[q] = q < k ? (uint32_t)keys[o + q] : 0xffffffffu;
+            vv[q] = q < k ? vals[o + q] : 0u;
+        }
+        // n rounds sort n elements; most tiny lists have <= 4 entries
+        auto network = [&](auto nn) {
+            constexpr uint32_t N = decltype(nn)::value;
+#pragma unroll
+            for (uint32_t r = 0; r < N; ++r) {
+#pragma unroll
+                for (uint32_t q = r & 1; q + 1 < N; q += 2) {
+                    const bool sw = kk[q] > kk[q + 1];
+                    const uint32_t a = kk[q], b = kk[q + 1], va = vv[q], vb = vv[q + 1];
+                    kk[q] = sw ? b : a;
+                    kk[q + 1] = sw ? a : b;
+                    vv[q] = sw ? vb : va;
+                    vv[q + 1] = sw ? va : vb;
+                }
+            }
+        };
+        if (k > 4) network(std::integral_constant<uint32_t, kTinySeg>{});
+        else if (k > 1) network(std::integral_constant<uint32_t, 4>{});
+#pragma unroll
+        for (uint32_t q = 0; q < kTinySeg; ++q)
+            if (q < k) {
+                keys2[o + q] = (unsigned long long)nd << 32 | kk[q];
+                vals2[o + q] = vv[q];
+            }
+    }
+}
+
+// one warp per listed small node (<= kSmallSeg entries): a bitonic sort of 64
+// (two per lane: positions lane and lane + 32) over shuffles
+__global__ void warp_sort_kernel(const uint32_t* __restrict__ list, const uint32_t* __restrict__ list_count,
+                                 const uint32_t* __restrict__ off, const uint32_t* __restrict__ cnt,
+                                 const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ vals,
+                                 unsigned long long* __restrict__ keys2, uint32_t* __restrict__ vals2) {
+    const uint32_t nl = *list_count, lane = threadIdx.x & 31;
+    const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nl; w += warps) {
+        const uint32_t nd = list[w], o = off[nd], k = cnt[nd];
+        uint32_t ka = lane < k ? (uint32_t)keys[o + lane] : 0xffffffffu;
+        uint32_t va = lane < k ? vals[o + lane] : 0u;
+        uint32_t kb = lane + 32 < k ? (uint32_t)keys[o + lane + 32] : 0xffffffffu;
+        uint32_t vb = lane + 32 < k ? vals[o + lane + 32] : 0u;
+        // element at position p: p < 32 in (ka, va) of lane p, else (kb, vb) of lane p - 32
+#pragma unroll
+        for (uint32_t size = 2; size <= 64; size <<= 1) {
+#pragma unroll
+            for (uint32_t j = size >> 1; j > 0; j >>= 1) {
+                if (j == 32) { // partners are the two elements of one lane (size == 64: ascending)
+                    const bool sw = ka > kb;
+                    const uint32_t k0 = sw ? kb : ka, k1 = sw ? ka : kb, v0 = sw ? vb : va, v1 = sw ? va : vb;
+                    ka = k0, kb = k1, va = v0, vb = v1;
+                } else {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        uint32_t& kx = h ? kb : ka;
+                        uint32_t& vx = h ? vb : va;
+                        const uint32_t p = lane + 32 * h;
+                        const uint32_t ko = __shfl_xor_sync(0xffffffffu, kx, j), vo = __shfl_xor_sync(0xffffffffu, vx, j);
+                        const bool up = (p & size) == 0, lower = (p & j) == 0;
+                        // the lower position keeps the min when ascending, the max when descending
+                        const bool take = lower == up ? ko < kx : ko > kx;
+                        kx = take ? ko : kx;
+                        vx = take ? vo : vx;
+                    }
+                }
+            }
+        }
+        if (lane < k) {
+            keys2[o + lane] = (unsigned long long)nd << 32 | ka;
+            vals2[o + lane] = va;
+        }
+        if (lane + 32 < k) {
+            keys2[o + lane + 32] = (unsigned long long)nd << 32 | kb;
+            vals2[o + lane + 32] = vb;
         }
     }
 }
@@ -580,7 +682,7 @@ __global__ void __launch_bounds__(T) node_sort_kernel(const uint32_t* __restrict
 
 struct Layout {
     uint64_t nv, ne, L, emax;
-    size_t o_meta, o_cs, o_cm, o_ch, o_fh, o_os, o_om, o_oh, o_rh, o_end, o_khi, o_big, o_mlist, o_tot;
+    size_t o_meta, o_cs, o_cm, o_ch, o_fh, o_os, o_om, o_oh, o_rh, o_khi, o_big, o_mlist, o_tot;
     size_t o_vk, o_vs, o_vid, o_vsid, o_vrank, o_V, o_m, o_cnt, o_off, o_keys, o_vals, o_keys2, o_vals2, o_erec, o_packed, o_flag, o_fbidx, o_fbcnt,
         o_fbpts, o_fbbits, o_fbebits, o_line, o_tmp, tmp_bytes, total;
 };
@@ -605,11 +707,7 @@ Layout layout(uint64_t nv, uint64_t ne, uint64_t n_pts) {
     cub::DeviceScan::ExclusiveSum(nullptr, t3, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)(2 * l.L + 1));
     cub::DeviceRadixSort::SortPairs(nullptr, t4, (unsigned long long*)nullptr, (unsigned long long*)nullptr,
                                     (uint32_t*)nullptr, (uint32_t*)nullptr, (int)l.emax, 0, 64);
-    size_t t5 = 0;
-    cub::DeviceSegmentedSort::SortPairs(nullptr, t5, (unsigned long long*)nullptr, (unsigned long long*)nullptr,
-                                        (uint32_t*)nullptr, (uint32_t*)nullptr, (int)l.emax, (int)(2 * l.L),
-                                        (uint32_t*)nullptr, (uint32_t*)nullptr);
-    l.tmp_bytes = std::max({t1, t2, t3, t4, t5, (size_t)256});
+    l.tmp_bytes = std::max({t1, t2, t3, t4, (size_t)256});
     size_t o = 0;
     auto put = [&](size_t bytes) {
         const size_t at = o;
@@ -625,11 +723,11 @@ Layout layout(uint64_t nv, uint64_t ne, uint64_t n_pts) {
     l.o_m = put(16);
     l.o_cnt = put((2 * l.L + 1) * 4);
     l.o_off = put((2 * l.L + 1) * 4);
-    for (size_t* o_split : {&l.o_cs, &l.o_cm, &l.o_ch, &l.o_fh, &l.o_os, &l.o_om, &l.o_oh, &l.o_rh, &l.o_end,
+    for (size_t* o_split : {&l.o_cs, &l.o_cm, &l.o_ch, &l.o_fh, &l.o_os, &l.o_om, &l.o_oh, &l.o_rh,
                             &l.o_khi, &l.o_big})
         *o_split = put((2 * l.L + 1) * 4);
-    l.o_mlist = put(3 * (2 * l.L + 1) * 4);
-    l.o_tot = put(32);
+    l.o_mlist = put(kClasses * (2 * l.L + 1) * 4);
+    l.o_tot = put(64);
     l.o_keys = put(l.emax * 8);
     l.o_vals = put(l.emax * 4);
     l.o_keys2 = put(l.emax * 8);
@@ -682,7 +780,7 @@ cudaError_t launch_tree_phase(const TreeArgs& a, void* scratch, cudaStream_t st,
     uint32_t* off = reinterpret_cast<uint32_t*>(s + l.o_off);
     auto u32 = [&](size_t o) { return reinterpret_cast<uint32_t*>(s + o); };
     uint32_t *cs = u32(l.o_cs), *cm = u32(l.o_cm), *ch = u32(l.o_ch), *fh = u32(l.o_fh), *os = u32(l.o_os),
-             *om = u32(l.o_om), *oh = u32(l.o_oh), *rh = u32(l.o_rh), *seg_end = u32(l.o_end), *khi = u32(l.o_khi),
+             *om = u32(l.o_om), *oh = u32(l.o_oh), *rh = u32(l.o_rh), *khi = u32(l.o_khi),
              *bignode = u32(l.o_big), *mlist = u32(l.o_mlist), *tot = u32(l.o_tot);
     unsigned long long* keys = reinterpret_cast<unsigned long long*>(s + l.o_keys);
     uint32_t* vals = reinterpret_cast<uint32_t*>(s + l.o_vals);
@@ -729,31 +827,33 @@ cudaError_t launch_tree_phase(const TreeArgs& a, void* scratch, cudaStream_t st,
             tmp_bytes = l.tmp_bytes;
             PC_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, in, out, n_nodes, st));
         }
-        PC_TRY(cudaMemsetAsync(tot, 0, 32, st));
-        offsets_kernel<<<grid, 256, 0, st>>>(cnt, (uint32_t)n_nodes, os, om, oh, rh, off, seg_end, khi, bignode, mlist,
+        PC_TRY(cudaMemsetAsync(tot, 0, 64, st));
+        offsets_kernel<<<grid, 256, 0, st>>>(cnt, (uint32_t)n_nodes, os, om, oh, rh, off, khi, bignode, mlist,
                                              (uint32_t)n_nodes, tot);
         PC_TRY(cudaMemsetAsync(cnt, 0, (2 * l.L + 1) * 4, st));
         edges_kernel<true><<<grid, 256, 0, st>>>(a.vx, a.vy, ro, a.n_rings, a.n_verts, a.bbox_keys, vr, V, m_dev, L, cnt,
                                                  off, khi, keys, vals, line);
         // the split sizes come to the host (item counts of the sorts, grid sizes)
-        uint32_t h_tot[7] = {0, 0, 0, 0, 0, 0, 0};
-        PC_TRY(cudaMemcpyAsync(h_tot, tot, 28, cudaMemcpyDeviceToHost, st));
+        uint32_t h_tot[4 + kClasses] = {};
+        PC_TRY(cudaMemcpyAsync(h_tot, tot, sizeof(h_tot), cudaMemcpyDeviceToHost, st));
         PC_TRY(cudaStreamSynchronize(st));
-        if (h_tot[0]) {
-            tmp_bytes = l.tmp_bytes;
-            PC_TRY(cub::DeviceSegmentedSort::SortPairs(tmp, tmp_bytes, keys, keys2, vals, vals2, (int)h_tot[0],
-                                                       n_nodes - 1, off, seg_end, st));
-        }
-        auto mid_grid = [&](uint32_t k) { return std::max(1u, std::min(k, (uint32_t)grid * 4)); };
-        if (h_tot[4])
-            node_sort_kernel<64, 4><<<mid_grid(h_tot[4]), 64, 0, st>>>(mlist, tot + 4, off, cnt, keys, vals, keys2,
-                                                                      vals2);
-        if (h_tot[5])
-            node_sort_kernel<128, 8><<<mid_grid(h_tot[5]), 128, 0, st>>>(mlist + n_nodes, tot + 5, off, cnt, keys, vals,
-                                                                        keys2, vals2);
+        auto cls_grid = [&](uint32_t k, uint32_t per_block) {
+            return std::max(1u, std::min((k + per_block - 1) / per_block, (uint32_t)grid * 4));
+        };
+        const uint32_t* lists = mlist;
+        if (h_tot[4]) tiny_sort_kernel<<<cls_grid(h_tot[4], 256), 256, 0, st>>>(lists, tot + 4, off, cnt, keys, vals, keys2,
+                                                                               vals2);
+        if (h_tot[5]) warp_sort_kernel<<<cls_grid(h_tot[5], 8), 256, 0, st>>>(lists + n_nodes, tot + 5, off, cnt, keys,
+                                                                             vals, keys2, vals2);
         if (h_tot[6])
-            node_sort_kernel<256, 16><<<mid_grid(h_tot[6]), 256, 0, st>>>(mlist + 2 * n_nodes, tot + 6, off, cnt, keys,
+            node_sort_kernel<64, 4><<<cls_grid(h_tot[6], 1), 64, 0, st>>>(lists + 2 * n_nodes, tot + 6, off, cnt, keys,
                                                                          vals, keys2, vals2);
+        if (h_tot[7])
+            node_sort_kernel<128, 8><<<cls_grid(h_tot[7], 1), 128, 0, st>>>(lists + 3 * n_nodes, tot + 7, off, cnt,
+                                                                           keys, vals, keys2, vals2);
+        if (h_tot[8])
+            node_sort_kernel<256, 16><<<cls_grid(h_tot[8], 1), 256, 0, st>>>(lists + 4 * n_nodes, tot + 8, off, cnt,
+                                                                            keys, vals, keys2, vals2);
         if (h_tot[2]) {
             const uint32_t o = h_tot[0] + h_tot[1];
             const int bits = 32 + (32 - __builtin_clz(std::max(h_tot[3], 1u)));
