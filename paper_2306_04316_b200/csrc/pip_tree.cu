@@ -117,11 +117,43 @@ __device__ __forceinline__ uint32_t ring_of(const unsigned long long* __restrict
 }
 
 __global__ void vkey_kernel(const double* __restrict__ vy, uint64_t nv, const unsigned long long* __restrict__ bbox_keys,
-                            uint64_t* __restrict__ vk, uint32_t* __restrict__ vid) {
+                            uint64_t* __restrict__ vk, uint32_t* __restrict__ vhi, uint32_t* __restrict__ vid) {
     const Map m = map_of(bbox_keys);
     for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nv; v += (uint64_t)gridDim.x * blockDim.x) {
-        vk[v] = key53(vy[v], m);
+        const uint64_t k = key53(vy[v], m);
+        vk[v] = k;
+        vhi[v] = (uint32_t)(k >> 21); // the top 32 of the 53 bits: the radix sort's key
         vid[v] = (uint32_t)v;
+    }
+}
+
+// full keys in the order of the 32-bit sort
+__global__ void vgather_kernel(const uint64_t* __restrict__ vk, const uint32_t* __restrict__ vsid, uint64_t nv,
+                               uint64_t* __restrict__ vs) {
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < nv; p += (uint64_t)gridDim.x * blockDim.x)
+        vs[p] = vk[vsid[p]];
+}
+
+// runs of equal top 32 bits (rare: y values within 2^-32 local of each other)
+// sorted by the full key, one thread per run (insertion sort, the ids move along)
+__global__ void vfix_kernel(const uint32_t* __restrict__ vhs, uint64_t nv, uint64_t* __restrict__ vs,
+                            uint32_t* __restrict__ vsid) {
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p + 1 < nv;
+         p += (uint64_t)gridDim.x * blockDim.x) {
+        if (vhs[p + 1] != vhs[p] || (p > 0 && vhs[p - 1] == vhs[p])) continue; // not a run start
+        uint64_t e = p + 1;
+        while (e < nv && vhs[e] == vhs[p]) ++e;
+        for (uint64_t i = p + 1; i < e; ++i) {
+            const uint64_t k = vs[i];
+            const uint32_t id = vsid[i];
+            uint64_t j = i;
+            for (; j > p && vs[j - 1] > k; --j) {
+                vs[j] = vs[j - 1];
+                vsid[j] = vsid[j - 1];
+            }
+            vs[j] = k;
+            vsid[j] = id;
+        }
     }
 }
 
@@ -683,7 +715,7 @@ __global__ void __launch_bounds__(T) node_sort_kernel(const uint32_t* __restrict
 struct Layout {
     uint64_t nv, ne, L, emax;
     size_t o_meta, o_cs, o_cm, o_ch, o_fh, o_os, o_om, o_oh, o_rh, o_khi, o_big, o_mlist, o_tot;
-    size_t o_vk, o_vs, o_vid, o_vsid, o_vrank, o_V, o_m, o_cnt, o_off, o_keys, o_vals, o_keys2, o_vals2, o_erec, o_packed, o_flag, o_fbidx, o_fbcnt,
+    size_t o_vk, o_vs, o_vid, o_vhi, o_vhs, o_vsid, o_vrank, o_V, o_m, o_cnt, o_off, o_keys, o_vals, o_keys2, o_vals2, o_erec, o_packed, o_flag, o_fbidx, o_fbcnt,
         o_fbpts, o_fbbits, o_fbebits, o_line, o_tmp, tmp_bytes, total;
 };
 
@@ -698,8 +730,8 @@ Layout layout(uint64_t nv, uint64_t ne, uint64_t n_pts) {
     l.emax = std::max<uint64_t>(ne * 2ull * (depth + 1), nv);
     // CUB temporary storage: the largest of the four primitives
     size_t t1 = 0, t2 = 0, t3 = 0, t4 = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, t1, (uint64_t*)nullptr, (uint64_t*)nullptr, (uint32_t*)nullptr,
-                                    (uint32_t*)nullptr, (int)nv, 0, 53);
+    cub::DeviceRadixSort::SortPairs(nullptr, t1, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                    (uint32_t*)nullptr, (int)nv, 0, 32);
     size_t t6 = 0;
     cub::DeviceScan::InclusiveSum(nullptr, t6, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)nv);
     t1 = std::max(t1, t6);
@@ -717,6 +749,8 @@ Layout layout(uint64_t nv, uint64_t ne, uint64_t n_pts) {
     l.o_vk = put(nv * 8);
     l.o_vs = put(nv * 8);
     l.o_vid = put(nv * 4);
+    l.o_vhi = put(nv * 4);
+    l.o_vhs = put(nv * 4);
     l.o_vsid = put(nv * 4);
     l.o_vrank = put(nv * 4);
     l.o_V = put(nv * 8);
@@ -772,6 +806,8 @@ cudaError_t launch_tree_phase(const TreeArgs& a, void* scratch, cudaStream_t st,
     uint64_t* vk = reinterpret_cast<uint64_t*>(s + l.o_vk);
     uint64_t* vs = reinterpret_cast<uint64_t*>(s + l.o_vs);
     uint32_t* vid = reinterpret_cast<uint32_t*>(s + l.o_vid);
+    uint32_t* vhi = reinterpret_cast<uint32_t*>(s + l.o_vhi);
+    uint32_t* vhs = reinterpret_cast<uint32_t*>(s + l.o_vhs);
     uint32_t* vsid = reinterpret_cast<uint32_t*>(s + l.o_vsid);
     uint32_t* vrank = reinterpret_cast<uint32_t*>(s + l.o_vrank);
     uint64_t* V = reinterpret_cast<uint64_t*>(s + l.o_V);
@@ -807,8 +843,12 @@ cudaError_t launch_tree_phase(const TreeArgs& a, void* scratch, cudaStream_t st,
     if ((e = (x)) != cudaSuccess) return e
     if (phase == kTreeBuild) {
         // ---- build ----
-        vkey_kernel<<<grid, 256, 0, st>>>(a.vy, a.n_verts, a.bbox_keys, vk, vid);
-        PC_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, vk, vs, vid, vsid, (int)a.n_verts, 0, 53, st));
+        // vertex keys sorted on their top 32 bits (4 radix passes instead of 7), then
+        // runs of equal top bits fixed up on the full 53
+        vkey_kernel<<<grid, 256, 0, st>>>(a.vy, a.n_verts, a.bbox_keys, vk, vhi, vid);
+        PC_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, vhi, vhs, vid, vsid, (int)a.n_verts, 0, 32, st));
+        vgather_kernel<<<grid, 256, 0, st>>>(vk, vsid, a.n_verts, vs);
+        vfix_kernel<<<grid, 256, 0, st>>>(vhs, a.n_verts, vs, vsid);
         tmp_bytes = l.tmp_bytes;
         PC_TRY(cub::DeviceSelect::Unique(tmp, tmp_bytes, vs, V, m_dev, (int)a.n_verts, st));
         // vertex ranks among the distinct keys (vid is free again: first-occurrence flags, then their sums)
@@ -864,7 +904,7 @@ cudaError_t launch_tree_phase(const TreeArgs& a, void* scratch, cudaStream_t st,
         erec_kernel<<<grid, 256, 0, st>>>(rec, (uint32_t)a.n_edges, erec);
         verify_pack_kernel<<<grid, 256, 0, st>>>(vals2, keys2, tot, bignode, L, V, m_dev, line, erec, packed, flag);
         meta_kernel<<<grid, 256, 0, st>>>(off, cnt, flag, (uint32_t)(2 * l.L), meta);
-        *launches += 17;
+        *launches += 19;
         return cudaGetLastError();
     }
     // ---- query ----

@@ -71,6 +71,25 @@ def test_points_on_vertices_levels_and_edges(tree_on):
     _check(tree_on, xy, poly)
 
 
+def test_vertex_y_clusters(tree_on):
+    """Vertices whose y differ below 2^-32 of the polygon's height (the vertex
+    keys' radix sort orders the top 32 of their 53 bits and fixes up such runs
+    on the full key), with points on, between and just off those y-levels."""
+    from paper_2306_04316_b200.engine import Polygon
+    rng = np.random.default_rng(21)
+    base = W.star_polygon(6000, seed=21)
+    vx, vy = base.vx.copy(), base.vy.copy()
+    # snap to a coarse grid of levels, then spread inside each level by < 2^-32
+    vy[:-1] = np.round(vy[:-1] * 64) / 64 + rng.integers(0, 8, len(vy) - 1) * 1e-12
+    vy[-1] = vy[0]
+    poly = Polygon(vx, vy, base.ring_off)
+    lv = np.unique(vy)
+    y = np.concatenate([lv, lv + 5e-13, np.nextafter(lv, np.inf), np.nextafter(lv, -np.inf)])
+    xy = np.stack([rng.uniform(-1, 1, len(y)), y], 1)
+    xy = np.ascontiguousarray(np.concatenate([xy, W.uniform_points(30_000, W.bounds(poly), 22)]))
+    _check(tree_on, xy, poly)
+
+
 def test_overlapping_holes_and_self_intersections(tree_on):
     rng = np.random.default_rng(12)
     rings = [np.stack([np.cos(t) * 100, np.sin(t) * 100], 1) for t in [np.linspace(0, 2 * np.pi, 3001)]]
