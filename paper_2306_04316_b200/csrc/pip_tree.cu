@@ -207,7 +207,7 @@ __global__ void edges_kernel(const double* __restrict__ vx, const double* __rest
                              const unsigned long long* __restrict__ bbox_keys, const uint32_t* __restrict__ vrank,
                              const uint64_t* __restrict__ V, const uint32_t* __restrict__ m_dev, uint32_t L,
                              uint32_t* __restrict__ cnt,
-                             const uint32_t* __restrict__ off, const uint32_t* __restrict__ khi,
+                             const uint2* __restrict__ okh, const double* __restrict__ nmid,
                              unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals,
                              double4* __restrict__ line) {
     const Map mp = map_of(bbox_keys);
@@ -248,9 +248,8 @@ __global__ void edges_kernel(const double* __restrict__ vx, const double* __rest
                 uint32_t base = 0;
                 if (lead) base = atomicAdd(&cnt[nd], lead);
                 base = __shfl_sync(same, base, __ffs(same) - 1);
-                const int d = 31 - __clz(nd);
-                const uint32_t span = L >> d, a = (nd - (1u << d)) * span, b = a + span;
-                const double ym = ((double)V[a] + (double)V[min(b, m - 1)]) * 0x1p-54; // middle, local units
+                const double ym = nmid[nd];   // the node's middle y, local units
+                const uint2 ok = okh[nd];      // {list offset, key high word}
                 // x at the middle as 32-bit fixed point: two edges the key misorders are
                 // within 2^-32 there, hence within 2^-31 over the whole range (the
                 // difference of two non-crossing segments is linear and keeps its sign)
@@ -258,8 +257,8 @@ __global__ void edges_kernel(const double* __restrict__ vx, const double* __rest
                 xm = xm > 0.0 ? xm : 0.0;
                 xm = xm < 4294967294.0 ? xm : 4294967294.0; // below the mid-node sort's padding key
                 const uint32_t key = (uint32_t)xm;
-                const uint32_t slot = off[nd] + base + rank;
-                keys[slot] = (unsigned long long)khi[nd] << 32 | key; // (node or big-node rank, x)
+                const uint32_t slot = ok.x + base + rank;
+                keys[slot] = (unsigned long long)ok.y << 32 | key; // (node or big-node rank, x)
                 vals[slot] = e;
             });
         }
@@ -554,7 +553,10 @@ __global__ void offsets_kernel(const uint32_t* __restrict__ cnt, uint32_t n, con
                                const uint32_t* __restrict__ rh, uint32_t* __restrict__ off,
                                uint32_t* __restrict__ khi,
                                uint32_t* __restrict__ bignode, uint32_t* __restrict__ mlist, uint32_t mcap,
-                               uint32_t* __restrict__ tot) {
+                               uint32_t* __restrict__ tot, const uint64_t* __restrict__ V,
+                               const uint32_t* __restrict__ m_dev, uint32_t L, uint2* __restrict__ okh,
+                               double* __restrict__ nmid) {
+    const uint32_t m = *m_dev;
     // cnt[n - 1] == 0: the last exclusive sums are the totals
     const uint32_t ts = os[n - 1], tm = om[n - 1];
     const uint32_t lane = threadIdx.x & 31;
@@ -564,9 +566,16 @@ __global__ void offsets_kernel(const uint32_t* __restrict__ cnt, uint32_t n, con
         const uint32_t c = i < n ? cnt[i] : 0u;
         const bool mid = c > kSmallSeg && c <= kMidSeg, huge = c > kMidSeg;
         if (i < n) {
-            off[i] = huge ? ts + tm + oh[i] : mid ? ts + om[i] : os[i];
-            khi[i] = huge ? rh[i] : i;
+            const uint32_t o = huge ? ts + tm + oh[i] : mid ? ts + om[i] : os[i], h = huge ? rh[i] : i;
+            off[i] = o;
+            khi[i] = h;
+            okh[i] = make_uint2(o, h);
             if (huge) bignode[rh[i]] = i;
+            if (c) { // the middle of the node's key range, local units (the fill's x-order point)
+                const int d = 31 - __clz(i);
+                const uint32_t span = L >> d, a = (i - (1u << d)) * span, b = a + span;
+                nmid[i] = ((double)V[a] + (double)V[min(b, m - 1)]) * 0x1p-54;
+            }
         }
         const int k = !c || huge ? kClasses
                       : c <= kTinySeg ? 0 : c <= kSmallSeg ? 1 : c <= kMidClass[0] ? 2 : c <= kMidClass[1] ? 3 : 4;
@@ -714,7 +723,7 @@ __global__ void __launch_bounds__(T) node_sort_kernel(const uint32_t* __restrict
 
 struct Layout {
     uint64_t nv, ne, L, emax;
-    size_t o_meta, o_cs, o_cm, o_ch, o_fh, o_os, o_om, o_oh, o_rh, o_khi, o_big, o_mlist, o_tot;
+    size_t o_meta, o_okh, o_nmid, o_cs, o_cm, o_ch, o_fh, o_os, o_om, o_oh, o_rh, o_khi, o_big, o_mlist, o_tot;
     size_t o_vk, o_vs, o_vid, o_vhi, o_vhs, o_vsid, o_vrank, o_V, o_m, o_cnt, o_off, o_keys, o_vals, o_keys2, o_vals2, o_erec, o_packed, o_flag, o_fbidx, o_fbcnt,
         o_fbpts, o_fbbits, o_fbebits, o_line, o_tmp, tmp_bytes, total;
 };
@@ -770,6 +779,8 @@ Layout layout(uint64_t nv, uint64_t ne, uint64_t n_pts) {
     l.o_packed = put(l.emax * 16);
     l.o_flag = put(2 * l.L);
     l.o_meta = put(2 * l.L * 8);
+    l.o_okh = put((2 * l.L + 1) * 8);
+    l.o_nmid = put((2 * l.L + 1) * 8);
     l.o_fbidx = put(n_pts * 4 + 4);
     l.o_fbcnt = put(16);
     l.o_fbpts = put(n_pts * 16 + 16);
@@ -826,6 +837,8 @@ cudaError_t launch_tree_phase(const TreeArgs& a, void* scratch, cudaStream_t st,
     float4* packed = reinterpret_cast<float4*>(s + l.o_packed);
     uint8_t* flag = reinterpret_cast<uint8_t*>(s + l.o_flag);
     uint2* meta = reinterpret_cast<uint2*>(s + l.o_meta);
+    uint2* okh = reinterpret_cast<uint2*>(s + l.o_okh);
+    double* nmid = reinterpret_cast<double*>(s + l.o_nmid);
     uint32_t* fb_idx = reinterpret_cast<uint32_t*>(s + l.o_fbidx);
     uint32_t* fb_cnt = reinterpret_cast<uint32_t*>(s + l.o_fbcnt);
     double* fb_pts = reinterpret_cast<double*>(s + l.o_fbpts);
@@ -869,10 +882,10 @@ cudaError_t launch_tree_phase(const TreeArgs& a, void* scratch, cudaStream_t st,
         }
         PC_TRY(cudaMemsetAsync(tot, 0, 64, st));
         offsets_kernel<<<grid, 256, 0, st>>>(cnt, (uint32_t)n_nodes, os, om, oh, rh, off, khi, bignode, mlist,
-                                             (uint32_t)n_nodes, tot);
+                                             (uint32_t)n_nodes, tot, V, m_dev, L, okh, nmid);
         PC_TRY(cudaMemsetAsync(cnt, 0, (2 * l.L + 1) * 4, st));
         edges_kernel<true><<<grid, 256, 0, st>>>(a.vx, a.vy, ro, a.n_rings, a.n_verts, a.bbox_keys, vr, V, m_dev, L, cnt,
-                                                 off, khi, keys, vals, line);
+                                                 okh, nmid, keys, vals, line);
         // the split sizes come to the host (item counts of the sorts, grid sizes)
         uint32_t h_tot[4 + kClasses] = {};
         PC_TRY(cudaMemcpyAsync(h_tot, tot, sizeof(h_tot), cudaMemcpyDeviceToHost, st));
