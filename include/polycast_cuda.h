@@ -101,7 +101,9 @@ int pc_count_crossings(pc_ctx* ctx, const double* pts_xy, uint64_t n, const doub
                        uint8_t* degenerate);
 
 /* Device-pointer variants on the context's GPU `dev_index`, enqueued on
- * `stream` (a cudaStream_t; NULL = the context's stream) and NOT synchronised.
+ * `stream` (a cudaStream_t; NULL = the context's stream) and NOT synchronised
+ * (the segment-tree path of pc_classify_dev waits on the stream twice for
+ * sizes it needs on the host: its node-list split and its fallback count).
  * d_inside_bits / d_aux_bits (ceil(n/32) words) and d_stats (4 x u64) are
  * required; d_verdicts is optional.  Used for kernel-only timing and by
  * callers that keep their data resident in HBM. */
