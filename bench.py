@@ -228,6 +228,8 @@ def run_ours(args, rank, world, local_rank):
     eng = Engine(devices=[local_rank])
     if args.bucket is not None:
         eng.set_bucketing(args.bucket)
+    if args.tree is not None:
+        eng.set_tree(args.tree)
     items = build_items(args.workload, rank, world)
     log(f"[rank {rank}] workload {args.workload}: {len(items)} items, "
         f"{sum(i.tests for i in items):.3e} tests/step, {sum(i.n_points for i in items)} points/step")
@@ -326,8 +328,8 @@ def run_ours(args, rank, world, local_rank):
                 "peak_source": "measured live: unfused DMUL+DADD probe (pc_measure_fp64_rate) on this GPU",
                 "flops_per_test": 2}
     roof["kernel"] = "pip_csr_kernel" if csr else "pip_single_kernel"
-    if not csr and args.mode == 0:
-        # C1 single polygons with >= 4096 vertices take the segment-tree path
+    if not csr and args.mode in (0, 1) and args.tree != 0:
+        # C1 / C2 single polygons with >= 4096 vertices take the segment-tree path
         # (pip_tree.cu, PC_OPT_TREE auto): O(log^2 n) comparisons per point instead
         # of a scan over the edges, so the reference-equivalent FP64 work per
         # second exceeds the FP64 peak by the algorithmic factor
@@ -526,6 +528,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--bucket", type=int, default=None, choices=[-1, 0, 1], help="y-bucketing: auto/off/on")
+    ap.add_argument("--tree", type=int, default=None, choices=[-1, 0, 1],
+                    help="segment tree for single polygons: auto/off (the linear scan only)/on")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)  # timing rule: at least 3 untimed warm-up steps (reported as run)
 
