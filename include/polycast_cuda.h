@@ -201,10 +201,18 @@ uint64_t pc_last_launch_count(const pc_ctx* ctx);
  *  PC_OPT_BUCKET_POINTS: -1 auto (default), 0 off, 1 on — y-bucket the points of
  *  a single-polygon call before classifying, for SIMT coherence (pip_sort.cu). */
 #define PC_OPT_BUCKET_POINTS 1
-/*  PC_OPT_TREE: -1 auto (default), 0 off, 1 on — C1 single polygons: count a
- *  point's crossings through a segment tree over the vertices' y-order
- *  (pip_tree.cu) instead of scanning the edges. */
+/*  PC_OPT_TREE: 0 off (default; -1 means the default), 1 on — an opt-in
+ *  extension OUTSIDE the reference's linear scan: C1/C2 single
+ *  polygons count a point's crossings through a segment tree over the
+ *  vertices' y-order (pip_tree.cu) instead of scanning the edges.  Never used
+ *  by the headline measurement. */
 #define PC_OPT_TREE 2
+/*  PC_OPT_EXACT: 0 off (default), 1 on — run only the literal binary64 loop of
+ *  the reference (pip_exact.cu: thread per point, every edge, __dadd_rn /
+ *  __dmul_rn in the reference's order; no filter keys, no fp32 certification,
+ *  no bucketing, no tree).  A checker for the fast path on full-size inputs;
+ *  results are identical by construction of the fast path. */
+#define PC_OPT_EXACT 3
 int pc_set_option(pc_ctx* ctx, int option, int64_t value);
 
 /* Measurement hooks (bench.py).  With profiling on, every call records a pair

@@ -72,7 +72,8 @@ struct pc_ctx {
     uint64_t launches = 0;
     bool profiling = false;
     int64_t bucket_mode = -1; // PC_OPT_BUCKET_POINTS: -1 auto, 0 off, 1 on
-    int64_t tree_mode = -1;   // PC_OPT_TREE: -1 auto, 0 off, 1 on
+    int64_t tree_mode = 0;    // PC_OPT_TREE: 0 off (default), 1 on (opt-in extension, not the reference scan)
+    bool exact = false;       // PC_OPT_EXACT: the literal binary64 loop only (pip_exact.cu)
 };
 
 namespace {
@@ -151,6 +152,23 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
     const uint64_t n_edges = n_verts - n_rings;
     if (n_edges > 0xffffffffull) invalid(c, "too many edges for one polygon (>= 2^32)");
     const uint64_t nwords = (n + 31) / 32;
+    if (c->exact) { // PC_OPT_EXACT: the literal loop over every (point, edge), then the same finalize
+        if (ready) {
+            const uint64_t cn = chunk && chunk < n ? chunk : n;
+            for (uint64_t lo = 0, k = 0; lo < n; lo += cn, ++k)
+                check(c, cudaStreamWaitEvent(st, ready[k], 0), "wait for the points upload");
+        }
+        check(c, d.bbox.ensure(8 * sizeof(double)), "alloc bbox");
+        check(c, cudaMemsetAsync(d_stats, 0, 4 * sizeof(unsigned long long), st), "clear stats");
+        mark_begin(c, d, st);
+        check(c, pcd::launch_exact_single(d_pts, n, d_vx, d_vy, d_ring_off, n_rings, prefilter, d.bbox.as<double>(),
+                                          mode, tol, d_inside, d_aux, st, &c->launches),
+              "exact kernel");
+        mark_end(c, d, st);
+        check(c, pcd::launch_finalize(n, d_inside, d_aux, d_verdicts, mode, d_stats, st, d.dev, &c->launches),
+              "finalize kernel");
+        return;
+    }
     check(c, d.filt.ensure(pcd::filt_words(n_edges) * sizeof(uint2)), "alloc edge keys");
     check(c, d.rec.ensure(std::max<uint64_t>(n_edges, 1) * pcd::edge_rec_bytes()), "alloc edge records");
     check(c, d.bbox.ensure(8 * sizeof(unsigned long long)), "alloc bbox"); // 4 keys + key map
@@ -171,7 +189,7 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
     pa.n_zero_words = nwords;
     check(c, pcd::launch_prep(pa, st, d.dev, &c->launches), "prep kernel");
     check(c, cudaMemsetAsync(d_aux, 0, nwords * 4, st), "clear aux plane");
-    const bool tree = (mode == 0 || mode == 1) /* C1, C2 */ && c->tree_mode != 0 && pcd::tree_eligible(n_verts, n, c->tree_mode == 1);
+    const bool tree = (mode == 0 || mode == 1) /* C1, C2 */ && c->tree_mode == 1 && pcd::tree_eligible(n_verts, n, true);
     const bool bucket = n < 0xffffffffull &&
                         (c->bucket_mode == 1 || (c->bucket_mode < 0 && n_edges >= 64 && n >= 4096));
     pcd::SingleArgs sa{};
@@ -290,10 +308,14 @@ void enqueue_csr(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts, u
     a.tol2 = tol * tol;
     a.inside_bits = d_inside;
     a.aux_bits = d_aux;
-    check(c, d.csr_meta.ensure(std::max<size_t>(pcd::csr_meta_bytes(n_polys), 16)), "alloc polygon metadata");
-    a.meta = d.csr_meta.p;
     mark_begin(c, d, st);
-    check(c, pcd::launch_csr(a, st, d.dev, &c->launches), "csr kernel");
+    if (c->exact) {
+        check(c, pcd::launch_exact_csr(a, n_points, st, &c->launches), "exact csr kernel");
+    } else {
+        check(c, d.csr_meta.ensure(std::max<size_t>(pcd::csr_meta_bytes(n_polys), 16)), "alloc polygon metadata");
+        a.meta = d.csr_meta.p;
+        check(c, pcd::launch_csr(a, st, d.dev, &c->launches), "csr kernel");
+    }
     mark_end(c, d, st);
     check(c, pcd::launch_finalize(n_points, d_inside, d_aux, d_verdicts, mode, d_stats, st, d.dev, &c->launches),
           "finalize kernel");
@@ -414,7 +436,11 @@ int pc_set_option(pc_ctx* c, int option, int64_t value) {
         return PC_OK;
     }
     if (option == PC_OPT_TREE && value >= -1 && value <= 1) {
-        c->tree_mode = value;
+        c->tree_mode = value == 1 ? 1 : 0;
+        return PC_OK;
+    }
+    if (option == PC_OPT_EXACT && (value == 0 || value == 1)) {
+        c->exact = value == 1;
         return PC_OK;
     }
     c->err = "unknown option or value";

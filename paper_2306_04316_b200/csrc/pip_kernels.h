@@ -153,6 +153,14 @@ cudaError_t launch_unbucket(uint64_t n, const uint32_t* n_dev, const uint32_t* s
                             const uint32_t* s_aux, uint32_t* inside_bits, uint32_t* aux_bits, cudaStream_t st, int dev,
                             uint64_t* launches);
 
+// The literal binary64 checker path (pip_exact.cu, PC_OPT_EXACT): writes every
+// word of both planes; box_scratch = 4 doubles of device memory (prefilter).
+cudaError_t launch_exact_single(const double* pts, uint64_t n, const double* vx, const double* vy,
+                                const uint64_t* ring_off, uint32_t n_rings, int prefilter, double* box_scratch,
+                                int mode, double tol, uint32_t* inside_bits, uint32_t* aux_bits, cudaStream_t st,
+                                uint64_t* launches);
+cudaError_t launch_exact_csr(const CsrArgs& a, uint64_t n_points, cudaStream_t st, uint64_t* launches);
+
 cudaError_t launch_fp64_probe(double* out, int iters, int dev, cudaStream_t st, double* flops);
 
 } // namespace pcd

@@ -199,9 +199,15 @@ class Engine:
         self.set_option(1, mode)
 
     def set_tree(self, mode: int):
-        """-1 auto, 0 off, 1 on (PC_OPT_TREE): the segment-tree C1 path for single
-        polygons; never changes results."""
+        """0 off (default), 1 on (PC_OPT_TREE): the opt-in segment-tree path for C1/C2
+        single polygons -- an extension outside the reference's linear scan; never
+        changes results."""
         self.set_option(2, mode)
+
+    def set_exact(self, on: bool):
+        """PC_OPT_EXACT: run only the literal binary64 loop (pip_exact.cu), the
+        full-size checker of the fast path."""
+        self.set_option(3, int(bool(on)))
 
     def set_profiling(self, on: bool = True):
         self._check(self.lib.pc_set_profiling(self.ctx, int(bool(on))), "pc_set_profiling")
