@@ -45,7 +45,7 @@ struct DevState {
     cudaStream_t stream = nullptr;
     cudaStream_t copy = nullptr; // points upload, overlapping polygon-only work on `stream` (made on first use)
     std::vector<cudaEvent_t> up_evs; // one per uploaded chunk
-    DevBuf pts, vx, vy, ring_off, pt_off, poly_ring_off, filt, rec, bbox, bits, verdicts, stats, counts, degen;
+    DevBuf pts, vx, vy, ring_off, pt_off, poly_ring_off, filt, qk, rec, bbox, bits, verdicts, stats, counts, degen;
     DevBuf bucket_scratch, sorted_pts, sorted_idx, bucket_blk; // y-bucketing (pip_sort.cu)
     DevBuf csr_meta;                                          // per-polygon records (pip_csr.cu)
     DevBuf cmp_blk, cmp_pts, cmp_idx, cmp_v, cmp_out;         // prefilter / scatter (pip_compact.cu)
@@ -169,7 +169,8 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
               "finalize kernel");
         return;
     }
-    check(c, d.filt.ensure(pcd::filt_words(n_edges) * sizeof(uint2)), "alloc edge keys");
+    check(c, d.filt.ensure(pcd::filt_words(n_edges) * sizeof(uint2)), "alloc edge filter words");
+    check(c, d.qk.ensure(pcd::qk_words(n_edges) * sizeof(uint32_t)), "alloc edge keys");
     check(c, d.rec.ensure(std::max<uint64_t>(n_edges, 1) * pcd::edge_rec_bytes()), "alloc edge records");
     check(c, d.bbox.ensure(8 * sizeof(unsigned long long)), "alloc bbox"); // 4 keys + key map
     pcd::PrepArgs pa{};
@@ -180,6 +181,7 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
     pa.n_rings = n_rings;
     pa.n_verts = n_verts;
     pa.filt = d.filt.as<uint2>();
+    pa.qk = d.qk.as<uint32_t>();
     pa.rec = d.rec.p;
     pa.bbox_keys = d.bbox.as<unsigned long long>();
     pa.stats = d_stats;
@@ -196,6 +198,7 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
     sa.mode = mode;
     sa.pts = d_pts;
     sa.n = n;
+    sa.qk = d.qk.as<uint32_t>();
     sa.filt = d.filt.as<uint2>();
     sa.rec = d.rec.p;
     sa.n_edges = (uint32_t)n_edges;
@@ -405,7 +408,7 @@ void pc_destroy(pc_ctx* c) {
     for (auto& d : c->devs) {
         cudaSetDevice(d.dev);
         cudaStreamSynchronize(d.stream);
-        for (DevBuf* b : {&d.pts, &d.vx, &d.vy, &d.ring_off, &d.pt_off, &d.poly_ring_off, &d.filt, &d.rec, &d.bbox,
+        for (DevBuf* b : {&d.pts, &d.vx, &d.vy, &d.ring_off, &d.pt_off, &d.poly_ring_off, &d.filt, &d.qk, &d.rec, &d.bbox,
                           &d.bits, &d.verdicts, &d.stats, &d.counts, &d.degen, &d.bucket_scratch, &d.sorted_pts,
                           &d.sorted_idx, &d.bucket_blk, &d.csr_meta, &d.cmp_blk, &d.cmp_pts, &d.cmp_idx, &d.cmp_v,
                           &d.cmp_out, &d.csv_text, &d.csv_state, &d.csv_res, &d.csv_out, &d.emit_recs,

@@ -74,6 +74,34 @@ __device__ __forceinline__ QMap qmap_from_bbox(const unsigned long long* bbox_ke
     return m;
 }
 
+// A map on an arbitrary y range [lo, hi] (pip_single.cu: the y range of a
+// CTA's points), keeping every point key strictly inside the key range:
+// y < lo -> 0, y > hi -> 32766, [lo, hi] -> 1 .. 32765.  So an edge that extends
+// past the CTA's points on one side never ties with the extreme point there.
+// Monotone non-decreasing (piecewise, each piece monotone and ordered), hence
+// exact as a filter like qkey15.
+struct CtaQMap {
+    double y0, y1, scale;
+};
+
+__device__ __forceinline__ CtaQMap ctaqmap_from_range(double y_lo, double y_hi) {
+    CtaQMap m;
+    m.y0 = q_collapse(y_lo);
+    m.y1 = q_collapse(y_hi);
+    const double h = __dsub_rn(m.y1, m.y0);
+    m.scale = (h > 0.0 && h < 1e300) ? __ddiv_rn(32764.0, h) : 0.0; // one y level: every point key is 1
+    return m;
+}
+
+__device__ __forceinline__ uint32_t qkey_cta(double y, const CtaQMap& m) {
+    const double c = q_collapse(y);
+    if (c < m.y0) return 0u;
+    if (c > m.y1) return 32766u;
+    double t = __dmul_rn(__dsub_rn(c, m.y0), m.scale);
+    t = t < 32764.0 ? t : 32764.0; // also NaN-free: c, y0 finite and scale < inf
+    return (uint32_t)t + 1u;
+}
+
 __device__ __forceinline__ uint32_t qkey15(double y, const QMap& m) {
     double t = __dmul_rn(__dsub_rn(q_collapse(y), m.y0), m.scale);
     t = t > 0.0 ? t : 0.0; // also maps a NaN product (0 * inf cannot occur: scale < inf) to 0
@@ -111,6 +139,22 @@ __device__ __forceinline__ LocalMap local_map_from_bbox(const unsigned long long
     return m;
 }
 
+// Per-edge scaling of a record's normal by the power of two 2^k that puts
+// max(|Nx|, |Ny|) in [1/2, 1) (exact; a zero normal stays zero).  Every fp32
+// operation of the side test then scales by exactly 2^k, so its sign is
+// unchanged, and the error bound of DESIGN.md §3.4 (derived for |Nx|, |Ny| <= 1)
+// holds as it stands: the fixed band B = 2^-20 becomes relative to the edge's
+// length instead of the polygon's size, so short edges (configs 2 and 4: local
+// lengths down to ~1e-5) are decided in fp32 instead of falling into the band.
+__device__ __forceinline__ void normalize_pow2(double& Nx, double& Ny) {
+    const double M = fmax(fabs(Nx), fabs(Ny));
+    if (M > 0.0 && M < 0.5) {
+        const double k = pow2_inv_above(M); // M * k in [1/2, 1)
+        Nx = __dmul_rn(Nx, k);
+        Ny = __dmul_rn(Ny, k);
+    }
+}
+
 // {Nx, Ny, c} of edge a->b with the reference's flipped normal (nx, ny); NaN
 // when the map is off or an endpoint lies outside the bbox (a hole poking out)
 __device__ __forceinline__ float3 local_side_record(const LocalMap& m, double ax, double ay, double bx, double by,
@@ -120,7 +164,8 @@ __device__ __forceinline__ float3 local_side_record(const LocalMap& m, double ax
     const bool ok = m.sx != 0.0 && axl >= 0.0 && axl < 1.0 && ayl >= 0.0 && ayl < 1.0 && bxl >= 0.0 && bxl < 1.0 &&
                     byl >= 0.0 && byl < 1.0;
     if (!ok) return make_float3(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
-    const double Nx = __dmul_rn(nx, m.sy), Ny = __dmul_rn(ny, m.sx);
+    double Nx = __dmul_rn(nx, m.sy), Ny = __dmul_rn(ny, m.sx);
+    normalize_pow2(Nx, Ny);
     const double cd = __dadd_rn(__dmul_rn(axl, Nx), __dmul_rn(ayl, Ny));
     // c + kLocalBand: the kernel's s' = s + B is then <= -0 (sign bit) for a sure
     // count and in [+0, 2B] for a band hit; the extra fp32 rounding of c + B
@@ -145,7 +190,8 @@ __device__ __forceinline__ float3 local_side_record_c2(const LocalMap& m, double
                     bxl < 1.0 && byl >= 0.0 && byl < 1.0;
     if (!ok) return make_float3(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
     const double sg = dy > 0.0 ? 1.0 : -1.0;
-    const double Nx = __dmul_rn(__dmul_rn(dy, m.sy), sg), Ny = __dmul_rn(__dmul_rn(-dx, m.sx), sg);
+    double Nx = __dmul_rn(__dmul_rn(dy, m.sy), sg), Ny = __dmul_rn(__dmul_rn(-dx, m.sx), sg);
+    normalize_pow2(Nx, Ny);
     const double cd = __dadd_rn(__dmul_rn(axl, Nx), __dmul_rn(ayl, Ny));
     return make_float3(__double2float_rn(Nx), __double2float_rn(Ny),
                        __double2float_rn(__dadd_rn(-cd, (double)kLocalBand)));

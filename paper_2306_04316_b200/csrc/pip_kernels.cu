@@ -72,18 +72,18 @@ __global__ void __launch_bounds__(256) prep_bbox_kernel(const double* __restrict
 }
 
 // One thread per vertex v: if (v, v+1) is an edge of the same ring, write its
-// filter pair and exact record at edge index e = v - ring(v).
-// The filter array is tile-blocked: for edge tile t (kEdgeTile edges) the
-// block filt[t*2*kEdgeTile ...] holds kEdgeTile key ranges (warp-level test)
-// followed by kEdgeTile per-point filter words, so one bulk copy stages both.
-//   C1/C2: range {q(ylo), q(yhi)}; word {(-q(ylo) mod 2^15) << 1 in both 16-bit
-//          halves, ((q(yhi) - q(ylo)) << 1) + 2 in both halves} (15-bit keys)
-//   Robust: range = word = {fkey(ylo), fkey(yhi)} (32-bit keys)
+// filter word, key word and exact record at edge index e = v - ring(v).
+//   key word (all modes): {0x7fff - q(ylo), q(yhi)} on the 15-bit map (the
+//          phase-1 key scan of pip_single.cu); padding words (edges >= n_edges
+//          up to qk_words) are 0, which never matches (q(ylo) would be 0x7fff)
+//   filter word C1/C2: {(-q(ylo) mod 2^15) << 1 in both 16-bit halves,
+//          ((q(yhi) - q(ylo)) << 1) + 2 in both halves} (15-bit keys)
+//   filter word Robust: {fkey(ylo), fkey(yhi)} (32-bit keys)
 template <int MODE>
 __global__ void __launch_bounds__(256) prep_edges_kernel(
     const double* __restrict__ vx, const double* __restrict__ vy, const uint64_t* __restrict__ ring_off,
-    uint32_t n_rings, uint64_t n_verts, uint2* __restrict__ filt, EdgeRec* __restrict__ rec,
-    unsigned long long* __restrict__ bbox_keys, double tol) {
+    uint32_t n_rings, uint64_t n_verts, uint2* __restrict__ filt, uint32_t* __restrict__ qk, uint64_t n_qk,
+    EdgeRec* __restrict__ rec, unsigned long long* __restrict__ bbox_keys, double tol) {
     const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const QMap qm = qmap_from_bbox(bbox_keys);
@@ -94,11 +94,11 @@ __global__ void __launch_bounds__(256) prep_edges_kernel(
         reinterpret_cast<double*>(bbox_keys)[6] = lm.sx;
         reinterpret_cast<double*>(bbox_keys)[7] = lm.sy;
     }
+    for (uint64_t e = n_verts - n_rings + tid; e < n_qk; e += stride) qk[e] = 0u;
     for (uint64_t v = tid; v < n_verts; v += stride) {
         const uint32_t r = ring_of(ring_off, n_rings, v);
         if (v + 1 >= ring_off[r + 1]) continue; // last (closing) vertex of its ring
         const uint64_t e = v - r;
-        const uint64_t fb = (e / kEdgeTile) * (2 * kEdgeTile) + e % kEdgeTile; // tile-blocked filter index
         const double ax = vx[v], ay = vy[v], bx = vx[v + 1], by = vy[v + 1];
         EdgeRec er;
 #pragma unroll
@@ -121,9 +121,7 @@ __global__ void __launch_bounds__(256) prep_edges_kernel(
             const float3 fr = local_side_record_c2(lr, ax, ay, bx, by, abx, aby);
             er.d[6] = __hiloint2double(__float_as_int(fr.y), __float_as_int(fr.x));
             er.d[7] = __hiloint2double(0, __float_as_int(fr.z));
-            const uint2 w = make_uint2((uint32_t)fkey(ylo), (uint32_t)fkey(yhi));
-            filt[fb] = w;
-            filt[fb + kEdgeTile] = w;
+            filt[e] = make_uint2((uint32_t)fkey(ylo), (uint32_t)fkey(yhi));
         } else {
             if (MODE == kC1) {
                 double nx = __dsub_rn(by, ay), ny = __dsub_rn(ax, bx);
@@ -151,9 +149,9 @@ __global__ void __launch_bounds__(256) prep_edges_kernel(
             // threshold + 1 in both halves: candidate iff min(d_lo, d_hi) < ((khi - klo) << 1) + 2
             // (<= 65534 since keys are <= 32766), see lane_candidate (pip_single.cu)
             const uint32_t thr1 = ((khi - klo) << 1) + 2u;
-            filt[fb] = make_uint2(klo, khi);
-            filt[fb + kEdgeTile] = make_uint2(neg | (neg << 16), thr1 | (thr1 << 16));
+            filt[e] = make_uint2(neg | (neg << 16), thr1 | (thr1 << 16));
         }
+        qk[e] = (0x7fffu - qkey15(ylo, qm)) | (qkey15(yhi, qm) << 16);
         rec[e] = er;
     }
 }
@@ -264,7 +262,8 @@ int sm_count(int dev) {
 
 } // namespace
 
-size_t filt_words(uint64_t n_edges) { return ((n_edges + kEdgeTile - 1) / kEdgeTile + 1) * 2 * kEdgeTile; }
+size_t filt_words(uint64_t n_edges) { return std::max<uint64_t>(n_edges, 1); }
+size_t qk_words(uint64_t n_edges) { return (std::max<uint64_t>(n_edges, 1) + kKeyTile - 1) / kKeyTile * kKeyTile; }
 
 size_t edge_rec_bytes() { return sizeof(EdgeRec); }
 
@@ -284,16 +283,16 @@ cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st, int dev, uint64_t* l
     const unsigned blocks = (unsigned)std::min<uint64_t>(a.n_verts / 256 + 1, (uint64_t)sm_count(dev) * 16);
     switch (a.mode) {
     case kC1:
-        prep_edges_kernel<kC1><<<blocks, 256, 0, st>>>(a.vx, a.vy, a.ring_off, a.n_rings, a.n_verts, a.filt,
-                                                       reinterpret_cast<EdgeRec*>(a.rec), a.bbox_keys, a.tol);
+        prep_edges_kernel<kC1><<<blocks, 256, 0, st>>>(a.vx, a.vy, a.ring_off, a.n_rings, a.n_verts, a.filt, a.qk,
+                                                       qk_words(a.n_verts - a.n_rings), reinterpret_cast<EdgeRec*>(a.rec), a.bbox_keys, a.tol);
         break;
     case kC2:
-        prep_edges_kernel<kC2><<<blocks, 256, 0, st>>>(a.vx, a.vy, a.ring_off, a.n_rings, a.n_verts, a.filt,
-                                                       reinterpret_cast<EdgeRec*>(a.rec), a.bbox_keys, a.tol);
+        prep_edges_kernel<kC2><<<blocks, 256, 0, st>>>(a.vx, a.vy, a.ring_off, a.n_rings, a.n_verts, a.filt, a.qk,
+                                                       qk_words(a.n_verts - a.n_rings), reinterpret_cast<EdgeRec*>(a.rec), a.bbox_keys, a.tol);
         break;
     default:
-        prep_edges_kernel<kRobust><<<blocks, 256, 0, st>>>(a.vx, a.vy, a.ring_off, a.n_rings, a.n_verts, a.filt,
-                                                           reinterpret_cast<EdgeRec*>(a.rec), a.bbox_keys, a.tol);
+        prep_edges_kernel<kRobust><<<blocks, 256, 0, st>>>(a.vx, a.vy, a.ring_off, a.n_rings, a.n_verts, a.filt, a.qk,
+                                                           qk_words(a.n_verts - a.n_rings), reinterpret_cast<EdgeRec*>(a.rec), a.bbox_keys, a.tol);
         break;
     }
     *launches += 2;

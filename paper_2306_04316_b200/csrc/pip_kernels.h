@@ -15,7 +15,8 @@ struct PrepArgs {
     const uint64_t* ring_off;
     uint32_t n_rings;
     uint64_t n_verts;
-    uint2* filt;                  // filter words, tile-blocked (see prep_edges_kernel)
+    uint2* filt;                  // per-edge per-point filter words (see prep_edges_kernel)
+    uint32_t* qk;                 // per-edge key words of the phase-1 key scan, padded to qk_words()
     void* rec;                    // n_edges EdgeRec (edge_rec_bytes() each)
     unsigned long long* bbox_keys; // 4 monotone keys: min x, min y, ~max x, ~max y; [4..5] 16-bit key map
     uint32_t* zero_words;          // output bit planes to clear (inside ++ aux, contiguous)
@@ -28,6 +29,7 @@ struct SingleArgs {
     int mode;
     const double* pts;
     uint64_t n;
+    const uint32_t* qk;
     const uint2* filt;
     const void* rec;
     uint32_t n_edges;
@@ -56,8 +58,9 @@ struct CsrArgs {
 };
 
 size_t edge_rec_bytes();
-constexpr int kEdgeTile = 256; // edges per filter block (= pip_single.cu's shared-memory stage)
-size_t filt_words(uint64_t n_edges); // uint2 entries of the tile-blocked filter array
+constexpr int kKeyTile = 2048;       // edge key words per stage of pip_single.cu's key scan
+size_t filt_words(uint64_t n_edges); // uint2 entries of the filter array
+size_t qk_words(uint64_t n_edges);   // uint32 entries of the key array (whole tiles, padding never matches)
 size_t csr_meta_bytes(uint64_t n_polys);
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st, int dev, uint64_t* launches);
 cudaError_t launch_single(const SingleArgs& a, cudaStream_t st, int dev, uint64_t* launches);

@@ -7,24 +7,25 @@
 // Error/Boundary flags OR-ed into the bit planes, so edge chunks combine
 // exactly like the reference's per-ring sums (geometry.hpp:285-299).
 //
-// Per thread: K points, of which only the 32-bit filter keys live in
-// registers (coordinates sit in shared memory, loaded once per CTA by one TMA
-// bulk copy); parity and aux flags are K-bit masks.  Warp w owns K*32
-// consecutive points (k-slice k = 32 consecutive points), which after
-// y-bucketing (pip_sort.cu) are y-adjacent, so an edge either misses the whole
-// warp or is a candidate for most of it.
+// Per thread: K points, of which only the filter keys live in registers
+// (coordinates sit in shared memory as polygon-local fp32, the binary64
+// fallbacks re-read them from L2); parity and aux flags are K-bit masks.  Warp
+// w owns K*32 consecutive points (k-slice k = 32 consecutive points), which
+// after y-bucketing (pip_sort.cu) are y-adjacent.
 //
-// Per edge (fast path, all points): d_k = key(p.y) - key(ylo) (mod 2^32) and
-// the running minimum of the d_k — one fused add+min (VIADDMNMX) per point —
-// then a single compare of the minimum against key(yhi)-key(ylo) decides, for
-// the whole warp, whether any point may straddle the edge (exactness argument
-// in DESIGN.md §3).  Only then (warp-uniform branch) does the slow path
-// re-derive which points are candidates and run the binary64 test of the
-// reference for them.
-//
-// Edge tiles (filter keys + exact records, precomputed by prep_edges_kernel)
-// stream into shared memory with TMA bulk copies, double-buffered on
-// mbarriers, while the previous tile is scanned.
+// The linear scan has two phases per CTA (every edge of the chunk is examined
+// for every CTA):
+//  1. Key scan.  The chunk's 4-byte edge key words (q(ylo), q(yhi) on the
+//     15-bit monotone map, prep_edges_kernel) stream through shared memory in
+//     8 KB tiles (TMA bulk copies, 2-stage mbarrier pipeline).  Each thread
+//     tests 8 edges per tile against the key range of ALL the CTA's points --
+//     one packed add + and per edge -- and appends the (rare) candidates to a
+//     shared list.  Exact: a non-candidate has both endpoints strictly above or
+//     below every point, so the reference counts nothing for it.
+//  2. Candidates.  The list's filter words and exact records are gathered
+//     from L2 into shared memory, 128 at a time, and every warp runs the
+//     per-point filter and the exact / certified edge test of the reference
+//     (slow_c1 / slow_c2 / slow_robust) on them.
 #include "pip_kernels.h"
 
 #include <cuda_runtime.h>
@@ -41,45 +42,30 @@ namespace pcd {
 namespace {
 
 constexpr int kTPB = 256;
-constexpr int kK = 16;      // points per thread
-constexpr int kTile = 256;  // edges per shared-memory stage (multiple of 2: 16-byte bulk copies)
-
-struct __align__(128) TileStage {
-    EdgeRec rec[kTile];
-    uint2 wkr[kTile];  // key range per edge (warp-level test)   } one bulk copy:
-    uint2 filt[kTile]; // per-point filter word                   } the tile-blocked block
-};
-static_assert(kTile == kEdgeTile, "the stage holds one filter block");
+constexpr int kK = 16;          // points per thread
+constexpr int kQTile = kKeyTile; // edge key words per shared-memory stage (8 KB; 8 per thread)
+constexpr int kListCap = 4096;  // candidate edge indices; a tile can add kQTile, so flush above kListCap - kQTile
+constexpr int kBatch = 128;     // candidates gathered per batch
+static_assert(kQTile == 8 * kTPB, "phase 1: 8 key words per thread per tile");
 
 // Every mode keeps only the polygon-local fp32 coordinates of its points in
 // shared memory (the certified fp32 side / intercept test); the binary64
 // fallbacks re-read the point from global memory (L2).
-template <int MODE>
 struct SingleShared {
-    using PointT = float2;
-    PointT pts[kTPB * kK]; // this CTA's points (bucketed order)
-    TileStage st[2];
+    float2 pts[kTPB * kK];       // this CTA's points (bucketed order), local fp32
+    uint4 qk[2][kQTile / 4];     // key-scan stages
+    uint32_t list[kListCap];     // candidate edges of the chunk (phase 1 -> phase 2)
+    uint2 bfilt[kBatch];         // gathered per-point filter words
+    EdgeRec brec[kBatch];        // gathered exact records
     unsigned long long full[2];
-    unsigned long long pbar;
+    uint32_t ncand;
+    uint32_t cta_lo, cta_hi;     // key range of the CTA's active points
+    unsigned long long cta_ylo, cta_yhi; // C1/C2: dkey of their min / max y (per-CTA key map)
+    uint32_t live;
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-
-// explicit shared-memory loads from a 32-bit shared address (kept in a
-// register by the caller, see the edge loop)
-__device__ __forceinline__ uint2 lds_u2(unsigned a) {
-    uint2 v;
-    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ EdgeRec lds_rec(unsigned a) {
-    EdgeRec r;
-#pragma unroll
-    for (int i = 0; i < 8; i += 2)
-        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r.d[i]), "=d"(r.d[i + 1]) : "r"(a + 8u * i));
-    return r;
 }
 
 __device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
@@ -97,22 +83,25 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
     }
 }
 
-// One elected thread: load tile [t0, t0+nt) of the edge arrays into stage s.
-template <class Shared>
-__device__ __forceinline__ void issue_tile(Shared& sh, int s, const uint2* filt, const EdgeRec* rec,
-                                           uint32_t t0, uint32_t nt) {
-    const unsigned fb = 2u * kTile * 8u; // the whole block of ranges + words (t0 is tile-aligned)
-    const unsigned rb = nt * (unsigned)sizeof(EdgeRec);
+// One elected thread: load key tile [t0, t0 + kQTile) into stage s (the key
+// array is padded to whole tiles with never-candidate words).
+__device__ __forceinline__ void issue_tile(SingleShared& sh, int s, const uint32_t* qk, uint32_t t0) {
+    const unsigned bytes = kQTile * 4u;
     const unsigned bar = smem_u32(&sh.full[s]);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(fb + rb) : "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(sh.st[s].wkr)),
-                 "l"(filt + 2ull * t0), "r"(fb), "r"(bar)
+                     smem_u32(sh.qk[s])),
+                 "l"(qk + t0), "r"(bytes), "r"(bar)
                  : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(sh.st[s].rec)),
-                 "l"(rec + t0), "r"(rb), "r"(bar)
-                 : "memory");
+}
+
+// Phase-1 test of one key word w = {0x7fff - q(ylo), q(yhi)} against the CTA
+// constant kc = {cta_hi + 1, 0x8000 - cta_lo}: each 16-bit half of w + kc
+// stays below 2^16 (keys <= 32767), and its top bit is set iff
+// q(ylo) <= cta_hi (low half) / q(yhi) >= cta_lo (high half).
+__device__ __forceinline__ uint32_t key_hit(uint32_t w, uint32_t kc) {
+    const uint32_t d = w + kc;
+    return (d & (d << 16)) >> 31;
 }
 
 // Per-thread point keys.  C1/C2: 15-bit keys (qkey15), two points per
@@ -358,37 +347,34 @@ __device__ __forceinline__ void slow_robust(const float2* my_l, const double2* _
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3) pip_tile_kernel(const double2* __restrict__ pts, uint64_t n,
-                                                        const uint2* __restrict__ filt,
-                                                        const EdgeRec* __restrict__ rec, uint32_t n_edges,
-                                                        uint32_t edges_per_chunk,
-                                                        const unsigned long long* __restrict__ bbox_keys,
-                                                        int prefilter, double tol, double tol2,
-                                                        uint32_t* __restrict__ inside_bits,
-                                                        uint32_t* __restrict__ aux_bits,
-                                                        const uint32_t* __restrict__ n_dev) {
+__global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3)
+    pip_tile_kernel(const double2* __restrict__ pts, uint64_t n, const uint32_t* __restrict__ qk,
+                    const uint2* __restrict__ filt, const EdgeRec* __restrict__ rec, uint32_t n_edges,
+                    uint32_t edges_per_chunk, const unsigned long long* __restrict__ bbox_keys, int prefilter,
+                    double tol, double tol2, uint32_t* __restrict__ inside_bits, uint32_t* __restrict__ aux_bits,
+                    const uint32_t* __restrict__ n_dev) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    SingleShared<MODE>& sh = *reinterpret_cast<SingleShared<MODE>*>(smem_raw);
+    SingleShared& sh = *reinterpret_cast<SingleShared*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (n_dev) n = min(n, (uint64_t)*n_dev); // bucketed input: only the in-box prefix is live
     const uint64_t cta_base = (uint64_t)blockIdx.x * (kTPB * kK);
     if (cta_base >= n) return;
     const uint32_t e_begin = blockIdx.y * edges_per_chunk;
     const uint32_t e_end = min(n_edges, e_begin + edges_per_chunk);
+    if (e_begin >= e_end) return;
     const uint64_t wbase = cta_base + (uint64_t)warp * 32 * kK; // this warp's first point (global)
 
     const uint32_t cta_n = (uint32_t)min((uint64_t)(kTPB * kK), n - cta_base);
     if (tid == 0) {
         mbar_init(&sh.full[0], 1);
         mbar_init(&sh.full[1], 1);
-        mbar_init(&sh.pbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    const uint32_t n_tiles = (e_end - e_begin + kTile - 1) / kTile;
-    if (tid == 0) {
-        for (uint32_t q = 0; q < 2 && q < n_tiles; ++q)
-            issue_tile(sh, (int)q, filt, rec, e_begin + q * kTile, min((uint32_t)kTile, e_end - e_begin - q * kTile));
+        sh.ncand = 0;
+        sh.cta_lo = 0xffffu;
+        sh.cta_hi = 0u;
+        sh.cta_ylo = ~0ull;
+        sh.cta_yhi = 0ull;
+        sh.live = 0;
     }
 
     // ---- keys of this thread's points (coordinates stay in shared memory) ----
@@ -408,8 +394,11 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3) pip_tile_kernel
         lm.sy = reinterpret_cast<const double*>(bbox_keys)[7];
     }
     Keys<MODE> K;
-    uint32_t act = 0, nonloc = 0; // nonloc (C1): active points without local fp32 coordinates
+    uint32_t act = 0, nonloc = 0; // nonloc: active points without local fp32 coordinates
+    uint32_t qlo = 0xffffu, qhi = 0u; // this thread's range of phase-1 keys
+    unsigned long long ylo_k = ~0ull, yhi_k = 0ull; // C1/C2: monotone keys of its min / max p.y
     const QMap qm = {reinterpret_cast<const double*>(bbox_keys)[4], reinterpret_cast<const double*>(bbox_keys)[5]};
+    __syncthreads(); // shared counters initialised
 #pragma unroll
     for (int k = 0; k < kK; ++k) {
         const uint32_t li = wloc + k * 32 + lane;
@@ -431,31 +420,23 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3) pip_tile_kernel
         if constexpr (MODE == kRobust) {
             K.ka[k] = a ? fkey(__dadd_rn(p.y, tol)) : INT_MIN;
             K.kb[k] = a ? fkey(__dsub_rn(p.y, tol)) : INT_MAX;
+            if (a) { // phase-1 range: q(RN(p.y - tol)) .. q(RN(p.y + tol))
+                qlo = min(qlo, qkey15(__dsub_rn(p.y, tol), qm));
+                qhi = max(qhi, qkey15(__dadd_rn(p.y, tol), qm));
+            }
         } else {
-            const uint32_t q = (a ? qkey15(p.y, qm) : 0x7fffu) << 1; // inactive: masked by `act` (slow path)
-            if (k & 1) K.k2[k >> 1] |= q << 16;
-            else K.k2[k >> 1] = q;
+            if (a) { // phase-1 range (global map) and the CTA's exact y range
+                const uint32_t q = qkey15(p.y, qm);
+                qlo = min(qlo, q);
+                qhi = max(qhi, q);
+                ylo_k = min(ylo_k, dkey(p.y));
+                yhi_k = max(yhi_k, dkey(p.y));
+            }
         }
         act |= (uint32_t)a << k;
     }
-    const bool warp_live = __any_sync(0xffffffffu, act != 0);
-    // key range of the warp's active points (C1 "all sure" shortcut)
-    uint32_t wkey_lo = 0xffffu, wkey_hi = 0u;
-    if constexpr (MODE != kRobust) {
-        uint32_t lo = 0xffffu, hi = 0u;
-#pragma unroll
-        for (int k = 0; k < kK; ++k) {
-            if (act >> k & 1u) {
-                const uint32_t q = (K.k2[k >> 1] >> (16 * (k & 1) + 1)) & 0x7fffu;
-                lo = min(lo, q);
-                hi = max(hi, q);
-            }
-        }
-        wkey_lo = __reduce_min_sync(0xffffffffu, lo);
-        wkey_hi = __reduce_max_sync(0xffffffffu, hi);
-    }
-    // warp-level interval test (Robust): some point may straddle only if
-    // max key(p.y + tol) >= key(ylo) and min key(p.y - tol) <= key(yhi)
+    // key range of the warp's active points (phase 1; C1/C2 re-key below)
+    uint32_t wkey_lo = __reduce_min_sync(0xffffffffu, qlo), wkey_hi = __reduce_max_sync(0xffffffffu, qhi);
     int wka_max = INT_MIN, wkb_min = INT_MAX;
     if constexpr (MODE == kRobust) {
         int hi = INT_MIN, lo = INT_MAX;
@@ -468,82 +449,165 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3) pip_tile_kernel
         }
         wka_max = __reduce_max_sync(0xffffffffu, hi);
         wkb_min = __reduce_min_sync(0xffffffffu, lo);
+    } else {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            ylo_k = min(ylo_k, __shfl_xor_sync(0xffffffffu, ylo_k, o));
+            yhi_k = max(yhi_k, __shfl_xor_sync(0xffffffffu, yhi_k, o));
+        }
     }
-    // may any active point of the warp straddle edge f?  (exact: the keys are
-    // monotone; the per-point filter and the slow path then decide per point)
-    auto warp_may = [&](uint32_t lo, uint32_t hi) {
-        if constexpr (MODE == kRobust) return ((int)lo <= wka_max) & ((int)hi >= wkb_min);
-        else return (lo <= wkey_hi) & (hi >= wkey_lo);
+    const bool warp_live = __any_sync(0xffffffffu, act != 0);
+    if (lane == 0 && warp_live) {
+        atomicMin(&sh.cta_lo, wkey_lo);
+        atomicMax(&sh.cta_hi, wkey_hi);
+        if constexpr (MODE != kRobust) {
+            atomicMin(&sh.cta_ylo, ylo_k);
+            atomicMax(&sh.cta_yhi, yhi_k);
+        }
+        sh.live = 1;
+    }
+    __syncthreads(); // points staged, CTA key range complete
+    if (!sh.live) return; // no active point: nothing to classify (uniform)
+    // C1/C2 per-point keys on the CTA's own y range (y-bucketed CTAs span a thin
+    // slab, so the 15-bit keys resolve ~2^27 levels over the polygon and key ties
+    // -- which take the binary64 path -- stay rare even for edges far shorter
+    // than the polygon's height / 2^15).  Any monotone map is exact.
+    CtaQMap cm{};
+    if constexpr (MODE != kRobust) {
+        cm = ctaqmap_from_range(dkey_inv(sh.cta_ylo), dkey_inv(sh.cta_yhi));
+        uint32_t lo = 0xffffu, hi = 0u;
+#pragma unroll
+        for (int k = 0; k < kK; ++k) {
+            const uint32_t li = wloc + k * 32 + lane;
+            const bool a = act >> k & 1u;
+            const uint32_t q = a ? qkey_cta(pts[cta_base + li].y, cm) : 0x7fffu; // inactive: masked by `act`
+            if (k & 1) K.k2[k >> 1] |= (q << 1) << 16;
+            else K.k2[k >> 1] = q << 1;
+            if (a) {
+                lo = min(lo, q);
+                hi = max(hi, q);
+            }
+        }
+        wkey_lo = __reduce_min_sync(0xffffffffu, lo);
+        wkey_hi = __reduce_max_sync(0xffffffffu, hi);
+    }
+    const uint32_t kc = (sh.cta_hi + 1u) | ((0x8000u - sh.cta_lo) << 16);
+
+    const uint32_t t_begin = e_begin, n_tiles = (e_end - e_begin + kQTile - 1) / kQTile;
+    if (tid == 0) {
+        for (uint32_t q = 0; q < 2 && q < n_tiles; ++q) issue_tile(sh, (int)q, qk, t_begin + q * kQTile);
+    }
+
+    // may any active point of the warp straddle the edge with filter word f?
+    // (exact: the keys are monotone; the per-point filter then decides per point)
+    auto warp_may = [&](uint2 f) {
+        if constexpr (MODE == kRobust) {
+            return ((int)f.x <= wka_max) & ((int)f.y >= wkb_min);
+        } else {
+            const uint32_t klo = (0x8000u - ((f.x & 0xffffu) >> 1)) & 0x7fffu;
+            const uint32_t khi = klo + (((f.y & 0xffffu) - 2u) >> 1);
+            return (klo <= wkey_hi) & (khi >= wkey_lo);
+        }
     };
 
     uint32_t par = 0, auxm = 0;
+    // ---- phase 2: classify against the listed candidate edges ----
+    auto flush = [&](uint32_t nc) { // nc = sh.ncand, read by every thread before any could append again
+        for (uint32_t b0 = 0; b0 < nc; b0 += kBatch) {
+            const uint32_t nb = min((uint32_t)kBatch, nc - b0);
+            { // gather: two threads per candidate (filter word + half of the record each)
+                const uint32_t i = (uint32_t)tid >> 1, h = (uint32_t)tid & 1u;
+                if (i < nb) {
+                    const uint32_t e = sh.list[b0 + i];
+                    const uint4* src = reinterpret_cast<const uint4*>(rec + e) + 2 * h;
+                    uint4* dst = reinterpret_cast<uint4*>(&sh.brec[i]) + 2 * h;
+                    const uint4 r0 = __ldg(src), r1 = __ldg(src + 1);
+                    if (h == 0) {
+                        if constexpr (MODE == kRobust) {
+                            sh.bfilt[i] = __ldg(filt + e);
+                        } else { // the per-point filter word on the CTA's key map (as prep_edges_kernel)
+                            const double ay = __hiloint2double((int)r0.w, (int)r0.z);
+                            const double by = __hiloint2double((int)r1.y, (int)r1.x);
+                            const double ylo = by < ay ? by : ay, yhi = ay < by ? by : ay;
+                            const uint32_t klo = qkey_cta(ylo, cm), khi = qkey_cta(yhi, cm);
+                            const uint32_t neg = ((0x8000u - klo) & 0x7fffu) << 1;
+                            const uint32_t thr1 = ((khi - klo) << 1) + 2u;
+                            sh.bfilt[i] = make_uint2(neg | (neg << 16), thr1 | (thr1 << 16));
+                        }
+                    }
+                    dst[0] = r0;
+                    dst[1] = r1;
+                }
+            }
+            __syncthreads();
+            if (warp_live) {
+                for (uint32_t g = 0; g < nb; g += 4) {
+                    bool c[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const uint2 f = sh.bfilt[min(g + u, nb - 1)];
+                        c[u] = (g + u < nb) && warp_may(f) && lane_candidate<MODE>(K, f);
+                    }
+                    if (!__any_sync(0xffffffffu, c[0] | c[1] | c[2] | c[3])) continue;
+                    uint32_t bits = 0;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) bits |= (uint32_t)c[u] << u;
+                    uint32_t todo = __reduce_or_sync(0xffffffffu, bits);
+                    while (todo) {
+                        const uint32_t i = g + (__ffs(todo) - 1);
+                        todo &= todo - 1;
+                        const uint2 f = sh.bfilt[i];
+                        const EdgeRec rec_e = sh.brec[i];
+                        if constexpr (MODE == kC1)
+                            slow_c1(sh.pts + wloc + lane, pts + cta_base + wloc + lane, K, act, nonloc, f, rec_e, par,
+                                    wkey_lo, wkey_hi);
+                        else if constexpr (MODE == kC2)
+                            slow_c2(sh.pts + wloc + lane, pts + cta_base + wloc + lane, K, act, nonloc, f, rec_e, par,
+                                    auxm, wkey_lo, wkey_hi);
+                        else
+                            slow_robust(sh.pts + wloc + lane, pts + cta_base + wloc + lane, K, act, nonloc, f, rec_e,
+                                        tol, tol2, par, auxm, wka_max, wkb_min);
+                    }
+                }
+            }
+            __syncthreads(); // batch buffers free
+        }
+        if (tid == 0) sh.ncand = 0;
+        __syncthreads();
+    };
+
+    // ---- phase 1: the key scan over the chunk ----
+    uint32_t pending = 0; // list size (uniform)
     for (uint32_t q = 0; q < n_tiles; ++q) {
         const int s = (int)(q & 1);
-        const uint32_t t0 = e_begin + q * kTile;
-        const uint32_t nt = min((uint32_t)kTile, e_end - t0);
+        const uint32_t t0 = t_begin + q * kQTile;
         mbar_wait(&sh.full[s], (q >> 1) & 1);
-        const TileStage& T = sh.st[s];
-        if (warp_live) {
-            // the stage's shared address, opaque to the compiler: kept in a
-            // register instead of being re-derived from the CTA's shared window
-            // base on every step of the edge loop
-            unsigned st_s = smem_u32(&T);
-            asm volatile("" : "+r"(st_s));
-            const unsigned filt_s = st_s + (unsigned)offsetof(TileStage, filt);
-            // process one group of 4 edges that passed the warp-level test
-            auto group = [&](uint32_t e0) {
-                // per-point filter of the 4 edges, then one warp-wide OR says
-                // which of them need the slow path
-                bool c[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) c[u] = lane_candidate<MODE>(K, lds_u2(filt_s + 8u * (e0 + u)));
-                // common case: no candidate in the warp for any of the 4 edges
-                if (!__any_sync(0xffffffffu, c[0] | c[1] | c[2] | c[3])) return;
-                uint32_t bits = 0;
-#pragma unroll
-                for (int u = 0; u < 4; ++u) bits |= (uint32_t)c[u] << u;
-                uint32_t todo = __reduce_or_sync(0xffffffffu, bits);
-                if (nt - e0 < 4) todo &= (1u << (nt - e0)) - 1u; // stale tail entries
-                while (todo) {
-                    const uint32_t e = e0 + (__ffs(todo) - 1);
-                    todo &= todo - 1;
-                    const uint2 f = lds_u2(filt_s + 8u * e);
-                    const EdgeRec rec_e = lds_rec(st_s + (unsigned)sizeof(EdgeRec) * e);
-                    // ---- slow path: exact binary64 test for the candidate points ----
-                    if constexpr (MODE == kC1)
-                        slow_c1(sh.pts + wloc + lane, pts + cta_base + wloc + lane, K, act, nonloc, f, rec_e, par,
-                                wkey_lo, wkey_hi);
-                    else if constexpr (MODE == kC2)
-                        slow_c2(sh.pts + wloc + lane, pts + cta_base + wloc + lane, K, act, nonloc, f, rec_e, par,
-                                auxm, wkey_lo, wkey_hi);
-                    else
-                        slow_robust(sh.pts + wloc + lane, pts + cta_base + wloc + lane, K, act, nonloc, f, rec_e,
-                                    tol, tol2, par, auxm, wka_max, wkb_min);
-                }
-            };
-            // warp-level interval test (warp-uniform: the key range of the warp's
-            // points against each edge's key range), 8 edges per step with the
-            // loads of both halves issued together; the stage's shared address is
-            // formed once per tile
-            const unsigned wkr_s = st_s + (unsigned)offsetof(TileStage, wkr);
-            for (uint32_t e0 = 0; e0 < nt; e0 += 8) {
-                uint4 r[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                                 : "=r"(r[j].x), "=r"(r[j].y), "=r"(r[j].z), "=r"(r[j].w)
-                                 : "r"(wkr_s + (e0 + 2 * j) * 8u));
-                const bool pa = warp_may(r[0].x, r[0].y) | warp_may(r[0].z, r[0].w) | warp_may(r[1].x, r[1].y) |
-                                warp_may(r[1].z, r[1].w);
-                const bool pb = warp_may(r[2].x, r[2].y) | warp_may(r[2].z, r[2].w) | warp_may(r[3].x, r[3].y) |
-                                warp_may(r[3].z, r[3].w);
-                if (pa) group(e0);
-                if (pb && e0 + 4 < nt) group(e0 + 4);
+        const uint4 w0 = sh.qk[s][2 * tid], w1 = sh.qk[s][2 * tid + 1];
+        uint32_t m = key_hit(w0.x, kc) | key_hit(w0.y, kc) << 1 | key_hit(w0.z, kc) << 2 | key_hit(w0.w, kc) << 3 |
+                     key_hit(w1.x, kc) << 4 | key_hit(w1.y, kc) << 5 | key_hit(w1.z, kc) << 6 |
+                     key_hit(w1.w, kc) << 7;
+        const bool mine = m != 0;
+        if (mine) { // rare: append this thread's candidates (edges past e_end are padding or the next chunk's)
+            const uint32_t e0 = t0 + 8u * (uint32_t)tid;
+            if (e0 + 8 > e_end) m &= e0 >= e_end ? 0u : (1u << (e_end - e0)) - 1u;
+            uint32_t pos = atomicAdd(&sh.ncand, (uint32_t)__popc(m));
+            while (m) {
+                sh.list[pos++] = e0 + (__ffs(m) - 1);
+                m &= m - 1;
             }
         }
-        __syncthreads(); // stage s fully consumed
-        if (tid == 0 && q + 2 < n_tiles)
-            issue_tile(sh, s, filt, rec, t0 + 2 * kTile, min((uint32_t)kTile, e_end - (t0 + 2 * kTile)));
+        // stage s consumed and this tile's candidates listed; the count of
+        // appending threads is uniform, so is the decision to read the list size
+        const int appended = __syncthreads_count(mine);
+        if (tid == 0 && q + 2 < n_tiles) issue_tile(sh, s, qk, t0 + 2 * kQTile);
+        if (appended) {
+            pending = sh.ncand;
+            __syncthreads(); // everyone has read it before anyone appends again
+        }
+        if (pending > kListCap - kQTile || (q + 1 == n_tiles && pending)) {
+            flush(pending);
+            pending = 0;
+        }
     }
 
     // ---- flags: one ballot word per k-slice ----
@@ -567,7 +631,7 @@ int sms(int dev) {
 
 template <int MODE>
 cudaError_t launch_t(const SingleArgs& a, cudaStream_t st, int dev, uint64_t* launches) {
-    const size_t smem = sizeof(SingleShared<MODE>);
+    const size_t smem = sizeof(SingleShared);
     static bool attr[64] = {};
     if (dev < 64 && !attr[dev]) {
         cudaFuncSetAttribute(pip_tile_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -579,15 +643,15 @@ cudaError_t launch_t(const SingleArgs& a, cudaStream_t st, int dev, uint64_t* la
     const uint64_t pts_per_cta = (uint64_t)kTPB * kK;
     const uint64_t n_ptiles = (a.n + pts_per_cta - 1) / pts_per_cta;
     const uint64_t slots = (uint64_t)sms(dev) * per_sm;
-    // Split the edges so the grid covers >= ~4 waves; chunks are whole tiles.
-    const uint64_t tiles = std::max<uint64_t>(1, (a.n_edges + kTile - 1) / kTile);
+    // Split the edges so the grid covers >= ~4 waves; chunks are whole key tiles.
+    const uint64_t tiles = std::max<uint64_t>(1, (a.n_edges + kQTile - 1) / kQTile);
     uint64_t chunks = std::max<uint64_t>(1, (4 * slots + n_ptiles - 1) / std::max<uint64_t>(n_ptiles, 1));
     chunks = std::min<uint64_t>(std::min<uint64_t>(chunks, tiles), 65535);
     const uint64_t tiles_per_chunk = (tiles + chunks - 1) / chunks;
-    const uint32_t per_chunk = (uint32_t)(tiles_per_chunk * kTile);
+    const uint32_t per_chunk = (uint32_t)(tiles_per_chunk * kQTile);
     chunks = (tiles + tiles_per_chunk - 1) / tiles_per_chunk;
     dim3 grid((unsigned)n_ptiles, (unsigned)chunks);
-    pip_tile_kernel<MODE><<<grid, kTPB, smem, st>>>(reinterpret_cast<const double2*>(a.pts), a.n, a.filt,
+    pip_tile_kernel<MODE><<<grid, kTPB, smem, st>>>(reinterpret_cast<const double2*>(a.pts), a.n, a.qk, a.filt,
                                                    reinterpret_cast<const EdgeRec*>(a.rec), a.n_edges, per_chunk,
                                                    a.bbox_keys, a.prefilter, a.tol, a.tol2, a.inside_bits,
                                                    a.aux_bits, a.n_dev);
