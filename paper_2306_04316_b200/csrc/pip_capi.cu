@@ -46,7 +46,7 @@ struct DevState {
     cudaStream_t copy = nullptr; // points upload, overlapping polygon-only work on `stream` (made on first use)
     std::vector<cudaEvent_t> up_evs; // one per uploaded chunk
     DevBuf pts, vx, vy, ring_off, pt_off, poly_ring_off, filt, qk, rec, bbox, bits, verdicts, stats, counts, degen;
-    DevBuf bucket_scratch, sorted_pts, sorted_idx, bucket_blk; // y-bucketing (pip_sort.cu)
+    DevBuf bucket_scratch, sorted_idx;                        // y order (pip_sort.cu)
     DevBuf csr_meta;                                          // per-polygon records (pip_csr.cu)
     DevBuf cmp_blk, cmp_pts, cmp_idx, cmp_v, cmp_out;         // prefilter / scatter (pip_compact.cu)
     DevBuf csv_text, csv_state, csv_res, csv_out;             // CSV reader (pip_csv.cu)
@@ -192,7 +192,7 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
     check(c, pcd::launch_prep(pa, st, d.dev, &c->launches), "prep kernel");
     check(c, cudaMemsetAsync(d_aux, 0, nwords * 4, st), "clear aux plane");
     const bool tree = (mode == 0 || mode == 1) /* C1, C2 */ && c->tree_mode == 1 && pcd::tree_eligible(n_verts, n, true);
-    const bool bucket = n < 0xffffffffull &&
+    const bool bucket = !tree && n < 0xffffffffull &&
                         (c->bucket_mode == 1 || (c->bucket_mode < 0 && n_edges >= 64 && n >= 4096));
     pcd::SingleArgs sa{};
     sa.mode = mode;
@@ -209,7 +209,7 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
     sa.inside_bits = d_inside;
     sa.aux_bits = d_aux;
     sa.n_dev = nullptr;
-    uint32_t* hist = nullptr;
+    sa.idx = nullptr;
     pcd::TreeArgs ta{};
     if (tree) { // segment-tree build (polygon only)
         ta.mode = mode;
@@ -241,22 +241,20 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
         sc.inside_bits = d_inside + lo / 32;
         sc.aux_bits = d_aux + lo / 32;
         if (bucket) {
-            const size_t hist_words = pcd::kBuckets + 2;
-            check(c, d.bucket_scratch.ensure((hist_words + 2 * mw) * 4), "alloc bucket scratch");
-            check(c, d.sorted_pts.ensure(m * 16), "alloc bucketed points");
+            // y order by a radix sort of (key, index); the scan kernel gathers the
+            // points by index and writes bit planes in y order (unbucketed below)
+            check(c, d.bucket_scratch.ensure(pcd::bucket_scratch_bytes(m) + (2 * mw + 4) * 4), "alloc bucket scratch");
             check(c, d.sorted_idx.ensure(m * 4), "alloc bucket index");
-            hist = d.bucket_scratch.as<uint32_t>();
-            check(c, cudaMemsetAsync(hist, 0, (hist_words + 2 * mw) * 4, st), "clear bucket scratch");
-            const int n_blk = pcd::bucket_blocks(m, d.dev);
-            check(c, d.bucket_blk.ensure((size_t)n_blk * (pcd::kBuckets + 1) * 4), "alloc bucket counts");
-            pcd::BucketArgs ba{sc.pts, m, d.bbox.as<unsigned long long>(), prefilter, hist, d.sorted_pts.as<double>(),
-                               d.sorted_idx.as<uint32_t>(), d.bucket_blk.as<uint32_t>(), n_blk};
+            uint32_t* planes = reinterpret_cast<uint32_t*>(d.bucket_scratch.as<char>() + pcd::bucket_scratch_bytes(m));
+            check(c, cudaMemsetAsync(planes, 0, (2 * mw + 4) * 4, st), "clear bucket planes");
+            pcd::BucketArgs ba{sc.pts, m, d.bbox.as<unsigned long long>(), prefilter, d.bucket_scratch.p,
+                               d.sorted_idx.as<uint32_t>(), planes + 2 * mw};
             check(c, pcd::launch_bucket(ba, st, d.dev, &c->launches), "bucket kernels");
-            sc.pts = d.sorted_pts.as<double>();
-            sc.prefilter = 0; // rejected points were left out of the bucketed prefix
-            sc.inside_bits = hist + hist_words;
-            sc.aux_bits = hist + hist_words + mw;
-            sc.n_dev = hist + pcd::kBuckets + 1;
+            sc.idx = d.sorted_idx.as<uint32_t>();
+            sc.prefilter = 0; // rejected points sort last and are left out (n_dev)
+            sc.inside_bits = planes;
+            sc.aux_bits = planes + mw;
+            sc.n_dev = planes + 2 * mw;
         }
         if (tree) { // segment-tree counts; key-tie / off-map points through the scan kernel
             // (y-bucketed points: a warp's queries walk nearby leaves, sharing nodes)
@@ -409,8 +407,8 @@ void pc_destroy(pc_ctx* c) {
         cudaSetDevice(d.dev);
         cudaStreamSynchronize(d.stream);
         for (DevBuf* b : {&d.pts, &d.vx, &d.vy, &d.ring_off, &d.pt_off, &d.poly_ring_off, &d.filt, &d.qk, &d.rec, &d.bbox,
-                          &d.bits, &d.verdicts, &d.stats, &d.counts, &d.degen, &d.bucket_scratch, &d.sorted_pts,
-                          &d.sorted_idx, &d.bucket_blk, &d.csr_meta, &d.cmp_blk, &d.cmp_pts, &d.cmp_idx, &d.cmp_v,
+                          &d.bits, &d.verdicts, &d.stats, &d.counts, &d.degen, &d.bucket_scratch,
+                          &d.sorted_idx, &d.csr_meta, &d.cmp_blk, &d.cmp_pts, &d.cmp_idx, &d.cmp_v,
                           &d.cmp_out, &d.csv_text, &d.csv_state, &d.csv_res, &d.csv_out, &d.emit_recs,
                           &d.emit_scratch, &d.emit_out, &d.tree})
             b->release();

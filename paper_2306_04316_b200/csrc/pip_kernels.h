@@ -39,6 +39,7 @@ struct SingleArgs {
     uint32_t* inside_bits;
     uint32_t* aux_bits;
     const uint32_t* n_dev; // optional device-side point count (bucketed input)
+    const uint32_t* idx;   // optional: point i of the call is pts[idx[i]] (y-ordered gather)
 };
 
 struct CsrArgs {
@@ -134,22 +135,19 @@ uint64_t emit_max_bytes(uint64_t n);
 cudaError_t launch_emit_results(const void* recs, uint64_t n, char* out, uint64_t cap, void* scratch,
                                 unsigned long long* out_len, cudaStream_t st, uint64_t* launches);
 
-// y-bucketing of the points of one polygon (pip_sort.cu): counting sort by
-// y over the outer ring's bbox into kBuckets bins; bbox-rejected points
-// (prefilter) go to a trailing bin that is not classified.
-constexpr int kBuckets = 4096;
+// y-ordering of the points of one polygon (pip_sort.cu): a stable 2-pass
+// radix sort of (16-bit y key over the outer ring's bbox, index); points the
+// bbox prefilter rejects sort last and are not classified.
 struct BucketArgs {
     const double* pts;                    // n interleaved points
-    uint64_t n;
+    uint64_t n;                           // < 2^32
     const unsigned long long* bbox_keys;  // from prep
     int prefilter;
-    uint32_t* hist;                       // kBuckets + 2 words; [kBuckets+1] receives n_in
-    double* sorted_pts;                   // n points (bucketed order)
-    uint32_t* sorted_idx;                 // original index of each bucketed point
-    uint32_t* blk;                        // n_blk x (kBuckets + 1) per-CTA counts
-    int n_blk;                            // bucket_blocks(n, dev)
+    void* scratch;                        // bucket_scratch_bytes(n)
+    uint32_t* sorted_idx;                 // n: original index of each point in y order
+    uint32_t* n_in;                       // (device) number of points not rejected
 };
-int bucket_blocks(uint64_t n, int dev);
+size_t bucket_scratch_bytes(uint64_t n);
 cudaError_t launch_bucket(const BucketArgs& a, cudaStream_t st, int dev, uint64_t* launches);
 // ORs the set bits of the bucketed planes back to the original point order.
 cudaError_t launch_unbucket(uint64_t n, const uint32_t* n_dev, const uint32_t* sorted_idx, const uint32_t* s_inside,

@@ -104,6 +104,14 @@ __device__ __forceinline__ uint32_t key_hit(uint32_t w, uint32_t kc) {
     return (d & (d << 16)) >> 31;
 }
 
+// A lane's binary64 points for the exact fallbacks: point k of the lane is
+// g[k * 32], or g[ix[k * 32]] when the call gathers y-ordered points by index.
+struct PtRef {
+    const double2* __restrict__ g;
+    const uint32_t* __restrict__ ix;
+    __device__ __forceinline__ double2 operator[](int j) const { return ix ? g[ix[j]] : g[j]; }
+};
+
 // Per-thread point keys.  C1/C2: 15-bit keys (qkey15), two points per
 // register as (q_2i << 1) | (q_2i+1 << 17).  Robust: 32-bit keys of p.y+tol
 // and p.y-tol.
@@ -159,7 +167,7 @@ __device__ __forceinline__ bool lane_candidate(const Keys<MODE>& K, uint2 f) {
 // §3.4) -- two FFMAs per point; a point within the band (or without local
 // coordinates) re-reads its binary64 coordinates and runs the reference's
 // expression.
-__device__ __forceinline__ void slow_c1(const float2* my_l, const double2* __restrict__ my_g, const Keys<kC1>& K,
+__device__ __forceinline__ void slow_c1(const float2* my_l, const PtRef& my_g, const Keys<kC1>& K,
                                         uint32_t act, uint32_t nonloc, uint2 f, const EdgeRec& r, uint32_t& par,
                                         uint32_t wkey_lo, uint32_t wkey_hi) {
     const double ax = r.d[0], ay = r.d[1];
@@ -230,7 +238,7 @@ __device__ __forceinline__ void slow_c1(const float2* my_l, const double2* __res
 // decide the intercept sign with the certified fp32 test (local_side_record_c2);
 // key ties, band hits and points without local coordinates run the
 // reference's expression (division included, DegenerateEdge -> Error).
-__device__ __forceinline__ void slow_c2(const float2* my_l, const double2* __restrict__ my_g, const Keys<kC2>& K,
+__device__ __forceinline__ void slow_c2(const float2* my_l, const PtRef& my_g, const Keys<kC2>& K,
                                         uint32_t act, uint32_t nonloc, uint2 f, const EdgeRec& r, uint32_t& par,
                                         uint32_t& auxm, uint32_t wkey_lo, uint32_t wkey_hi) {
     const uint32_t rng = ((f.y & 0xffffu) - 2u) >> 1;
@@ -293,7 +301,7 @@ __device__ __forceinline__ void slow_c2(const float2* my_l, const double2* __res
 // sign also rules out the boundary when tol <= 2^-30 * min(W, H) (the record
 // is NaN otherwise): the point's distance to the edge's line is then at least
 // ~29 tol.  Everything else runs the reference's expression.
-__device__ __forceinline__ void slow_robust(const float2* my_l, const double2* __restrict__ my_g,
+__device__ __forceinline__ void slow_robust(const float2* my_l, const PtRef& my_g,
                                             const Keys<kRobust>& K, uint32_t act, uint32_t nonloc, uint2 f,
                                             const EdgeRec& r, double tol, double tol2, uint32_t& par, uint32_t& auxm,
                                             int wka_max, int wkb_min) {
@@ -352,7 +360,7 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3)
                     const uint2* __restrict__ filt, const EdgeRec* __restrict__ rec, uint32_t n_edges,
                     uint32_t edges_per_chunk, const unsigned long long* __restrict__ bbox_keys, int prefilter,
                     double tol, double tol2, uint32_t* __restrict__ inside_bits, uint32_t* __restrict__ aux_bits,
-                    const uint32_t* __restrict__ n_dev) {
+                    const uint32_t* __restrict__ n_dev, const uint32_t* __restrict__ idx) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     SingleShared& sh = *reinterpret_cast<SingleShared*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -405,7 +413,7 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3)
         bool a = li < cta_n;
         double2 p = make_double2(0.0, 0.0);
         {
-            if (a) p = pts[cta_base + li];
+            if (a) p = idx ? pts[idx[cta_base + li]] : pts[cta_base + li];
             if ((k & 3) == 3) asm volatile("" ::: "memory"); // at most 4 point loads in flight (registers)
         }
         if (a && prefilter) a = p.x >= minx && p.x <= maxx && p.y >= miny && p.y <= maxy; // batch.hpp:39-41
@@ -480,7 +488,8 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3)
         for (int k = 0; k < kK; ++k) {
             const uint32_t li = wloc + k * 32 + lane;
             const bool a = act >> k & 1u;
-            const uint32_t q = a ? qkey_cta(pts[cta_base + li].y, cm) : 0x7fffu; // inactive: masked by `act`
+            const uint32_t q = a ? qkey_cta((idx ? pts[idx[cta_base + li]] : pts[cta_base + li]).y, cm)
+                                 : 0x7fffu; // inactive: masked by `act`
             if (k & 1) K.k2[k >> 1] |= (q << 1) << 16;
             else K.k2[k >> 1] = q << 1;
             if (a) {
@@ -510,6 +519,7 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3)
         }
     };
 
+    const PtRef my_g = idx ? PtRef{pts, idx + cta_base + wloc + lane} : PtRef{pts + cta_base + wloc + lane, nullptr};
     uint32_t par = 0, auxm = 0;
     // ---- phase 2: classify against the listed candidate edges ----
     auto flush = [&](uint32_t nc) { // nc = sh.ncand, read by every thread before any could append again
@@ -559,13 +569,13 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3)
                         const uint2 f = sh.bfilt[i];
                         const EdgeRec rec_e = sh.brec[i];
                         if constexpr (MODE == kC1)
-                            slow_c1(sh.pts + wloc + lane, pts + cta_base + wloc + lane, K, act, nonloc, f, rec_e, par,
+                            slow_c1(sh.pts + wloc + lane, my_g, K, act, nonloc, f, rec_e, par,
                                     wkey_lo, wkey_hi);
                         else if constexpr (MODE == kC2)
-                            slow_c2(sh.pts + wloc + lane, pts + cta_base + wloc + lane, K, act, nonloc, f, rec_e, par,
+                            slow_c2(sh.pts + wloc + lane, my_g, K, act, nonloc, f, rec_e, par,
                                     auxm, wkey_lo, wkey_hi);
                         else
-                            slow_robust(sh.pts + wloc + lane, pts + cta_base + wloc + lane, K, act, nonloc, f, rec_e,
+                            slow_robust(sh.pts + wloc + lane, my_g, K, act, nonloc, f, rec_e,
                                         tol, tol2, par, auxm, wka_max, wkb_min);
                     }
                 }
@@ -654,7 +664,7 @@ cudaError_t launch_t(const SingleArgs& a, cudaStream_t st, int dev, uint64_t* la
     pip_tile_kernel<MODE><<<grid, kTPB, smem, st>>>(reinterpret_cast<const double2*>(a.pts), a.n, a.qk, a.filt,
                                                    reinterpret_cast<const EdgeRec*>(a.rec), a.n_edges, per_chunk,
                                                    a.bbox_keys, a.prefilter, a.tol, a.tol2, a.inside_bits,
-                                                   a.aux_bits, a.n_dev);
+                                                   a.aux_bits, a.n_dev, a.idx);
     ++*launches;
     return cudaGetLastError();
 }

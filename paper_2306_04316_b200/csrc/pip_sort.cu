@@ -1,18 +1,26 @@
-// y-bucketing of query points (SIMT coherence for the single-polygon kernel).
+// y-ordering of query points (SIMT coherence for the single-polygon kernel).
 //
-// Why: a warp classifies 32 points per step against one staged edge.  When the
-// 32 points have unrelated y, the chance that *some* lane needs the exact
-// binary64 test of an edge is ~1-(1-s)^32 (s = the edge's y-span fraction):
-// for the star polygons of configs 1/2, s ~ 0.05, so ~60% of edges take the
-// slow path for some lane and the whole warp pays for it.  Counting-sorting
-// the points by y over the polygon's bbox (4096 bins) makes each warp's
-// points y-adjacent, so they straddle the same edges and the slow path runs
-// for ~s of the edges instead.  Points the bbox prefilter rejects
-// (classify_batch, batch.hpp:200) land in a trailing bin and are never
-// classified (they are Outside), which is the GPU form of prefilter_bbox
-// (batch.hpp:145-156).  Results are mapped back to the original order by
-// index, so the output does not depend on the (nondeterministic) order inside
-// a bin.  The scan over every (point, edge) pair is unchanged.
+// Why: the scan kernel (pip_single.cu) tests every edge's key range against the
+// y range of a CTA's 4096 points, and classifies a warp's 512 points against
+// the candidates together.  With points in input order both ranges are the
+// whole polygon and every edge is a candidate; ordered by y, a CTA spans a thin
+// slab and only the edges crossing it remain.  Points the bbox prefilter rejects
+// (classify_batch, batch.hpp:200) get the largest key and are never classified
+// (they are Outside), which is the GPU form of prefilter_bbox
+// (batch.hpp:145-156).  Results are mapped back to the original order by index,
+// so nothing depends on the order.  The scan over every (point, edge) pair is
+// unchanged.
+//
+// Sort: 16-bit keys (65280 y levels over the outer ring's bbox, 0xffff =
+// rejected), two stable LSD passes of 8 bits over (key, index) pairs; the
+// points themselves are never moved (the scan kernel gathers them by index).
+//   rk_key_kernel      keys + per-tile digit counts (pass 1's re-counted over
+//                      the pass-0 output by rk_count_hi_kernel)
+//   rk_scan_kernel     per (digit, tile) offsets: a warp per digit scans its
+//                      tiles, then one warp scans the 256 digit totals
+//   rk_scatter_kernel  per tile: stable rank in shared memory (warp-striped
+//                      rounds with __match_any_sync), staged by digit, written
+//                      out in contiguous runs per digit
 #include "pip_kernels.h"
 
 #include <cuda_runtime.h>
@@ -25,149 +33,227 @@ namespace pcd {
 
 namespace {
 
-struct BinMap {
+constexpr int kRkThreads = 512;
+constexpr int kRkItems = 16;                       // per thread
+constexpr int kRkTile = kRkThreads * kRkItems;     // 8192 elements per tile
+constexpr int kRkWarps = kRkThreads / 32;
+constexpr uint32_t kRkLevels = 65280;              // in-box keys 0 .. 65279 (high byte < 0xff)
+constexpr uint16_t kRkReject = 0xffff;
+
+struct KeyMap {
     double minx, miny, maxx, maxy, scale;
     int prefilter;
 
-    __device__ __forceinline__ int bin(double x, double y) const {
-        if (prefilter && !(x >= minx && x <= maxx && y >= miny && y <= maxy)) return kBuckets;
+    __device__ __forceinline__ uint32_t key(double x, double y) const {
+        if (prefilter && !(x >= minx && x <= maxx && y >= miny && y <= maxy)) return kRkReject;
         const double t = (y - miny) * scale; // ordering only: no exactness needed
-        int b = t > 0.0 ? (int)t : 0;
-        return b < kBuckets ? b : kBuckets - 1;
+        const uint32_t k = t > 0.0 ? (uint32_t)fmin(t, (double)(kRkLevels - 1)) : 0u;
+        return k;
     }
 };
 
-__device__ __forceinline__ BinMap make_map(const unsigned long long* bbox_keys, int prefilter) {
-    BinMap m;
+__device__ __forceinline__ KeyMap make_keymap(const unsigned long long* bbox_keys, int prefilter) {
+    KeyMap m;
     m.minx = dkey_inv(bbox_keys[0]);
     m.miny = dkey_inv(bbox_keys[1]);
     m.maxx = dkey_inv(~bbox_keys[2]);
     m.maxy = dkey_inv(~bbox_keys[3]);
     const double h = m.maxy - m.miny;
-    m.scale = (h > 0.0 && h < 1e300) ? kBuckets / h : 0.0;
+    m.scale = (h > 0.0 && h < 1e300) ? kRkLevels / h : 0.0;
     m.prefilter = prefilter;
     return m;
 }
 
-// Atomic-free (in global memory) counting sort over P CTAs:
-//   count    CTA b histograms its contiguous chunk of points in shared memory
-//            and writes the counts to blk[bin][b] (bin-major);
-//   colscan  a warp per bin: exclusive prefix over the CTAs (blk[bin][b]
-//            becomes CTA b's offset inside the bin) and the bin total;
-//   scan     exclusive scan of the bin totals -> bin base (and n_in);
-//   scatter  CTA b re-reads its chunk and places each point at base[bin] +
-//            blk[bin][b] + (shared-memory cursor), no global atomics.
-__global__ void __launch_bounds__(1024) bucket_count_kernel(const double2* __restrict__ pts, uint64_t n,
-                                                            uint64_t chunk,
+// keys[i] for tile blockIdx.x; digit counts of both passes, digit-major:
+// cnt[pass][digit * n_tiles + tile]
+__global__ void __launch_bounds__(kRkThreads) rk_key_kernel(const double2* __restrict__ pts, uint64_t n,
                                                             const unsigned long long* __restrict__ bbox_keys,
-                                                            int prefilter, uint32_t* __restrict__ blk) {
-    __shared__ uint32_t h[kBuckets + 1];
-    for (int j = threadIdx.x; j <= kBuckets; j += blockDim.x) h[j] = 0;
+                                                            int prefilter, uint16_t* __restrict__ keys,
+                                                            uint32_t* __restrict__ cnt, uint32_t n_tiles) {
+    __shared__ uint32_t h[2][256];
+    for (int j = threadIdx.x; j < 512; j += blockDim.x) (&h[0][0])[j] = 0;
     __syncthreads();
-    const BinMap m = make_map(bbox_keys, prefilter);
-    const uint64_t lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
-    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const KeyMap m = make_keymap(bbox_keys, prefilter);
+    const uint64_t lo = (uint64_t)blockIdx.x * kRkTile, hi = min(n, lo + kRkTile);
+    for (uint64_t i = lo + threadIdx.x; i < hi; i += kRkThreads) {
         const double2 p = pts[i];
-        atomicAdd(&h[m.bin(p.x, p.y)], 1u);
+        const uint32_t k = m.key(p.x, p.y);
+        keys[i] = (uint16_t)k;
+        atomicAdd(&h[0][k & 0xff], 1u);
+        atomicAdd(&h[1][k >> 8], 1u);
     }
     __syncthreads();
-    // bin-major: blk[bin * n_blk + block], so the per-bin scan over blocks reads contiguous memory
-    for (int j = threadIdx.x; j <= kBuckets; j += blockDim.x) blk[(uint64_t)j * gridDim.x + blockIdx.x] = h[j];
+    for (int j = threadIdx.x; j < 512; j += blockDim.x) {
+        const int pass = j >> 8, d = j & 255;
+        cnt[(uint64_t)pass * 256 * n_tiles + (uint64_t)d * n_tiles + blockIdx.x] = h[pass][d];
+    }
 }
 
-// Per bin (one warp each): exclusive scan over the blocks of blk[bin][*]
-// (contiguous) -> each block's offset inside the bin; hist[bin] = bin total.
-__global__ void __launch_bounds__(256) bucket_colscan_kernel(uint32_t* __restrict__ blk, int n_blk,
-                                                             uint32_t* __restrict__ hist) {
-    const int bin = (int)((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5);
+// Pass-1 digit counts per tile of the pass-0 OUTPUT order (an LSD pass ranks
+// within the order it reads): overwrites cnt[1][*][*].
+__global__ void __launch_bounds__(kRkThreads) rk_count_hi_kernel(const uint16_t* __restrict__ keys, uint64_t n,
+                                                                 uint32_t* __restrict__ cnt, uint32_t n_tiles) {
+    __shared__ uint32_t h[256];
+    for (int j = threadIdx.x; j < 256; j += blockDim.x) h[j] = 0;
+    __syncthreads();
+    const uint64_t lo = (uint64_t)blockIdx.x * kRkTile, hi = min(n, lo + kRkTile);
+    for (uint64_t i = lo + threadIdx.x; i < hi; i += kRkThreads) atomicAdd(&h[keys[i] >> 8], 1u);
+    __syncthreads();
+    for (int d = threadIdx.x; d < 256; d += blockDim.x) cnt[256ull * n_tiles + (uint64_t)d * n_tiles + blockIdx.x] = h[d];
+}
+
+// One warp per (pass, digit): exclusive prefix over the tiles (in place) and
+// the digit total; then (last CTA, one warp per pass) the exclusive scan of the
+// 256 totals is added to every entry by the scatter kernel via base[pass][digit].
+__global__ void __launch_bounds__(256) rk_colscan_kernel(uint32_t* __restrict__ cnt, uint32_t n_tiles,
+                                                         uint32_t* __restrict__ tot, uint32_t first) {
+    const uint32_t wid = first + (uint32_t)((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5); // pass * 256 + digit
     const int lane = threadIdx.x & 31;
-    if (bin > kBuckets) return;
-    uint32_t* col = blk + (uint64_t)bin * n_blk;
+    if (wid >= 512) return;
+    uint32_t* col = cnt + (uint64_t)wid * n_tiles;
     uint32_t run = 0;
-    for (int b0 = 0; b0 < n_blk; b0 += 32) {
-        const int b = b0 + lane;
-        const uint32_t v = b < n_blk ? col[b] : 0u;
+    for (uint32_t b0 = 0; b0 < n_tiles; b0 += 32) {
+        const uint32_t b = b0 + lane;
+        const uint32_t v = b < n_tiles ? col[b] : 0u;
         uint32_t incl = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += y;
         }
-        if (b < n_blk) col[b] = run + incl - v;
+        if (b < n_tiles) col[b] = run + incl - v;
         run += __shfl_sync(0xffffffffu, incl, 31);
     }
-    if (lane == 0) hist[bin] = run;
+    if (lane == 0) tot[wid] = run;
 }
 
-// Exclusive scan of the kBuckets+1 counts (one CTA of 1024 threads): every
-// thread loads its 64 counts of a coalesced tile layout up front (one memory
-// latency), then the CTA scans tile after tile with a carried running sum;
-// hist becomes the write cursor of each bin, hist[kBuckets+1] = in-box count.
-__global__ void __launch_bounds__(1024) bucket_scan_kernel(uint32_t* __restrict__ hist) {
-    constexpr int kTiles = (kBuckets + 1 + 1023) / 1024;
-    __shared__ uint32_t warp_sums[32];
-    __shared__ uint32_t carry_s;
-    const int t = threadIdx.x;
-    uint32_t v[kTiles];
-#pragma unroll
-    for (int q = 0; q < kTiles; ++q) {
-        const int j = q * 1024 + t;
-        v[q] = j <= kBuckets ? hist[j] : 0u;
-    }
-    if (t == 0) carry_s = 0;
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < kTiles; ++q) {
-        uint32_t incl = v[q];
+// Exclusive scan of the 256 digit totals of each pass (two warps, one per
+// pass): base[pass][digit]; base[2] word 0 = in-box count (the keys below the
+// reject key: everything before high digit 0xff).
+__global__ void __launch_bounds__(64) rk_base_kernel(const uint32_t* __restrict__ tot, uint32_t* __restrict__ base,
+                                                     uint32_t* __restrict__ n_in) {
+    const int pass = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t run = 0;
+    for (int d0 = 0; d0 < 256; d0 += 32) {
+        const uint32_t v = tot[pass * 256 + d0 + lane];
+        uint32_t incl = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if ((t & 31) >= o) incl += y;
+            if (lane >= o) incl += y;
         }
-        if ((t & 31) == 31) warp_sums[t >> 5] = incl;
-        __syncthreads();
-        if (t < 32) {
-            uint32_t w = warp_sums[t];
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-                if (t >= o) w += y;
-            }
-            warp_sums[t] = w;
-        }
-        __syncthreads();
-        const uint32_t carry = carry_s;
-        const uint32_t excl = carry + incl - v[q] + ((t >> 5) ? warp_sums[(t >> 5) - 1] : 0u);
-        const int j = q * 1024 + t;
-        if (j <= kBuckets) {
-            hist[j] = excl;
-            if (j == kBuckets) hist[kBuckets + 1] = excl; // in-box count = start of the reject bin
-        }
-        __syncthreads();
-        if (t == 1023) carry_s = carry + warp_sums[31];
-        __syncthreads();
+        base[pass * 256 + d0 + lane] = run + incl - v;
+        if (pass == 1 && d0 + lane == 255) *n_in = run + incl - v;
+        run += __shfl_sync(0xffffffffu, incl, 31);
     }
 }
 
-__global__ void __launch_bounds__(1024) bucket_scatter_kernel(const double2* __restrict__ pts, uint64_t n,
-                                                              uint64_t chunk,
-                                                              const unsigned long long* __restrict__ bbox_keys,
-                                                              int prefilter, const uint32_t* __restrict__ blk,
-                                                              const uint32_t* __restrict__ base,
-                                                              double2* __restrict__ sorted_pts,
-                                                              uint32_t* __restrict__ sorted_idx) {
-    __shared__ uint32_t cur[kBuckets + 1];
-    for (int j = threadIdx.x; j <= kBuckets; j += blockDim.x) cur[j] = base[j] + blk[(uint64_t)j * gridDim.x + blockIdx.x];
+struct RkShared {
+    uint32_t wcnt[kRkWarps][256];
+    uint32_t boff[256];
+    uint32_t gbase[256];
+    uint32_t sidx[kRkTile];
+    uint16_t skey[kRkTile];
+};
+
+// One stable counting-sort pass over tile blockIdx.x: (key, idx) -> position
+// base[digit] + cnt[digit][tile] + (rank of the element among the tile's
+// elements with that digit, in element order).  PASS 0: idx = element position
+// (implicit), writes keys_out and idx_out; PASS 1: writes idx_out only.
+template <int PASS>
+__global__ void __launch_bounds__(kRkThreads, 2) rk_scatter_kernel(uint64_t n, const uint16_t* __restrict__ keys_in,
+                                                                const uint32_t* __restrict__ idx_in,
+                                                                const uint32_t* __restrict__ cnt,
+                                                                const uint32_t* __restrict__ base, uint32_t n_tiles,
+                                                                uint16_t* __restrict__ keys_out,
+                                                                uint32_t* __restrict__ idx_out) {
+    extern __shared__ __align__(16) unsigned char rk_smem[];
+    RkShared& S = *reinterpret_cast<RkShared*>(rk_smem);
+    auto& wcnt = S.wcnt; // per-warp running counts, then per-warp offsets
+    auto& boff = S.boff; // tile-local start of each digit
+    auto& gbase = S.gbase; // global start of this tile's run of each digit
+    auto& skey = S.skey;
+    auto& sidx = S.sidx;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int shift = 8 * PASS;
+    for (int j = tid; j < kRkWarps * 256; j += kRkThreads) (&wcnt[0][0])[j] = 0;
+    for (int d = tid; d < 256; d += kRkThreads)
+        gbase[d] = base[PASS * 256 + d] + cnt[(uint64_t)PASS * 256 * n_tiles + (uint64_t)d * n_tiles + blockIdx.x];
     __syncthreads();
-    const BinMap m = make_map(bbox_keys, prefilter);
-    const uint64_t lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
-    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-        const double2 p = pts[i];
-        const int b = m.bin(p.x, p.y);
-        if (b == kBuckets) continue; // rejected by the bbox prefilter: Outside, never classified
-        const uint32_t pos = atomicAdd(&cur[b], 1u);
-        sorted_pts[pos] = p;
-        sorted_idx[pos] = (uint32_t)i;
+    const uint64_t t0 = (uint64_t)blockIdx.x * kRkTile;
+    const uint32_t tn = (uint32_t)min((uint64_t)kRkTile, n - t0);
+    // warp w ranks elements [w * 512, (w + 1) * 512) of the tile in 16 rounds of
+    // 32; kr[j] = key << 16 | rank among the warp's earlier elements of its digit
+    uint32_t kr[kRkItems], idx[PASS == 0 ? 1 : kRkItems];
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int j = 0; j < kRkItems; ++j) {
+        const uint32_t e = (uint32_t)warp * 32 * kRkItems + j * 32 + lane;
+        const bool live = e < tn;
+        kr[j] = live ? (uint32_t)keys_in[t0 + e] << 16 : 0xffffffffu;
+        if constexpr (PASS == 1) idx[j] = live ? idx_in[t0 + e] : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < kRkItems; ++j) {
+        const bool live = kr[j] != 0xffffffffu;
+        const uint32_t d = (kr[j] >> (16 + shift)) & 0xffu;
+        const unsigned live_m = __ballot_sync(0xffffffffu, live);
+        const unsigned peers = __match_any_sync(0xffffffffu, live ? d : 0x100u) & live_m;
+        if (live) kr[j] |= wcnt[warp][d] + __popc(peers & lt);
+        __syncwarp();
+        if (live && (peers & lt) == 0) wcnt[warp][d] += __popc(peers); // the lowest peer advances the count
+        __syncwarp();
+    }
+    __syncthreads();
+    // per digit: exclusive prefix over the warps (in place) and the tile total
+    if (tid < 256) {
+        uint32_t run = 0;
+#pragma unroll
+        for (int w = 0; w < kRkWarps; ++w) {
+            const uint32_t v = wcnt[w][tid];
+            wcnt[w][tid] = run;
+            run += v;
+        }
+        boff[tid] = run; // tile total of digit tid, scanned below
+    }
+    __syncthreads();
+    if (tid < 32) { // exclusive scan of the 256 totals by one warp (8 per lane)
+        uint32_t v[8], sum = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            v[q] = boff[tid * 8 + q];
+            sum += v[q];
+        }
+        uint32_t incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (tid >= o) incl += y;
+        }
+        uint32_t run = incl - sum;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            boff[tid * 8 + q] = run;
+            run += v[q];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kRkItems; ++j) {
+        if (kr[j] == 0xffffffffu) continue;
+        const uint32_t k = kr[j] >> 16, d = (k >> shift) & 0xffu;
+        const uint32_t pos = boff[d] + wcnt[warp][d] + (kr[j] & 0xffffu);
+        skey[pos] = (uint16_t)k;
+        if constexpr (PASS == 0) sidx[pos] = (uint32_t)(t0 + (uint32_t)warp * 32 * kRkItems + j * 32 + lane);
+        else sidx[pos] = idx[j];
+    }
+    __syncthreads();
+    // contiguous runs per digit: element at tile position L goes to gbase[d] + (L - boff[d])
+    for (uint32_t L = tid; L < tn; L += kRkThreads) {
+        const uint32_t k = skey[L], d = (k >> shift) & 0xffu;
+        const uint64_t g = (uint64_t)gbase[d] + (L - boff[d]);
+        if (PASS == 0) keys_out[g] = (uint16_t)k;
+        idx_out[g] = sidx[L];
     }
 }
 
@@ -199,21 +285,47 @@ int sms(int dev) {
 
 } // namespace
 
-cudaError_t launch_bucket(const BucketArgs& a, cudaStream_t st, int dev, uint64_t* launches) {
-    const double2* p = reinterpret_cast<const double2*>(a.pts);
-    const int n_blk = a.n_blk;
-    const uint64_t chunk = (a.n + n_blk - 1) / n_blk;
-    bucket_count_kernel<<<n_blk, 1024, 0, st>>>(p, a.n, chunk, a.bbox_keys, a.prefilter, a.blk);
-    bucket_colscan_kernel<<<(kBuckets + 1 + 7) / 8, 256, 0, st>>>(a.blk, n_blk, a.hist);
-    bucket_scan_kernel<<<1, 1024, 0, st>>>(a.hist);
-    bucket_scatter_kernel<<<n_blk, 1024, 0, st>>>(p, a.n, chunk, a.bbox_keys, a.prefilter, a.blk, a.hist,
-                                                  reinterpret_cast<double2*>(a.sorted_pts), a.sorted_idx);
-    *launches += 4;
-    return cudaGetLastError();
+uint64_t bucket_tiles(uint64_t n) { return std::max<uint64_t>(1, (n + kRkTile - 1) / kRkTile); }
+
+size_t bucket_scratch_bytes(uint64_t n) {
+    const uint64_t nt = bucket_tiles(n);
+    // keys, keys1 (u16), idx1, sorted idx (u32), counts (2 x 256 x tiles), totals + bases (2 x 512) + n_in
+    return 2 * ((n * 2 + 15) / 16 * 16) + 2 * ((n * 4 + 15) / 16 * 16) + 2 * 256 * nt * 4 + 4 * 512 * 4 + 64;
 }
 
-int bucket_blocks(uint64_t n, int dev) {
-    return (int)std::max<uint64_t>(1, std::min<uint64_t>((n + 4095) / 4096, (uint64_t)sms(dev)));
+cudaError_t launch_bucket(const BucketArgs& a, cudaStream_t st, int dev, uint64_t* launches) {
+    const double2* p = reinterpret_cast<const double2*>(a.pts);
+    const uint64_t n = a.n, nt = bucket_tiles(n);
+    char* sp = static_cast<char*>(a.scratch);
+    auto take = [&](size_t bytes) {
+        char* r = sp;
+        sp += (bytes + 15) / 16 * 16;
+        return r;
+    };
+    uint16_t* keys = reinterpret_cast<uint16_t*>(take(n * 2));
+    uint16_t* keys1 = reinterpret_cast<uint16_t*>(take(n * 2));
+    uint32_t* idx1 = reinterpret_cast<uint32_t*>(take(n * 4));
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(take(2 * 256 * nt * 4));
+    uint32_t* tot = reinterpret_cast<uint32_t*>(take(512 * 4));
+    uint32_t* base = reinterpret_cast<uint32_t*>(take(512 * 4));
+    rk_key_kernel<<<(unsigned)nt, kRkThreads, 0, st>>>(p, n, a.bbox_keys, a.prefilter, keys, cnt, (uint32_t)nt);
+    // pass-0 offsets; both passes' digit totals (order-independent) for the bases
+    rk_colscan_kernel<<<512 / 8, 256, 0, st>>>(cnt, (uint32_t)nt, tot, 0u);
+    rk_base_kernel<<<1, 64, 0, st>>>(tot, base, a.n_in);
+    static bool attr[64] = {};
+    if (dev >= 0 && dev < 64 && !attr[dev]) {
+        cudaFuncSetAttribute(rk_scatter_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RkShared));
+        cudaFuncSetAttribute(rk_scatter_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RkShared));
+        attr[dev] = true;
+    }
+    const size_t sm = sizeof(RkShared);
+    rk_scatter_kernel<0><<<(unsigned)nt, kRkThreads, sm, st>>>(n, keys, nullptr, cnt, base, (uint32_t)nt, keys1, idx1);
+    rk_count_hi_kernel<<<(unsigned)nt, kRkThreads, 0, st>>>(keys1, n, cnt, (uint32_t)nt);
+    rk_colscan_kernel<<<256 / 8, 256, 0, st>>>(cnt, (uint32_t)nt, tot, 256u);
+    rk_scatter_kernel<1><<<(unsigned)nt, kRkThreads, sm, st>>>(n, keys1, idx1, cnt, base, (uint32_t)nt, nullptr,
+                                                              a.sorted_idx);
+    *launches += 7;
+    return cudaGetLastError();
 }
 
 cudaError_t launch_unbucket(uint64_t n, const uint32_t* n_dev, const uint32_t* sorted_idx, const uint32_t* s_inside,
