@@ -46,7 +46,7 @@ struct DevState {
     cudaStream_t copy = nullptr; // points upload, overlapping polygon-only work on `stream` (made on first use)
     std::vector<cudaEvent_t> up_evs; // one per uploaded chunk
     DevBuf pts, vx, vy, ring_off, pt_off, poly_ring_off, filt, qk, rec, bbox, bits, verdicts, stats, counts, degen;
-    DevBuf bucket_scratch, sorted_idx;                        // y order (pip_sort.cu)
+    DevBuf bucket_scratch, sorted_pts, sorted_idx;            // y order (pip_sort.cu)
     DevBuf csr_meta;                                          // per-polygon records (pip_csr.cu)
     DevBuf cmp_blk, cmp_pts, cmp_idx, cmp_v, cmp_out;         // prefilter / scatter (pip_compact.cu)
     DevBuf csv_text, csv_state, csv_res, csv_out;             // CSV reader (pip_csv.cu)
@@ -241,16 +241,17 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
         sc.inside_bits = d_inside + lo / 32;
         sc.aux_bits = d_aux + lo / 32;
         if (bucket) {
-            // y order by a radix sort of (key, index); the scan kernel gathers the
-            // points by index and writes bit planes in y order (unbucketed below)
+            // y order by a radix sort of (key, point, index); the scan kernel reads
+            // the y-ordered points and writes bit planes in y order (unbucketed below)
             check(c, d.bucket_scratch.ensure(pcd::bucket_scratch_bytes(m) + (2 * mw + 4) * 4), "alloc bucket scratch");
             check(c, d.sorted_idx.ensure(m * 4), "alloc bucket index");
+            check(c, d.sorted_pts.ensure(m * 16), "alloc y-ordered points");
             uint32_t* planes = reinterpret_cast<uint32_t*>(d.bucket_scratch.as<char>() + pcd::bucket_scratch_bytes(m));
             check(c, cudaMemsetAsync(planes, 0, (2 * mw + 4) * 4, st), "clear bucket planes");
             pcd::BucketArgs ba{sc.pts, m, d.bbox.as<unsigned long long>(), prefilter, d.bucket_scratch.p,
-                               d.sorted_idx.as<uint32_t>(), planes + 2 * mw};
+                               d.sorted_pts.as<double>(), d.sorted_idx.as<uint32_t>(), planes + 2 * mw};
             check(c, pcd::launch_bucket(ba, st, d.dev, &c->launches), "bucket kernels");
-            sc.idx = d.sorted_idx.as<uint32_t>();
+            sc.pts = d.sorted_pts.as<double>();
             sc.prefilter = 0; // rejected points sort last and are left out (n_dev)
             sc.inside_bits = planes;
             sc.aux_bits = planes + mw;
@@ -408,7 +409,7 @@ void pc_destroy(pc_ctx* c) {
         cudaStreamSynchronize(d.stream);
         for (DevBuf* b : {&d.pts, &d.vx, &d.vy, &d.ring_off, &d.pt_off, &d.poly_ring_off, &d.filt, &d.qk, &d.rec, &d.bbox,
                           &d.bits, &d.verdicts, &d.stats, &d.counts, &d.degen, &d.bucket_scratch,
-                          &d.sorted_idx, &d.csr_meta, &d.cmp_blk, &d.cmp_pts, &d.cmp_idx, &d.cmp_v,
+                          &d.sorted_pts, &d.sorted_idx, &d.csr_meta, &d.cmp_blk, &d.cmp_pts, &d.cmp_idx, &d.cmp_v,
                           &d.cmp_out, &d.csv_text, &d.csv_state, &d.csv_res, &d.csv_out, &d.emit_recs,
                           &d.emit_scratch, &d.emit_out, &d.tree})
             b->release();

@@ -136,7 +136,7 @@ cudaError_t launch_emit_results(const void* recs, uint64_t n, char* out, uint64_
                                 unsigned long long* out_len, cudaStream_t st, uint64_t* launches);
 
 // y-ordering of the points of one polygon (pip_sort.cu): a stable 2-pass
-// radix sort of (16-bit y key over the outer ring's bbox, index); points the
+// radix sort of (16-bit y key over the outer ring's bbox, point, index); points the
 // bbox prefilter rejects sort last and are not classified.
 struct BucketArgs {
     const double* pts;                    // n interleaved points
@@ -144,6 +144,7 @@ struct BucketArgs {
     const unsigned long long* bbox_keys;  // from prep
     int prefilter;
     void* scratch;                        // bucket_scratch_bytes(n)
+    double* sorted_pts;                   // n points in y order
     uint32_t* sorted_idx;                 // n: original index of each point in y order
     uint32_t* n_in;                       // (device) number of points not rejected
 };

@@ -85,14 +85,27 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
 
 // One elected thread: load key tile [t0, t0 + kQTile) into stage s (the key
 // array is padded to whole tiles with never-candidate words).
+// The key array is re-read by every CTA: keep it in L2 (evict_last), while the
+// point gathers stream past it (evict_first, see load_pt).
 __device__ __forceinline__ void issue_tile(SingleShared& sh, int s, const uint32_t* qk, uint32_t t0) {
     const unsigned bytes = kQTile * 4u;
     const unsigned bar = smem_u32(&sh.full[s]);
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(sh.qk[s])),
-                 "l"(qk + t0), "r"(bytes), "r"(bar)
-                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(sh.qk[s])),
+        "l"(qk + t0), "r"(bytes), "r"(bar), "l"(pol)
+        : "memory");
+}
+
+__device__ __forceinline__ double2 load_pt(const double2* p) {
+    unsigned long long pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    double2 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+    return v;
 }
 
 // Phase-1 test of one key word w = {0x7fff - q(ylo), q(yhi)} against the CTA
@@ -413,7 +426,7 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3)
         bool a = li < cta_n;
         double2 p = make_double2(0.0, 0.0);
         {
-            if (a) p = idx ? pts[idx[cta_base + li]] : pts[cta_base + li];
+            if (a) p = load_pt(idx ? pts + idx[cta_base + li] : pts + cta_base + li);
             if ((k & 3) == 3) asm volatile("" ::: "memory"); // at most 4 point loads in flight (registers)
         }
         if (a && prefilter) a = p.x >= minx && p.x <= maxx && p.y >= miny && p.y <= maxy; // batch.hpp:39-41

@@ -12,8 +12,10 @@
 // unchanged.
 //
 // Sort: 16-bit keys (65280 y levels over the outer ring's bbox, 0xffff =
-// rejected), two stable LSD passes of 8 bits over (key, index) pairs; the
-// points themselves are never moved (the scan kernel gathers them by index).
+// rejected), two stable LSD passes of 8 bits over (key, point, index); each
+// pass reads its tile coalesced, ranks it in shared memory and writes
+// contiguous runs per digit, so the points move in whole lines (a gather by
+// index would pull a 128-byte line per 16-byte point).
 //   rk_key_kernel      keys + per-tile digit counts (pass 1's re-counted over
 //                      the pass-0 output by rk_count_hi_kernel)
 //   rk_scan_kernel     per (digit, tile) offsets: a warp per digit scans its
@@ -34,8 +36,8 @@ namespace pcd {
 namespace {
 
 constexpr int kRkThreads = 512;
-constexpr int kRkItems = 16;                       // per thread
-constexpr int kRkTile = kRkThreads * kRkItems;     // 8192 elements per tile
+constexpr int kRkItems = 8;                        // per thread
+constexpr int kRkTile = kRkThreads * kRkItems;     // 4096 elements per tile
 constexpr int kRkWarps = kRkThreads / 32;
 constexpr uint32_t kRkLevels = 65280;              // in-box keys 0 .. 65279 (high byte < 0xff)
 constexpr uint16_t kRkReject = 0xffff;
@@ -149,6 +151,7 @@ __global__ void __launch_bounds__(64) rk_base_kernel(const uint32_t* __restrict_
 }
 
 struct RkShared {
+    double2 spts[kRkTile];
     uint32_t wcnt[kRkWarps][256];
     uint32_t boff[256];
     uint32_t gbase[256];
@@ -162,6 +165,8 @@ struct RkShared {
 // (implicit), writes keys_out and idx_out; PASS 1: writes idx_out only.
 template <int PASS>
 __global__ void __launch_bounds__(kRkThreads, 2) rk_scatter_kernel(uint64_t n, const uint16_t* __restrict__ keys_in,
+                                                                const double2* __restrict__ pts_in,
+                                                                double2* __restrict__ pts_out,
                                                                 const uint32_t* __restrict__ idx_in,
                                                                 const uint32_t* __restrict__ cnt,
                                                                 const uint32_t* __restrict__ base, uint32_t n_tiles,
@@ -174,6 +179,7 @@ __global__ void __launch_bounds__(kRkThreads, 2) rk_scatter_kernel(uint64_t n, c
     auto& gbase = S.gbase; // global start of this tile's run of each digit
     auto& skey = S.skey;
     auto& sidx = S.sidx;
+    auto& spts = S.spts;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int shift = 8 * PASS;
     for (int j = tid; j < kRkWarps * 256; j += kRkThreads) (&wcnt[0][0])[j] = 0;
@@ -243,8 +249,10 @@ __global__ void __launch_bounds__(kRkThreads, 2) rk_scatter_kernel(uint64_t n, c
         if (kr[j] == 0xffffffffu) continue;
         const uint32_t k = kr[j] >> 16, d = (k >> shift) & 0xffu;
         const uint32_t pos = boff[d] + wcnt[warp][d] + (kr[j] & 0xffffu);
+        const uint32_t e = (uint32_t)warp * 32 * kRkItems + j * 32 + lane;
         skey[pos] = (uint16_t)k;
-        if constexpr (PASS == 0) sidx[pos] = (uint32_t)(t0 + (uint32_t)warp * 32 * kRkItems + j * 32 + lane);
+        spts[pos] = pts_in[t0 + e]; // coalesced read, staged in digit order
+        if constexpr (PASS == 0) sidx[pos] = (uint32_t)(t0 + e);
         else sidx[pos] = idx[j];
     }
     __syncthreads();
@@ -253,6 +261,7 @@ __global__ void __launch_bounds__(kRkThreads, 2) rk_scatter_kernel(uint64_t n, c
         const uint32_t k = skey[L], d = (k >> shift) & 0xffu;
         const uint64_t g = (uint64_t)gbase[d] + (L - boff[d]);
         if (PASS == 0) keys_out[g] = (uint16_t)k;
+        pts_out[g] = spts[L];
         idx_out[g] = sidx[L];
     }
 }
@@ -285,12 +294,13 @@ int sms(int dev) {
 
 } // namespace
 
+
 uint64_t bucket_tiles(uint64_t n) { return std::max<uint64_t>(1, (n + kRkTile - 1) / kRkTile); }
 
 size_t bucket_scratch_bytes(uint64_t n) {
     const uint64_t nt = bucket_tiles(n);
-    // keys, keys1 (u16), idx1, sorted idx (u32), counts (2 x 256 x tiles), totals + bases (2 x 512) + n_in
-    return 2 * ((n * 2 + 15) / 16 * 16) + 2 * ((n * 4 + 15) / 16 * 16) + 2 * 256 * nt * 4 + 4 * 512 * 4 + 64;
+    // keys, keys1 (u16), idx1 (u32), pts1 (2 x f64), counts (2 x 256 x tiles), totals + bases (2 x 512)
+    return 2 * ((n * 2 + 15) / 16 * 16) + (n * 4 + 15) / 16 * 16 + n * 16 + 2 * 256 * nt * 4 + 4 * 512 * 4 + 64;
 }
 
 cudaError_t launch_bucket(const BucketArgs& a, cudaStream_t st, int dev, uint64_t* launches) {
@@ -305,6 +315,7 @@ cudaError_t launch_bucket(const BucketArgs& a, cudaStream_t st, int dev, uint64_
     uint16_t* keys = reinterpret_cast<uint16_t*>(take(n * 2));
     uint16_t* keys1 = reinterpret_cast<uint16_t*>(take(n * 2));
     uint32_t* idx1 = reinterpret_cast<uint32_t*>(take(n * 4));
+    double2* pts1 = reinterpret_cast<double2*>(take(n * 16));
     uint32_t* cnt = reinterpret_cast<uint32_t*>(take(2 * 256 * nt * 4));
     uint32_t* tot = reinterpret_cast<uint32_t*>(take(512 * 4));
     uint32_t* base = reinterpret_cast<uint32_t*>(take(512 * 4));
@@ -319,11 +330,13 @@ cudaError_t launch_bucket(const BucketArgs& a, cudaStream_t st, int dev, uint64_
         attr[dev] = true;
     }
     const size_t sm = sizeof(RkShared);
-    rk_scatter_kernel<0><<<(unsigned)nt, kRkThreads, sm, st>>>(n, keys, nullptr, cnt, base, (uint32_t)nt, keys1, idx1);
+    rk_scatter_kernel<0><<<(unsigned)nt, kRkThreads, sm, st>>>(n, keys, p, pts1, nullptr, cnt, base, (uint32_t)nt,
+                                                              keys1, idx1);
     rk_count_hi_kernel<<<(unsigned)nt, kRkThreads, 0, st>>>(keys1, n, cnt, (uint32_t)nt);
     rk_colscan_kernel<<<256 / 8, 256, 0, st>>>(cnt, (uint32_t)nt, tot, 256u);
-    rk_scatter_kernel<1><<<(unsigned)nt, kRkThreads, sm, st>>>(n, keys1, idx1, cnt, base, (uint32_t)nt, nullptr,
-                                                              a.sorted_idx);
+    rk_scatter_kernel<1><<<(unsigned)nt, kRkThreads, sm, st>>>(n, keys1, pts1,
+                                                              reinterpret_cast<double2*>(a.sorted_pts), idx1, cnt,
+                                                              base, (uint32_t)nt, nullptr, a.sorted_idx);
     *launches += 7;
     return cudaGetLastError();
 }

@@ -12,17 +12,17 @@ int main(int argc, char** argv){
   std::mt19937_64 rng(1); std::uniform_real_distribution<double> U(-1,1);
   std::vector<double> xy(2*n); for (auto& v: xy) v = U(rng);
   unsigned long long bb[8] = {hkey(-0.9), hkey(-1.0), ~hkey(0.9), ~hkey(1.0), 0,0,0,0};
-  double *dp; unsigned long long* db; void* scr; uint32_t *sidx, *nin;
+  double *dp; unsigned long long* db; void* scr; uint32_t *sidx, *nin; double* spts;
   cudaMalloc(&dp, 16*n); cudaMemcpy(dp, xy.data(), 16*n, cudaMemcpyHostToDevice);
   cudaMalloc(&db, 64); cudaMemcpy(db, bb, 64, cudaMemcpyHostToDevice);
-  cudaMalloc(&scr, pcd::bucket_scratch_bytes(n)); cudaMalloc(&sidx, 4*n); cudaMalloc(&nin, 4);
+  cudaMalloc(&scr, pcd::bucket_scratch_bytes(n)); cudaMalloc(&sidx, 4*n); cudaMalloc(&nin, 4); cudaMalloc(&spts, 16*n);
   uint64_t L=0;
-  pcd::BucketArgs a{dp, n, db, 1, scr, sidx, nin};
+  pcd::BucketArgs a{dp, n, db, 1, scr, spts, sidx, nin};
   cudaError_t e = pcd::launch_bucket(a, 0, 0, &L); cudaDeviceSynchronize();
   printf("launch %s sync %s\n", cudaGetErrorString(e), cudaGetErrorString(cudaGetLastError()));
   std::vector<uint32_t> h(n); uint32_t hn; cudaMemcpy(h.data(), sidx, 4*n, cudaMemcpyDeviceToHost); cudaMemcpy(&hn, nin, 4, cudaMemcpyDeviceToHost);
   uint64_t expect_in=0; for (uint64_t i=0;i<n;++i) if (xy[2*i]>=-0.9 && xy[2*i]<=0.9) ++expect_in;
-  { uint64_t nt=(n+8191)/8192; size_t o=((n*2+15)/16*16)*2+((n*4+15)/16*16);
+  { uint64_t nt=(n+4095)/4096; size_t o=((n*2+15)/16*16)*2+((n*4+15)/16*16)+n*16;
     std::vector<uint32_t> cnt(2*256*nt), tot(512), base(512);
     cudaMemcpy(cnt.data(), (char*)scr+o, 4*cnt.size(), cudaMemcpyDeviceToHost); o += (2*256*nt*4+15)/16*16;
     cudaMemcpy(tot.data(), (char*)scr+o, 2048, cudaMemcpyDeviceToHost); o+=2048;
@@ -32,6 +32,8 @@ int main(int argc, char** argv){
     for (int d=250; d<256; ++d) printf("d%d: tot1 %u base1 %u | ", d, tot[256+d], base[256+d]); printf("\n");
   }
   printf("n_in %u expect %llu\n", hn, (unsigned long long)expect_in);
+  { std::vector<double> hp(2*n); cudaMemcpy(hp.data(), spts, 16*n, cudaMemcpyDeviceToHost); uint64_t bad=0;
+    for (uint64_t i=0;i<n;++i) if (h[i]<n && (hp[2*i]!=xy[2*h[i]] || hp[2*i+1]!=xy[2*h[i]+1])) ++bad; printf("point mismatches %llu\n",(unsigned long long)bad); }
   std::vector<char> seen(n,0); uint64_t dup=0, oob=0;
   for (uint64_t i=0;i<n;++i){ if (h[i]>=n){++oob;continue;} if (seen[h[i]]) ++dup; seen[h[i]]=1; }
   uint64_t inv=0; double prev=-1e300;
