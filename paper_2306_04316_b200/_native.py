@@ -92,6 +92,9 @@ def workloads_lib() -> C.CDLL:
         lib.wl_uniform_points.argtypes = [C.c_uint64, C.c_double, C.c_double, C.c_double, C.c_double, C.c_uint64,
                                           _vp, C.c_int]
         lib.wl_uniform_points.restype = None
+        lib.wl_uniform_points_range.argtypes = [C.c_uint64, C.c_uint64, C.c_double, C.c_double, C.c_double,
+                                                C.c_double, C.c_uint64, _vp, C.c_int]
+        lib.wl_uniform_points_range.restype = None
         lib.wl_bounds.argtypes = [_vp, _vp, C.c_uint64, _vp]
         lib.wl_bounds.restype = None
         lib.wl_csr_new.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, C.c_int]

@@ -284,6 +284,25 @@ void wl_uniform_points(uint64_t n, double x0, double y0, double x1, double y1, u
     });
 }
 
+// Points [lo, hi) of the same seeded sequence as wl_uniform_points(n, ...) for
+// any n >= hi (a rank generates only its shard; identical bytes).
+void wl_uniform_points_range(uint64_t lo, uint64_t hi, double x0, double y0, double x1, double y1,
+                             uint64_t seed, double* xy, int threads) {
+    if (hi <= lo) return;
+    const uint64_t c0 = lo / kChunk, c1 = (hi + kChunk - 1) / kChunk;
+    parallel_chunks(c1 - c0, threads, [&](uint64_t k) {
+        const uint64_t c = c0 + k;
+        Rng rng({seed, c, 0x9017});
+        for (uint64_t i = c * kChunk; i < std::min(hi, (c + 1) * kChunk); ++i) {
+            const double x = rng.uniform(x0, x1), y = rng.uniform(y0, y1);
+            if (i >= lo) {
+                xy[2 * (i - lo)] = x;
+                xy[2 * (i - lo) + 1] = y;
+            }
+        }
+    });
+}
+
 // Tight bounds of a vertex range (used to place points "in the bounding box").
 void wl_bounds(const double* vx, const double* vy, uint64_t n, double* box) {
     box[0] = box[2] = vx[0];

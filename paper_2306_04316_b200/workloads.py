@@ -46,6 +46,14 @@ def uniform_points(n: int, box, seed: int, threads=0) -> np.ndarray:
     return xy
 
 
+def uniform_points_range(lo: int, hi: int, box, seed: int, threads=0) -> np.ndarray:
+    """Points [lo, hi) of uniform_points(n, box, seed) for any n >= hi (one rank's shard)."""
+    xy = np.empty((max(hi - lo, 0), 2), np.float64)
+    x0, y0, x1, y1 = box
+    _native.workloads_lib().wl_uniform_points_range(lo, hi, x0, y0, x1, y1, seed, _p(xy), threads)
+    return xy
+
+
 def bounds(poly: Polygon):
     """Tight box of the outer ring (== bbox_of)."""
     b = np.empty(4, np.float64)
@@ -100,7 +108,10 @@ def config2(n: int, seed=SEED, n_points=1_000_000):
     return poly, uniform_points(n_points, bounds(poly), seed + 2 + n)
 
 
-def config4(seed=SEED, n_points=100_000_000, threads=0):
-    """c4: 200,000-vertex fractal star, 1e8 points uniform in its bbox."""
+def config4(seed=SEED, n_points=100_000_000, threads=0, shard=None):
+    """c4: 200,000-vertex fractal star, 1e8 points uniform in its bbox;
+    shard = (lo, hi) generates only points [lo, hi) of the same sequence."""
     poly = fractal_polygon(200_000, seed, threads=threads)
+    if shard is not None:
+        return poly, uniform_points_range(shard[0], shard[1], bounds(poly), seed + 4, threads)
     return poly, uniform_points(n_points, bounds(poly), seed + 4, threads)

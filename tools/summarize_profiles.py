@@ -5,7 +5,9 @@ usage: python tools/summarize_profiles.py <evidence dir> <round tag>
   writes profiles/<tag>_ncu_<name>.csv   (key metrics of each full capture)
          profiles/<tag>_launches_default.csv (per-launch device times, kernel shares)
          profiles/<tag>_bench.jsonl       (the bench lines)
-         profiles/ncu_traffic.json        (DRAM bytes per launch of the dominant kernels, read by bench.py)
+         profiles/ncu_traffic.json        (DRAM bytes per launch of the dominant kernels)
+         profiles/ncu_kernels.json        (per capture <workload>_<mode>: instructions, DRAM bytes, IPC,
+                                           pipe utilisation per launch -- read by bench.py's roofline)
 """
 import csv
 import glob
@@ -24,7 +26,8 @@ METRICS = [
     "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
     "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "dram__bytes_read.sum", "dram__bytes_write.sum",
     "dram__throughput.avg.pct_of_peak_sustained_elapsed", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
-    "lts__t_bytes.sum", "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+    "lts__t_bytes.sum", "lts__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct",
+    "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
     "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem", "smsp__thread_inst_executed_per_inst_executed.ratio",
 ]
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
@@ -54,6 +57,8 @@ def main():
     os.makedirs(prof, exist_ok=True)
     traffic_path = os.path.join(prof, "ncu_traffic.json")
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
+    kern_path = os.path.join(prof, "ncu_kernels.json")
+    kernels = json.load(open(kern_path)) if os.path.exists(kern_path) else {}
     for rep in sorted(glob.glob(os.path.join(src, "full_*.ncu-rep"))):
         name = os.path.basename(rep)[5:-8]
         h, units, data = ncu_raw(rep)
@@ -78,7 +83,25 @@ def main():
             ent["note"] = "captured on a 1e7-point launch (bench c4 uses 1e8); not used as the bench traffic"
         traffic[key] = ent
         print(f"{name}: {rd + wb:.3e} DRAM bytes per launch")
+
+        def num(m):
+            return float(row[h.index(m)]) if m in h and row[h.index(m)] not in ("", "n/a") else None
+        kernels[name] = {
+            "kernel": row[h.index("Kernel Name")][:60], "source": f"profiles/{tag}_ncu_{name}.csv",
+            "duration_ms": num("gpu__time_duration.sum") * (1e-3 if units[h.index("gpu__time_duration.sum")] == "us"
+                                                             else 1.0),
+            "inst_per_launch": num("smsp__inst_executed.sum"), "dram_bytes_per_launch": rd + wb,
+            "ipc": num("sm__inst_executed.avg.per_cycle_active"),
+            "alu_pct": num("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+            "fma_pct": num("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+            "fp64_pct": num("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+            "lsu_pct": num("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"),
+            "lts_pct": num("lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+            "dram_pct": num("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+            "warps_active_pct": num("sm__warps_active.avg.pct_of_peak_sustained_active"),
+        }
     json.dump(traffic, open(traffic_path, "w"), indent=1)
+    json.dump(kernels, open(kern_path, "w"), indent=1, sort_keys=True)
     for lc in sorted(glob.glob(os.path.join(src, "launches_*.csv"))):
         summarize_launches(lc, os.path.join(prof, f"{tag}_{os.path.basename(lc)}"))
     write_bench(src, prof, tag)
