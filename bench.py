@@ -483,21 +483,59 @@ def run_sweep(args, eng, dev):
             "fit": sweep_fit(items, ms)}
 
 
+def lsq_fit(x, t):
+    """Least-squares line t = slope * x + intercept, solved exactly as the
+    reference's least_squares_fit (proj/include/polycast/bench.hpp:123-150):
+    sequential means, centred sums Sxx, Sxy, slope = Sxy / Sxx, intercept =
+    mean_t - slope * mean_x (same operation order, so bit-identical results;
+    tests/test_lsq_fit.py checks it against the reference)."""
+    x = [float(v) for v in x]
+    t = [float(v) for v in t]
+    if len(x) < 2:
+        raise ValueError("least_squares_fit: need at least 2 samples")
+    mx = mt = 0.0
+    for a, b in zip(x, t):
+        mx += a
+        mt += b
+    mx /= len(x)
+    mt /= len(x)
+    sxx = sxy = 0.0
+    for a, b in zip(x, t):
+        d = a - mx
+        sxx += d * d
+        sxy += d * (b - mt)
+    if sxx == 0.0:
+        raise ValueError("least_squares_fit: all samples share one n_points value")
+    slope = sxy / sxx
+    return slope, mt - slope * mx
+
+
+def error_rows(slope, intercept, x, t):
+    """The reference's error_report (bench.hpp:176-198) for one fit:
+    (predicted, absolute error, relative error or None) per sample."""
+    out = []
+    for a, b in zip(x, t):
+        pred = slope * float(a) + intercept
+        ab = abs(pred - float(b))
+        out.append((pred, ab, ab / float(b) if float(b) > 0.0 else None))
+    return out
+
+
 def sweep_fit(items, per_item_ms):
     """The paper's O(n) claim on the GPU: least-squares line of kernel time vs n
-    (vertices) over the sweep, solved on centred data as the reference's
-    least_squares_fit (bench.hpp:120-148), with its per-sample relative
-    prediction error (error_report, bench.hpp:172-199) and R^2."""
-    n = np.array([it.tests / it.n_points for it in items], dtype=np.float64)  # edges
-    t = np.asarray(per_item_ms, dtype=np.float64) / 1e3
-    dn, dt = n - n.mean(), t - t.mean()
-    slope = float((dn * dt).sum() / (dn * dn).sum())
-    icpt = float(t.mean() - slope * n.mean())
-    pred = slope * n + icpt
-    ss_res, ss_tot = float(((t - pred) ** 2).sum()), float((dt * dt).sum())
+    (edges) over the sweep (lsq_fit, the reference's least_squares_fit), its
+    per-sample relative prediction error (error_rows, the reference's
+    error_report) and R^2."""
+    n = [it.tests / it.n_points for it in items]  # edges
+    t = [float(m) / 1e3 for m in per_item_ms]
+    slope, icpt = lsq_fit(n, t)
+    rows = error_rows(slope, icpt, n, t)
+    mt = sum(t) / len(t)
+    ss_res = sum((b - r[0]) ** 2 for b, r in zip(t, rows))
+    ss_tot = sum((b - mt) ** 2 for b in t)
     return {"x": "edges n", "y": "kernel seconds per 1e6-point launch", "slope_s_per_edge": slope,
             "intercept_s": icpt, "r2": 1.0 - ss_res / ss_tot if ss_tot > 0 else 1.0,
-            "rel_err": {it.label: float(abs(p - a) / a) for it, p, a in zip(items, pred, t)}}
+            "rel_err": {it.label: r[2] for it, r in zip(items, rows)}}
 
 
 def job_totals(items, world, dev):

@@ -188,7 +188,9 @@ inline std::size_t ring_count(const Point2& p, const Ring& ring, int mode, const
     uint8_t deg = 0;
     pc_ctx* ctx = device::context();
     device::throw_on(pc_count_crossings(ctx, &p.x, 1, x.data(), y.data(), x.size(), mode, &cnt, &deg), ctx, who);
-    if (deg) throw DegenerateEdge(std::string(who) + ": horizontal edge lies on the query ray");
+    // the reference's message names the first degenerate edge (geometry.hpp:219-220);
+    // the engine reports its index in place of the count
+    if (deg) throw DegenerateEdge(std::string(who) + ": horizontal edge " + std::to_string(cnt) + " lies on the query ray");
     return static_cast<std::size_t>(cnt);
 }
 
@@ -216,7 +218,11 @@ inline Classification contains(const Point2& p, const Polygon& poly, CrossingMod
     switch (verdict) {
     case PC_INSIDE: return Classification::Inside;
     case PC_BOUNDARY: return Classification::Boundary;
-    case PC_ERROR: throw DegenerateEdge("contains: horizontal edge lies on the query ray");
+    case PC_ERROR:
+        // the reference's contains propagates count_crossings_c2's exception from
+        // the first ring (in ring order) whose loop meets a horizontal edge on the ray
+        for (const Ring& ring : poly.rings()) detail::ring_count(p, ring, PC_MODE_C2, "count_crossings_c2");
+        throw DegenerateEdge("count_crossings_c2: horizontal edge lies on the query ray");
     default: return Classification::Outside;
     }
 }

@@ -95,7 +95,8 @@ int pc_classify_csr(pc_ctx* ctx, const double* pts_xy, const uint64_t* pt_off, u
 /* count_crossings_c1 (mode 0) / count_crossings_c2 (mode 1) of one closed
  * ring of nv vertices for n points (geometry.hpp:182-229).  counts[i] is the
  * crossing count; degenerate[i] = 1 where the reference throws DegenerateEdge
- * (C2, horizontal edge on the ray; the count is then undefined). */
+ * (C2, horizontal edge on the ray), and counts[i] is then the index of the
+ * first such edge (the index in the reference's message, geometry.hpp:219). */
 int pc_count_crossings(pc_ctx* ctx, const double* pts_xy, uint64_t n, const double* vx,
                        const double* vy, uint64_t nv, int mode, uint64_t* counts,
                        uint8_t* degenerate);

@@ -52,6 +52,14 @@ struct DevState {
     DevBuf csv_text, csv_state, csv_res, csv_out;             // CSV reader (pip_csv.cu)
     DevBuf emit_recs, emit_scratch, emit_out;                 // results-CSV writer (pip_emit.cu)
     DevBuf tree;                                              // segment tree + fallback (pip_tree.cu)
+    // small calls (pip_small.cu): the last polygon, by content (host copy for the
+    // comparison), with its outer bbox; pinned staging of points in / results out
+    std::vector<double> cvx, cvy;
+    std::vector<uint64_t> cro;
+    bool cvalid = false;
+    DevBuf c_vx, c_vy, c_ro, c_box, small_pts, small_out;
+    unsigned char* h_small = nullptr;
+    size_t h_small_cap = 0;
     unsigned long long* h_stats = nullptr; // pinned 4 x u64
     pch::Stager* stager = nullptr;         // pageable host copies (host_stage.h), made on first use
     // profiling: one event pair per main-kernel launch since the last take
@@ -353,6 +361,79 @@ void merge_bits(uint32_t* dst, const uint32_t* src, uint64_t bit_off, uint64_t n
     }
 }
 
+// The polygon of a small call on the device: reused while the caller passes the
+// same vertices (compared by content, so a changed polygon is never stale).
+void cache_polygon(pc_ctx* c, DevState& d, const double* vx, const double* vy, const uint64_t* ring_off,
+                   uint32_t n_rings, cudaStream_t st) {
+    const uint64_t nv = ring_off[n_rings];
+    if (d.cvalid && d.cro.size() == (size_t)n_rings + 1 && d.cvx.size() == nv &&
+        std::memcmp(d.cro.data(), ring_off, (n_rings + 1) * sizeof(uint64_t)) == 0 &&
+        std::memcmp(d.cvx.data(), vx, nv * 8) == 0 && std::memcmp(d.cvy.data(), vy, nv * 8) == 0)
+        return;
+    d.cvalid = false;
+    d.cvx.assign(vx, vx + nv);
+    d.cvy.assign(vy, vy + nv);
+    d.cro.assign(ring_off, ring_off + n_rings + 1);
+    check(c, d.c_vx.ensure(std::max<uint64_t>(nv * 8, 16)), "alloc cached polygon");
+    check(c, d.c_vy.ensure(std::max<uint64_t>(nv * 8, 16)), "alloc cached polygon");
+    check(c, d.c_ro.ensure((n_rings + 1) * 8ull), "alloc cached polygon");
+    check(c, d.c_box.ensure(4 * sizeof(double)), "alloc cached bbox");
+    check(c, cudaMemcpyAsync(d.c_vx.p, d.cvx.data(), nv * 8, cudaMemcpyHostToDevice, st), "upload polygon");
+    check(c, cudaMemcpyAsync(d.c_vy.p, d.cvy.data(), nv * 8, cudaMemcpyHostToDevice, st), "upload polygon");
+    check(c, cudaMemcpyAsync(d.c_ro.p, d.cro.data(), (n_rings + 1) * 8ull, cudaMemcpyHostToDevice, st),
+          "upload polygon");
+    if (nv > 0) check(c, pcd::launch_outer_bbox(d.c_vx.as<double>(), d.c_vy.as<double>(), d.c_ro.as<uint64_t>(),
+                                                d.c_box.as<double>(), st, &c->launches), "bbox kernel");
+    check(c, cudaStreamSynchronize(st), "upload polygon"); // the host copies may change with the next call
+    d.cvalid = true;
+}
+
+unsigned char* small_staging(pc_ctx* c, DevState& d, size_t bytes) {
+    if (bytes > d.h_small_cap) {
+        if (d.h_small) cudaFreeHost(d.h_small);
+        d.h_small = nullptr;
+        d.h_small_cap = 0;
+        const size_t want = std::max<size_t>(bytes, 1 << 16);
+        check(c, cudaMallocHost(&d.h_small, want), "alloc pinned staging");
+        d.h_small_cap = want;
+    }
+    return d.h_small;
+}
+
+// classify_batch / contains on at most kSmallN points: one upload, one launch, one download
+constexpr uint64_t kSmallN = 2048;
+
+void classify_small(pc_ctx* c, const double* pts_xy, uint64_t n, const double* vx, const double* vy,
+                    const uint64_t* ring_off, uint32_t n_rings, int mode, double tol, int prefilter,
+                    uint8_t* verdicts, uint32_t* inside_bits, uint32_t* aux_bits, uint64_t* stats) {
+    DevState& d = c->devs[0];
+    check(c, cudaSetDevice(d.dev), "cudaSetDevice");
+    cudaStream_t st = d.stream;
+    cache_polygon(c, d, vx, vy, ring_off, n_rings, st);
+    const size_t ob = pcd::small_out_bytes(n), ib = n * 16;
+    unsigned char* h = small_staging(c, d, ib + ob);
+    std::memcpy(h, pts_xy, ib);
+    check(c, d.small_pts.ensure(ib), "alloc points");
+    check(c, d.small_out.ensure(ob), "alloc results");
+    check(c, cudaMemcpyAsync(d.small_pts.p, h, ib, cudaMemcpyHostToDevice, st), "upload points");
+    check(c, cudaMemsetAsync(d.small_out.p, 0, ob, st), "clear results");
+    mark_begin(c, d, st);
+    check(c, pcd::launch_small(d.small_pts.as<double>(), n, d.c_vx.as<double>(), d.c_vy.as<double>(),
+                               d.c_ro.as<uint64_t>(), n_rings, prefilter ? d.c_box.as<double>() : nullptr, mode, tol,
+                               d.small_out.p, nullptr, nullptr, st, &c->launches),
+          "small classify kernel");
+    mark_end(c, d, st);
+    check(c, cudaMemcpyAsync(h + ib, d.small_out.p, ob, cudaMemcpyDeviceToHost, st), "download results");
+    check(c, cudaStreamSynchronize(st), "classify");
+    const uint64_t nw = (n + 31) / 32;
+    const unsigned char* o = h + ib;
+    if (verdicts) std::memcpy(verdicts, o, n);
+    const unsigned char* planes = o + ((n + 15) & ~15ull);
+    if (inside_bits) std::memcpy(inside_bits, planes, nw * 4);
+    if (aux_bits) std::memcpy(aux_bits, planes + nw * 4, nw * 4);
+    if (stats) std::memcpy(stats, planes + 2 * nw * 4, 32);
+}
+
 } // namespace
 
 extern "C" {
@@ -414,6 +495,8 @@ void pc_destroy(pc_ctx* c) {
                           &d.emit_scratch, &d.emit_out, &d.tree})
             b->release();
         if (d.h_stats) cudaFreeHost(d.h_stats);
+        if (d.h_small) cudaFreeHost(d.h_small);
+        for (DevBuf* b : {&d.c_vx, &d.c_vy, &d.c_ro, &d.c_box, &d.small_pts, &d.small_out}) b->release();
         delete d.stager;
         for (auto& e : d.evs) {
             cudaEventDestroy(e.first);
@@ -522,6 +605,11 @@ int pc_classify(pc_ctx* c, const double* pts_xy, uint64_t n, const double* vx, c
             return;
         }
         const uint64_t n_verts = ring_off[n_rings];
+        if (n <= kSmallN) { // the drop-in API's single-point calls and tiny batches
+            classify_small(c, pts_xy, n, vx, vy, ring_off, n_rings, mode, tol, prefilter, verdicts, inside_bits,
+                           aux_bits, stats);
+            return;
+        }
         // contiguous shards, 32-point aligned so every device owns whole words
         const uint64_t ndev = std::min<uint64_t>(c->devs.size(), std::max<uint64_t>(1, n / 32));
         uint64_t shard = (n + ndev - 1) / ndev;
@@ -685,6 +773,26 @@ int pc_count_crossings(pc_ctx* c, const double* pts_xy, uint64_t n, const double
         DevState& d = c->devs[0];
         check(c, cudaSetDevice(d.dev), "cudaSetDevice");
         cudaStream_t st = d.stream;
+        if (n <= kSmallN) { // cached ring, a CTA per point, one round trip
+            const uint64_t ro[2] = {0, nv};
+            cache_polygon(c, d, vx, vy, ro, 1, st);
+            const size_t ib = n * 16, cb = n * 8;
+            unsigned char* h = small_staging(c, d, ib + cb + n);
+            std::memcpy(h, pts_xy, ib);
+            check(c, d.small_pts.ensure(ib), "alloc points");
+            check(c, d.small_out.ensure(cb + n + 16), "alloc results");
+            check(c, cudaMemcpyAsync(d.small_pts.p, h, ib, cudaMemcpyHostToDevice, st), "upload points");
+            unsigned long long* dc = d.small_out.as<unsigned long long>();
+            check(c, pcd::launch_small(d.small_pts.as<double>(), n, d.c_vx.as<double>(), d.c_vy.as<double>(),
+                                       d.c_ro.as<uint64_t>(), 1, nullptr, mode, 0.0, nullptr, dc,
+                                       reinterpret_cast<uint8_t*>(dc + n), st, &c->launches),
+                  "count kernel");
+            check(c, cudaMemcpyAsync(h + ib, d.small_out.p, cb + n, cudaMemcpyDeviceToHost, st), "download counts");
+            check(c, cudaStreamSynchronize(st), "count_crossings");
+            std::memcpy(counts, h + ib, cb);
+            std::memcpy(degenerate, h + ib + cb, n);
+            return;
+        }
         h2d(c, d, d.pts, pts_xy, n * 16, st, "upload points");
         h2d(c, d, d.vx, vx, nv * 8, st, "upload vx");
         h2d(c, d, d.vy, vy, nv * 8, st, "upload vy");

@@ -216,6 +216,13 @@ cudaError_t launch_exact_single(const double* pts, uint64_t n, const double* vx,
     return cudaGetLastError();
 }
 
+cudaError_t launch_outer_bbox(const double* vx, const double* vy, const uint64_t* ring_off, double* box,
+                              cudaStream_t st, uint64_t* launches) {
+    exact_bbox_kernel<<<1, kXTPB, 0, st>>>(vx, vy, ring_off, box);
+    ++*launches;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_exact_csr(const CsrArgs& a, uint64_t n_points, cudaStream_t st, uint64_t* launches) {
     if (n_points == 0) return cudaSuccess;
     const unsigned grid = (unsigned)((n_points + kXTPB - 1) / kXTPB);

@@ -224,17 +224,19 @@ __global__ void __launch_bounds__(256) count_kernel(const double2* __restrict__ 
     const double2 q = pts[i];
     int cnt = 0;
     bool aux = false;
+    uint64_t first = 0; // the reference throws DegenerateEdge at the first such edge: report its index
     if (nv >= 2) {
         double ax = vx[0], ay = vy[0];
         double f_prev = __dsub_rn(ay, q.y);
-        for (uint64_t v = 1; v < nv; ++v) {
+        for (uint64_t v = 1; v < nv && !aux; ++v) {
             const double bx = vx[v], by = vy[v];
             raw_edge<MODE>(q.x, q.y, 0.0, 0.0, ax, ay, bx, by, f_prev, cnt, aux);
+            first = v - 1;
             ax = bx;
             ay = by;
         }
     }
-    counts[i] = (unsigned long long)cnt;
+    counts[i] = aux ? (unsigned long long)first : (unsigned long long)cnt;
     degenerate[i] = aux ? 1 : 0;
 }
 

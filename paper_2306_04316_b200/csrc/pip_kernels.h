@@ -163,6 +163,20 @@ cudaError_t launch_exact_single(const double* pts, uint64_t n, const double* vx,
                                 uint64_t* launches);
 cudaError_t launch_exact_csr(const CsrArgs& a, uint64_t n_points, cudaStream_t st, uint64_t* launches);
 
+// bbox_of (batch.hpp:121-133) of the outer ring into box[4] (one CTA).
+cudaError_t launch_outer_bbox(const double* vx, const double* vy, const uint64_t* ring_off, double* box,
+                              cudaStream_t st, uint64_t* launches);
+
+// Small calls (pip_small.cu): a CTA per point over all edges.  classify (counts
+// == nullptr): out = small_out_bytes(n) zeroed bytes -> verdicts | inside |
+// aux | stats; box = outer bbox (prefilter) or nullptr.  count (counts != nullptr,
+// ring_off = {0, nv}, n_rings = 1, mode C1/C2): counts[i] = crossings, or the
+// first degenerate edge's index where degen[i] = 1.
+size_t small_out_bytes(uint64_t n);
+cudaError_t launch_small(const double* pts, uint64_t n, const double* vx, const double* vy, const uint64_t* ring_off,
+                         uint32_t n_rings, const double* box, int mode, double tol, void* out,
+                         unsigned long long* counts, uint8_t* degen, cudaStream_t st, uint64_t* launches);
+
 cudaError_t launch_fp64_probe(double* out, int iters, int dev, cudaStream_t st, double* flops);
 
 } // namespace pcd

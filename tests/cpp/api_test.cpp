@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstring>
 #include <fstream>
+#include <functional>
 #include <numbers>
 #include <random>
 #include <string>
@@ -74,6 +75,64 @@ using RefReadCsv = int (*)(const char*, const char*, uint64_t, const char*, uint
 RefReadCsv g_ref_csv = nullptr;
 using RefWriteResults = int (*)(const char*, const uint64_t*, const double*, const uint8_t*, uint64_t);
 RefWriteResults g_ref_write = nullptr;
+using RefRandomBatch = void (*)(const double*, uint64_t, uint64_t, double*);
+RefRandomBatch g_ref_rb = nullptr;
+
+std::string what_of(const std::function<void()>& f) {
+    try {
+        f();
+    } catch (const std::exception& e) {
+        return e.what();
+    }
+    return "";
+}
+
+// DegenerateEdge text names the first degenerate edge (geometry.hpp:219-220),
+// through count_crossings_c2 and through contains (which propagates it)
+void degenerate_messages() {
+    const Ring sq = square();
+    CHECK(what_of([&] { (void)count_crossings_c2({0.5, 0.0}, sq); }) ==
+          "count_crossings_c2: horizontal edge 0 lies on the query ray");
+    CHECK(what_of([&] { (void)count_crossings_c2({0.5, 1.0}, sq); }) ==
+          "count_crossings_c2: horizontal edge 2 lies on the query ray");
+    CHECK(what_of([&] { (void)contains({0.5, 0.0}, Polygon(sq), CrossingMode::C2); }) ==
+          "count_crossings_c2: horizontal edge 0 lies on the query ray");
+    // a hole's horizontal edge (index 1 of the hole ring), the outer ring clean at y = 5
+    const Ring outer({{0, 0}, {10, 1}, {11, 11}, {-1, 10}, {0, 0}});
+    const Ring hole({{2, 4}, {2, 5}, {4, 5}, {4, 4}, {2, 4}});
+    const Polygon holed(outer, {hole});
+    CHECK(what_of([&] { (void)contains({3.0, 5.0}, holed, CrossingMode::C2); }) ==
+          "count_crossings_c2: horizontal edge 1 lies on the query ray");
+}
+
+// bench.hpp: random_batch identical to the reference's; a GPU scaling run
+void bench_harness() {
+    const BBox box(-2.0, -1.0, 3.0, 4.0);
+    const PointBatch b = random_batch(box, 1000, 42);
+    if (g_ref_rb) {
+        std::vector<double> ref(2000);
+        const double bx[4] = {-2.0, -1.0, 3.0, 4.0};
+        g_ref_rb(bx, 1000, 42, ref.data());
+        bool eq = true;
+        for (std::size_t i = 0; i < 1000; ++i) eq = eq && b.points[i].x == ref[2 * i] && b.points[i].y == ref[2 * i + 1];
+        CHECK(eq);
+    }
+    std::mt19937_64 g(5);
+    const Polygon poly(star(g, 500, {0, 0}, 0.5, 1.0));
+    const std::vector<std::size_t> sizes{10000, 20000, 40000, 80000};
+    const auto samples = run_scaling_bench(poly, sizes, CrossingMode::C1, 4, 2, 9);
+    CHECK(samples.size() == 4 && samples[0].algorithm == "c1_p" && samples[3].n_points == 80000);
+    bool pos = true;
+    for (const auto& s : samples) pos = pos && s.elapsed_seconds > 0.0;
+    CHECK(pos);
+    const GroupedFits fits = fit_per_algorithm(samples);
+    CHECK(fits.fits.size() == 1 && fits.degenerate.empty());
+    const ErrorReport rep = error_report(fits.fits, samples);
+    CHECK(rep.size() == 4 && rep[0].relative_error.has_value());
+    CHECK_THROWS(run_scaling_bench(poly, std::vector<std::size_t>{5, 5}, CrossingMode::C1, 1, 1, 0), std::invalid_argument);
+    CHECK_THROWS(least_squares_fit(std::vector<TimingSample>{{5, "a", 1.0}}), DegenerateFit);
+    CHECK_THROWS(error_report(fits.fits, std::vector<TimingSample>{{5, "zz", 1.0}}), MissingFit);
+}
 
 void kats() {
     const Ring sq = square();
@@ -536,10 +595,13 @@ int main(int argc, char** argv) {
         g_ref = reinterpret_cast<RefClassify>(dlsym(h, "ref_classify"));
         g_ref_csv = reinterpret_cast<RefReadCsv>(dlsym(h, "ref_read_points_csv"));
         g_ref_write = reinterpret_cast<RefWriteResults>(dlsym(h, "ref_write_results_csv"));
+        g_ref_rb = reinterpret_cast<RefRandomBatch>(dlsym(h, "ref_random_batch"));
     }
     else std::printf("note: reference shim not found at %s; reference cross-check skipped\n", ref_path);
     try {
         kats();
+        degenerate_messages();
+        bench_harness();
         randomized();
         prefilter_scatter();
         csv_vs_reference();
