@@ -58,7 +58,7 @@ class Item:
                           + 8 * len(csr.ring_off))
 
 
-def build_items(workload, rank, world):
+def build_items(workload, rank, world, c4_total=100_000_000):
     from paper_2306_04316_b200 import workloads as W
     seed = W.SEED + 1000 * rank
     if workload == "c2_sweep":
@@ -72,7 +72,7 @@ def build_items(workload, rank, world):
         return [Item("star1000", poly, W.uniform_points(1_000_000, (-1.0, -1.0, 1.0, 1.0), seed + 1))]
     if workload == "c4":
         from paper_2306_04316_b200.dist import shard_range
-        total = 100_000_000
+        total = c4_total
         lo, hi = shard_range(total, rank, world)
         poly, xy = W.config4(W.SEED, total, shard=(lo, hi))  # this rank's shard only
         return [Item("fractal200k", poly, xy)]
@@ -652,6 +652,40 @@ def run_cpu_baseline(args, items):
             "seconds": tsum}
 
 
+def run_dist_check(args, rank, world):
+    """CPU check of this script's torchrun path (gloo, any world size): each rank
+    builds only its configs[3] shard (build_items), a per-point stand-in flag
+    (y above the bbox centre: no classification happens here) is packed into a
+    bit plane and all-gathered with the same helper the GPU run uses, and the
+    job totals / max-over-ranks reductions run; rank 0 checks everything
+    against the single-process result and prints one JSON line."""
+    import torch.distributed as dist
+
+    from paper_2306_04316_b200 import pack_bits
+    from paper_2306_04316_b200 import workloads as W
+    from paper_2306_04316_b200.dist import gather_bit_planes, job_totals, max_over_ranks, shard_range
+    import torch
+    total = args.dist_check_points
+    items = build_items("c4", rank, world, c4_total=total)
+    it = items[0]
+    lo, hi = shard_range(total, rank, world)
+    assert it.n_points == hi - lo
+    box = W.bounds(it.poly)
+    cy = 0.5 * (box[1] + box[3])
+    local = torch.from_numpy(pack_bits(it.xy[:, 1] > cy).view(np.int32).copy())
+    full = gather_bit_planes(local, total, world)
+    units, pts = job_totals(it.tests, it.n_points, world)
+    mx = max_over_ranks(float(rank + 1), world)
+    ok = True
+    if rank == 0:
+        _, xy = W.config4(W.SEED, total)
+        ok = (np.array_equal(full, pack_bits(xy[:, 1] > cy)) and pts == total
+              and units == total * it.poly.n_edges and mx == float(world))
+        print(json.dumps({"dist_check": "ok" if ok else "FAILED", "world": world, "points": total,
+                          "backend": dist.get_backend()}), flush=True)
+    return ok
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -660,6 +694,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c4", choices=list(WORKLOAD_NAMES))
     ap.add_argument("--no-sweep", action="store_true", help="c4: skip the configs[1] sweep sub-line")
+    ap.add_argument("--dist-check", action="store_true",
+                    help="CPU/gloo check of the torchrun plumbing (shards, gather, reductions); no GPU, no timing")
+    ap.add_argument("--dist-check-points", type=int, default=1_000_003)
     ap.add_argument("--mode", type=int, default=0, choices=[0, 1, 2])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -675,6 +712,14 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    if args.dist_check:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        try:
+            ok = run_dist_check(args, rank, world)
+        finally:
+            dist.destroy_process_group()
+        raise SystemExit(0 if ok else 1)
     if world > 1:
         import torch
         import torch.distributed as dist

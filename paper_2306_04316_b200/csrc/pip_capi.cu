@@ -15,6 +15,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 namespace {
@@ -61,6 +62,7 @@ struct DevState {
     unsigned char* h_small = nullptr;
     size_t h_small_cap = 0;
     unsigned long long* h_stats = nullptr; // pinned 4 x u64
+    uint64_t launches = 0;                 // kernels this device launched in the current call
     pch::Stager* stager = nullptr;         // pageable host copies (host_stage.h), made on first use
     // profiling: one event pair per main-kernel launch since the last take
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
@@ -77,7 +79,6 @@ struct pc_ctx {
     std::vector<DevState> devs;
     std::string err;
     std::mutex mu;
-    uint64_t launches = 0;
     bool profiling = false;
     int64_t bucket_mode = -1; // PC_OPT_BUCKET_POINTS: -1 auto, 0 off, 1 on
     int64_t tree_mode = 0;    // PC_OPT_TREE: 0 off (default), 1 on (opt-in extension, not the reference scan)
@@ -86,32 +87,60 @@ struct pc_ctx {
 
 namespace {
 
+// An error carries its message, so per-device host threads never write the
+// context's shared error string concurrently (guarded() publishes it).
 struct Fail {
     int code;
+    std::string msg;
 };
 
-void check(pc_ctx* c, cudaError_t e, const char* what) {
+void check(pc_ctx*, cudaError_t e, const char* what) {
     if (e == cudaSuccess) return;
-    c->err = std::string(what) + ": " + cudaGetErrorString(e);
+    std::string m = std::string(what) + ": " + cudaGetErrorString(e);
     cudaGetLastError(); // clear sticky-free errors
-    throw Fail{e == cudaErrorMemoryAllocation ? PC_ENOMEM : PC_ECUDA};
+    throw Fail{e == cudaErrorMemoryAllocation ? PC_ENOMEM : PC_ECUDA, std::move(m)};
 }
 
-void invalid(pc_ctx* c, const char* msg) {
-    c->err = msg;
-    throw Fail{PC_EINVAL};
+void invalid(pc_ctx*, const char* msg) { throw Fail{PC_EINVAL, msg}; }
+
+// Runs fn(i) for every device index i, each on its own host thread when there
+// are several (enqueue, copies and the final wait of one device never wait on
+// another's); rethrows the first failure.
+template <class Fn>
+void per_device(size_t n, Fn&& fn) {
+    if (n <= 1) {
+        if (n == 1) fn(size_t(0));
+        return;
+    }
+    std::vector<Fail> errs(n, Fail{PC_OK, {}});
+    std::vector<std::thread> th;
+    th.reserve(n);
+    for (size_t i = 0; i < n; ++i)
+        th.emplace_back([&, i] {
+            try {
+                fn(i);
+            } catch (const Fail& f) {
+                errs[i] = f;
+            } catch (const std::exception& e) {
+                errs[i] = Fail{PC_ENOMEM, e.what()};
+            }
+        });
+    for (auto& t : th) t.join();
+    for (auto& f : errs)
+        if (f.code != PC_OK) throw f;
 }
 
 template <class Fn>
 int guarded(pc_ctx* c, Fn&& fn) {
     if (!c) return PC_EINVAL;
     std::lock_guard<std::mutex> lk(c->mu);
-    c->launches = 0;
+    for (auto& d : c->devs) d.launches = 0;
     try {
         fn();
         c->err.clear();
         return PC_OK;
     } catch (const Fail& f) {
+        c->err = f.msg;
         return f.code;
     } catch (const std::exception& e) {
         c->err = e.what();
@@ -170,10 +199,10 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
         check(c, cudaMemsetAsync(d_stats, 0, 4 * sizeof(unsigned long long), st), "clear stats");
         mark_begin(c, d, st);
         check(c, pcd::launch_exact_single(d_pts, n, d_vx, d_vy, d_ring_off, n_rings, prefilter, d.bbox.as<double>(),
-                                          mode, tol, d_inside, d_aux, st, &c->launches),
+                                          mode, tol, d_inside, d_aux, st, &d.launches),
               "exact kernel");
         mark_end(c, d, st);
-        check(c, pcd::launch_finalize(n, d_inside, d_aux, d_verdicts, mode, d_stats, st, d.dev, &c->launches),
+        check(c, pcd::launch_finalize(n, d_inside, d_aux, d_verdicts, mode, d_stats, st, d.dev, &d.launches),
               "finalize kernel");
         return;
     }
@@ -197,7 +226,7 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
     // inside and aux are zeroed separately (they need not be contiguous)
     pa.zero_words = d_inside;
     pa.n_zero_words = nwords;
-    check(c, pcd::launch_prep(pa, st, d.dev, &c->launches), "prep kernel");
+    check(c, pcd::launch_prep(pa, st, d.dev, &d.launches), "prep kernel");
     check(c, cudaMemsetAsync(d_aux, 0, nwords * 4, st), "clear aux plane");
     const bool tree = (mode == 0 || mode == 1) /* C1, C2 */ && c->tree_mode == 1 && pcd::tree_eligible(n_verts, n, true);
     const bool bucket = !tree && n < 0xffffffffull &&
@@ -233,7 +262,7 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
         ta.bbox_keys = d.bbox.as<unsigned long long>();
         check(c, d.tree.ensure(pcd::tree_scratch_bytes(n_verts, n_edges, ta.n_layout)), "alloc segment tree");
         mark_begin(c, d, st);
-        check(c, pcd::launch_tree_phase(ta, d.tree.p, st, d.dev, &c->launches, pcd::kTreeBuild), "segment-tree build");
+        check(c, pcd::launch_tree_phase(ta, d.tree.p, st, d.dev, &d.launches, pcd::kTreeBuild), "segment-tree build");
         mark_end(c, d, st);
     }
     // the points in chunks of `chunk` (one chunk when the caller uploads them in one
@@ -258,7 +287,7 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
             check(c, cudaMemsetAsync(planes, 0, (2 * mw + 4) * 4, st), "clear bucket planes");
             pcd::BucketArgs ba{sc.pts, m, d.bbox.as<unsigned long long>(), prefilter, d.bucket_scratch.p,
                                d.sorted_pts.as<double>(), d.sorted_idx.as<uint32_t>(), planes + 2 * mw};
-            check(c, pcd::launch_bucket(ba, st, d.dev, &c->launches), "bucket kernels");
+            check(c, pcd::launch_bucket(ba, st, d.dev, &d.launches), "bucket kernels");
             sc.pts = d.sorted_pts.as<double>();
             sc.prefilter = 0; // rejected points sort last and are left out (n_dev)
             sc.inside_bits = planes;
@@ -276,20 +305,20 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
             ta.single = sc;
             ta.single.n_dev = nullptr;
             mark_begin(c, d, st, true); // one measurement with the build
-            check(c, pcd::launch_tree_phase(ta, d.tree.p, st, d.dev, &c->launches, pcd::kTreeQuery),
+            check(c, pcd::launch_tree_phase(ta, d.tree.p, st, d.dev, &d.launches, pcd::kTreeQuery),
                   "segment-tree query");
             mark_end(c, d, st);
         } else {
             mark_begin(c, d, st, k > 0);
-            check(c, pcd::launch_single(sc, st, d.dev, &c->launches), "classify kernel");
+            check(c, pcd::launch_single(sc, st, d.dev, &d.launches), "classify kernel");
             mark_end(c, d, st);
         }
         if (bucket)
             check(c, pcd::launch_unbucket(m, sc.n_dev, d.sorted_idx.as<uint32_t>(), sc.inside_bits, sc.aux_bits,
-                                          d_inside + lo / 32, d_aux + lo / 32, st, d.dev, &c->launches),
+                                          d_inside + lo / 32, d_aux + lo / 32, st, d.dev, &d.launches),
                   "unbucket kernel");
     }
-    check(c, pcd::launch_finalize(n, d_inside, d_aux, d_verdicts, mode, d_stats, st, d.dev, &c->launches),
+    check(c, pcd::launch_finalize(n, d_inside, d_aux, d_verdicts, mode, d_stats, st, d.dev, &d.launches),
           "finalize kernel");
 }
 
@@ -320,14 +349,14 @@ void enqueue_csr(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts, u
     a.aux_bits = d_aux;
     mark_begin(c, d, st);
     if (c->exact) {
-        check(c, pcd::launch_exact_csr(a, n_points, st, &c->launches), "exact csr kernel");
+        check(c, pcd::launch_exact_csr(a, n_points, st, &d.launches), "exact csr kernel");
     } else {
         check(c, d.csr_meta.ensure(std::max<size_t>(pcd::csr_meta_bytes(n_polys), 16)), "alloc polygon metadata");
         a.meta = d.csr_meta.p;
-        check(c, pcd::launch_csr(a, st, d.dev, &c->launches), "csr kernel");
+        check(c, pcd::launch_csr(a, st, d.dev, &d.launches), "csr kernel");
     }
     mark_end(c, d, st);
-    check(c, pcd::launch_finalize(n_points, d_inside, d_aux, d_verdicts, mode, d_stats, st, d.dev, &c->launches),
+    check(c, pcd::launch_finalize(n_points, d_inside, d_aux, d_verdicts, mode, d_stats, st, d.dev, &d.launches),
           "finalize kernel");
 }
 
@@ -383,7 +412,7 @@ void cache_polygon(pc_ctx* c, DevState& d, const double* vx, const double* vy, c
     check(c, cudaMemcpyAsync(d.c_ro.p, d.cro.data(), (n_rings + 1) * 8ull, cudaMemcpyHostToDevice, st),
           "upload polygon");
     if (nv > 0) check(c, pcd::launch_outer_bbox(d.c_vx.as<double>(), d.c_vy.as<double>(), d.c_ro.as<uint64_t>(),
-                                                d.c_box.as<double>(), st, &c->launches), "bbox kernel");
+                                                d.c_box.as<double>(), st, &d.launches), "bbox kernel");
     check(c, cudaStreamSynchronize(st), "upload polygon"); // the host copies may change with the next call
     d.cvalid = true;
 }
@@ -420,7 +449,7 @@ void classify_small(pc_ctx* c, const double* pts_xy, uint64_t n, const double* v
     mark_begin(c, d, st);
     check(c, pcd::launch_small(d.small_pts.as<double>(), n, d.c_vx.as<double>(), d.c_vy.as<double>(),
                                d.c_ro.as<uint64_t>(), n_rings, prefilter ? d.c_box.as<double>() : nullptr, mode, tol,
-                               d.small_out.p, nullptr, nullptr, st, &c->launches),
+                               d.small_out.p, nullptr, nullptr, st, &d.launches),
           "small classify kernel");
     mark_end(c, d, st);
     check(c, cudaMemcpyAsync(h + ib, d.small_out.p, ob, cudaMemcpyDeviceToHost, st), "download results");
@@ -511,7 +540,12 @@ void pc_destroy(pc_ctx* c) {
 
 const char* pc_last_error(const pc_ctx* c) { return c ? c->err.c_str() : "null context"; }
 int pc_device_count(const pc_ctx* c) { return c ? (int)c->devs.size() : 0; }
-uint64_t pc_last_launch_count(const pc_ctx* c) { return c ? c->launches : 0; }
+uint64_t pc_last_launch_count(const pc_ctx* c) {
+    uint64_t n = 0;
+    if (c)
+        for (const auto& d : c->devs) n += d.launches;
+    return n;
+}
 
 int pc_set_option(pc_ctx* c, int option, int64_t value) {
     if (!c) return PC_EINVAL;
@@ -622,7 +656,8 @@ int pc_classify(pc_ctx* c, const double* pts_xy, uint64_t n, const double* vx, c
             const uint64_t lo = std::min(n, d * shard), hi = std::min(n, (d + 1) * shard);
             if (hi > lo) parts.push_back({lo, hi});
         }
-        for (size_t i = 0; i < parts.size(); ++i) {
+        // one host thread per device: upload, enqueue, download and wait for its shard
+        per_device(parts.size(), [&](size_t i) {
             DevState& d = c->devs[i];
             const uint64_t m = parts[i].hi - parts[i].lo, nwords = (m + 31) / 32;
             check(c, cudaSetDevice(d.dev), "cudaSetDevice");
@@ -671,13 +706,10 @@ int pc_classify(pc_ctx* c, const double* pts_xy, uint64_t n, const double* vx, c
                 check(c, cudaMemcpyAsync(verdicts + parts[i].lo, dv, m, cudaMemcpyDeviceToHost, st),
                       "download verdicts");
             check(c, cudaMemcpyAsync(d.h_stats, d.stats.p, 32, cudaMemcpyDeviceToHost, st), "download stats");
-        }
-        for (size_t i = 0; i < parts.size(); ++i) {
-            DevState& d = c->devs[i];
-            check(c, cudaSetDevice(d.dev), "cudaSetDevice");
-            check(c, cudaStreamSynchronize(d.stream), "classify");
-            for (int k = 0; k < 4; ++k) tot[k] += d.h_stats[k];
-        }
+            check(c, cudaStreamSynchronize(st), "classify");
+        });
+        for (size_t i = 0; i < parts.size(); ++i)
+            for (int k = 0; k < 4; ++k) tot[k] += c->devs[i].h_stats[k];
         if (stats) std::memcpy(stats, tot, sizeof(tot));
     });
 }
@@ -700,6 +732,7 @@ int pc_classify_csr(pc_ctx* c, const double* pts_xy, const uint64_t* pt_off, uin
                 invalid(c, "CSR offsets must be non-decreasing");
         const uint64_t P0 = pt_off[0];
         const uint64_t nwords_all = (n_points + 31) / 32;
+        std::mutex merge_mu;
         if (inside_bits) std::memset(inside_bits, 0, nwords_all * 4);
         if (aux_bits) std::memset(aux_bits, 0, nwords_all * 4);
         // shard polygons so each device gets ~n_points/ndev points
@@ -712,12 +745,14 @@ int pc_classify_csr(pc_ctx* c, const double* pts_xy, const uint64_t* pt_off, uin
             cut.push_back(std::min(p, n_polys));
         }
         cut.push_back(n_polys);
-        std::vector<std::vector<uint32_t>> tmp_in(ndev), tmp_aux(ndev);
-        for (uint64_t i = 0; i < ndev; ++i) {
+        // one host thread per device; its bit planes come back into pinned
+        // per-device buffers and are OR-ed into the caller's planes at the
+        // shard's bit offset (a shard starts at a polygon, not a word boundary)
+        per_device(ndev, [&](size_t i) {
             const uint64_t p0 = cut[i], p1 = cut[i + 1];
+            if (p1 == p0) return;
             DevState& d = c->devs[i];
             const uint64_t s = pt_off[p0], t = pt_off[p1], m = t - s, nwords = (m + 31) / 32;
-            if (p1 == p0) continue;
             check(c, cudaSetDevice(d.dev), "cudaSetDevice");
             cudaStream_t st = d.stream;
             const uint64_t r0 = poly_ring_off[p0], r1 = poly_ring_off[p1];
@@ -740,26 +775,24 @@ int pc_classify_csr(pc_ctx* c, const double* pts_xy, const uint64_t* pt_off, uin
             enqueue_csr(c, d, st, d.pts.as<double>(), m, d.pt_off.as<uint64_t>(), p1 - p0, d.vx.as<double>(),
                         d.vy.as<double>(), d.ring_off.as<uint64_t>(), d.poly_ring_off.as<uint64_t>(), s, r0, v0, mode,
                         tol, dv, din, daux, d.stats.as<unsigned long long>());
-            tmp_in[i].resize(nwords);
-            tmp_aux[i].resize(nwords);
-            if (inside_bits)
-                check(c, cudaMemcpyAsync(tmp_in[i].data(), din, nwords * 4, cudaMemcpyDeviceToHost, st), "download");
-            if (aux_bits)
-                check(c, cudaMemcpyAsync(tmp_aux[i].data(), daux, nwords * 4, cudaMemcpyDeviceToHost, st), "download");
+            uint32_t* hp = nullptr;
+            if (inside_bits || aux_bits) {
+                hp = reinterpret_cast<uint32_t*>(small_staging(c, d, 2 * nwords * 4));
+                check(c, cudaMemcpyAsync(hp, din, 2 * nwords * 4, cudaMemcpyDeviceToHost, st), "download planes");
+            }
             if (verdicts)
                 check(c, cudaMemcpyAsync(verdicts + (s - P0), dv, m, cudaMemcpyDeviceToHost, st), "download verdicts");
             check(c, cudaMemcpyAsync(d.h_stats, d.stats.p, 32, cudaMemcpyDeviceToHost, st), "download stats");
-        }
-        for (uint64_t i = 0; i < ndev; ++i) {
-            if (cut[i + 1] == cut[i]) continue;
-            DevState& d = c->devs[i];
-            check(c, cudaSetDevice(d.dev), "cudaSetDevice");
-            check(c, cudaStreamSynchronize(d.stream), "classify_csr");
-            for (int k = 0; k < 4; ++k) tot[k] += d.h_stats[k];
-            const uint64_t s = pt_off[cut[i]] - P0, m = pt_off[cut[i + 1]] - pt_off[cut[i]];
-            if (inside_bits) merge_bits(inside_bits, tmp_in[i].data(), s, m);
-            if (aux_bits) merge_bits(aux_bits, tmp_aux[i].data(), s, m);
-        }
+            check(c, cudaStreamSynchronize(st), "classify_csr");
+            if (hp) {
+                std::lock_guard<std::mutex> lk(merge_mu); // neighbouring shards share boundary words
+                if (inside_bits) merge_bits(inside_bits, hp, s - P0, m);
+                if (aux_bits) merge_bits(aux_bits, hp + nwords, s - P0, m);
+            }
+        });
+        for (uint64_t i = 0; i < ndev; ++i)
+            if (cut[i + 1] != cut[i])
+                for (int k = 0; k < 4; ++k) tot[k] += c->devs[i].h_stats[k];
         if (stats) std::memcpy(stats, tot, sizeof(tot));
     });
 }
@@ -785,7 +818,7 @@ int pc_count_crossings(pc_ctx* c, const double* pts_xy, uint64_t n, const double
             unsigned long long* dc = d.small_out.as<unsigned long long>();
             check(c, pcd::launch_small(d.small_pts.as<double>(), n, d.c_vx.as<double>(), d.c_vy.as<double>(),
                                        d.c_ro.as<uint64_t>(), 1, nullptr, mode, 0.0, nullptr, dc,
-                                       reinterpret_cast<uint8_t*>(dc + n), st, &c->launches),
+                                       reinterpret_cast<uint8_t*>(dc + n), st, &d.launches),
                   "count kernel");
             check(c, cudaMemcpyAsync(h + ib, d.small_out.p, cb + n, cudaMemcpyDeviceToHost, st), "download counts");
             check(c, cudaStreamSynchronize(st), "count_crossings");
@@ -799,7 +832,7 @@ int pc_count_crossings(pc_ctx* c, const double* pts_xy, uint64_t n, const double
         check(c, d.counts.ensure(n * 8), "alloc counts");
         check(c, d.degen.ensure(n), "alloc flags");
         check(c, pcd::launch_count(d.pts.as<double>(), n, d.vx.as<double>(), d.vy.as<double>(), nv, mode,
-                                   d.counts.as<unsigned long long>(), d.degen.as<uint8_t>(), st, &c->launches),
+                                   d.counts.as<unsigned long long>(), d.degen.as<uint8_t>(), st, &d.launches),
               "count kernel");
         check(c, cudaMemcpyAsync(counts, d.counts.p, n * 8, cudaMemcpyDeviceToHost, st), "download counts");
         check(c, cudaMemcpyAsync(degenerate, d.degen.p, n, cudaMemcpyDeviceToHost, st), "download flags");
@@ -820,7 +853,7 @@ unsigned long long* enqueue_prefilter(pc_ctx* c, DevState& d, cudaStream_t st, c
     const int nb = pcd::compact_blocks(n, d.dev);
     check(c, d.cmp_blk.ensure((size_t)(nb + 1) * 8), "alloc prefilter scratch");
     unsigned long long* blk = d.cmp_blk.as<unsigned long long>();
-    check(c, pcd::launch_prefilter(d_pts, n, box, nb, blk, d_out, d_idx, st, &c->launches), "prefilter kernels");
+    check(c, pcd::launch_prefilter(d_pts, n, box, nb, blk, d_out, d_idx, st, &d.launches), "prefilter kernels");
     return blk + nb;
 }
 
@@ -870,7 +903,7 @@ int pc_scatter_verdicts(pc_ctx* c, const uint64_t* idx, const uint8_t* inbox_ver
         unsigned* bad = reinterpret_cast<unsigned*>(o + off);
         check(c, cudaMemsetAsync(bad, 0, 4, st), "clear flag");
         check(c, pcd::launch_scatter_verdicts(d.cmp_idx.as<unsigned long long>(), d.cmp_v.as<uint8_t>(), n_inbox,
-                                              n_total, o, bad, st, d.dev, &c->launches),
+                                              n_total, o, bad, st, d.dev, &d.launches),
               "scatter kernel");
         unsigned b = 0;
         check(c, cudaMemcpyAsync(&b, bad, 4, cudaMemcpyDeviceToHost, st), "download flag");
@@ -912,7 +945,7 @@ int pc_scatter_verdicts_dev(pc_ctx* c, int dev_index, void* stream, const uint64
         check(c, cudaSetDevice(d.dev), "cudaSetDevice");
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d.stream;
         check(c, pcd::launch_scatter_verdicts(reinterpret_cast<const unsigned long long*>(d_idx), d_inbox_verdicts,
-                                              n_inbox, n_total, d_out, d_bad, st, d.dev, &c->launches),
+                                              n_inbox, n_total, d_out, d_bad, st, d.dev, &d.launches),
               "scatter kernel");
     });
 }
@@ -941,7 +974,7 @@ int pc_parse_points_csv(pc_ctx* c, const char* text, uint64_t len, uint64_t data
         mark_begin(c, d, st);
         check(c, pcd::launch_csv_points(d.csv_text.as<char>(), len, data_start, x_col, y_col, delim,
                                         d.csv_out.as<double>(), dev_cap, d.csv_state.p,
-                                        res, st, &c->launches),
+                                        res, st, &d.launches),
               "csv kernel");
         mark_end(c, d, st);
         check(c, cudaMemcpyAsync(d.h_stats, res, 32, cudaMemcpyDeviceToHost, st), "download counts");
@@ -975,7 +1008,7 @@ int pc_parse_points_csv_dev(pc_ctx* c, int dev_index, void* stream, const char* 
         mark_begin(c, d, st);
         check(c, pcd::launch_csv_points(d_text, len, data_start, x_col, y_col, delim, d_out_xy, cap_points,
                                         d.csv_state.p,
-                                        reinterpret_cast<unsigned long long*>(d_result), st, &c->launches),
+                                        reinterpret_cast<unsigned long long*>(d_result), st, &d.launches),
               "csv kernel");
         mark_end(c, d, st);
     });
@@ -998,7 +1031,7 @@ int pc_format_results_csv(pc_ctx* c, const pc_result_record* recs, uint64_t n, c
         unsigned long long* dl = d.csv_res.as<unsigned long long>();
         mark_begin(c, d, st);
         check(c, pcd::launch_emit_results(d.emit_recs.p, n, d.emit_out.as<char>(), dev_cap, d.emit_scratch.p, dl, st,
-                                          &c->launches),
+                                          &d.launches),
               "emit kernels");
         mark_end(c, d, st);
         check(c, cudaMemcpyAsync(d.h_stats, dl, 8, cudaMemcpyDeviceToHost, st), "download length");
@@ -1022,7 +1055,7 @@ int pc_format_results_csv_dev(pc_ctx* c, int dev_index, void* stream, const pc_r
         check(c, d.emit_scratch.ensure(pcd::emit_scratch_bytes(n)), "alloc emit scratch");
         mark_begin(c, d, st);
         check(c, pcd::launch_emit_results(d_recs, n, d_out, cap, d.emit_scratch.p,
-                                          reinterpret_cast<unsigned long long*>(d_len), st, &c->launches),
+                                          reinterpret_cast<unsigned long long*>(d_len), st, &d.launches),
               "emit kernels");
         mark_end(c, d, st);
     });

@@ -220,17 +220,23 @@ def test_many_holes_and_huge_ring(engine):
         check_single(xy, big, mode, engine.classify(xy, big, mode))
 
 
-def test_multi_shard_identical():
-    """Shard logic across 'GPUs' (here: 3 shards on one device) gives identical output."""
+@pytest.mark.parametrize("shards", [2, 3])
+def test_multi_shard_identical(shards):
+    """Shard logic across 'GPUs' (here: 2 or 3 logical devices on one GPU, each
+    enqueued from its own host thread) gives bit-identical output -- the
+    reference's determinism check at 1e6 points (acceptance.cpp:345-357,
+    batch_test.cpp:87-105): a star, 1e6 points of configs[3], a CSR set."""
     poly, xy = W.config2(1000, n_points=300_017)
+    p4, x4 = W.config4(n_points=1_000_000)
     s = W.degenerate(20_000, allow_dups=True, seed=3)
-    with Engine(devices=[0]) as one, Engine(devices=[0, 0, 0]) as three:
-        assert three.device_count == 3
+    with Engine(devices=[0]) as one, Engine(devices=[0] * shards) as many:
+        assert many.device_count == shards
         for mode in MODES:
-            a, b = one.classify_batch(xy, poly, mode), three.classify_batch(xy, poly, mode)
-            assert np.array_equal(a.verdicts, b.verdicts) and np.array_equal(a.inside_bits, b.inside_bits)
-            assert np.array_equal(a.aux_bits, b.aux_bits) and np.array_equal(a.stats, b.stats)
-            a, b = one.classify_csr(s, mode), three.classify_csr(s, mode)
+            for P, X in ((poly, xy), (p4, x4)):
+                a, b = one.classify_batch(X, P, mode), many.classify_batch(X, P, mode)
+                assert np.array_equal(a.verdicts, b.verdicts) and np.array_equal(a.inside_bits, b.inside_bits)
+                assert np.array_equal(a.aux_bits, b.aux_bits) and np.array_equal(a.stats, b.stats)
+            a, b = one.classify_csr(s, mode), many.classify_csr(s, mode)
             assert np.array_equal(a.verdicts, b.verdicts) and np.array_equal(a.inside_bits, b.inside_bits)
             assert np.array_equal(a.aux_bits, b.aux_bits) and np.array_equal(a.stats, b.stats)
 

@@ -80,3 +80,21 @@ def test_two_rank_gather_matches_single_process():
     v, _ = oracle.port_classify(xy, poly.vx, poly.vy, poly.ring_off, 0)
     assert np.array_equal(full, pack_bits(v == 0))
     assert units == n * poly.n_edges and pts == n and mx == 2.0
+
+
+def test_bench_torchrun_path_gloo():
+    """bench.py's own torchrun code path (two ranks, gloo, CPU): per-rank shard
+    generation, bit-plane all-gather, job totals and max over ranks."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    port = _free_port()
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(root, "bench.py"),
+                        "--gpus", "2", "--dist-check", "--dist-check-points", "300007"],
+                       capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["dist_check"] == "ok" and line["world"] == 2
