@@ -11,7 +11,10 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(_HERE, "lib")
-CUDA_LIB = os.path.join(LIB_DIR, "libpolycast_cuda.so")
+# POLYCAST_LIB_VARIANT=debug selects the checking build (lib/debug: device-side
+# bounds checks, `make -C paper_2306_04316_b200 debug`)
+CUDA_LIB = os.path.join(LIB_DIR, "debug" if os.environ.get("POLYCAST_LIB_VARIANT") == "debug" else "",
+                        "libpolycast_cuda.so")
 WORKLOADS_LIB = os.path.join(LIB_DIR, "libpolycast_workloads.so")
 
 PC_OK, PC_EINVAL, PC_ECUDA, PC_ENOMEM, PC_ENCCL = 0, 1, 2, 3, 4

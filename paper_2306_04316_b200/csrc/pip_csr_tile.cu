@@ -285,6 +285,7 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
                     if (m == 0) continue;
                     const uint32_t i = i0 + __ffs(m) - 1;
                     m &= m - 1;
+                    PC_DCHECK(i + 1 < e1 && i >= e0);
                     const double2 a = ws.vert[i], b = ws.vert[i + 1];
                     if (MODE == kRobust) { // robust_ray_crossings (geometry.hpp:242-270), literally
                         int c = 0;
@@ -410,10 +411,12 @@ __global__ void __launch_bounds__(kBThreads, 7) pip_csr_tile_kernel(
             for (int u = 0; u < kWV / 32; ++u) {
                 const uint32_t i = lane + 32 * u;
                 if (i < total) {
+                    PC_DCHECK(i < (uint32_t)kWV);
                     // owner: the last batch polygon whose first vertex is <= i
                     int o = __popc(ws.starts[u] & (0xffffffffu >> (31 - lane))) - 1;
 #pragma unroll
                     for (int w = 0; w < u; ++w) o += __popc(ws.starts[w]);
+                    PC_DCHECK(o >= 0 && o < nb);
                     ws.owner[i] = (unsigned char)o;
                     const unsigned long long v = ws.v0s[o] + (i - ws.off[o]);
                     ws.vert[i] = make_double2(vx[v], vy[v]);
@@ -497,6 +500,7 @@ __global__ void __launch_bounds__(kBThreads, 7) pip_csr_tile_kernel(
                                          : make_int4(kv, 0, 0, __float_as_int(1.f));
                 int2 gg = MODE == kRobust ? make_int2(0, __float_as_int(1.f)) : make_int2(kFastSentinelLo, 0);
                 if (!is_ring_end(ws, i)) {
+                    PC_DCHECK(i + 1 < total);
                     const double2 b = ws.vert[i + 1];
                     const int qb = __double2int_rz(__dmul_rn(__dmul_rn(__dsub_rn(b.y, by0), sy), 0x1p30));
                     double Nx, Ny;

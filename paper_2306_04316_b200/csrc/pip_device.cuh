@@ -8,6 +8,28 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
+
+// Device-side bounds / invariant checks, compiled in only for the checking
+// build (make -C paper_2306_04316_b200 debug -> lib/debug/, selected with
+// POLYCAST_LIB_VARIANT=debug): a failed check prints its location and traps,
+// so the call returns PC_ECUDA.  This pool has no compute-sanitizer; these
+// checks on every shared- and global-memory index the kernels compute are the
+// substitute (tools/gpu_devchecks.sh runs tools/sanitize_cases.py with them).
+#ifdef PC_DEVICE_CHECKS
+#define PC_DCHECK(cond)                                                                       \
+    do {                                                                                      \
+        if (!(cond)) {                                                                        \
+            printf("PC_DCHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                        \
+            __trap();                                                                         \
+        }                                                                                     \
+    } while (0)
+#else
+#define PC_DCHECK(cond) \
+    do {                \
+    } while (0)
+#endif
 
 namespace pcd {
 

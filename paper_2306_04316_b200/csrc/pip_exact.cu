@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(kXTPB) exact_csr_kernel(const double2* __restr
             if (pt_off[mid] <= g) lo = mid; else hi = mid;
         }
         const uint64_t p = lo;
+        PC_DCHECK(p < n_polys && pt_off[p] <= g && g < pt_off[p + 1]);
         const uint64_t r0 = poly_ring_off[p] - ring_base, r1 = poly_ring_off[p + 1] - ring_base;
         const double2 q = pts[i];
         if (r1 > r0) {

@@ -426,6 +426,7 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3)
         bool a = li < cta_n;
         double2 p = make_double2(0.0, 0.0);
         {
+            PC_DCHECK(!a || cta_base + li < n);
             if (a) p = load_pt(idx ? pts + idx[cta_base + li] : pts + cta_base + li);
             if ((k & 3) == 3) asm volatile("" ::: "memory"); // at most 4 point loads in flight (registers)
         }
@@ -541,7 +542,9 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3)
             { // gather: two threads per candidate (filter word + half of the record each)
                 const uint32_t i = (uint32_t)tid >> 1, h = (uint32_t)tid & 1u;
                 if (i < nb) {
+                    PC_DCHECK(b0 + i < (uint32_t)kListCap && i < (uint32_t)kBatch);
                     const uint32_t e = sh.list[b0 + i];
+                    PC_DCHECK(e >= e_begin && e < e_end);
                     const uint4* src = reinterpret_cast<const uint4*>(rec + e) + 2 * h;
                     uint4* dst = reinterpret_cast<uint4*>(&sh.brec[i]) + 2 * h;
                     const uint4 r0 = __ldg(src), r1 = __ldg(src + 1);
@@ -605,6 +608,7 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3)
         const int s = (int)(q & 1);
         const uint32_t t0 = t_begin + q * kQTile;
         mbar_wait(&sh.full[s], (q >> 1) & 1);
+        PC_DCHECK(t0 >= e_begin && t0 < e_end);
         const uint4 w0 = sh.qk[s][2 * tid], w1 = sh.qk[s][2 * tid + 1];
         uint32_t m = key_hit(w0.x, kc) | key_hit(w0.y, kc) << 1 | key_hit(w0.z, kc) << 2 | key_hit(w0.w, kc) << 3 |
                      key_hit(w1.x, kc) << 4 | key_hit(w1.y, kc) << 5 | key_hit(w1.z, kc) << 6 |
@@ -614,6 +618,7 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3)
             const uint32_t e0 = t0 + 8u * (uint32_t)tid;
             if (e0 + 8 > e_end) m &= e0 >= e_end ? 0u : (1u << (e_end - e0)) - 1u;
             uint32_t pos = atomicAdd(&sh.ncand, (uint32_t)__popc(m));
+            PC_DCHECK(pos + (uint32_t)__popc(m) <= (uint32_t)kListCap);
             while (m) {
                 sh.list[pos++] = e0 + (__ffs(m) - 1);
                 m &= m - 1;

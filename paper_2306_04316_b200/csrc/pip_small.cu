@@ -63,6 +63,7 @@ __global__ void __launch_bounds__(kSTPB) small_kernel(const double2* __restrict_
                 const uint32_t r = ring_of_small(ring_off, n_rings, v);
                 if (v + 1 >= ring_off[r + 1]) continue; // last vertex of its ring: no edge
             }
+            PC_DCHECK(v + 1 < nv);
             const double ax = vx[v], ay = vy[v], bx = vx[v + 1], by = vy[v + 1];
             double f_prev = __dsub_rn(ay, p.y); // geometry.hpp:185/:223 (carried as b.y - p.y of the previous edge)
             bool a = false;

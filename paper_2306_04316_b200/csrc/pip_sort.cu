@@ -249,6 +249,7 @@ __global__ void __launch_bounds__(kRkThreads, 2) rk_scatter_kernel(uint64_t n, c
         if (kr[j] == 0xffffffffu) continue;
         const uint32_t k = kr[j] >> 16, d = (k >> shift) & 0xffu;
         const uint32_t pos = boff[d] + wcnt[warp][d] + (kr[j] & 0xffffu);
+        PC_DCHECK(pos < tn);
         const uint32_t e = (uint32_t)warp * 32 * kRkItems + j * 32 + lane;
         skey[pos] = (uint16_t)k;
         spts[pos] = pts_in[t0 + e]; // coalesced read, staged in digit order
@@ -260,6 +261,7 @@ __global__ void __launch_bounds__(kRkThreads, 2) rk_scatter_kernel(uint64_t n, c
     for (uint32_t L = tid; L < tn; L += kRkThreads) {
         const uint32_t k = skey[L], d = (k >> shift) & 0xffu;
         const uint64_t g = (uint64_t)gbase[d] + (L - boff[d]);
+        PC_DCHECK(g < n && L >= boff[d]);
         if (PASS == 0) keys_out[g] = (uint16_t)k;
         pts_out[g] = spts[L];
         idx_out[g] = sidx[L];
@@ -280,6 +282,7 @@ __global__ void __launch_bounds__(256) unbucket_kernel(uint64_t n, const uint32_
         const uint32_t bit = 1u << (i & 31);
         if ((wi | wa) & bit) {
             const uint32_t o = sorted_idx[i];
+            PC_DCHECK(o < n);
             if (wi & bit) atomicOr(&inside_bits[o >> 5], 1u << (o & 31));
             if (wa & bit) atomicOr(&aux_bits[o >> 5], 1u << (o & 31));
         }
