@@ -223,11 +223,10 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
     pa.bbox_keys = d.bbox.as<unsigned long long>();
     pa.stats = d_stats;
     pa.tol = tol;
-    // inside and aux are zeroed separately (they need not be contiguous)
     pa.zero_words = d_inside;
+    pa.zero_words2 = d_aux;
     pa.n_zero_words = nwords;
     check(c, pcd::launch_prep(pa, st, d.dev, &d.launches), "prep kernel");
-    check(c, cudaMemsetAsync(d_aux, 0, nwords * 4, st), "clear aux plane");
     const bool tree = (mode == 0 || mode == 1) /* C1, C2 */ && c->tree_mode == 1 && pcd::tree_eligible(n_verts, n, true);
     const bool bucket = !tree && n < 0xffffffffull &&
                         (c->bucket_mode == 1 || (c->bucket_mode < 0 && n_edges >= 64 && n >= 4096));
@@ -246,7 +245,7 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
     sa.inside_bits = d_inside;
     sa.aux_bits = d_aux;
     sa.n_dev = nullptr;
-    sa.idx = nullptr;
+    sa.orig = nullptr;
     pcd::TreeArgs ta{};
     if (tree) { // segment-tree build (polygon only)
         ta.mode = mode;
@@ -279,20 +278,18 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
         sc.aux_bits = d_aux + lo / 32;
         if (bucket) {
             // y order by a radix sort of (key, point, index); the scan kernel reads
-            // the y-ordered points and writes bit planes in y order (unbucketed below)
-            check(c, d.bucket_scratch.ensure(pcd::bucket_scratch_bytes(m) + (2 * mw + 4) * 4), "alloc bucket scratch");
+            // the y-ordered points and sets the bits of their original positions
+            check(c, d.bucket_scratch.ensure(pcd::bucket_scratch_bytes(m) + 16), "alloc bucket scratch");
             check(c, d.sorted_idx.ensure(m * 4), "alloc bucket index");
             check(c, d.sorted_pts.ensure(m * 16), "alloc y-ordered points");
-            uint32_t* planes = reinterpret_cast<uint32_t*>(d.bucket_scratch.as<char>() + pcd::bucket_scratch_bytes(m));
-            check(c, cudaMemsetAsync(planes, 0, (2 * mw + 4) * 4, st), "clear bucket planes");
+            uint32_t* n_in = reinterpret_cast<uint32_t*>(d.bucket_scratch.as<char>() + pcd::bucket_scratch_bytes(m));
             pcd::BucketArgs ba{sc.pts, m, d.bbox.as<unsigned long long>(), prefilter, d.bucket_scratch.p,
-                               d.sorted_pts.as<double>(), d.sorted_idx.as<uint32_t>(), planes + 2 * mw};
+                               d.sorted_pts.as<double>(), d.sorted_idx.as<uint32_t>(), n_in};
             check(c, pcd::launch_bucket(ba, st, d.dev, &d.launches), "bucket kernels");
             sc.pts = d.sorted_pts.as<double>();
             sc.prefilter = 0; // rejected points sort last and are left out (n_dev)
-            sc.inside_bits = planes;
-            sc.aux_bits = planes + mw;
-            sc.n_dev = planes + 2 * mw;
+            sc.orig = d.sorted_idx.as<uint32_t>();
+            sc.n_dev = n_in;
         }
         if (tree) { // segment-tree counts; key-tie / off-map points through the scan kernel
             // (y-bucketed points: a warp's queries walk nearby leaves, sharing nodes)
@@ -313,10 +310,6 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
             check(c, pcd::launch_single(sc, st, d.dev, &d.launches), "classify kernel");
             mark_end(c, d, st);
         }
-        if (bucket)
-            check(c, pcd::launch_unbucket(m, sc.n_dev, d.sorted_idx.as<uint32_t>(), sc.inside_bits, sc.aux_bits,
-                                          d_inside + lo / 32, d_aux + lo / 32, st, d.dev, &d.launches),
-                  "unbucket kernel");
     }
     check(c, pcd::launch_finalize(n, d_inside, d_aux, d_verdicts, mode, d_stats, st, d.dev, &d.launches),
           "finalize kernel");

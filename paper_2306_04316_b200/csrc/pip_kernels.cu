@@ -41,11 +41,14 @@ __device__ __forceinline__ uint32_t ring_of(const uint64_t* ring_off, uint32_t n
 __global__ void __launch_bounds__(256) prep_bbox_kernel(const double* __restrict__ vx, const double* __restrict__ vy,
                                                         const uint64_t* __restrict__ ring_off,
                                                         unsigned long long* __restrict__ bbox_keys,
-                                                        uint32_t* __restrict__ zero_words, uint64_t n_zero_words,
-                                                        unsigned long long* __restrict__ stats) {
+                                                        uint32_t* __restrict__ zero_words, uint32_t* __restrict__ zero_words2,
+                                                        uint64_t n_zero_words, unsigned long long* __restrict__ stats) {
     const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t w = tid; w < n_zero_words; w += stride) zero_words[w] = 0u;
+    for (uint64_t w = tid; w < n_zero_words; w += stride) {
+        zero_words[w] = 0u;
+        zero_words2[w] = 0u;
+    }
     if (tid < 4) stats[tid] = 0ull;
     const uint64_t outer_end = ring_off[1];
     unsigned long long kminx = ~0ull, kminy = ~0ull, kmaxx = ~0ull, kmaxy = ~0ull;
@@ -80,12 +83,11 @@ __global__ void __launch_bounds__(256) prep_bbox_kernel(const double* __restrict
 //          ((q(yhi) - q(ylo)) << 1) + 2 in both halves} (15-bit keys)
 //   filter word Robust: {fkey(ylo), fkey(yhi)} (32-bit keys)
 template <int MODE>
-__global__ void __launch_bounds__(256) prep_edges_kernel(
+__device__ __forceinline__ void prep_edges_body(
     const double* __restrict__ vx, const double* __restrict__ vy, const uint64_t* __restrict__ ring_off,
     uint32_t n_rings, uint64_t n_verts, uint2* __restrict__ filt, uint32_t* __restrict__ qk, uint64_t n_qk,
-    EdgeRec* __restrict__ rec, unsigned long long* __restrict__ bbox_keys, double tol) {
-    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    EdgeRec* __restrict__ rec, unsigned long long* __restrict__ bbox_keys, double tol, uint64_t tid,
+    uint64_t stride) {
     const QMap qm = qmap_from_bbox(bbox_keys);
     const LocalMap lm = local_map_from_bbox(bbox_keys);
     if (tid == 0) { // published for the classify kernels (bbox_keys[4..7])
@@ -154,6 +156,60 @@ __global__ void __launch_bounds__(256) prep_edges_kernel(
         qk[e] = (0x7fffu - qkey15(ylo, qm)) | (qkey15(yhi, qm) << 16);
         rec[e] = er;
     }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) prep_edges_kernel(
+    const double* __restrict__ vx, const double* __restrict__ vy, const uint64_t* __restrict__ ring_off,
+    uint32_t n_rings, uint64_t n_verts, uint2* __restrict__ filt, uint32_t* __restrict__ qk, uint64_t n_qk,
+    EdgeRec* __restrict__ rec, unsigned long long* __restrict__ bbox_keys, double tol) {
+    prep_edges_body<MODE>(vx, vy, ring_off, n_rings, n_verts, filt, qk, n_qk, rec, bbox_keys, tol,
+                          blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, (uint64_t)gridDim.x * blockDim.x);
+}
+
+// Polygons of up to kPrepSmall vertices: the whole prep in one CTA -- plane and
+// stats zeroing, the outer-ring bbox (a block reduction instead of atomics, so
+// no pre-set), then the edge records -- one launch instead of a memset and two.
+constexpr int kPrepThreads = 1024;
+constexpr uint64_t kPrepSmall = 16384;
+template <int MODE>
+__global__ void __launch_bounds__(kPrepThreads) prep_small_kernel(
+    const double* __restrict__ vx, const double* __restrict__ vy, const uint64_t* __restrict__ ring_off,
+    uint32_t n_rings, uint64_t n_verts, uint2* __restrict__ filt, uint32_t* __restrict__ qk, uint64_t n_qk,
+    EdgeRec* __restrict__ rec, unsigned long long* __restrict__ bbox_keys, double tol,
+    uint32_t* __restrict__ zero_words, uint32_t* __restrict__ zero_words2, uint64_t n_zero_words,
+    unsigned long long* __restrict__ stats) {
+    __shared__ unsigned long long red[kPrepThreads / 32][4];
+    const uint32_t tid = threadIdx.x;
+    for (uint64_t w = tid; w < n_zero_words; w += kPrepThreads) {
+        zero_words[w] = 0u;
+        zero_words2[w] = 0u;
+    }
+    if (tid < 4) stats[tid] = 0ull;
+    unsigned long long k[4] = {~0ull, ~0ull, ~0ull, ~0ull};
+    for (uint64_t v = tid; v < ring_off[1]; v += kPrepThreads) {
+        const unsigned long long kx = dkey(vx[v]), ky = dkey(vy[v]);
+        k[0] = min(k[0], kx);
+        k[1] = min(k[1], ky);
+        k[2] = min(k[2], ~kx);
+        k[3] = min(k[3], ~ky);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) k[j] = min(k[j], __shfl_xor_sync(0xffffffffu, k[j], o));
+    if ((tid & 31) == 0)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) red[tid >> 5][j] = k[j];
+    __syncthreads();
+    if (tid < 4) {
+        unsigned long long m = ~0ull;
+        for (int w = 0; w < kPrepThreads / 32; ++w) m = min(m, red[w][tid]);
+        bbox_keys[tid] = m;
+    }
+    __syncthreads(); // the bbox keys are visible to the whole CTA
+    prep_edges_body<MODE>(vx, vy, ring_off, n_rings, n_verts, filt, qk, n_qk, rec, bbox_keys, tol, tid,
+                          kPrepThreads);
 }
 
 // Bit planes -> verdict bytes + stats.  One thread per 32-point word.
@@ -277,24 +333,41 @@ cudaError_t launch_fp64_probe(double* out, int iters, int dev, cudaStream_t st, 
 }
 
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st, int dev, uint64_t* launches) {
+    const uint64_t nqk = qk_words(a.n_verts - a.n_rings);
+    EdgeRec* rec = reinterpret_cast<EdgeRec*>(a.rec);
+    if (a.n_verts <= kPrepSmall) {
+#define PC_PREP_SMALL(M)                                                                                        \
+    prep_small_kernel<M><<<1, kPrepThreads, 0, st>>>(a.vx, a.vy, a.ring_off, a.n_rings, a.n_verts, a.filt, a.qk, \
+                                                     nqk, rec, a.bbox_keys, a.tol, a.zero_words, a.zero_words2,  \
+                                                     a.n_zero_words, a.stats)
+        switch (a.mode) {
+        case kC1: PC_PREP_SMALL(kC1); break;
+        case kC2: PC_PREP_SMALL(kC2); break;
+        default: PC_PREP_SMALL(kRobust);
+        }
+#undef PC_PREP_SMALL
+        *launches += 1;
+        return cudaGetLastError();
+    }
     cudaError_t e = cudaMemsetAsync(a.bbox_keys, 0xff, 4 * sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
     const unsigned bb = (unsigned)std::min<uint64_t>(std::max<uint64_t>(a.n_verts, a.n_zero_words) / 256 + 1,
                                                      (uint64_t)sm_count(dev) * 8);
-    prep_bbox_kernel<<<bb, 256, 0, st>>>(a.vx, a.vy, a.ring_off, a.bbox_keys, a.zero_words, a.n_zero_words, a.stats);
+    prep_bbox_kernel<<<bb, 256, 0, st>>>(a.vx, a.vy, a.ring_off, a.bbox_keys, a.zero_words, a.zero_words2,
+                                         a.n_zero_words, a.stats);
     const unsigned blocks = (unsigned)std::min<uint64_t>(a.n_verts / 256 + 1, (uint64_t)sm_count(dev) * 16);
     switch (a.mode) {
     case kC1:
         prep_edges_kernel<kC1><<<blocks, 256, 0, st>>>(a.vx, a.vy, a.ring_off, a.n_rings, a.n_verts, a.filt, a.qk,
-                                                       qk_words(a.n_verts - a.n_rings), reinterpret_cast<EdgeRec*>(a.rec), a.bbox_keys, a.tol);
+                                                       nqk, rec, a.bbox_keys, a.tol);
         break;
     case kC2:
         prep_edges_kernel<kC2><<<blocks, 256, 0, st>>>(a.vx, a.vy, a.ring_off, a.n_rings, a.n_verts, a.filt, a.qk,
-                                                       qk_words(a.n_verts - a.n_rings), reinterpret_cast<EdgeRec*>(a.rec), a.bbox_keys, a.tol);
+                                                       nqk, rec, a.bbox_keys, a.tol);
         break;
     default:
-        prep_edges_kernel<kRobust><<<blocks, 256, 0, st>>>(a.vx, a.vy, a.ring_off, a.n_rings, a.n_verts, a.filt, a.qk,
-                                                           qk_words(a.n_verts - a.n_rings), reinterpret_cast<EdgeRec*>(a.rec), a.bbox_keys, a.tol);
+        prep_edges_kernel<kRobust><<<blocks, 256, 0, st>>>(a.vx, a.vy, a.ring_off, a.n_rings, a.n_verts, a.filt,
+                                                           a.qk, nqk, rec, a.bbox_keys, a.tol);
         break;
     }
     *launches += 2;

@@ -19,7 +19,8 @@ struct PrepArgs {
     uint32_t* qk;                 // per-edge key words of the phase-1 key scan, padded to qk_words()
     void* rec;                    // n_edges EdgeRec (edge_rec_bytes() each)
     unsigned long long* bbox_keys; // 4 monotone keys: min x, min y, ~max x, ~max y; [4..5] 16-bit key map
-    uint32_t* zero_words;          // output bit planes to clear (inside ++ aux, contiguous)
+    uint32_t* zero_words;          // output bit planes to clear: inside ...
+    uint32_t* zero_words2;         // ... and aux (n_zero_words each)
     uint64_t n_zero_words;
     unsigned long long* stats;     // 4 counters to clear
     double tol;                    // Robust boundary tolerance (gates its fp32 side records)
@@ -39,7 +40,7 @@ struct SingleArgs {
     uint32_t* inside_bits;
     uint32_t* aux_bits;
     const uint32_t* n_dev; // optional device-side point count (bucketed input)
-    const uint32_t* idx;   // optional: point i of the call is pts[idx[i]] (y-ordered gather)
+    const uint32_t* orig;  // optional (y-ordered input): results of point i go to bit orig[i] of the planes
 };
 
 struct CsrArgs {

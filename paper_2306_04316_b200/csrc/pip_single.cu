@@ -83,12 +83,13 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
     }
 }
 
-// One elected thread: load key tile [t0, t0 + kQTile) into stage s (the key
-// array is padded to whole tiles with never-candidate words).
+// One elected thread: load key words [t0, t0 + nw) into stage s (nw <= kQTile,
+// a multiple of 4: 16-byte bulk copies; the key array is padded with
+// never-candidate words to whole tiles, so nw may run past the chunk's end).
 // The key array is re-read by every CTA: keep it in L2 (evict_last), while the
-// point gathers stream past it (evict_first, see load_pt).
-__device__ __forceinline__ void issue_tile(SingleShared& sh, int s, const uint32_t* qk, uint32_t t0) {
-    const unsigned bytes = kQTile * 4u;
+// point loads stream past it (evict_first, see load_pt).
+__device__ __forceinline__ void issue_tile(SingleShared& sh, int s, const uint32_t* qk, uint32_t t0, uint32_t nw) {
+    const unsigned bytes = nw * 4u;
     const unsigned bar = smem_u32(&sh.full[s]);
     unsigned long long pol;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
@@ -117,12 +118,10 @@ __device__ __forceinline__ uint32_t key_hit(uint32_t w, uint32_t kc) {
     return (d & (d << 16)) >> 31;
 }
 
-// A lane's binary64 points for the exact fallbacks: point k of the lane is
-// g[k * 32], or g[ix[k * 32]] when the call gathers y-ordered points by index.
+// A lane's binary64 points for the exact fallbacks: point k of the lane is g[k * 32].
 struct PtRef {
     const double2* __restrict__ g;
-    const uint32_t* __restrict__ ix;
-    __device__ __forceinline__ double2 operator[](int j) const { return ix ? g[ix[j]] : g[j]; }
+    __device__ __forceinline__ double2 operator[](int j) const { return g[j]; }
 };
 
 // Per-thread point keys.  C1/C2: 15-bit keys (qkey15), two points per
@@ -373,7 +372,7 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3)
                     const uint2* __restrict__ filt, const EdgeRec* __restrict__ rec, uint32_t n_edges,
                     uint32_t edges_per_chunk, const unsigned long long* __restrict__ bbox_keys, int prefilter,
                     double tol, double tol2, uint32_t* __restrict__ inside_bits, uint32_t* __restrict__ aux_bits,
-                    const uint32_t* __restrict__ n_dev, const uint32_t* __restrict__ idx) {
+                    const uint32_t* __restrict__ n_dev, const uint32_t* __restrict__ orig) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     SingleShared& sh = *reinterpret_cast<SingleShared*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -427,7 +426,7 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3)
         double2 p = make_double2(0.0, 0.0);
         {
             PC_DCHECK(!a || cta_base + li < n);
-            if (a) p = load_pt(idx ? pts + idx[cta_base + li] : pts + cta_base + li);
+            if (a) p = load_pt(pts + cta_base + li);
             if ((k & 3) == 3) asm volatile("" ::: "memory"); // at most 4 point loads in flight (registers)
         }
         if (a && prefilter) a = p.x >= minx && p.x <= maxx && p.y >= miny && p.y <= maxy; // batch.hpp:39-41
@@ -502,8 +501,7 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3)
         for (int k = 0; k < kK; ++k) {
             const uint32_t li = wloc + k * 32 + lane;
             const bool a = act >> k & 1u;
-            const uint32_t q = a ? qkey_cta((idx ? pts[idx[cta_base + li]] : pts[cta_base + li]).y, cm)
-                                 : 0x7fffu; // inactive: masked by `act`
+            const uint32_t q = a ? qkey_cta(pts[cta_base + li].y, cm) : 0x7fffu; // inactive: masked by `act`
             if (k & 1) K.k2[k >> 1] |= (q << 1) << 16;
             else K.k2[k >> 1] = q << 1;
             if (a) {
@@ -517,8 +515,10 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3)
     const uint32_t kc = (sh.cta_hi + 1u) | ((0x8000u - sh.cta_lo) << 16);
 
     const uint32_t t_begin = e_begin, n_tiles = (e_end - e_begin + kQTile - 1) / kQTile;
+    // words of tile q: whole tiles, the chunk's last one rounded up to 4 words
+    auto tile_words = [&](uint32_t q) { return min((uint32_t)kQTile, (e_end - (t_begin + q * kQTile) + 3u) & ~3u); };
     if (tid == 0) {
-        for (uint32_t q = 0; q < 2 && q < n_tiles; ++q) issue_tile(sh, (int)q, qk, t_begin + q * kQTile);
+        for (uint32_t q = 0; q < 2 && q < n_tiles; ++q) issue_tile(sh, (int)q, qk, t_begin + q * kQTile, tile_words(q));
     }
 
     // may any active point of the warp straddle the edge with filter word f?
@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3)
         }
     };
 
-    const PtRef my_g = idx ? PtRef{pts, idx + cta_base + wloc + lane} : PtRef{pts + cta_base + wloc + lane, nullptr};
+    const PtRef my_g{pts + cta_base + wloc + lane};
     uint32_t par = 0, auxm = 0;
     // ---- phase 2: classify against the listed candidate edges ----
     auto flush = [&](uint32_t nc) { // nc = sh.ncand, read by every thread before any could append again
@@ -627,7 +627,7 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3)
         // stage s consumed and this tile's candidates listed; the count of
         // appending threads is uniform, so is the decision to read the list size
         const int appended = __syncthreads_count(mine);
-        if (tid == 0 && q + 2 < n_tiles) issue_tile(sh, s, qk, t0 + 2 * kQTile);
+        if (tid == 0 && q + 2 < n_tiles) issue_tile(sh, s, qk, t0 + 2 * kQTile, tile_words(q + 2));
         if (appended) {
             pending = sh.ncand;
             __syncthreads(); // everyone has read it before anyone appends again
@@ -638,15 +638,30 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3)
         }
     }
 
-    // ---- flags: one ballot word per k-slice ----
+    // ---- flags ----
+    if (orig) {
+        // y-ordered input: each set bit goes to its point's original position
+        // (XOR: partial parities of the edge chunks combine; OR: aux)
 #pragma unroll
-    for (int k = 0; k < kK; ++k) {
-        const uint32_t b = __ballot_sync(0xffffffffu, (par & act) >> k & 1u);
-        const uint32_t a = __ballot_sync(0xffffffffu, (auxm & act) >> k & 1u);
-        const uint64_t i0 = wbase + k * 32;
-        if (lane == 0 && i0 < n) {
-            if (b) atomicXor(&inside_bits[i0 >> 5], b);
-            if (a) atomicOr(&aux_bits[i0 >> 5], a);
+        for (int k = 0; k < kK; ++k) {
+            const uint32_t pb = (par & act) >> k & 1u, ab = (auxm & act) >> k & 1u;
+            if (pb | ab) {
+                const uint32_t o = orig[cta_base + wloc + k * 32 + lane];
+                if (pb) atomicXor(&inside_bits[o >> 5], 1u << (o & 31));
+                if (ab) atomicOr(&aux_bits[o >> 5], 1u << (o & 31));
+            }
+        }
+    } else {
+        // one ballot word per k-slice
+#pragma unroll
+        for (int k = 0; k < kK; ++k) {
+            const uint32_t b = __ballot_sync(0xffffffffu, (par & act) >> k & 1u);
+            const uint32_t a = __ballot_sync(0xffffffffu, (auxm & act) >> k & 1u);
+            const uint64_t i0 = wbase + k * 32;
+            if (lane == 0 && i0 < n) {
+                if (b) atomicXor(&inside_bits[i0 >> 5], b);
+                if (a) atomicOr(&aux_bits[i0 >> 5], a);
+            }
         }
     }
 }
@@ -671,18 +686,20 @@ cudaError_t launch_t(const SingleArgs& a, cudaStream_t st, int dev, uint64_t* la
     const uint64_t pts_per_cta = (uint64_t)kTPB * kK;
     const uint64_t n_ptiles = (a.n + pts_per_cta - 1) / pts_per_cta;
     const uint64_t slots = (uint64_t)sms(dev) * per_sm;
-    // Split the edges so the grid covers >= ~4 waves; chunks are whole key tiles.
-    const uint64_t tiles = std::max<uint64_t>(1, (a.n_edges + kQTile - 1) / kQTile);
-    uint64_t chunks = std::max<uint64_t>(1, (4 * slots + n_ptiles - 1) / std::max<uint64_t>(n_ptiles, 1));
-    chunks = std::min<uint64_t>(std::min<uint64_t>(chunks, tiles), 65535);
-    const uint64_t tiles_per_chunk = (tiles + chunks - 1) / chunks;
-    const uint32_t per_chunk = (uint32_t)(tiles_per_chunk * kQTile);
-    chunks = (tiles + tiles_per_chunk - 1) / tiles_per_chunk;
+    // Split the edges so the grid covers several waves: long CTAs (many edges)
+    // ~8 waves, so the last one is short; few edges ~2 (a chunk re-stages its
+    // CTA's points, which then dominates).  Chunks are multiples of 64 edges.
+    const uint64_t ne = std::max<uint64_t>(1, a.n_edges);
+    const uint64_t waves = ne >= 32768 ? 8 : 2;
+    uint64_t chunks = std::max<uint64_t>(1, (waves * slots + n_ptiles - 1) / std::max<uint64_t>(n_ptiles, 1));
+    chunks = std::min<uint64_t>(std::min<uint64_t>(chunks, (ne + 63) / 64), 65535);
+    const uint32_t per_chunk = (uint32_t)(((ne + chunks - 1) / chunks + 63) / 64 * 64);
+    chunks = (ne + per_chunk - 1) / per_chunk;
     dim3 grid((unsigned)n_ptiles, (unsigned)chunks);
     pip_tile_kernel<MODE><<<grid, kTPB, smem, st>>>(reinterpret_cast<const double2*>(a.pts), a.n, a.qk, a.filt,
                                                    reinterpret_cast<const EdgeRec*>(a.rec), a.n_edges, per_chunk,
                                                    a.bbox_keys, a.prefilter, a.tol, a.tol2, a.inside_bits,
-                                                   a.aux_bits, a.n_dev, a.idx);
+                                                   a.aux_bits, a.n_dev, a.orig);
     ++*launches;
     return cudaGetLastError();
 }

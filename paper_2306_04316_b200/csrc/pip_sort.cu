@@ -41,6 +41,7 @@ constexpr int kRkTile = kRkThreads * kRkItems;     // 4096 elements per tile
 constexpr int kRkWarps = kRkThreads / 32;
 constexpr uint32_t kRkLevels = 65280;              // in-box keys 0 .. 65279 (high byte < 0xff)
 constexpr uint16_t kRkReject = 0xffff;
+constexpr uint64_t kRkOnePassMax = 1ull << 22; // up to this many points: one pass on the high byte
 
 struct KeyMap {
     double minx, miny, maxx, maxy, scale;
@@ -71,7 +72,9 @@ __device__ __forceinline__ KeyMap make_keymap(const unsigned long long* bbox_key
 __global__ void __launch_bounds__(kRkThreads) rk_key_kernel(const double2* __restrict__ pts, uint64_t n,
                                                             const unsigned long long* __restrict__ bbox_keys,
                                                             int prefilter, uint16_t* __restrict__ keys,
-                                                            uint32_t* __restrict__ cnt, uint32_t n_tiles) {
+                                                            uint32_t* __restrict__ cnt, uint32_t n_tiles,
+                                                            unsigned int* __restrict__ ticket) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *ticket = 0u; // the colscan's completion counter
     __shared__ uint32_t h[2][256];
     for (int j = threadIdx.x; j < 512; j += blockDim.x) (&h[0][0])[j] = 0;
     __syncthreads();
@@ -107,47 +110,62 @@ __global__ void __launch_bounds__(kRkThreads) rk_count_hi_kernel(const uint16_t*
 // One warp per (pass, digit): exclusive prefix over the tiles (in place) and
 // the digit total; then (last CTA, one warp per pass) the exclusive scan of the
 // 256 totals is added to every entry by the scatter kernel via base[pass][digit].
-__global__ void __launch_bounds__(256) rk_colscan_kernel(uint32_t* __restrict__ cnt, uint32_t n_tiles,
-                                                         uint32_t* __restrict__ tot, uint32_t first) {
-    const uint32_t wid = first + (uint32_t)((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5); // pass * 256 + digit
-    const int lane = threadIdx.x & 31;
-    if (wid >= 512) return;
-    uint32_t* col = cnt + (uint64_t)wid * n_tiles;
-    uint32_t run = 0;
-    for (uint32_t b0 = 0; b0 < n_tiles; b0 += 32) {
-        const uint32_t b = b0 + lane;
-        const uint32_t v = b < n_tiles ? col[b] : 0u;
-        uint32_t incl = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        if (b < n_tiles) col[b] = run + incl - v;
-        run += __shfl_sync(0xffffffffu, incl, 31);
-    }
-    if (lane == 0) tot[wid] = run;
-}
-
-// Exclusive scan of the 256 digit totals of each pass (two warps, one per
-// pass): base[pass][digit]; base[2] word 0 = in-box count (the keys below the
-// reject key: everything before high digit 0xff).
-__global__ void __launch_bounds__(64) rk_base_kernel(const uint32_t* __restrict__ tot, uint32_t* __restrict__ base,
-                                                     uint32_t* __restrict__ n_in) {
-    const int pass = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// Exclusive scan of 256 digit totals (one warp): base[digit]; the in-box
+// count (keys below the reject key, i.e. everything before high digit 0xff)
+// is the last pass's base[255].
+__device__ __forceinline__ void rk_digit_bases(const uint32_t* tot, uint32_t* base, uint32_t* n_in, int lane) {
     uint32_t run = 0;
     for (int d0 = 0; d0 < 256; d0 += 32) {
-        const uint32_t v = tot[pass * 256 + d0 + lane];
+        const uint32_t v = tot[d0 + lane];
         uint32_t incl = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += y;
         }
-        base[pass * 256 + d0 + lane] = run + incl - v;
-        if (pass == 1 && d0 + lane == 255) *n_in = run + incl - v;
+        base[d0 + lane] = run + incl - v;
+        if (n_in && d0 + lane == 255) *n_in = run + incl - v;
         run += __shfl_sync(0xffffffffu, incl, 31);
     }
+}
+
+// One warp per (pass, digit) in [first, last): exclusive prefix over the tiles
+// (in place) and the digit total; the last CTA to finish (ticket) then forms
+// the digit bases of the passes it covered and resets the ticket.
+__global__ void __launch_bounds__(256) rk_colscan_kernel(uint32_t* __restrict__ cnt, uint32_t n_tiles,
+                                                         uint32_t* __restrict__ tot, uint32_t first, uint32_t last,
+                                                         uint32_t* __restrict__ base, uint32_t* __restrict__ n_in,
+                                                         unsigned int* __restrict__ ticket) {
+    const uint32_t wid = first + (uint32_t)((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5); // pass * 256 + digit
+    const int lane = threadIdx.x & 31;
+    if (wid < last) {
+        uint32_t* col = cnt + (uint64_t)wid * n_tiles;
+        uint32_t run = 0;
+        for (uint32_t b0 = 0; b0 < n_tiles; b0 += 32) {
+            const uint32_t b = b0 + lane;
+            const uint32_t v = b < n_tiles ? col[b] : 0u;
+            uint32_t incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (b < n_tiles) col[b] = run + incl - v;
+            run += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0) tot[wid] = run;
+    }
+    __shared__ bool is_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    const int w = threadIdx.x >> 5;
+    for (uint32_t pass = first / 256; pass < last / 256; ++pass)
+        if (w == (int)(pass - first / 256)) rk_digit_bases(tot + pass * 256, base + pass * 256, pass == 1 ? n_in : nullptr, lane);
+    if (threadIdx.x == 0) *ticket = 0u;
 }
 
 struct RkShared {
@@ -163,7 +181,7 @@ struct RkShared {
 // base[digit] + cnt[digit][tile] + (rank of the element among the tile's
 // elements with that digit, in element order).  PASS 0: idx = element position
 // (implicit), writes keys_out and idx_out; PASS 1: writes idx_out only.
-template <int PASS>
+template <int PASS, bool IMPLICIT = PASS == 0>
 __global__ void __launch_bounds__(kRkThreads, 2) rk_scatter_kernel(uint64_t n, const uint16_t* __restrict__ keys_in,
                                                                 const double2* __restrict__ pts_in,
                                                                 double2* __restrict__ pts_out,
@@ -190,14 +208,14 @@ __global__ void __launch_bounds__(kRkThreads, 2) rk_scatter_kernel(uint64_t n, c
     const uint32_t tn = (uint32_t)min((uint64_t)kRkTile, n - t0);
     // warp w ranks elements [w * 512, (w + 1) * 512) of the tile in 16 rounds of
     // 32; kr[j] = key << 16 | rank among the warp's earlier elements of its digit
-    uint32_t kr[kRkItems], idx[PASS == 0 ? 1 : kRkItems];
+    uint32_t kr[kRkItems], idx[IMPLICIT ? 1 : kRkItems];
     const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
     for (int j = 0; j < kRkItems; ++j) {
         const uint32_t e = (uint32_t)warp * 32 * kRkItems + j * 32 + lane;
         const bool live = e < tn;
         kr[j] = live ? (uint32_t)keys_in[t0 + e] << 16 : 0xffffffffu;
-        if constexpr (PASS == 1) idx[j] = live ? idx_in[t0 + e] : 0u;
+        if constexpr (!IMPLICIT) idx[j] = live ? idx_in[t0 + e] : 0u;
     }
 #pragma unroll
     for (int j = 0; j < kRkItems; ++j) {
@@ -253,7 +271,7 @@ __global__ void __launch_bounds__(kRkThreads, 2) rk_scatter_kernel(uint64_t n, c
         const uint32_t e = (uint32_t)warp * 32 * kRkItems + j * 32 + lane;
         skey[pos] = (uint16_t)k;
         spts[pos] = pts_in[t0 + e]; // coalesced read, staged in digit order
-        if constexpr (PASS == 0) sidx[pos] = (uint32_t)(t0 + e);
+        if constexpr (IMPLICIT) sidx[pos] = (uint32_t)(t0 + e);
         else sidx[pos] = idx[j];
     }
     __syncthreads();
@@ -303,7 +321,7 @@ uint64_t bucket_tiles(uint64_t n) { return std::max<uint64_t>(1, (n + kRkTile - 
 size_t bucket_scratch_bytes(uint64_t n) {
     const uint64_t nt = bucket_tiles(n);
     // keys, keys1 (u16), idx1 (u32), pts1 (2 x f64), counts (2 x 256 x tiles), totals + bases (2 x 512)
-    return 2 * ((n * 2 + 15) / 16 * 16) + (n * 4 + 15) / 16 * 16 + n * 16 + 2 * 256 * nt * 4 + 4 * 512 * 4 + 64;
+    return 2 * ((n * 2 + 15) / 16 * 16) + (n * 4 + 15) / 16 * 16 + n * 16 + 2 * 256 * nt * 4 + 4 * 512 * 4 + 80;
 }
 
 cudaError_t launch_bucket(const BucketArgs& a, cudaStream_t st, int dev, uint64_t* launches) {
@@ -322,25 +340,38 @@ cudaError_t launch_bucket(const BucketArgs& a, cudaStream_t st, int dev, uint64_
     uint32_t* cnt = reinterpret_cast<uint32_t*>(take(2 * 256 * nt * 4));
     uint32_t* tot = reinterpret_cast<uint32_t*>(take(512 * 4));
     uint32_t* base = reinterpret_cast<uint32_t*>(take(512 * 4));
-    rk_key_kernel<<<(unsigned)nt, kRkThreads, 0, st>>>(p, n, a.bbox_keys, a.prefilter, keys, cnt, (uint32_t)nt);
-    // pass-0 offsets; both passes' digit totals (order-independent) for the bases
-    rk_colscan_kernel<<<512 / 8, 256, 0, st>>>(cnt, (uint32_t)nt, tot, 0u);
-    rk_base_kernel<<<1, 64, 0, st>>>(tot, base, a.n_in);
+    unsigned int* ticket = reinterpret_cast<unsigned int*>(take(16));
+    rk_key_kernel<<<(unsigned)nt, kRkThreads, 0, st>>>(p, n, a.bbox_keys, a.prefilter, keys, cnt, (uint32_t)nt,
+                                                       ticket);
     static bool attr[64] = {};
     if (dev >= 0 && dev < 64 && !attr[dev]) {
         cudaFuncSetAttribute(rk_scatter_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RkShared));
         cudaFuncSetAttribute(rk_scatter_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RkShared));
+        cudaFuncSetAttribute(rk_scatter_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(RkShared));
         attr[dev] = true;
     }
     const size_t sm = sizeof(RkShared);
+    if (n <= kRkOnePassMax) {
+        // one pass on the high byte (255 y levels): for up to ~4M points a CTA's
+        // 4096 points span a slab this thin anyway; 3 launches instead of 6
+        rk_colscan_kernel<<<256 / 8, 256, 0, st>>>(cnt, (uint32_t)nt, tot, 256u, 512u, base, a.n_in, ticket);
+        rk_scatter_kernel<1, true><<<(unsigned)nt, kRkThreads, sm, st>>>(
+            n, keys, p, reinterpret_cast<double2*>(a.sorted_pts), nullptr, cnt, base, (uint32_t)nt, nullptr,
+            a.sorted_idx);
+        *launches += 3;
+        return cudaGetLastError();
+    }
+    // pass-0 offsets; both passes' digit totals (order-independent) and bases
+    rk_colscan_kernel<<<512 / 8, 256, 0, st>>>(cnt, (uint32_t)nt, tot, 0u, 512u, base, a.n_in, ticket);
     rk_scatter_kernel<0><<<(unsigned)nt, kRkThreads, sm, st>>>(n, keys, p, pts1, nullptr, cnt, base, (uint32_t)nt,
                                                               keys1, idx1);
     rk_count_hi_kernel<<<(unsigned)nt, kRkThreads, 0, st>>>(keys1, n, cnt, (uint32_t)nt);
-    rk_colscan_kernel<<<256 / 8, 256, 0, st>>>(cnt, (uint32_t)nt, tot, 256u);
+    rk_colscan_kernel<<<256 / 8, 256, 0, st>>>(cnt, (uint32_t)nt, tot, 256u, 512u, base, a.n_in, ticket);
     rk_scatter_kernel<1><<<(unsigned)nt, kRkThreads, sm, st>>>(n, keys1, pts1,
                                                               reinterpret_cast<double2*>(a.sorted_pts), idx1, cnt,
                                                               base, (uint32_t)nt, nullptr, a.sorted_idx);
-    *launches += 7;
+    *launches += 6;
     return cudaGetLastError();
 }
 
