@@ -604,17 +604,38 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3)
 
     // ---- phase 1: the key scan over the chunk ----
     uint32_t pending = 0; // list size (uniform)
+    // this thread's 8 key words in stage 0 (a shared address kept in a register)
+    unsigned qk_s = smem_u32(&sh.qk[0][2 * tid]);
+    asm volatile("" : "+r"(qk_s));
     for (uint32_t q = 0; q < n_tiles; ++q) {
         const int s = (int)(q & 1);
         const uint32_t t0 = t_begin + q * kQTile;
         mbar_wait(&sh.full[s], (q >> 1) & 1);
         PC_DCHECK(t0 >= e_begin && t0 < e_end);
-        const uint4 w0 = sh.qk[s][2 * tid], w1 = sh.qk[s][2 * tid + 1];
-        uint32_t m = key_hit(w0.x, kc) | key_hit(w0.y, kc) << 1 | key_hit(w0.z, kc) << 2 | key_hit(w0.w, kc) << 3 |
-                     key_hit(w1.x, kc) << 4 | key_hit(w1.y, kc) << 5 | key_hit(w1.z, kc) << 6 |
-                     key_hit(w1.w, kc) << 7;
-        const bool mine = m != 0;
+        uint32_t d[8];
+        {
+            const unsigned a = qk_s + (unsigned)s * (kQTile * 4u);
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
+                         : "r"(a));
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7])
+                         : "r"(a + 16u));
+        }
+        // d + kc has the top bit of both halves set iff the edge may meet a point
+        // (key_hit); the common no-candidate case costs one add and one LOP3 +
+        // shift per edge, the exact mask is formed only when some edge hits
+        uint32_t acc = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            d[i] += kc;
+            acc |= d[i] & (d[i] << 16);
+        }
+        const bool mine = (int)acc < 0;
         if (mine) { // rare: append this thread's candidates (edges past e_end are padding or the next chunk's)
+            uint32_t m = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) m |= ((d[i] & (d[i] << 16)) >> 31) << i;
             const uint32_t e0 = t0 + 8u * (uint32_t)tid;
             if (e0 + 8 > e_end) m &= e0 >= e_end ? 0u : (1u << (e_end - e0)) - 1u;
             uint32_t pos = atomicAdd(&sh.ncand, (uint32_t)__popc(m));
