@@ -10,6 +10,9 @@ reference classify_batch (oracle/_ref/libpolycast_ref.so, built from
   c4/Robust  the first 1e7 points (tol 1e-12)                           2e12 tests
   c2/n1e5    all 1e6 points of the sweep's 1e5-vertex star, 3 modes     3e11 tests
   c2/n1e6    all 1e6 points of the sweep's 1e6-vertex star, 3 modes     3e12 tests
+  c1         all 1e6 points of configs[0], 3 modes                      3e9 tests
+  c3         all 6.4e7 points of configs[2] (1e6 footprints; the reference
+             classify_batch per polygon, its CSR loop), 3 modes
 
 and writes the bit planes (inside, aux; bit i%32 of word i//32) to
 golden_cache/ (git-ignored, NOT gpurun-ignored: it travels to the GPU box),
@@ -59,6 +62,9 @@ def cases():
     for n in (100_000, 1_000_000):
         for m, mn in ((0, "C1"), (1, "C2"), (2, "Robust")):
             out[f"c2_n{n}_{mn}"] = (f"c2:{n}", m, 1_000_000)
+    for m, mn in ((0, "C1"), (1, "C2"), (2, "Robust")):
+        out[f"c1_{mn}"] = ("c1", m, 1_000_000)
+        out[f"c3_{mn}"] = ("c3", m, 64_000_000)
     return out
 
 
@@ -69,12 +75,43 @@ def inputs(kind):
     if kind not in _inputs:
         if kind == "c4":
             _inputs[kind] = W.config4()
+        elif kind == "c1":
+            _inputs[kind] = W.config1()
+        elif kind == "c3":
+            _inputs[kind] = W.footprints()
         else:
             _inputs[kind] = W.config2(int(kind.split(":")[1]))
     return _inputs[kind]
 
 
+def run_csr_case(name, kind, mode):
+    s = inputs(kind)
+    f = os.path.join(CACHE, "parts", name + ".npz")
+    os.makedirs(os.path.dirname(f), exist_ok=True)
+    if not os.path.exists(f):
+        t0 = time.time()
+        v, st = oracle.ref_classify_csr(s, mode, TOL, threads=0)
+        i_b, a_b = verdicts_to_bits(v, mode)
+        np.savez(f, inside=i_b, aux=a_b, stats=st)
+        print(f"[{name}] {s.n_points} points: {time.time() - t0:.1f} s", flush=True)
+    z = np.load(f)
+    np.save(os.path.join(CACHE, f"{name}_inside.npy"), z["inside"])
+    np.save(os.path.join(CACHE, f"{name}_aux.npy"), z["aux"])
+    return {
+        "config": kind, "mode": mode, "n_points": int(s.n_points), "tol": TOL, "csr": True,
+        "points_sha256": sha(s.xy), "vx_sha256": sha(s.vx), "vy_sha256": sha(s.vy),
+        "pt_off_sha256": sha(s.pt_off), "ring_off_sha256": sha(s.ring_off), "poly_ring_off_sha256": sha(s.poly_ring_off),
+        "inside_file": f"{name}_inside.npy", "inside_sha256": sha(z["inside"]),
+        "aux_file": f"{name}_aux.npy", "aux_sha256": sha(z["aux"]),
+        "stats": [int(x) for x in z["stats"]],
+        "source": "reference classify_batch per polygon (oracle/_ref ref_classify_csr, unmodified "
+                  "/root/reference/proj/include), all host threads",
+    }
+
+
 def run_case(name, kind, mode, n):
+    if kind == "c3":
+        return run_csr_case(name, kind, mode)
     poly, xy = inputs(kind)
     xy = xy[:n]
     parts_dir = os.path.join(CACHE, "parts", name)
@@ -121,8 +158,11 @@ def main():
         man = json.load(open(MANIFEST))
     want = [s for s in args.only.split(",") if s] or list(cases())
     # cheap ones first, then the headline c4/C1, so partial runs still leave usable goldens
-    pri = ["c2_n100000_C1", "c2_n100000_C2", "c2_n100000_Robust", "c2_n1000000_C1", "c4_C1",
+    pri = ["c1_C1", "c1_C2", "c1_Robust", "c3_C1", "c3_C2", "c3_Robust",
+           "c2_n100000_C1", "c2_n100000_C2", "c2_n100000_Robust", "c2_n1000000_C1", "c4_C1",
            "c2_n1000000_C2", "c4_C2", "c2_n1000000_Robust", "c4_Robust"]
+    done = {k for k, v in man.items() if os.path.exists(os.path.join(CACHE, v["inside_file"]))}
+    want = [k for k in want if k not in done or args.only]
     order = sorted(want, key=lambda k: pri.index(k) if k in pri else len(pri))
     for name in order:
         kind, mode, n = cases()[name]
