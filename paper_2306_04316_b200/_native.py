@@ -11,10 +11,9 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(_HERE, "lib")
-# POLYCAST_LIB_VARIANT=debug selects the checking build (lib/debug: device-side
-# bounds checks, `make -C paper_2306_04316_b200 debug`)
-CUDA_LIB = os.path.join(LIB_DIR, "debug" if os.environ.get("POLYCAST_LIB_VARIANT") == "debug" else "",
-                        "libpolycast_cuda.so")
+# POLYCAST_LIB_VARIANT=<dir> selects a build under lib/<dir>: "debug" is the
+# checking build (device-side bounds checks, `make -C paper_2306_04316_b200 debug`)
+CUDA_LIB = os.path.join(LIB_DIR, os.environ.get("POLYCAST_LIB_VARIANT", ""), "libpolycast_cuda.so")
 WORKLOADS_LIB = os.path.join(LIB_DIR, "libpolycast_workloads.so")
 
 PC_OK, PC_EINVAL, PC_ECUDA, PC_ENOMEM, PC_ENCCL = 0, 1, 2, 3, 4

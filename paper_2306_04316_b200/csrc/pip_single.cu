@@ -44,6 +44,10 @@ namespace {
 constexpr int kTPB = 256;
 constexpr int kK = 16;          // points per thread
 constexpr int kQTile = kKeyTile; // edge key words per shared-memory stage (8 KB; 8 per thread)
+#ifndef PC_QSTAGES
+#define PC_QSTAGES 2
+#endif
+constexpr int kStages = PC_QSTAGES; // key-scan stages in flight
 constexpr int kListCap = 4096;  // candidate edge indices; a tile can add kQTile, so flush above kListCap - kQTile
 constexpr int kBatch = 128;     // candidates gathered per batch
 static_assert(kQTile == 8 * kTPB, "phase 1: 8 key words per thread per tile");
@@ -53,11 +57,11 @@ static_assert(kQTile == 8 * kTPB, "phase 1: 8 key words per thread per tile");
 // fallbacks re-read the point from global memory (L2).
 struct SingleShared {
     float2 pts[kTPB * kK];       // this CTA's points (bucketed order), local fp32
-    uint4 qk[2][kQTile / 4];     // key-scan stages
+    uint4 qk[kStages][kQTile / 4]; // key-scan stages
     uint32_t list[kListCap];     // candidate edges of the chunk (phase 1 -> phase 2)
     uint2 bfilt[kBatch];         // gathered per-point filter words
     EdgeRec brec[kBatch];        // gathered exact records
-    unsigned long long full[2];
+    unsigned long long full[kStages];
     uint32_t ncand;
     uint32_t cta_lo, cta_hi;     // key range of the CTA's active points
     unsigned long long cta_ylo, cta_yhi; // C1/C2: dkey of their min / max y (per-CTA key map)
@@ -386,8 +390,7 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3)
 
     const uint32_t cta_n = (uint32_t)min((uint64_t)(kTPB * kK), n - cta_base);
     if (tid == 0) {
-        mbar_init(&sh.full[0], 1);
-        mbar_init(&sh.full[1], 1);
+        for (int k = 0; k < kStages; ++k) mbar_init(&sh.full[k], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         sh.ncand = 0;
         sh.cta_lo = 0xffffu;
@@ -518,7 +521,8 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3)
     // words of tile q: whole tiles, the chunk's last one rounded up to 4 words
     auto tile_words = [&](uint32_t q) { return min((uint32_t)kQTile, (e_end - (t_begin + q * kQTile) + 3u) & ~3u); };
     if (tid == 0) {
-        for (uint32_t q = 0; q < 2 && q < n_tiles; ++q) issue_tile(sh, (int)q, qk, t_begin + q * kQTile, tile_words(q));
+        for (uint32_t q = 0; q < (uint32_t)kStages && q < n_tiles; ++q)
+            issue_tile(sh, (int)q, qk, t_begin + q * kQTile, tile_words(q));
     }
 
     // may any active point of the warp straddle the edge with filter word f?
@@ -608,9 +612,9 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3)
     unsigned qk_s = smem_u32(&sh.qk[0][2 * tid]);
     asm volatile("" : "+r"(qk_s));
     for (uint32_t q = 0; q < n_tiles; ++q) {
-        const int s = (int)(q & 1);
+        const int s = (int)(q % kStages);
         const uint32_t t0 = t_begin + q * kQTile;
-        mbar_wait(&sh.full[s], (q >> 1) & 1);
+        mbar_wait(&sh.full[s], (q / kStages) & 1);
         PC_DCHECK(t0 >= e_begin && t0 < e_end);
         uint32_t d[8];
         {
@@ -648,7 +652,7 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3)
         // stage s consumed and this tile's candidates listed; the count of
         // appending threads is uniform, so is the decision to read the list size
         const int appended = __syncthreads_count(mine);
-        if (tid == 0 && q + 2 < n_tiles) issue_tile(sh, s, qk, t0 + 2 * kQTile, tile_words(q + 2));
+        if (tid == 0 && q + kStages < n_tiles) issue_tile(sh, s, qk, t0 + kStages * kQTile, tile_words(q + kStages));
         if (appended) {
             pending = sh.ncand;
             __syncthreads(); // everyone has read it before anyone appends again
