@@ -281,7 +281,10 @@ def run_ours(args, rank, world, local_rank):
             d["gather"] = torch.zeros(world * nw, dtype=torch.int32, device=dev)
         dv.append(d)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=dev)  # 256 MiB > 126 MB L2
-    eng.set_profiling(True)
+    # timed steps run as the library runs repeated device-pointer calls: replayed
+    # CUDA graphs (PC_OPT_GRAPH; captured during the warm-up); the kernel times of
+    # the roofline come from separate profiled steps right after the timed region
+    eng.set_profiling(False)
     launches = [0]
 
     def step():
@@ -321,15 +324,23 @@ def run_ours(args, rank, world, local_rank):
         dist.barrier()
     torch.cuda.synchronize()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    kern_ms = eng.profile_take(0)
     tot_ms = sum(step_ms)
+    timed_launches = launches[0]
+    n_prof = min(args.steps, 5)
+    eng.set_profiling(True)  # per-kernel events (no graph replay while profiling)
+    for _ in range(n_prof):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    kern_ms = eng.profile_take(0)
+    eng.set_profiling(False)
     from paper_2306_04316_b200.dist import max_over_ranks
     max_ms = max_over_ranks(tot_ms, world, dev)
     tot_units, tot_pts = job_totals(items, world, dev)
     value = tot_units / (max_ms / args.steps / 1e3)
 
     # ---- roofline of the dominant kernel (rank 0's device) -----------------------------
-    per_item_ms = np.array(kern_ms, dtype=np.float64).reshape(args.steps, len(items)).mean(0)
+    per_item_ms = np.array(kern_ms, dtype=np.float64).reshape(n_prof, len(items)).mean(0)
     roof = roofline(args, eng, items, per_item_ms, tot_ms)
 
     line = {"metric": "point-edge tests/s", "value": value, "unit": "tests/s", "n_gpus": world,
@@ -339,7 +350,7 @@ def run_ours(args, rank, world, local_rank):
             "config": dict(workload_config(args, world), points_per_step=tot_pts, tests_per_step=tot_units),
             "points_per_s": tot_pts / (max_ms / args.steps / 1e3),
             "per_item_tests_per_s": {i.label: i.tests / (ms / 1e3) for i, ms in zip(items, per_item_ms)},
-            "roofline": roof, "gpu_launches": launches[0]}
+            "roofline": roof, "gpu_launches": timed_launches}
 
     if args.workload == "c2_sweep":
         line["sweep_fit"] = sweep_fit(items, per_item_ms)
@@ -464,6 +475,7 @@ def run_sweep(args, eng, dev):
     items = build_items("c2_sweep", 0, 1)
     stream = torch.cuda.current_stream().cuda_stream
     ms = np.zeros(len(items))
+    eng.set_profiling(True)
     for j, it in enumerate(items):
         xy = torch.from_numpy(it.xy).to(dev)
         vx, vy = torch.from_numpy(it.poly.vx).to(dev), torch.from_numpy(it.poly.vy).to(dev)
@@ -477,6 +489,7 @@ def run_sweep(args, eng, dev):
                              1e-12, True, bits[:nw], bits[nw:], stats)
         torch.cuda.synchronize()
         ms[j] = float(np.mean(eng.profile_take(0)[1:]))
+    eng.set_profiling(False)
     return {"workload": WORKLOAD_NAMES["c2_sweep"], "mode": MODE_NAMES[args.mode],
             "kernel_ms": {it.label: float(m) for it, m in zip(items, ms)},
             "tests_per_s": {it.label: it.tests / (m / 1e3) for it, m in zip(items, ms)},

@@ -214,6 +214,11 @@ uint64_t pc_last_launch_count(const pc_ctx* ctx);
  *  no bucketing, no tree).  A checker for the fast path on full-size inputs;
  *  results are identical by construction of the fast path. */
 #define PC_OPT_EXACT 3
+/*  PC_OPT_GRAPH: 1 on (default), 0 off — a device-pointer call (pc_classify_dev,
+ *  pc_classify_csr_dev) repeated with identical arguments is captured once as
+ *  a CUDA graph and replayed (one launch for the call's kernels and memsets).
+ *  Not used while profiling (pc_set_profiling) or with PC_OPT_TREE. */
+#define PC_OPT_GRAPH 4
 int pc_set_option(pc_ctx* ctx, int option, int64_t value);
 
 /* Measurement hooks (bench.py).  With profiling on, every call records a pair

@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -20,11 +21,16 @@
 
 namespace {
 
+// bumped whenever a scratch buffer is (re)allocated: captured graphs that
+// embed the old addresses are then stale
+std::atomic<uint64_t> g_alloc_gen{0};
+
 struct DevBuf {
     void* p = nullptr;
     size_t cap = 0;
     cudaError_t ensure(size_t bytes) {
         if (bytes <= cap) return cudaSuccess;
+        ++g_alloc_gen;
         if (p) cudaFree(p);
         p = nullptr;
         cap = 0;
@@ -63,6 +69,16 @@ struct DevState {
     size_t h_small_cap = 0;
     unsigned long long* h_stats = nullptr; // pinned 4 x u64
     uint64_t launches = 0;                 // kernels this device launched in the current call
+    // device-pointer calls replayed as CUDA graphs (PC_OPT_GRAPH): key = every
+    // argument and option of the call; exec == nullptr: seen once (the next
+    // identical call is captured, after this one settled the scratch sizes)
+    struct Graph {
+        std::vector<uint64_t> key;
+        cudaGraphExec_t exec = nullptr;
+        uint64_t gen = 0, launches = 0;
+        bool failed = false;
+    };
+    std::vector<Graph> graphs;
     pch::Stager* stager = nullptr;         // pageable host copies (host_stage.h), made on first use
     // profiling: one event pair per main-kernel launch since the last take
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
@@ -83,6 +99,7 @@ struct pc_ctx {
     int64_t bucket_mode = -1; // PC_OPT_BUCKET_POINTS: -1 auto, 0 off, 1 on
     int64_t tree_mode = 0;    // PC_OPT_TREE: 0 off (default), 1 on (opt-in extension, not the reference scan)
     bool exact = false;       // PC_OPT_EXACT: the literal binary64 loop only (pip_exact.cu)
+    bool graphs = true;       // PC_OPT_GRAPH: replay repeated device-pointer calls as CUDA graphs
 };
 
 namespace {
@@ -383,6 +400,78 @@ void merge_bits(uint32_t* dst, const uint32_t* src, uint64_t bit_off, uint64_t n
     }
 }
 
+// Runs `enqueue` (which launches the whole call on stream st) directly, or --
+// for the second and later identical device-pointer calls -- as a captured
+// CUDA graph: one launch instead of one per kernel and memset.  Profiling, the
+// opt-in segment tree (host syncs) and the first call of a key run directly.
+template <class Fn>
+void run_maybe_graph(pc_ctx* c, DevState& d, cudaStream_t st, std::vector<uint64_t> key, bool allow, Fn&& enqueue) {
+    if (!c->graphs || c->profiling || !allow) {
+        enqueue();
+        return;
+    }
+    key.push_back(c->bucket_mode);
+    key.push_back(c->tree_mode);
+    key.push_back(c->exact);
+    DevState::Graph* g = nullptr;
+    for (auto& e : d.graphs)
+        if (e.key == key) g = &e;
+    const uint64_t gen = g_alloc_gen.load();
+    if (g && g->exec && g->gen == gen) {
+        check(c, cudaGraphLaunch(g->exec, st), "graph launch");
+        d.launches = g->launches;
+        return;
+    }
+    if (!g || g->failed || (g->exec && g->gen != gen) || !g->exec) {
+        const bool capture_now = g && !g->failed && g->gen == gen && !g->exec; // seen once, sizes settled
+        if (!capture_now) {
+            if (!g) {
+                if (d.graphs.size() >= 16) { // bounded cache: drop the oldest
+                    if (d.graphs.front().exec) cudaGraphExecDestroy(d.graphs.front().exec);
+                    d.graphs.erase(d.graphs.begin());
+                }
+                d.graphs.push_back(DevState::Graph{key, nullptr, 0, 0, false});
+                g = &d.graphs.back();
+            } else if (g->exec) {
+                cudaGraphExecDestroy(g->exec);
+                g->exec = nullptr;
+            }
+            enqueue();
+            g->gen = g_alloc_gen.load();
+            return;
+        }
+    }
+    // capture the call's launches
+    cudaGraph_t graph = nullptr;
+    const uint64_t l0 = d.launches;
+    check(c, cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
+    try {
+        enqueue();
+    } catch (...) {
+        cudaStreamEndCapture(st, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        cudaGetLastError();
+        g->failed = true;
+        enqueue(); // outside capture
+        return;
+    }
+    const cudaError_t ce = cudaStreamEndCapture(st, &graph);
+    cudaGraphExec_t exec = nullptr;
+    if (ce != cudaSuccess || g_alloc_gen.load() != gen ||
+        cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+        if (graph) cudaGraphDestroy(graph);
+        cudaGetLastError();
+        g->failed = true;
+        enqueue();
+        return;
+    }
+    cudaGraphDestroy(graph);
+    g->exec = exec;
+    g->gen = gen;
+    g->launches = d.launches - l0;
+    check(c, cudaGraphLaunch(exec, st), "graph launch");
+}
+
 // The polygon of a small call on the device: reused while the caller passes the
 // same vertices (compared by content, so a changed polygon is never stale).
 void cache_polygon(pc_ctx* c, DevState& d, const double* vx, const double* vy, const uint64_t* ring_off,
@@ -524,6 +613,8 @@ void pc_destroy(pc_ctx* c) {
             cudaEventDestroy(e.first);
             cudaEventDestroy(e.second);
         }
+        for (auto& g : d.graphs)
+            if (g.exec) cudaGraphExecDestroy(g.exec);
         if (d.copy) cudaStreamDestroy(d.copy);
         for (cudaEvent_t e : d.up_evs) cudaEventDestroy(e);
         cudaStreamDestroy(d.stream);
@@ -553,6 +644,10 @@ int pc_set_option(pc_ctx* c, int option, int64_t value) {
     }
     if (option == PC_OPT_EXACT && (value == 0 || value == 1)) {
         c->exact = value == 1;
+        return PC_OK;
+    }
+    if (option == PC_OPT_GRAPH && (value == 0 || value == 1)) {
+        c->graphs = value == 1;
         return PC_OK;
     }
     c->err = "unknown option or value";
@@ -1070,8 +1165,18 @@ int pc_classify_dev(pc_ctx* c, int dev_index, void* stream, const double* d_pts_
             check(c, cudaMemsetAsync(d_stats, 0, 32, st), "clear stats");
             return;
         }
-        enqueue_single(c, d, st, d_pts_xy, n, d_vx, d_vy, d_ring_off, n_rings, n_verts, mode, tol, prefilter,
-                       d_verdicts, d_inside, d_aux, reinterpret_cast<unsigned long long*>(d_stats));
+        uint64_t tolbits;
+        std::memcpy(&tolbits, &tol, 8);
+        const std::vector<uint64_t> key{0, (uint64_t)dev_index, (uint64_t)(uintptr_t)st, (uint64_t)(uintptr_t)d_pts_xy,
+                                        n, (uint64_t)(uintptr_t)d_vx, (uint64_t)(uintptr_t)d_vy,
+                                        (uint64_t)(uintptr_t)d_ring_off, n_rings, n_verts, (uint64_t)mode, tolbits,
+                                        (uint64_t)prefilter, (uint64_t)(uintptr_t)d_verdicts,
+                                        (uint64_t)(uintptr_t)d_inside, (uint64_t)(uintptr_t)d_aux,
+                                        (uint64_t)(uintptr_t)d_stats};
+        run_maybe_graph(c, d, st, key, c->tree_mode != 1, [&] {
+            enqueue_single(c, d, st, d_pts_xy, n, d_vx, d_vy, d_ring_off, n_rings, n_verts, mode, tol, prefilter,
+                           d_verdicts, d_inside, d_aux, reinterpret_cast<unsigned long long*>(d_stats));
+        });
     });
 }
 
@@ -1090,8 +1195,18 @@ int pc_classify_csr_dev(pc_ctx* c, int dev_index, void* stream, const double* d_
             check(c, cudaMemsetAsync(d_stats, 0, 32, st), "clear stats");
             return;
         }
-        enqueue_csr(c, d, st, d_pts_xy, n_points, d_pt_off, n_polys, d_vx, d_vy, d_ring_off, d_poly_ring_off, 0, 0, 0,
-                    mode, tol, d_verdicts, d_inside, d_aux, reinterpret_cast<unsigned long long*>(d_stats));
+        uint64_t tolbits;
+        std::memcpy(&tolbits, &tol, 8);
+        const std::vector<uint64_t> key{1, (uint64_t)dev_index, (uint64_t)(uintptr_t)st, (uint64_t)(uintptr_t)d_pts_xy,
+                                        (uint64_t)(uintptr_t)d_pt_off, n_polys, n_points, (uint64_t)(uintptr_t)d_vx,
+                                        (uint64_t)(uintptr_t)d_vy, (uint64_t)(uintptr_t)d_ring_off,
+                                        (uint64_t)(uintptr_t)d_poly_ring_off, (uint64_t)mode, tolbits,
+                                        (uint64_t)(uintptr_t)d_verdicts, (uint64_t)(uintptr_t)d_inside,
+                                        (uint64_t)(uintptr_t)d_aux, (uint64_t)(uintptr_t)d_stats};
+        run_maybe_graph(c, d, st, key, true, [&] {
+            enqueue_csr(c, d, st, d_pts_xy, n_points, d_pt_off, n_polys, d_vx, d_vy, d_ring_off, d_poly_ring_off, 0,
+                        0, 0, mode, tol, d_verdicts, d_inside, d_aux, reinterpret_cast<unsigned long long*>(d_stats));
+        });
     });
 }
 

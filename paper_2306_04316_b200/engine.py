@@ -204,6 +204,11 @@ class Engine:
         changes results."""
         self.set_option(2, mode)
 
+    def set_graphs(self, on: bool):
+        """PC_OPT_GRAPH (default on): repeated identical device-pointer calls replay
+        a captured CUDA graph."""
+        self.set_option(4, int(bool(on)))
+
     def set_exact(self, on: bool):
         """PC_OPT_EXACT: run only the literal binary64 loop (pip_exact.cu), the
         full-size checker of the fast path."""

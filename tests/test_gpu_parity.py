@@ -596,3 +596,42 @@ def test_csr_robust_tolerances(engine):
         want_v, want_s = oracle.port_classify_csr(s, CrossingMode.Robust, tol=tol, threads=THREADS)
         assert np.array_equal(got.verdicts, want_v), (tol, int((got.verdicts != want_v).sum()))
         assert np.array_equal(got.stats, want_s)
+
+
+def test_graph_replay_matches_direct_calls():
+    """PC_OPT_GRAPH: the 2nd identical device-pointer call is captured, later ones
+    replay the graph; results must equal direct (graph-off) calls, follow changed
+    input contents at the same addresses, and survive scratch re-allocation
+    (a bigger call in between invalidates the captured addresses)."""
+    import torch
+    dev = torch.device("cuda:0")
+    poly, xy = W.config2(1000, n_points=200_000)
+    big = W.uniform_points(3_000_000, W.bounds(poly), 5)
+    t = {k: torch.from_numpy(v).to(dev) for k, v in (("vx", poly.vx), ("vy", poly.vy))}
+    ro = torch.from_numpy(np.ascontiguousarray(poly.ring_off).view(np.int64)).to(dev)
+    d_xy = torch.from_numpy(xy).to(dev)
+    d_big = torch.from_numpy(big).to(dev)
+    with Engine(devices=[0]) as g, Engine(devices=[0]) as direct:
+        direct.set_graphs(False)
+        for mode in MODES:
+            def run(eng, pts, n):
+                nw = (n + 31) // 32
+                bits = torch.zeros(2 * nw, dtype=torch.int32, device=dev)
+                st = torch.zeros(4, dtype=torch.int64, device=dev)
+                s = torch.cuda.current_stream().cuda_stream
+                eng.classify_dev(0, s, pts, n, t["vx"], t["vy"], ro, poly.n_rings, poly.n_verts, mode, 1e-12, True,
+                                 bits[:nw], bits[nw:], st)
+                torch.cuda.synchronize()
+                return bits.cpu().numpy(), st.cpu().numpy()
+            want = run(direct, d_xy, len(xy))
+            for _ in range(4):  # direct, capture, replay, replay
+                got = run(g, d_xy, len(xy))
+                assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+            want_big = run(direct, d_big, len(big))
+            got_big = run(g, d_big, len(big))  # grows the scratch: captured graphs are stale
+            assert np.array_equal(got_big[0], want_big[0])
+            d_xy.copy_(torch.flip(d_xy, [0]))  # new contents, same address
+            want2 = run(direct, d_xy, len(xy))
+            for _ in range(3):
+                got2 = run(g, d_xy, len(xy))
+                assert np.array_equal(got2[0], want2[0]) and np.array_equal(got2[1], want2[1])
