@@ -41,16 +41,24 @@ namespace pcd {
 
 namespace {
 
-constexpr int kTPB = 256;
-constexpr int kK = 16;          // points per thread
+#ifndef PC_TPB
+#define PC_TPB 256
+#endif
+#ifndef PC_KPT
+#define PC_KPT 16
+#endif
+constexpr int kTPB = PC_TPB;    // threads per CTA
+constexpr int kK = PC_KPT;      // points per thread (a CTA holds kTPB * kK points)
+constexpr uint32_t kAllK = kK >= 32 ? 0xffffffffu : (1u << kK) - 1u; // a mask of all of a thread's points
 constexpr int kQTile = kKeyTile; // edge key words per shared-memory stage (8 KB; 8 per thread)
 #ifndef PC_QSTAGES
 #define PC_QSTAGES 2
 #endif
 constexpr int kStages = PC_QSTAGES; // key-scan stages in flight
 constexpr int kListCap = 4096;  // candidate edge indices; a tile can add kQTile, so flush above kListCap - kQTile
-constexpr int kBatch = 128;     // candidates gathered per batch
-static_assert(kQTile == 8 * kTPB, "phase 1: 8 key words per thread per tile");
+constexpr int kBatch = PC_TPB / 2; // candidates gathered per batch (two threads each)
+constexpr int kEPT = kQTile / kTPB; // phase 1: key words per thread per tile
+static_assert(kEPT == 8 || kEPT == 4, "phase 1 reads 1 or 2 uint4 per thread");
 
 // Every mode keeps only the polygon-local fp32 coordinates of its points in
 // shared memory (the certified fp32 side / intercept test); the binary64
@@ -227,7 +235,7 @@ __device__ __forceinline__ void slow_c1(const float2* my_l, const PtRef& my_g, c
     }
     // undecided: band hits (rare: per point only then), points without local
     // coordinates (nonloc) and edges without a record (NaN: every point)
-    uint32_t und = nonloc | ((nxf == nxf) ? 0u : 0xffffu);
+    uint32_t und = nonloc | ((nxf == nxf) ? 0u : kAllK);
     if (umin <= k2B) {
 #pragma unroll
         for (int k = 0; k < kK; ++k) {
@@ -283,7 +291,7 @@ __device__ __forceinline__ void slow_c2(const float2* my_l, const PtRef& my_g, c
         hit = (hit << 1) | (u >> 31);
         umin = min(umin, u);
     }
-    uint32_t und = nonloc | ((nxf == nxf) ? 0u : 0xffffu);
+    uint32_t und = nonloc | ((nxf == nxf) ? 0u : kAllK);
     if (umin <= k2B) {
 #pragma unroll
         for (int k = 0; k < kK; ++k) {
@@ -344,7 +352,7 @@ __device__ __forceinline__ void slow_robust(const float2* my_l, const PtRef& my_
         hit = (hit << 1) | (u >> 31);
         umin = min(umin, u);
     }
-    uint32_t und = nonloc | ((nxf == nxf) ? 0u : 0xffffu);
+    uint32_t und = nonloc | ((nxf == nxf) ? 0u : kAllK);
     if (umin <= k2B) {
 #pragma unroll
         for (int k = 0; k < kK; ++k) {
@@ -371,7 +379,7 @@ __device__ __forceinline__ void slow_robust(const float2* my_l, const PtRef& my_
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3)
+__global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 : 3))
     pip_tile_kernel(const double2* __restrict__ pts, uint64_t n, const uint32_t* __restrict__ qk,
                     const uint2* __restrict__ filt, const EdgeRec* __restrict__ rec, uint32_t n_edges,
                     uint32_t edges_per_chunk, const unsigned long long* __restrict__ bbox_keys, int prefilter,
@@ -608,30 +616,29 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3)
 
     // ---- phase 1: the key scan over the chunk ----
     uint32_t pending = 0; // list size (uniform)
-    // this thread's 8 key words in stage 0 (a shared address kept in a register)
-    unsigned qk_s = smem_u32(&sh.qk[0][2 * tid]);
+    // this thread's kEPT key words in stage 0 (a shared address kept in a register)
+    unsigned qk_s = smem_u32(&sh.qk[0][(kEPT / 4) * tid]);
     asm volatile("" : "+r"(qk_s));
     for (uint32_t q = 0; q < n_tiles; ++q) {
         const int s = (int)(q % kStages);
         const uint32_t t0 = t_begin + q * kQTile;
         mbar_wait(&sh.full[s], (q / kStages) & 1);
         PC_DCHECK(t0 >= e_begin && t0 < e_end);
-        uint32_t d[8];
+        uint32_t d[kEPT];
         {
             const unsigned a = qk_s + (unsigned)s * (kQTile * 4u);
-            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
-                         : "r"(a));
-            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7])
-                         : "r"(a + 16u));
+#pragma unroll
+            for (int j = 0; j < kEPT / 4; ++j)
+                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(d[4 * j]), "=r"(d[4 * j + 1]), "=r"(d[4 * j + 2]), "=r"(d[4 * j + 3])
+                             : "r"(a + 16u * j));
         }
         // d + kc has the top bit of both halves set iff the edge may meet a point
         // (key_hit); the common no-candidate case costs one add and one LOP3 +
         // shift per edge, the exact mask is formed only when some edge hits
         uint32_t acc = 0;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < kEPT; ++i) {
             d[i] += kc;
             acc |= d[i] & (d[i] << 16);
         }
@@ -639,9 +646,9 @@ __global__ void __launch_bounds__(kTPB, MODE == kRobust ? 2 : 3)
         if (mine) { // rare: append this thread's candidates (edges past e_end are padding or the next chunk's)
             uint32_t m = 0;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) m |= ((d[i] & (d[i] << 16)) >> 31) << i;
-            const uint32_t e0 = t0 + 8u * (uint32_t)tid;
-            if (e0 + 8 > e_end) m &= e0 >= e_end ? 0u : (1u << (e_end - e0)) - 1u;
+            for (int i = 0; i < kEPT; ++i) m |= ((d[i] & (d[i] << 16)) >> 31) << i;
+            const uint32_t e0 = t0 + (uint32_t)kEPT * (uint32_t)tid;
+            if (e0 + kEPT > e_end) m &= e0 >= e_end ? 0u : (1u << (e_end - e0)) - 1u;
             uint32_t pos = atomicAdd(&sh.ncand, (uint32_t)__popc(m));
             PC_DCHECK(pos + (uint32_t)__popc(m) <= (uint32_t)kListCap);
             while (m) {
