@@ -103,10 +103,12 @@ int pc_count_crossings(pc_ctx* ctx, const double* pts_xy, uint64_t n, const doub
 
 /* Device-pointer variants on the context's GPU `dev_index`, enqueued on
  * `stream` (a cudaStream_t; NULL = the context's stream) and NOT synchronised
- * (the segment-tree path of pc_classify_dev waits on the stream twice for
- * sizes it needs on the host: its node-list split and its fallback count).
+ * (the opt-in segment-tree path of pc_classify_dev waits on the stream twice
+ * for sizes it needs on the host).  d_pts_xy must be 16-byte aligned (the
+ * kernels load points as double2; cudaMalloc memory always is).
  * d_inside_bits / d_aux_bits (ceil(n/32) words) and d_stats (4 x u64) are
- * required; d_verdicts is optional.  Used for kernel-only timing and by
+ * required; d_verdicts is optional.  Repeated identical calls replay a
+ * captured CUDA graph (PC_OPT_GRAPH).  Used for kernel-only timing and by
  * callers that keep their data resident in HBM. */
 int pc_classify_dev(pc_ctx* ctx, int dev_index, void* stream, const double* d_pts_xy, uint64_t n,
                     const double* d_vx, const double* d_vy, const uint64_t* d_ring_off,

@@ -1158,6 +1158,7 @@ int pc_classify_dev(pc_ctx* c, int dev_index, void* stream, const double* d_pts_
         if (mode < 0 || mode > 2) invalid(c, "mode must be 0 (C1), 1 (C2) or 2 (Robust)");
         if (n_rings < 1 || n_verts < n_rings) invalid(c, "bad ring layout");
         if (!d_inside || !d_aux || !d_stats) invalid(c, "null output planes");
+        if (reinterpret_cast<uintptr_t>(d_pts_xy) & 15) invalid(c, "device points must be 16-byte aligned");
         DevState& d = c->devs[dev_index];
         check(c, cudaSetDevice(d.dev), "cudaSetDevice");
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d.stream;
