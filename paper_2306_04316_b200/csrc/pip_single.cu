@@ -50,15 +50,30 @@ namespace {
 constexpr int kTPB = PC_TPB;    // threads per CTA
 constexpr int kK = PC_KPT;      // points per thread (a CTA holds kTPB * kK points)
 constexpr uint32_t kAllK = kK >= 32 ? 0xffffffffu : (1u << kK) - 1u; // a mask of all of a thread's points
-constexpr int kQTile = kKeyTile; // edge key words per shared-memory stage (8 KB; 8 per thread)
+#ifndef PC_QTILE
+#define PC_QTILE kKeyTile
+#endif
+#ifndef PC_LISTCAP
+#define PC_LISTCAP 4096
+#endif
+#ifndef PC_BATCH
+#define PC_BATCH (PC_TPB / 2)
+#endif
+#ifndef PC_MINB
+#define PC_MINB 3
+#endif
+constexpr int kQTile = PC_QTILE; // edge key words per shared-memory stage (8 KB; 8 per thread)
+static_assert(kKeyTile % kQTile == 0 || kQTile % kKeyTile == 0, "tiles and the key array's padding");
 #ifndef PC_QSTAGES
 #define PC_QSTAGES 2
 #endif
 constexpr int kStages = PC_QSTAGES; // key-scan stages in flight
-constexpr int kListCap = 4096;  // candidate edge indices; a tile can add kQTile, so flush above kListCap - kQTile
-constexpr int kBatch = PC_TPB / 2; // candidates gathered per batch (two threads each)
+constexpr int kListCap = PC_LISTCAP; // candidate edge indices; a tile can add kQTile, so flush above kListCap - kQTile
+static_assert(kListCap >= kQTile, "the list must hold one tile's candidates");
+constexpr int kBatch = PC_BATCH;     // candidates gathered per batch (two threads each)
+static_assert(kBatch <= PC_TPB / 2, "the gather uses two threads per candidate");
 constexpr int kEPT = kQTile / kTPB; // phase 1: key words per thread per tile
-static_assert(kEPT == 8 || kEPT == 4, "phase 1 reads 1 or 2 uint4 per thread");
+static_assert(kEPT == 16 || kEPT == 8 || kEPT == 4, "phase 1 reads 1, 2 or 4 uint4 per thread");
 
 // Every mode keeps only the polygon-local fp32 coordinates of its points in
 // shared memory (the certified fp32 side / intercept test); the binary64
@@ -379,7 +394,7 @@ __device__ __forceinline__ void slow_robust(const float2* my_l, const PtRef& my_
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 : 3))
+__global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 : PC_MINB))
     pip_tile_kernel(const double2* __restrict__ pts, uint64_t n, const uint32_t* __restrict__ qk,
                     const uint2* __restrict__ filt, const EdgeRec* __restrict__ rec, uint32_t n_edges,
                     uint32_t edges_per_chunk, const unsigned long long* __restrict__ bbox_keys, int prefilter,

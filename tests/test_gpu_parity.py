@@ -635,3 +635,19 @@ def test_graph_replay_matches_direct_calls():
             for _ in range(3):
                 got2 = run(g, d_xy, len(xy))
                 assert np.array_equal(got2[0], want2[0]) and np.array_equal(got2[1], want2[1])
+
+
+@pytest.mark.parametrize("n_edges", [3, 63, 64, 65, 1023, 2047, 2048, 2049, 4095, 4097, 6143, 32767, 32769])
+def test_scan_chunk_and_tile_boundaries(engine, n_edges):
+    """Edge counts around the scan kernel's key tiles (2048), 4-word copy
+    granularity, 64-edge chunks and the 32768-edge wave switch: the fast path
+    equals the literal loop (PC_OPT_EXACT) on 300k y-ordered points, all modes."""
+    poly = W.star_polygon(n_edges, seed=n_edges)
+    xy = W.uniform_points(300_000, W.bounds(poly), n_edges + 1)
+    with Engine(devices=[0]) as ex:
+        ex.set_exact(True)
+        for mode in MODES:
+            a = engine.classify(xy, poly, mode, verdicts=False)
+            b = ex.classify(xy, poly, mode, verdicts=False)
+            assert np.array_equal(a.inside_bits, b.inside_bits) and np.array_equal(a.aux_bits, b.aux_bits), mode
+            assert np.array_equal(a.stats, b.stats)
