@@ -12,7 +12,8 @@
 // unchanged.
 //
 // Sort: 16-bit keys (65280 y levels over the outer ring's bbox, 0xffff =
-// rejected), two stable LSD passes of 8 bits over (key, point, index); each
+// rejected), two LSD passes of 8 bits over (key, point, index), stable at tile
+// granularity (rk_scatter_kernel); each
 // pass reads its tile coalesced, ranks it in shared memory and writes
 // contiguous runs per digit, so the points move in whole lines (a gather by
 // index would pull a 128-byte line per 16-byte point).
@@ -20,9 +21,9 @@
 //                      the pass-0 output by rk_count_hi_kernel)
 //   rk_scan_kernel     per (digit, tile) offsets: a warp per digit scans its
 //                      tiles, then one warp scans the 256 digit totals
-//   rk_scatter_kernel  per tile: stable rank in shared memory (warp-striped
-//                      rounds with __match_any_sync), staged by digit, written
-//                      out in contiguous runs per digit
+//   rk_scatter_kernel  per tile: rank in shared memory (atomics on the tile's
+//                      digit histogram), staged by digit, written out in
+//                      contiguous runs per digit
 #include "pip_kernels.h"
 
 #include <cuda_runtime.h>
@@ -170,17 +171,22 @@ __global__ void __launch_bounds__(256) rk_colscan_kernel(uint32_t* __restrict__ 
 
 struct RkShared {
     double2 spts[kRkTile];
-    uint32_t wcnt[kRkWarps][256];
-    uint32_t boff[256];
-    uint32_t gbase[256];
+    uint32_t hist[256];  // per digit: the tile's running count, then its start in the tile
+    uint32_t gbase[256]; // global start of this tile's run of each digit
     uint32_t sidx[kRkTile];
     uint16_t skey[kRkTile];
 };
 
-// One stable counting-sort pass over tile blockIdx.x: (key, idx) -> position
+// One counting-sort pass over tile blockIdx.x: (key, idx) -> position
 // base[digit] + cnt[digit][tile] + (rank of the element among the tile's
-// elements with that digit, in element order).  PASS 0: idx = element position
-// (implicit), writes keys_out and idx_out; PASS 1: writes idx_out only.
+// elements with that digit).  The rank inside a tile comes from shared-memory
+// atomics, so elements of one digit may leave a tile in any order: the runs
+// keep the tile order (the passes stay stable at tile granularity), and in the
+// second pass a tile's elements of one high digit nearly all share the low
+// digit too.  The y-order only steers performance -- every result is exact for
+// any order (pip_single.cu) -- so this is all the scan kernel needs.
+// PASS 0: idx = element position (implicit), writes keys_out and idx_out;
+// PASS 1: writes idx_out only.
 template <int PASS, bool IMPLICIT = PASS == 0>
 __global__ void __launch_bounds__(kRkThreads, 2) rk_scatter_kernel(uint64_t n, const uint16_t* __restrict__ keys_in,
                                                                 const double2* __restrict__ pts_in,
@@ -192,60 +198,37 @@ __global__ void __launch_bounds__(kRkThreads, 2) rk_scatter_kernel(uint64_t n, c
                                                                 uint32_t* __restrict__ idx_out) {
     extern __shared__ __align__(16) unsigned char rk_smem[];
     RkShared& S = *reinterpret_cast<RkShared*>(rk_smem);
-    auto& wcnt = S.wcnt; // per-warp running counts, then per-warp offsets
-    auto& boff = S.boff; // tile-local start of each digit
-    auto& gbase = S.gbase; // global start of this tile's run of each digit
-    auto& skey = S.skey;
-    auto& sidx = S.sidx;
-    auto& spts = S.spts;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x;
     const int shift = 8 * PASS;
-    for (int j = tid; j < kRkWarps * 256; j += kRkThreads) (&wcnt[0][0])[j] = 0;
-    for (int d = tid; d < 256; d += kRkThreads)
-        gbase[d] = base[PASS * 256 + d] + cnt[(uint64_t)PASS * 256 * n_tiles + (uint64_t)d * n_tiles + blockIdx.x];
-    __syncthreads();
     const uint64_t t0 = (uint64_t)blockIdx.x * kRkTile;
     const uint32_t tn = (uint32_t)min((uint64_t)kRkTile, n - t0);
-    // warp w ranks elements [w * 512, (w + 1) * 512) of the tile in 16 rounds of
-    // 32; kr[j] = key << 16 | rank among the warp's earlier elements of its digit
-    uint32_t kr[kRkItems], idx[IMPLICIT ? 1 : kRkItems];
-    const unsigned lt = (1u << lane) - 1u;
+    // this thread's elements e = j * kRkThreads + tid: keys, indices and points
+    // are all requested before the ranking, so their latency overlaps it
+    uint32_t key[kRkItems], idx[IMPLICIT ? 1 : kRkItems];
+    double2 pt[kRkItems];
 #pragma unroll
     for (int j = 0; j < kRkItems; ++j) {
-        const uint32_t e = (uint32_t)warp * 32 * kRkItems + j * 32 + lane;
+        const uint32_t e = j * kRkThreads + tid;
         const bool live = e < tn;
-        kr[j] = live ? (uint32_t)keys_in[t0 + e] << 16 : 0xffffffffu;
+        key[j] = live ? (uint32_t)keys_in[t0 + e] : 0xffffffffu;
         if constexpr (!IMPLICIT) idx[j] = live ? idx_in[t0 + e] : 0u;
+        pt[j] = live ? pts_in[t0 + e] : make_double2(0.0, 0.0);
     }
-#pragma unroll
-    for (int j = 0; j < kRkItems; ++j) {
-        const bool live = kr[j] != 0xffffffffu;
-        const uint32_t d = (kr[j] >> (16 + shift)) & 0xffu;
-        const unsigned live_m = __ballot_sync(0xffffffffu, live);
-        const unsigned peers = __match_any_sync(0xffffffffu, live ? d : 0x100u) & live_m;
-        if (live) kr[j] |= wcnt[warp][d] + __popc(peers & lt);
-        __syncwarp();
-        if (live && (peers & lt) == 0) wcnt[warp][d] += __popc(peers); // the lowest peer advances the count
-        __syncwarp();
+    for (int d = tid; d < 256; d += kRkThreads) {
+        S.hist[d] = 0;
+        S.gbase[d] = base[PASS * 256 + d] + cnt[(uint64_t)PASS * 256 * n_tiles + (uint64_t)d * n_tiles + blockIdx.x];
     }
     __syncthreads();
-    // per digit: exclusive prefix over the warps (in place) and the tile total
-    if (tid < 256) {
-        uint32_t run = 0;
+    uint32_t rank[kRkItems];
 #pragma unroll
-        for (int w = 0; w < kRkWarps; ++w) {
-            const uint32_t v = wcnt[w][tid];
-            wcnt[w][tid] = run;
-            run += v;
-        }
-        boff[tid] = run; // tile total of digit tid, scanned below
-    }
+    for (int j = 0; j < kRkItems; ++j)
+        if (key[j] != 0xffffffffu) rank[j] = atomicAdd(&S.hist[(key[j] >> shift) & 0xffu], 1u);
     __syncthreads();
-    if (tid < 32) { // exclusive scan of the 256 totals by one warp (8 per lane)
+    if (tid < 32) { // exclusive scan of the 256 digit counts by one warp (8 per lane)
         uint32_t v[8], sum = 0;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            v[q] = boff[tid * 8 + q];
+            v[q] = S.hist[tid * 8 + q];
             sum += v[q];
         }
         uint32_t incl = sum;
@@ -257,32 +240,31 @@ __global__ void __launch_bounds__(kRkThreads, 2) rk_scatter_kernel(uint64_t n, c
         uint32_t run = incl - sum;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            boff[tid * 8 + q] = run;
+            S.hist[tid * 8 + q] = run;
             run += v[q];
         }
     }
     __syncthreads();
+    // staged in digit order
 #pragma unroll
     for (int j = 0; j < kRkItems; ++j) {
-        if (kr[j] == 0xffffffffu) continue;
-        const uint32_t k = kr[j] >> 16, d = (k >> shift) & 0xffu;
-        const uint32_t pos = boff[d] + wcnt[warp][d] + (kr[j] & 0xffffu);
+        if (key[j] == 0xffffffffu) continue;
+        const uint32_t pos = S.hist[(key[j] >> shift) & 0xffu] + rank[j];
         PC_DCHECK(pos < tn);
-        const uint32_t e = (uint32_t)warp * 32 * kRkItems + j * 32 + lane;
-        skey[pos] = (uint16_t)k;
-        spts[pos] = pts_in[t0 + e]; // coalesced read, staged in digit order
-        if constexpr (IMPLICIT) sidx[pos] = (uint32_t)(t0 + e);
-        else sidx[pos] = idx[j];
+        S.skey[pos] = (uint16_t)key[j];
+        S.spts[pos] = pt[j];
+        if constexpr (IMPLICIT) S.sidx[pos] = (uint32_t)(t0 + j * kRkThreads + tid);
+        else S.sidx[pos] = idx[j];
     }
     __syncthreads();
-    // contiguous runs per digit: element at tile position L goes to gbase[d] + (L - boff[d])
+    // contiguous runs per digit: element at tile position L goes to gbase[d] + (L - hist[d])
     for (uint32_t L = tid; L < tn; L += kRkThreads) {
-        const uint32_t k = skey[L], d = (k >> shift) & 0xffu;
-        const uint64_t g = (uint64_t)gbase[d] + (L - boff[d]);
-        PC_DCHECK(g < n && L >= boff[d]);
+        const uint32_t k = S.skey[L], d = (k >> shift) & 0xffu;
+        const uint64_t g = (uint64_t)S.gbase[d] + (L - S.hist[d]);
+        PC_DCHECK(g < n && L >= S.hist[d]);
         if (PASS == 0) keys_out[g] = (uint16_t)k;
-        pts_out[g] = spts[L];
-        idx_out[g] = sidx[L];
+        pts_out[g] = S.spts[L];
+        idx_out[g] = S.sidx[L];
     }
 }
 
