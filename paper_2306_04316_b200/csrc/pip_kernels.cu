@@ -167,11 +167,13 @@ __global__ void __launch_bounds__(256) prep_edges_kernel(
                           blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, (uint64_t)gridDim.x * blockDim.x);
 }
 
-// Polygons of up to kPrepSmall vertices: the whole prep in one CTA -- plane and
-// stats zeroing, the outer-ring bbox (a block reduction instead of atomics, so
-// no pre-set), then the edge records -- one launch instead of a memset and two.
+// Polygons of up to kPrepSmall vertices: the whole prep in one launch -- CTA 0
+// does the stats zeroing, the outer-ring bbox (a block reduction instead of
+// atomics, so no pre-set) and the edge records, the other CTAs clear the
+// output planes -- one launch instead of a memset and two.
 constexpr int kPrepThreads = 1024;
 constexpr uint64_t kPrepSmall = 16384;
+constexpr uint64_t kPrepZero = 8192; // plane words cleared per extra CTA of prep_small_kernel
 template <int MODE>
 __global__ void __launch_bounds__(kPrepThreads) prep_small_kernel(
     const double* __restrict__ vx, const double* __restrict__ vy, const uint64_t* __restrict__ ring_off,
@@ -181,9 +183,13 @@ __global__ void __launch_bounds__(kPrepThreads) prep_small_kernel(
     unsigned long long* __restrict__ stats) {
     __shared__ unsigned long long red[kPrepThreads / 32][4];
     const uint32_t tid = threadIdx.x;
-    for (uint64_t w = tid; w < n_zero_words; w += kPrepThreads) {
-        zero_words[w] = 0u;
-        zero_words2[w] = 0u;
+    if (blockIdx.x > 0) { // the other CTAs clear the output planes, kPrepZero words each
+        const uint64_t w0 = (uint64_t)(blockIdx.x - 1) * kPrepZero, w1 = min(n_zero_words, w0 + kPrepZero);
+        for (uint64_t w = w0 + tid; w < w1; w += kPrepThreads) {
+            zero_words[w] = 0u;
+            zero_words2[w] = 0u;
+        }
+        return;
     }
     if (tid < 4) stats[tid] = 0ull;
     unsigned long long k[4] = {~0ull, ~0ull, ~0ull, ~0ull};
@@ -337,7 +343,7 @@ cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st, int dev, uint64_t* l
     EdgeRec* rec = reinterpret_cast<EdgeRec*>(a.rec);
     if (a.n_verts <= kPrepSmall) {
 #define PC_PREP_SMALL(M)                                                                                        \
-    prep_small_kernel<M><<<1, kPrepThreads, 0, st>>>(a.vx, a.vy, a.ring_off, a.n_rings, a.n_verts, a.filt, a.qk, \
+    prep_small_kernel<M><<<(unsigned)(1 + (a.n_zero_words + kPrepZero - 1) / kPrepZero), kPrepThreads, 0, st>>>(a.vx, a.vy, a.ring_off, a.n_rings, a.n_verts, a.filt, a.qk, \
                                                      nqk, rec, a.bbox_keys, a.tol, a.zero_words, a.zero_words2,  \
                                                      a.n_zero_words, a.stats)
         switch (a.mode) {

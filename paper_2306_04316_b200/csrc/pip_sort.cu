@@ -19,8 +19,10 @@
 // index would pull a 128-byte line per 16-byte point).
 //   rk_key_kernel      keys + per-tile digit counts (pass 1's re-counted over
 //                      the pass-0 output by rk_count_hi_kernel)
-//   rk_scan_kernel     per (digit, tile) offsets: a warp per digit scans its
-//                      tiles, then one warp scans the 256 digit totals
+//   rk_colscan_kernel  per (digit, tile) offsets: a warp per digit scans its
+//                      tiles, then one warp scans the 256 digit totals (two
+//                      passes); one pass (<= 4M points) uses a decoupled
+//                      look-back inside the scatter instead
 //   rk_scatter_kernel  per tile: rank in shared memory (atomics on the tile's
 //                      digit histogram), staged by digit, written out in
 //                      contiguous runs per digit
@@ -74,7 +76,8 @@ __global__ void __launch_bounds__(kRkThreads) rk_key_kernel(const double2* __res
                                                             const unsigned long long* __restrict__ bbox_keys,
                                                             int prefilter, uint16_t* __restrict__ keys,
                                                             uint32_t* __restrict__ cnt, uint32_t n_tiles,
-                                                            unsigned int* __restrict__ ticket) {
+                                                            unsigned int* __restrict__ ticket,
+                                                            uint32_t* __restrict__ tot1, uint32_t* __restrict__ status) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *ticket = 0u; // the colscan's completion counter
     __shared__ uint32_t h[2][256];
     for (int j = threadIdx.x; j < 512; j += blockDim.x) (&h[0][0])[j] = 0;
@@ -89,6 +92,13 @@ __global__ void __launch_bounds__(kRkThreads) rk_key_kernel(const double2* __res
         atomicAdd(&h[1][k >> 8], 1u);
     }
     __syncthreads();
+    if (tot1) { // one pass with a look-back scan: high-digit totals, this tile's status row cleared
+        for (int d = threadIdx.x; d < 256; d += blockDim.x) {
+            if (h[1][d]) atomicAdd(&tot1[d], h[1][d]);
+            status[(uint64_t)blockIdx.x * 256 + d] = 0u;
+        }
+        return;
+    }
     for (int j = threadIdx.x; j < 512; j += blockDim.x) {
         const int pass = j >> 8, d = j & 255;
         cnt[(uint64_t)pass * 256 * n_tiles + (uint64_t)d * n_tiles + blockIdx.x] = h[pass][d];
@@ -187,7 +197,13 @@ struct RkShared {
 // any order (pip_single.cu) -- so this is all the scan kernel needs.
 // PASS 0: idx = element position (implicit), writes keys_out and idx_out;
 // PASS 1: writes idx_out only.
-template <int PASS, bool IMPLICIT = PASS == 0>
+// LOOKBACK (one pass on the high digit, n <= kRkOnePassMax): instead of the
+// column scan's offsets, the digit bases come from the totals rk_key_kernel
+// accumulated and each tile's offsets from a decoupled look-back over the
+// earlier tiles' published per-digit counts (status word: 1 << 30 | own count
+// once counted, 2 << 30 | inclusive prefix once known); CTAs start in tile
+// order, so a tile only ever waits on tiles already running.
+template <int PASS, bool IMPLICIT = PASS == 0, bool LOOKBACK = false>
 __global__ void __launch_bounds__(kRkThreads, 2) rk_scatter_kernel(uint64_t n, const uint16_t* __restrict__ keys_in,
                                                                 const double2* __restrict__ pts_in,
                                                                 double2* __restrict__ pts_out,
@@ -195,7 +211,10 @@ __global__ void __launch_bounds__(kRkThreads, 2) rk_scatter_kernel(uint64_t n, c
                                                                 const uint32_t* __restrict__ cnt,
                                                                 const uint32_t* __restrict__ base, uint32_t n_tiles,
                                                                 uint16_t* __restrict__ keys_out,
-                                                                uint32_t* __restrict__ idx_out) {
+                                                                uint32_t* __restrict__ idx_out,
+                                                                const uint32_t* __restrict__ tot1 = nullptr,
+                                                                uint32_t* status = nullptr,
+                                                                uint32_t* __restrict__ n_in = nullptr) {
     extern __shared__ __align__(16) unsigned char rk_smem[];
     RkShared& S = *reinterpret_cast<RkShared*>(rk_smem);
     const int tid = threadIdx.x;
@@ -214,9 +233,34 @@ __global__ void __launch_bounds__(kRkThreads, 2) rk_scatter_kernel(uint64_t n, c
         if constexpr (!IMPLICIT) idx[j] = live ? idx_in[t0 + e] : 0u;
         pt[j] = live ? pts_in[t0 + e] : make_double2(0.0, 0.0);
     }
-    for (int d = tid; d < 256; d += kRkThreads) {
-        S.hist[d] = 0;
-        S.gbase[d] = base[PASS * 256 + d] + cnt[(uint64_t)PASS * 256 * n_tiles + (uint64_t)d * n_tiles + blockIdx.x];
+    if constexpr (LOOKBACK) {
+        if (tid < 256) S.hist[tid] = 0;
+        if (tid < 32) { // digit bases: exclusive scan of the totals (8 per lane)
+            uint32_t v[8], sum = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                v[q] = tot1[tid * 8 + q];
+                sum += v[q];
+            }
+            uint32_t incl = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (tid >= o) incl += y;
+            }
+            uint32_t run = incl - sum;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                S.gbase[tid * 8 + q] = run;
+                run += v[q];
+            }
+            if (blockIdx.x == 0 && tid == 31 && n_in) *n_in = run - v[7]; // points below high digit 0xff: in the box
+        }
+    } else {
+        for (int d = tid; d < 256; d += kRkThreads) {
+            S.hist[d] = 0;
+            S.gbase[d] = base[PASS * 256 + d] + cnt[(uint64_t)PASS * 256 * n_tiles + (uint64_t)d * n_tiles + blockIdx.x];
+        }
     }
     __syncthreads();
     uint32_t rank[kRkItems];
@@ -224,6 +268,26 @@ __global__ void __launch_bounds__(kRkThreads, 2) rk_scatter_kernel(uint64_t n, c
     for (int j = 0; j < kRkItems; ++j)
         if (key[j] != 0xffffffffu) rank[j] = atomicAdd(&S.hist[(key[j] >> shift) & 0xffu], 1u);
     __syncthreads();
+    if constexpr (LOOKBACK) {
+        if (tid < 256) {
+            volatile uint32_t* st = status;
+            const uint32_t own = S.hist[tid];
+            const uint64_t me = (uint64_t)blockIdx.x * 256 + tid;
+            st[me] = (blockIdx.x == 0 ? 2u << 30 : 1u << 30) | own;
+            uint32_t excl = 0;
+            for (int64_t t = (int64_t)blockIdx.x - 1; t >= 0; --t) {
+                uint32_t v;
+                do {
+                    v = st[(uint64_t)t * 256 + tid];
+                } while ((v >> 30) == 0u);
+                excl += v & 0x3fffffffu;
+                if ((v >> 30) == 2u) break;
+            }
+            if (blockIdx.x > 0) st[me] = (2u << 30) | (excl + own);
+            S.gbase[tid] += excl;
+        }
+        __syncthreads();
+    }
     if (tid < 32) { // exclusive scan of the 256 digit counts by one warp (8 per lane)
         uint32_t v[8], sum = 0;
 #pragma unroll
@@ -302,8 +366,10 @@ uint64_t bucket_tiles(uint64_t n) { return std::max<uint64_t>(1, (n + kRkTile - 
 
 size_t bucket_scratch_bytes(uint64_t n) {
     const uint64_t nt = bucket_tiles(n);
-    // keys, keys1 (u16), idx1 (u32), pts1 (2 x f64), counts (2 x 256 x tiles), totals + bases (2 x 512)
-    return 2 * ((n * 2 + 15) / 16 * 16) + (n * 4 + 15) / 16 * 16 + n * 16 + 2 * 256 * nt * 4 + 4 * 512 * 4 + 80;
+    // keys, keys1 (u16), idx1 (u32), pts1 (2 x f64), counts (2 x 256 x tiles), totals + bases (2 x 512),
+    // look-back totals (256) and status (256 x tiles)
+    return 2 * ((n * 2 + 15) / 16 * 16) + (n * 4 + 15) / 16 * 16 + n * 16 + 2 * 256 * nt * 4 + 4 * 512 * 4 + 80 +
+           256 * 4 + 256 * nt * 4 + 32;
 }
 
 cudaError_t launch_bucket(const BucketArgs& a, cudaStream_t st, int dev, uint64_t* launches) {
@@ -323,25 +389,34 @@ cudaError_t launch_bucket(const BucketArgs& a, cudaStream_t st, int dev, uint64_
     uint32_t* tot = reinterpret_cast<uint32_t*>(take(512 * 4));
     uint32_t* base = reinterpret_cast<uint32_t*>(take(512 * 4));
     unsigned int* ticket = reinterpret_cast<unsigned int*>(take(16));
+    uint32_t* tot1 = reinterpret_cast<uint32_t*>(take(256 * 4));
+    uint32_t* status = reinterpret_cast<uint32_t*>(take(256 * nt * 4));
+    const bool one_pass = n <= kRkOnePassMax;
+    if (one_pass) {
+        const cudaError_t e = cudaMemsetAsync(tot1, 0, 256 * 4, st);
+        if (e != cudaSuccess) return e;
+    }
     rk_key_kernel<<<(unsigned)nt, kRkThreads, 0, st>>>(p, n, a.bbox_keys, a.prefilter, keys, cnt, (uint32_t)nt,
-                                                       ticket);
+                                                       ticket, one_pass ? tot1 : nullptr, status);
     static bool attr[64] = {};
     if (dev >= 0 && dev < 64 && !attr[dev]) {
         cudaFuncSetAttribute(rk_scatter_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RkShared));
         cudaFuncSetAttribute(rk_scatter_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RkShared));
         cudaFuncSetAttribute(rk_scatter_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(RkShared));
+        cudaFuncSetAttribute(rk_scatter_kernel<1, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(RkShared));
         attr[dev] = true;
     }
     const size_t sm = sizeof(RkShared);
-    if (n <= kRkOnePassMax) {
+    if (one_pass) {
         // one pass on the high byte (255 y levels): for up to ~4M points a CTA's
-        // 4096 points span a slab this thin anyway; 3 launches instead of 6
-        rk_colscan_kernel<<<256 / 8, 256, 0, st>>>(cnt, (uint32_t)nt, tot, 256u, 512u, base, a.n_in, ticket);
-        rk_scatter_kernel<1, true><<<(unsigned)nt, kRkThreads, sm, st>>>(
+        // 4096 points span a slab this thin anyway; the tile offsets by look-back,
+        // so the key pass and the scatter are the only launches
+        rk_scatter_kernel<1, true, true><<<(unsigned)nt, kRkThreads, sm, st>>>(
             n, keys, p, reinterpret_cast<double2*>(a.sorted_pts), nullptr, cnt, base, (uint32_t)nt, nullptr,
-            a.sorted_idx);
-        *launches += 3;
+            a.sorted_idx, tot1, status, a.n_in);
+        *launches += 2;
         return cudaGetLastError();
     }
     // pass-0 offsets; both passes' digit totals (order-independent) and bases

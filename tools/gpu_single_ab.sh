@@ -9,6 +9,6 @@ timeout 600 python bench.py --workload $w --steps 5 --warmup 3 --no-cpu-baseline
 python -c "import json;d=json.loads(open('$O/bench_$w.json').read().strip().splitlines()[-1]);print('$w', '%.4g'%d['value'], 'ms/step', round(d['ms_per_step'],4), 'kernel ms', round(d['roofline'].get('kernel_ms_per_step') or 0,4))"
 done
 if [ "${LAUNCHES:-1}" = 1 ]; then
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c4.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-sweep > $O/ncu_launch.log 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c4.csv python bench.py --workload ${LAUNCH_W:-c4} --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-sweep > $O/ncu_launch.log 2>&1
 python tools/launch_summary.py $O/launches_c4.csv 2>/dev/null | head -12
 fi
