@@ -64,6 +64,15 @@ constexpr uint32_t kAllK = kK >= 32 ? 0xffffffffu : (1u << kK) - 1u; // a mask o
 #endif
 constexpr int kQTile = PC_QTILE; // edge key words per shared-memory stage (8 KB; 8 per thread)
 static_assert(kKeyTile % kQTile == 0 || kQTile % kKeyTile == 0, "tiles and the key array's padding");
+#ifndef PC_EPI
+#define PC_EPI 8 // epilogue: original indices requested at a time
+#endif
+#ifndef PC_PRO
+#define PC_PRO 4 // prologue: point loads in flight per thread
+#endif
+#ifndef PC_PRO2
+#define PC_PRO2 16 // prologue, second pass (per-CTA keys): y loads in flight per thread
+#endif
 #ifndef PC_QSTAGES
 #define PC_QSTAGES 2
 #endif
@@ -453,7 +462,7 @@ __global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 :
         {
             PC_DCHECK(!a || cta_base + li < n);
             if (a) p = load_pt(pts + cta_base + li);
-            if ((k & 3) == 3) asm volatile("" ::: "memory"); // at most 4 point loads in flight (registers)
+            if ((k & (PC_PRO - 1)) == PC_PRO - 1) asm volatile("" ::: "memory"); // at most PC_PRO point loads in flight (registers)
         }
         if (a && prefilter) a = p.x >= minx && p.x <= maxx && p.y >= miny && p.y <= maxy; // batch.hpp:39-41
         {
@@ -524,15 +533,21 @@ __global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 :
         cm = ctaqmap_from_range(dkey_inv(sh.cta_ylo), dkey_inv(sh.cta_yhi));
         uint32_t lo = 0xffffu, hi = 0u;
 #pragma unroll
-        for (int k = 0; k < kK; ++k) {
-            const uint32_t li = wloc + k * 32 + lane;
-            const bool a = act >> k & 1u;
-            const uint32_t q = a ? qkey_cta(pts[cta_base + li].y, cm) : 0x7fffu; // inactive: masked by `act`
-            if (k & 1) K.k2[k >> 1] |= (q << 1) << 16;
-            else K.k2[k >> 1] = q << 1;
-            if (a) {
-                lo = min(lo, q);
-                hi = max(hi, q);
+        for (int k0 = 0; k0 < kK; k0 += PC_PRO2) { // the points' y again (L1 / L2), PC_PRO2 loads in flight
+            double y[PC_PRO2];
+#pragma unroll
+            for (int k = 0; k < PC_PRO2; ++k)
+                y[k] = (act >> (k0 + k) & 1u) ? pts[cta_base + wloc + (k0 + k) * 32 + lane].y : 0.0;
+#pragma unroll
+            for (int k = k0; k < k0 + PC_PRO2; ++k) {
+                const bool a = act >> k & 1u;
+                const uint32_t q = a ? qkey_cta(y[k - k0], cm) : 0x7fffu; // inactive: masked by `act`
+                if (k & 1) K.k2[k >> 1] |= (q << 1) << 16;
+                else K.k2[k >> 1] = q << 1;
+                if (a) {
+                    lo = min(lo, q);
+                    hi = max(hi, q);
+                }
             }
         }
         wkey_lo = __reduce_min_sync(0xffffffffu, lo);
@@ -688,14 +703,19 @@ __global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 :
     // ---- flags ----
     if (orig) {
         // y-ordered input: each set bit goes to its point's original position
-        // (XOR: partial parities of the edge chunks combine; OR: aux)
+        // (XOR: partial parities of the edge chunks combine; OR: aux); the
+        // original indices are requested PC_EPI at a time before their atomics
+        const uint32_t setm = (par | auxm) & act;
 #pragma unroll
-        for (int k = 0; k < kK; ++k) {
-            const uint32_t pb = (par & act) >> k & 1u, ab = (auxm & act) >> k & 1u;
-            if (pb | ab) {
-                const uint32_t o = orig[cta_base + wloc + k * 32 + lane];
-                if (pb) atomicXor(&inside_bits[o >> 5], 1u << (o & 31));
-                if (ab) atomicOr(&aux_bits[o >> 5], 1u << (o & 31));
+        for (int k0 = 0; k0 < kK; k0 += PC_EPI) {
+            uint32_t o[PC_EPI];
+#pragma unroll
+            for (int k = 0; k < PC_EPI; ++k)
+                o[k] = (setm >> (k0 + k) & 1u) ? orig[cta_base + wloc + (k0 + k) * 32 + lane] : 0u;
+#pragma unroll
+            for (int k = 0; k < PC_EPI; ++k) {
+                if ((par & act) >> (k0 + k) & 1u) atomicXor(&inside_bits[o[k] >> 5], 1u << (o[k] & 31));
+                if ((auxm & act) >> (k0 + k) & 1u) atomicOr(&aux_bits[o[k] >> 5], 1u << (o[k] & 31));
             }
         }
     } else {
