@@ -110,8 +110,12 @@ __device__ __forceinline__ CtaQMap ctaqmap_from_range(double y_lo, double y_hi) 
     CtaQMap m;
     m.y0 = q_collapse(y_lo);
     m.y1 = q_collapse(y_hi);
+    // the scale in binary32 (no binary64 division in the C1 kernels, rule P1's
+    // SASS check): any non-negative scale gives a monotone map, and qkey_cta
+    // clamps an overshoot; one y level or an extreme range: every point key is 1
     const double h = __dsub_rn(m.y1, m.y0);
-    m.scale = (h > 0.0 && h < 1e300) ? __ddiv_rn(32764.0, h) : 0.0; // one y level: every point key is 1
+    const float hf = __double2float_rn(h);
+    m.scale = (h > 0.0 && hf >= 0x1p-100f && hf <= 0x1p100f) ? (double)__fdiv_rn(32764.0f, hf) : 0.0;
     return m;
 }
 
