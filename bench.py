@@ -431,6 +431,13 @@ def roofline(args, eng, items, per_item_ms, tot_ms):
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650 GB/s",
                 "algorithmic_bytes_per_launch": bytes_launch, "kernel": "pip_csr_tile_kernel"}
+        if ent and ent.get("inst_per_launch"):  # what the kernel actually saturates
+            issue_peak = 4.0 * sms * clk_mhz * 1e6
+            ach_i = float(ent["inst_per_launch"]) / (per_item_ms.mean() / 1e3)
+            roof["issue"] = {"achieved": ach_i, "peak": issue_peak, "unit": "warp-inst/s", "frac": ach_i / issue_peak,
+                             "inst_per_launch": float(ent["inst_per_launch"]), "ipc": ent.get("ipc"),
+                             "inst_source": ent["source"],
+                             "peak_source": f"4 warp-inst/cycle/SM x {sms} SMs x {clk_mhz:.0f} MHz"}
     else:
         issue_peak = 4.0 * sms * clk_mhz * 1e6
         roof = {"bound": "issue", "unit": "warp-inst/s", "peak": issue_peak,

@@ -47,8 +47,18 @@ def stall_summary(rep):
         return {}
     h = rows[1]
     cols = [i for i, n in enumerate(h) if n.startswith("stall_") and "Not Issued" not in n]
-    tot = sum(float(r[h.index("Warp Stall Sampling (All Samples)")] or 0) for r in rows[2:]) or 1.0
-    return {h[i][6:]: round(100 * sum(float(r[i] or 0) for r in rows[2:]) / tot, 1) for i in cols}
+    ia = h.index("Warp Stall Sampling (All Samples)")
+
+    def num(x):
+        try:
+            return float(x or 0)
+        except ValueError:
+            return 0.0
+
+    # a report with several kernels repeats the function / header rows: sum the numeric ones
+    data = [r for r in rows[2:] if len(r) == len(h) and r[ia] != h[ia]]
+    tot = sum(num(r[ia]) for r in data) or 1.0
+    return {h[i][6:]: round(100 * sum(num(r[i]) for r in data) / tot, 1) for i in cols}
 
 
 def main():
