@@ -45,6 +45,32 @@ __device__ __forceinline__ void fast_toggle(uint32_t& fpar, uint32_t bit, unsign
         : "r"(bit), "f"(s), "r"(d1), "r"(rng1), "f"(-kFastBand));
 }
 
+// Packed binary32 pairs (sm_100 FFMA2): each half is an IEEE fma.rn of its own,
+// bit-identical to a scalar fmaf on that half.  A broadcast operand (f, f) is
+// folded by ptxas into FFMA2's scalar-operand form (no register pair needed).
+__device__ __forceinline__ unsigned long long f32x2(float lo, float hi) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b, unsigned long long c) {
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+// (a.lo, a.hi) * (f, f) + (g, g)
+__device__ __forceinline__ unsigned long long ffma2_bb(unsigned long long a, float f, float g) {
+    return ffma2(a, f32x2(f, f), f32x2(g, g));
+}
+// (a.lo, a.hi) * (f, f) + c
+__device__ __forceinline__ unsigned long long ffma2_b(unsigned long long a, float f, unsigned long long c) {
+    return ffma2(a, f32x2(f, f), c);
+}
+// the high 16 bits of both halves in one word (sign bits at 15 / 31)
+__device__ __forceinline__ uint32_t hi16x2(unsigned long long s) {
+    return __byte_perm((uint32_t)s, (uint32_t)(s >> 32), 0x7632);
+}
+
 __device__ __forceinline__ double pow2_below_inv(double w) { // 2^-(E+1) for w in [2^E, 2^(E+1))
     const int e = (__double2hiint(w) >> 20) & 0x7ff;
     return __hiloint2double((2045 - e) << 20, 0);

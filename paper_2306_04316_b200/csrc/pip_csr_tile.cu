@@ -43,7 +43,13 @@ namespace {
 
 constexpr int kBThreads = 128;
 constexpr int kBWarps = kBThreads / 32;
-constexpr int kWV = 96; // vertex budget of one batch (per warp)
+#ifndef PC_CSR_WV
+#define PC_CSR_WV 96
+#endif
+#ifndef PC_CSR_MINB
+#define PC_CSR_MINB 7
+#endif
+constexpr int kWV = PC_CSR_WV; // vertex budget of one batch (per warp)
 
 struct BPoly {
     double bx0, by0, bx1, by1; // exact closed bbox of the outer ring
@@ -149,33 +155,25 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
         uint32_t acc = 0u, tm = 0xffffffffu, bm = 0xffffffffu;
         const uint32_t dfirst = Q - (uint32_t)ws.rec[e0].x;
         uint32_t dprev = dfirst, pprev = 0u;
-        auto step2 = [&](uint32_t i, uint32_t j) { // records i, j (consecutive, or clamped repeats)
-            const int4 fi = ws.rec[i], fj = ws.rec[j];
+        // both points' local coordinates as packed pairs: one FFMA2 per term and
+        // record serves the two points (each half an IEEE fmaf: the same values)
+        const unsigned long long LX = f32x2(lx[0], lx[1]), LY = f32x2(ly[0], ly[1]);
+        // every stored vertex of the polygon (a ring's last vertex carries the
+        // no-toggle sentinel record) -- except a closed single ring's last vertex,
+        // which repeats the first: its edge closes with d(first) below.  Two
+        // records per iteration; an odd count re-reads the last record as the
+        // second (d ^ d = 0: no toggle, the same tie / band values).
+        const uint32_t stop = e0 + (tp.nloop & 0x3fffffffu), last = stop - 1u;
+        for (uint32_t i = e0; i < stop; i += 2) {
+            const int4 fi = ws.rec[i], fj = ws.rec[min(i + 1u, last)];
             const uint32_t di = Q - (uint32_t)fi.x, dj = Q - (uint32_t)fj.x;
-            const uint32_t pi = __byte_perm(__float_as_uint(fmaf(lx[0], __int_as_float(fi.y), fmaf(ly[0], __int_as_float(fi.z), __int_as_float(fi.w)))),
-                                            __float_as_uint(fmaf(lx[1], __int_as_float(fi.y), fmaf(ly[1], __int_as_float(fi.z), __int_as_float(fi.w)))), 0x7632);
-            const uint32_t pj = __byte_perm(__float_as_uint(fmaf(lx[0], __int_as_float(fj.y), fmaf(ly[0], __int_as_float(fj.z), __int_as_float(fj.w)))),
-                                            __float_as_uint(fmaf(lx[1], __int_as_float(fj.y), fmaf(ly[1], __int_as_float(fj.z), __int_as_float(fj.w)))), 0x7632);
+            const uint32_t pi = hi16x2(ffma2_b(LX, __int_as_float(fi.y), ffma2_bb(LY, __int_as_float(fi.z), __int_as_float(fi.w))));
+            const uint32_t pj = hi16x2(ffma2_b(LX, __int_as_float(fj.y), ffma2_bb(LY, __int_as_float(fj.z), __int_as_float(fj.w))));
             acc ^= ((dprev ^ di) & pprev) ^ ((di ^ dj) & pi);
             tm = __vimin3_u16x2(tm, di, dj);
             bm = __vimin3_u16x2(bm, pi, pj);
             dprev = dj;
             pprev = pj;
-        };
-        // every stored vertex of the polygon (a ring's last vertex carries the
-        // no-toggle sentinel record) -- except a closed single ring's last vertex,
-        // which repeats the first: its edge closes with d(first) below; reads past
-        // the end re-read the last record (d ^ d = 0: no toggle, the same tie /
-        // band values)
-        const uint32_t stop = e0 + (tp.nloop & 0x3fffffffu), last = stop - 1u;
-        uint32_t i = e0;
-        for (; i + 4 <= stop; i += 4) {
-            step2(i, i + 1);
-            step2(i + 2, i + 3);
-        }
-        if (i < stop) {
-            step2(i, min(i + 1, last));
-            step2(min(i + 2, last), min(i + 3, last));
         }
         acc ^= (dprev ^ dfirst) & pprev; // the closing edge (a sentinel's pprev is +: no toggle)
         const uint32_t fpar = (acc >> 15 & 1u) | (acc >> 30 & 2u);
@@ -190,12 +188,13 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
         // sign bit of x & ~y & s' toggles the parity; +0 <= s' <= 2B is a band hit
         int acc0 = 0, acc1 = 0;
         uint32_t t0 = 0xffffffffu, t1 = 0xffffffffu, u0 = 0xffffffffu, u1 = 0xffffffffu;
+        const unsigned long long LX = f32x2(lx[0], lx[1]), LY = f32x2(ly[0], ly[1]);
         auto rec = [&](uint32_t i) {
             const int4 f = ws.rec[i];
-            const float2 g = make_float2(__int_as_float(ws.rec2[i].x), __int_as_float(ws.rec2[i].y));
-            const float nxf = __int_as_float(f.w);
-            const float s0 = fmaf(lx[0], nxf, fmaf(ly[0], g.x, g.y));
-            const float s1 = fmaf(lx[1], nxf, fmaf(ly[1], g.x, g.y));
+            const int2 g = ws.rec2[i];
+            // both points in one FFMA2 per term (each half an IEEE fmaf)
+            const unsigned long long s = ffma2_b(LX, __int_as_float(f.w), ffma2_bb(LY, __int_as_float(g.x), __int_as_float(g.y)));
+            const float s0 = __uint_as_float((uint32_t)s), s1 = __uint_as_float((uint32_t)(s >> 32));
             acc0 ^= (qp[0] - f.y) & ~(qm[0] - f.x) & __float_as_int(s0);
             acc1 ^= (qp[1] - f.y) & ~(qm[1] - f.x) & __float_as_int(s1);
             u0 = min(u0, __float_as_uint(s0)); // band hits
@@ -331,7 +330,7 @@ __device__ __forceinline__ int classify_item(const WarpSmem& ws, int j, uint32_t
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kBThreads, 7) pip_csr_tile_kernel(
+__global__ void __launch_bounds__(kBThreads, PC_CSR_MINB) pip_csr_tile_kernel(
     const double2* __restrict__ pts, const unsigned long long* __restrict__ pt_off, unsigned long long n_polys,
     const double* __restrict__ vx, const double* __restrict__ vy, const unsigned long long* __restrict__ ring_off,
     const unsigned long long* __restrict__ poly_ring_off, unsigned long long pt_base, unsigned long long ring_base,
