@@ -76,9 +76,12 @@ __global__ void __launch_bounds__(256) prep_bbox_kernel(const double* __restrict
 
 // One thread per vertex v: if (v, v+1) is an edge of the same ring, write its
 // filter word, key word and exact record at edge index e = v - ring(v).
-//   key word (all modes): {0x7fff - q(ylo), q(yhi)} on the 15-bit map (the
-//          phase-1 key scan of pip_single.cu); padding words (edges >= n_edges
-//          up to qk_words) are 0, which never matches (q(ylo) would be 0x7fff)
+//   key halves (all modes), on the 15-bit map, for the phase-1 key scan of
+//          pip_single.cu: per group of 8 edges, 8 words = 16 halves: half j is
+//          q(ylo) of edge j, half 8 + j is 0x7fff - q(yhi) of edge j (word 2i
+//          / 2i+1 thus pairs edges 2i, 2i+1 in its low / high half, so one
+//          packed add-max tests two edges); padding edges (>= n_edges up to
+//          qk_words) have both halves 0x7fff, which never matches (keys <= 0x7ffe)
 //   filter word C1/C2: {(-q(ylo) mod 2^15) << 1 in both 16-bit halves,
 //          ((q(yhi) - q(ylo)) << 1) + 2 in both halves} (15-bit keys)
 //   filter word Robust: {fkey(ylo), fkey(yhi)} (32-bit keys)
@@ -96,7 +99,11 @@ __device__ __forceinline__ void prep_edges_body(
         reinterpret_cast<double*>(bbox_keys)[6] = lm.sx;
         reinterpret_cast<double*>(bbox_keys)[7] = lm.sy;
     }
-    for (uint64_t e = n_verts - n_rings + tid; e < n_qk; e += stride) qk[e] = 0u;
+    uint16_t* const qh = reinterpret_cast<uint16_t*>(qk);
+    for (uint64_t e = n_verts - n_rings + tid; e < n_qk; e += stride) {
+        qh[qk_half(e)] = 0x7fffu;
+        qh[qk_half(e) + 8] = 0x7fffu;
+    }
     for (uint64_t v = tid; v < n_verts; v += stride) {
         const uint32_t r = ring_of(ring_off, n_rings, v);
         if (v + 1 >= ring_off[r + 1]) continue; // last (closing) vertex of its ring
@@ -153,7 +160,8 @@ __device__ __forceinline__ void prep_edges_body(
             const uint32_t thr1 = ((khi - klo) << 1) + 2u;
             filt[e] = make_uint2(neg | (neg << 16), thr1 | (thr1 << 16));
         }
-        qk[e] = (0x7fffu - qkey15(ylo, qm)) | (qkey15(yhi, qm) << 16);
+        qh[qk_half(e)] = (uint16_t)qkey15(ylo, qm);
+        qh[qk_half(e) + 8] = (uint16_t)(0x7fffu - qkey15(yhi, qm));
         rec[e] = er;
     }
 }

@@ -63,6 +63,9 @@ size_t edge_rec_bytes();
 constexpr int kKeyTile = 2048;       // edge key words per stage of pip_single.cu's key scan
 size_t filt_words(uint64_t n_edges); // uint2 entries of the filter array
 size_t qk_words(uint64_t n_edges);   // uint32 entries of the key array (whole tiles, padding never matches)
+// position of edge e's q(ylo) half in the key array (its 0x7fff - q(yhi) half is 8 further):
+// groups of 8 edges, 16 halves each (pip_kernels.cu prep_edges_body)
+__host__ __device__ __forceinline__ uint64_t qk_half(uint64_t e) { return (e >> 3) * 16 + (e & 7); }
 size_t csr_meta_bytes(uint64_t n_polys);
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st, int dev, uint64_t* launches);
 cudaError_t launch_single(const SingleArgs& a, cudaStream_t st, int dev, uint64_t* launches);

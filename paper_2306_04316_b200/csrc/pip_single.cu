@@ -82,7 +82,7 @@ static_assert(kListCap >= kQTile, "the list must hold one tile's candidates");
 constexpr int kBatch = PC_BATCH;     // candidates gathered per batch (two threads each)
 static_assert(kBatch <= PC_TPB / 2, "the gather uses two threads per candidate");
 constexpr int kEPT = kQTile / kTPB; // phase 1: key words per thread per tile
-static_assert(kEPT == 16 || kEPT == 8 || kEPT == 4, "phase 1 reads 1, 2 or 4 uint4 per thread");
+static_assert(kEPT == 16 || kEPT == 8, "phase 1: whole groups of 8 edges (8 key words) per thread");
 
 // Every mode keeps only the polygon-local fp32 coordinates of its points in
 // shared memory (the certified fp32 side / intercept test); the binary64
@@ -108,19 +108,19 @@ __device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count)
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
 }
 
-__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+__device__ __forceinline__ void mbar_wait_at(unsigned bar, unsigned parity) { // bar: shared-window address
     unsigned done = 0;
     while (!done) {
         asm volatile(
             "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
             : "=r"(done)
-            : "r"(smem_u32(b)), "r"(parity)
+            : "r"(bar), "r"(parity)
             : "memory");
     }
 }
 
 // One elected thread: load key words [t0, t0 + nw) into stage s (nw <= kQTile,
-// a multiple of 4: 16-byte bulk copies; the key array is padded with
+// a multiple of 8: whole key groups, 16-byte bulk copies; the key array is padded with
 // never-candidate words to whole tiles, so nw may run past the chunk's end).
 // The key array is re-read by every CTA: keep it in L2 (evict_last), while the
 // point loads stream past it (evict_first, see load_pt).
@@ -145,13 +145,15 @@ __device__ __forceinline__ double2 load_pt(const double2* p) {
     return v;
 }
 
-// Phase-1 test of one key word w = {0x7fff - q(ylo), q(yhi)} against the CTA
-// constant kc = {cta_hi + 1, 0x8000 - cta_lo}: each 16-bit half of w + kc
-// stays below 2^16 (keys <= 32767), and its top bit is set iff
-// q(ylo) <= cta_hi (low half) / q(yhi) >= cta_lo (high half).
-__device__ __forceinline__ uint32_t key_hit(uint32_t w, uint32_t kc) {
-    const uint32_t d = w + kc;
-    return (d & (d << 16)) >> 31;
+// Phase-1 test of two edges at once.  A = {q(ylo) of edge 2i, of edge 2i+1}
+// and B = {0x7fff - q(yhi), ...} (the key array's layout, prep_edges_body);
+// with the CTA constants KA = 0x7fff - cta_hi and KB = cta_lo in both halves,
+// per half u = q(ylo) + KA and v = (0x7fff - q(yhi)) + KB stay below 2^16
+// (keys <= 0x7ffe), u <= 0x7fff iff q(ylo) <= cta_hi and v <= 0x7fff iff
+// q(yhi) >= cta_lo.  So the top bit of max(u, v) -- one VIADDMNMX.U16x2 after
+// the add of B -- is clear iff the edge's key range meets the CTA's.
+__device__ __forceinline__ uint32_t key_pair(uint32_t a, uint32_t b, uint32_t ka, uint32_t kb) {
+    return __viaddmax_u16x2(a, ka, b + kb);
 }
 
 // A lane's binary64 points for the exact fallbacks: point k of the lane is g[k * 32].
@@ -553,11 +555,11 @@ __global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 :
         wkey_lo = __reduce_min_sync(0xffffffffu, lo);
         wkey_hi = __reduce_max_sync(0xffffffffu, hi);
     }
-    const uint32_t kc = (sh.cta_hi + 1u) | ((0x8000u - sh.cta_lo) << 16);
+    const uint32_t ka = (0x7fffu - sh.cta_hi) * 0x10001u, kb = sh.cta_lo * 0x10001u; // key_pair constants
 
     const uint32_t t_begin = e_begin, n_tiles = (e_end - e_begin + kQTile - 1) / kQTile;
-    // words of tile q: whole tiles, the chunk's last one rounded up to 4 words
-    auto tile_words = [&](uint32_t q) { return min((uint32_t)kQTile, (e_end - (t_begin + q * kQTile) + 3u) & ~3u); };
+    // words of tile q: whole tiles, the chunk's last one rounded up to a group of 8
+    auto tile_words = [&](uint32_t q) { return min((uint32_t)kQTile, (e_end - (t_begin + q * kQTile) + 7u) & ~7u); };
     if (tid == 0) {
         for (uint32_t q = 0; q < (uint32_t)kStages && q < n_tiles; ++q)
             issue_tile(sh, (int)q, qk, t_begin + q * kQTile, tile_words(q));
@@ -649,10 +651,12 @@ __global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 :
     // this thread's kEPT key words in stage 0 (a shared address kept in a register)
     unsigned qk_s = smem_u32(&sh.qk[0][(kEPT / 4) * tid]);
     asm volatile("" : "+r"(qk_s));
+    const unsigned bar0 = smem_u32(&sh.full[0]); // stage s's mbarrier: bar0 + 8 s
+    asm volatile("" : "+r"(bar0));
     for (uint32_t q = 0; q < n_tiles; ++q) {
         const int s = (int)(q % kStages);
         const uint32_t t0 = t_begin + q * kQTile;
-        mbar_wait(&sh.full[s], (q / kStages) & 1);
+        mbar_wait_at(bar0 + 8u * (unsigned)s, (q / kStages) & 1);
         PC_DCHECK(t0 >= e_begin && t0 < e_end);
         uint32_t d[kEPT];
         {
@@ -663,20 +667,29 @@ __global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 :
                              : "=r"(d[4 * j]), "=r"(d[4 * j + 1]), "=r"(d[4 * j + 2]), "=r"(d[4 * j + 3])
                              : "r"(a + 16u * j));
         }
-        // d + kc has the top bit of both halves set iff the edge may meet a point
-        // (key_hit); the common no-candidate case costs one add and one LOP3 +
-        // shift per edge, the exact mask is formed only when some edge hits
-        uint32_t acc = 0;
+        // per group of 8 edges: words 0..3 the q(ylo) pairs, 4..7 the
+        // 0x7fff - q(yhi) pairs; t has a half with its top bit clear iff that
+        // edge may meet a point (key_pair): 1.25 instructions per edge on the
+        // common no-candidate path, the exact mask only when some edge hits
+        uint32_t t[kEPT / 2];
 #pragma unroll
-        for (int i = 0; i < kEPT; ++i) {
-            d[i] += kc;
-            acc |= d[i] & (d[i] << 16);
-        }
-        const bool mine = (int)acc < 0;
+        for (int g = 0; g < kEPT / 8; ++g)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) t[4 * g + i] = key_pair(d[8 * g + i], d[8 * g + 4 + i], ka, kb);
+        uint32_t mn = __vimin3_u16x2(t[0], t[1], t[2]);
+#pragma unroll
+        for (int i = 3; i < kEPT / 2; i += 2) mn = __vimin3_u16x2(mn, t[i], t[min(i + 1, kEPT / 2 - 1)]);
+        const bool mine = (mn & 0x80008000u) != 0x80008000u;
         if (mine) { // rare: append this thread's candidates (edges past e_end are padding or the next chunk's)
             uint32_t m = 0;
 #pragma unroll
-            for (int i = 0; i < kEPT; ++i) m |= ((d[i] & (d[i] << 16)) >> 31) << i;
+            for (int g = 0; g < kEPT / 8; ++g)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const uint32_t nt = ~t[4 * g + i];
+                    m |= ((nt >> 15) & 1u) << (8 * g + 2 * i);
+                    m |= (nt >> 31) << (8 * g + 2 * i + 1);
+                }
             const uint32_t e0 = t0 + (uint32_t)kEPT * (uint32_t)tid;
             if (e0 + kEPT > e_end) m &= e0 >= e_end ? 0u : (1u << (e_end - e0)) - 1u;
             uint32_t pos = atomicAdd(&sh.ncand, (uint32_t)__popc(m));
