@@ -19,7 +19,7 @@
 // index would pull a 128-byte line per 16-byte point).
 //   rk_key_kernel      keys + per-tile digit counts (pass 1's re-counted over
 //                      the pass-0 output by rk_count_hi_kernel)
-//   rk_colscan_kernel  per (digit, tile) offsets: a warp per digit scans its
+//   rk_colscan_kernel  per (digit, tile) offsets: a CTA per digit scans its
 //                      tiles, then one warp scans the 256 digit totals (two
 //                      passes); one pass (<= 4M points) uses a decoupled
 //                      look-back inside the scatter instead
@@ -70,8 +70,8 @@ __device__ __forceinline__ KeyMap make_keymap(const unsigned long long* bbox_key
     return m;
 }
 
-// keys[i] for tile blockIdx.x; digit counts of both passes, digit-major:
-// cnt[pass][digit * n_tiles + tile]
+// keys[i] for tile blockIdx.x; pass-0 digit counts, digit-major:
+// cnt[0][digit * n_tiles + tile] (one pass: the high-digit totals instead)
 __global__ void __launch_bounds__(kRkThreads) rk_key_kernel(const double2* __restrict__ pts, uint64_t n,
                                                             const unsigned long long* __restrict__ bbox_keys,
                                                             int prefilter, uint16_t* __restrict__ keys,
@@ -88,8 +88,8 @@ __global__ void __launch_bounds__(kRkThreads) rk_key_kernel(const double2* __res
         const double2 p = pts[i];
         const uint32_t k = m.key(p.x, p.y);
         keys[i] = (uint16_t)k;
-        atomicAdd(&h[0][k & 0xff], 1u);
-        atomicAdd(&h[1][k >> 8], 1u);
+        if (tot1) atomicAdd(&h[1][k >> 8], 1u); // one pass: the high digit only
+        else atomicAdd(&h[0][k & 0xff], 1u);    // two passes: pass 1 is recounted over the pass-0 output
     }
     __syncthreads();
     if (tot1) { // one pass with a look-back scan: high-digit totals, this tile's status row cleared
@@ -99,10 +99,7 @@ __global__ void __launch_bounds__(kRkThreads) rk_key_kernel(const double2* __res
         }
         return;
     }
-    for (int j = threadIdx.x; j < 512; j += blockDim.x) {
-        const int pass = j >> 8, d = j & 255;
-        cnt[(uint64_t)pass * 256 * n_tiles + (uint64_t)d * n_tiles + blockIdx.x] = h[pass][d];
-    }
+    for (int d = threadIdx.x; d < 256; d += blockDim.x) cnt[(uint64_t)d * n_tiles + blockIdx.x] = h[0][d];
 }
 
 // Pass-1 digit counts per tile of the pass-0 OUTPUT order (an LSD pass ranks
@@ -140,43 +137,66 @@ __device__ __forceinline__ void rk_digit_bases(const uint32_t* tot, uint32_t* ba
     }
 }
 
-// One warp per (pass, digit) in [first, last): exclusive prefix over the tiles
-// (in place) and the digit total; the last CTA to finish (ticket) then forms
-// the digit bases of the passes it covered and resets the ticket.
-__global__ void __launch_bounds__(256) rk_colscan_kernel(uint32_t* __restrict__ cnt, uint32_t n_tiles,
-                                                         uint32_t* __restrict__ tot, uint32_t first, uint32_t last,
-                                                         uint32_t* __restrict__ base, uint32_t* __restrict__ n_in,
-                                                         unsigned int* __restrict__ ticket) {
-    const uint32_t wid = first + (uint32_t)((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5); // pass * 256 + digit
-    const int lane = threadIdx.x & 31;
-    if (wid < last) {
-        uint32_t* col = cnt + (uint64_t)wid * n_tiles;
-        uint32_t run = 0;
-        for (uint32_t b0 = 0; b0 < n_tiles; b0 += 32) {
-            const uint32_t b = b0 + lane;
-            const uint32_t v = b < n_tiles ? col[b] : 0u;
-            uint32_t incl = v;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
-            }
-            if (b < n_tiles) col[b] = run + incl - v;
-            run += __shfl_sync(0xffffffffu, incl, 31);
-        }
-        if (lane == 0) tot[wid] = run;
-    }
+// One CTA per (pass, digit) column in [first, last): exclusive prefix over the
+// column's tiles (in place) and the digit total, 2048 tiles per round (8
+// consecutive counts per thread, a block scan of the 256 thread sums); the last
+// CTA to finish (ticket) then forms the digit bases of the passes it covered
+// and resets the ticket.
+constexpr int kCsThreads = 256;
+__global__ void __launch_bounds__(kCsThreads) rk_colscan_kernel(uint32_t* __restrict__ cnt, uint32_t n_tiles,
+                                                                uint32_t* __restrict__ tot, uint32_t first,
+                                                                uint32_t last, uint32_t* __restrict__ base,
+                                                                uint32_t* __restrict__ n_in,
+                                                                unsigned int* __restrict__ ticket) {
+    __shared__ uint32_t wsum[kCsThreads / 32];
     __shared__ bool is_last;
+    const uint32_t wid = first + blockIdx.x; // pass * 256 + digit
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint32_t* col = cnt + (uint64_t)wid * n_tiles;
+    uint32_t run = 0;
+    for (uint32_t c0 = 0; c0 < n_tiles; c0 += 8 * kCsThreads) {
+        const uint32_t b = c0 + 8u * (uint32_t)tid;
+        uint32_t v[8], ts = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            v[j] = b + j < n_tiles ? col[b + j] : 0u;
+            ts += v[j];
+        }
+        // block-wide exclusive scan of the thread sums
+        uint32_t incl = ts;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        uint32_t wpre = 0, rtot = 0;
+#pragma unroll
+        for (int w = 0; w < kCsThreads / 32; ++w) {
+            const uint32_t x = wsum[w];
+            wpre += w < warp ? x : 0u;
+            rtot += x;
+        }
+        __syncthreads(); // wsum is rewritten next round
+        uint32_t r = run + wpre + incl - ts;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (b + j < n_tiles) col[b + j] = r;
+            r += v[j];
+        }
+        run += rtot;
+    }
+    if (tid == 0) tot[wid] = run;
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    if (tid == 0) is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
     __syncthreads();
     if (!is_last) return;
     __threadfence();
-    const int w = threadIdx.x >> 5;
     for (uint32_t pass = first / 256; pass < last / 256; ++pass)
-        if (w == (int)(pass - first / 256)) rk_digit_bases(tot + pass * 256, base + pass * 256, pass == 1 ? n_in : nullptr, lane);
-    if (threadIdx.x == 0) *ticket = 0u;
+        if (warp == (int)(pass - first / 256)) rk_digit_bases(tot + pass * 256, base + pass * 256, pass == 1 ? n_in : nullptr, lane);
+    if (tid == 0) *ticket = 0u;
 }
 
 struct RkShared {
@@ -419,12 +439,12 @@ cudaError_t launch_bucket(const BucketArgs& a, cudaStream_t st, int dev, uint64_
         *launches += 2;
         return cudaGetLastError();
     }
-    // pass-0 offsets; both passes' digit totals (order-independent) and bases
-    rk_colscan_kernel<<<512 / 8, 256, 0, st>>>(cnt, (uint32_t)nt, tot, 0u, 512u, base, a.n_in, ticket);
+    // pass-0 offsets, totals and bases (pass 1's come from its recount below)
+    rk_colscan_kernel<<<256, kCsThreads, 0, st>>>(cnt, (uint32_t)nt, tot, 0u, 256u, base, a.n_in, ticket);
     rk_scatter_kernel<0><<<(unsigned)nt, kRkThreads, sm, st>>>(n, keys, p, pts1, nullptr, cnt, base, (uint32_t)nt,
                                                               keys1, idx1);
     rk_count_hi_kernel<<<(unsigned)nt, kRkThreads, 0, st>>>(keys1, n, cnt, (uint32_t)nt);
-    rk_colscan_kernel<<<256 / 8, 256, 0, st>>>(cnt, (uint32_t)nt, tot, 256u, 512u, base, a.n_in, ticket);
+    rk_colscan_kernel<<<256, kCsThreads, 0, st>>>(cnt, (uint32_t)nt, tot, 256u, 512u, base, a.n_in, ticket);
     rk_scatter_kernel<1><<<(unsigned)nt, kRkThreads, sm, st>>>(n, keys1, pts1,
                                                               reinterpret_cast<double2*>(a.sorted_pts), idx1, cnt,
                                                               base, (uint32_t)nt, nullptr, a.sorted_idx);
