@@ -618,8 +618,37 @@ def run_e2e(args, eng, items, world, rank):
     dev = torch.device("cuda", torch.cuda.current_device())
     dt = max_over_ranks(dt, world, dev) / args.steps
     units, _ = job_totals(items, world, dev)
-    return {"value": units / dt, "unit": "tests/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "ms_per_step": dt * 1e3, "api": "pc_classify / pc_classify_csr (host pointers; all input and output buffers pinned)"}
+    out = {"value": units / dt, "unit": "tests/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+           "ms_per_step": dt * 1e3, "api": "pc_classify / pc_classify_csr (host pointers; all input and output buffers pinned)"}
+    out["link"] = link_bound(host, dev, h2d, d2h, dt)
+    return out
+
+
+def link_bound(host, dev, h2d, d2h, dt):
+    """The host link's share of the e2e step: the pinned host->device copy rate
+    measured on this box (the largest input array of the step, copied 3 times
+    into a device buffer, CUDA events on a side stream), the time the step's
+    h2d + d2h bytes need at that rate, and that time / the measured e2e step."""
+    import torch
+    arrs = [a for xy, poly, cs, _ in host for a in ((xy,) if cs is None else (cs.xy,))]
+    src = max(arrs, key=lambda a: a.nbytes)
+    h = torch.from_numpy(src.view(np.uint8).reshape(-1))
+    d = torch.empty(h.numel(), dtype=torch.uint8, device=dev)
+    st = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(st):
+        d.copy_(h, non_blocking=True)  # warm
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(3):
+            d.copy_(h, non_blocking=True)
+        e1.record(st)
+    e1.synchronize()
+    gbs = 3 * h.numel() / (e0.elapsed_time(e1) * 1e-3) / 1e9
+    need_ms = (h2d + d2h) / (gbs * 1e9) * 1e3
+    del d
+    return {"h2d_gbs_measured": gbs, "copy_bytes": int(h.numel()), "achieved_gbs": (h2d + d2h) / dt / 1e9,
+            "link_ms_per_step": need_ms, "frac": need_ms / (dt * 1e3),
+            "note": "pinned torch copy_ of the step's largest input array, 3 reps, CUDA events; frac = (h2d + d2h bytes at that rate) / e2e ms"}
 
 
 def run_cpu_baseline(args, items):

@@ -46,6 +46,12 @@ constexpr int kBWarps = kBThreads / 32;
 #ifndef PC_CSR_WV
 #define PC_CSR_WV 96
 #endif
+#ifndef PC_CSR_WALK_NS
+#define PC_CSR_WALK_NS 16
+#endif
+#ifndef PC_CSR_WALK_ROBUST
+#define PC_CSR_WALK_ROBUST 1
+#endif
 #ifndef PC_CSR_MINB
 #define PC_CSR_MINB 7
 #endif
@@ -564,7 +570,7 @@ __global__ void __launch_bounds__(kBThreads, PC_CSR_MINB) pip_csr_tile_kernel(
                 // mode choice: after an fp32 pass that left >= 1/4 of the points
                 // undecided, walk everything for the next 16 steps, then probe again
                 if (walk_left > 0) --walk_left;
-                else if (ns >= 16) walk_left = 16;
+                else if (ns >= PC_CSR_WALK_NS && (MODE != kRobust || PC_CSR_WALK_ROBUST)) walk_left = 16;
             }
             __syncwarp(); // the next batch rewrites this warp's shared slice
             todo &= ~batch;
