@@ -77,8 +77,14 @@ static_assert(kKeyTile % kQTile == 0 || kQTile % kKeyTile == 0, "tiles and the k
 #define PC_QSTAGES 2
 #endif
 constexpr int kStages = PC_QSTAGES; // key-scan stages in flight
+#ifndef PC_WARPKEYS
+#define PC_WARPKEYS 0 // 1: phase 1 per warp (own bulk-copy stages and mbarriers, no CTA barrier per tile)
+#endif
+constexpr int kWarpsCta = PC_TPB / 32;
+constexpr uint32_t kWT = kQTile / kWarpsCta; // per-warp tile: edge key words per stage (8 per lane)
+static_assert(!PC_WARPKEYS || kWT == 256u, "per-warp tiles of 8 key words per lane");
 constexpr int kListCap = PC_LISTCAP; // candidate edge indices; a tile can add kQTile, so flush above kListCap - kQTile
-static_assert(kListCap >= kQTile, "the list must hold one tile's candidates");
+static_assert(kListCap >= (PC_WARPKEYS ? kQTile / (PC_TPB / 32) : kQTile), "the list must hold one tile's candidates");
 constexpr int kBatch = PC_BATCH;     // candidates gathered per batch (two threads each)
 static_assert(kBatch <= PC_TPB / 2, "the gather uses two threads per candidate");
 constexpr int kEPT = kQTile / kTPB; // phase 1: key words per thread per tile
@@ -93,8 +99,10 @@ struct SingleShared {
     uint32_t list[kListCap];     // candidate edges of the chunk (phase 1 -> phase 2)
     uint2 bfilt[kBatch];         // gathered per-point filter words
     EdgeRec brec[kBatch];        // gathered exact records
-    unsigned long long full[kStages];
+    unsigned long long full[PC_WARPKEYS ? kStages * kWarpsCta : kStages];
     uint32_t ncand;
+    uint32_t valid_end;          // per-warp phase 1: end of the reservations that fit the list
+    uint32_t any_ovf;            // per-warp phase 1: some warp stopped on a full list
     uint32_t cta_lo, cta_hi;     // key range of the CTA's active points
     unsigned long long cta_ylo, cta_yhi; // C1/C2: dkey of their min / max y (per-CTA key map)
     uint32_t live;
@@ -424,9 +432,11 @@ __global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 :
 
     const uint32_t cta_n = (uint32_t)min((uint64_t)(kTPB * kK), n - cta_base);
     if (tid == 0) {
-        for (int k = 0; k < kStages; ++k) mbar_init(&sh.full[k], 1);
+        for (int k = 0; k < (PC_WARPKEYS ? kStages * kWarpsCta : kStages); ++k) mbar_init(&sh.full[k], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         sh.ncand = 0;
+        sh.valid_end = 0;
+        sh.any_ovf = 0;
         sh.cta_lo = 0xffffu;
         sh.cta_hi = 0u;
         sh.cta_ylo = ~0ull;
@@ -560,10 +570,39 @@ __global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 :
     const uint32_t t_begin = e_begin, n_tiles = (e_end - e_begin + kQTile - 1) / kQTile;
     // words of tile q: whole tiles, the chunk's last one rounded up to a group of 8
     auto tile_words = [&](uint32_t q) { return min((uint32_t)kQTile, (e_end - (t_begin + q * kQTile) + 7u) & ~7u); };
+#if PC_WARPKEYS
+    // per-warp key stream: warp w scans warp tiles j = w, w + kWarpsCta, ... (kWT
+    // edges each) through its own kStages 1 KB stages; copy k of the warp uses
+    // stage k % kStages at mbarrier parity (k / kStages) & 1
+    const uint32_t n_wt = (e_end - e_begin + kWT - 1) / kWT;
+    const unsigned wbar0 = smem_u32(&sh.full[warp * kStages]);
+    const unsigned wst0 = smem_u32(&sh.qk[0][0]) + (unsigned)warp * kStages * (kWT * 4u);
+    uint32_t j_issue = (uint32_t)warp, seq_issued = 0; // uniform per warp
+    auto issue_w = [&]() {
+        if (lane == 0) {
+            const uint32_t t0 = e_begin + j_issue * kWT;
+            const unsigned bytes = min(kWT, (e_end - t0 + 7u) & ~7u) * 4u; // whole groups of 8 (padded array)
+            const unsigned st = seq_issued % kStages;
+            const unsigned bar = wbar0 + 8u * st;
+            unsigned long long pol;
+            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+                    wst0 + st * (kWT * 4u)),
+                "l"(qk + t0), "r"(bytes), "r"(bar), "l"(pol)
+                : "memory");
+        }
+        ++seq_issued;
+        j_issue += kWarpsCta;
+    };
+    while (seq_issued < (uint32_t)kStages && j_issue < n_wt) issue_w();
+#else
     if (tid == 0) {
         for (uint32_t q = 0; q < (uint32_t)kStages && q < n_tiles; ++q)
             issue_tile(sh, (int)q, qk, t_begin + q * kQTile, tile_words(q));
     }
+#endif
 
     // may any active point of the warp straddle the edge with filter word f?
     // (exact: the keys are monotone; the per-point filter then decides per point)
@@ -642,11 +681,96 @@ __global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 :
             }
             __syncthreads(); // batch buffers free
         }
-        if (tid == 0) sh.ncand = 0;
+        if (tid == 0) {
+            sh.ncand = 0;
+            sh.valid_end = 0;
+            sh.any_ovf = 0;
+        }
         __syncthreads();
     };
 
     // ---- phase 1: the key scan over the chunk ----
+#if PC_WARPKEYS
+    {
+        uint32_t seq_done = 0, j_cur = (uint32_t)warp; // uniform per warp
+        for (;;) { // rounds: a round ends when every warp finished or stopped on a full list
+            bool stopped = false;
+            while (j_cur < n_wt) {
+                const unsigned st = seq_done % kStages;
+                mbar_wait_at(wbar0 + 8u * st, (seq_done / kStages) & 1u);
+                uint32_t d[8];
+                {
+                    const unsigned a = wst0 + st * (kWT * 4u) + 32u * (unsigned)lane;
+                    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]) : "r"(a));
+                    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]) : "r"(a + 16u));
+                }
+                uint32_t t[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) t[i] = key_pair(d[i], d[4 + i], ka, kb);
+                const uint32_t mn = __vimin3_u16x2(__vimin3_u16x2(t[0], t[1], t[2]), t[3], t[3]);
+                const bool mine = (mn & 0x80008000u) != 0x80008000u;
+                ++seq_done;
+                if (__any_sync(0xffffffffu, mine)) { // rare: reserve the warp's candidates at once
+                    uint32_t m = 0;
+                    if (mine) {
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const uint32_t nt = ~t[i];
+                            m |= ((nt >> 15) & 1u) << (2 * i);
+                            m |= (nt >> 31) << (2 * i + 1);
+                        }
+                    }
+                    const uint32_t e0 = e_begin + j_cur * kWT + 8u * (uint32_t)lane;
+                    if (e0 + 8u > e_end) m &= e0 >= e_end ? 0u : (1u << (e_end - e0)) - 1u;
+                    const uint32_t c = (uint32_t)__popc(m);
+                    uint32_t incl = c;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += y;
+                    }
+                    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+                    uint32_t base = 0;
+                    if (lane == 0 && total) base = atomicAdd(&sh.ncand, total);
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    if (base + total <= (uint32_t)kListCap) {
+                        uint32_t pos = base + incl - c;
+                        while (m) {
+                            sh.list[pos++] = e0 + (__ffs(m) - 1);
+                            m &= m - 1;
+                        }
+                        if (lane == 0 && total) atomicMax(&sh.valid_end, base + total);
+                    } else {
+                        stopped = true; // uniform: this warp tile is redone after the flush
+                    }
+                }
+                if (stopped) break;
+                __syncwarp(); // every lane has read stage st
+                if (j_issue < n_wt) issue_w();
+                j_cur += kWarpsCta;
+            }
+            if (stopped) { // drain this warp's copies in flight, so its mbarriers agree with seq_*
+                while (seq_done < seq_issued) {
+                    mbar_wait_at(wbar0 + 8u * (seq_done % kStages), (seq_done / kStages) & 1u);
+                    ++seq_done;
+                }
+                if (lane == 0) sh.any_ovf = 1u;
+            }
+            __syncthreads();
+            const uint32_t nc = sh.valid_end;
+            const bool again = sh.any_ovf != 0u;
+            __syncthreads(); // read by everyone before flush resets them
+            flush(nc);
+            if (!again) break;
+            if (stopped) { // resume at the tile that did not fit
+                j_issue = j_cur;
+                while (seq_issued < seq_done + (uint32_t)kStages && j_issue < n_wt) issue_w();
+            }
+        }
+    }
+#else
     uint32_t pending = 0; // list size (uniform)
     // this thread's kEPT key words in stage 0 (a shared address kept in a register)
     unsigned qk_s = smem_u32(&sh.qk[0][(kEPT / 4) * tid]);
@@ -712,6 +836,7 @@ __global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 :
             pending = 0;
         }
     }
+#endif
 
     // ---- flags ----
     if (orig) {
