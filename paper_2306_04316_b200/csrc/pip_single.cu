@@ -81,6 +81,9 @@ constexpr int kStages = PC_QSTAGES; // key-scan stages in flight
 #define PC_WARPKEYS 0 // 1: phase 1 per warp (own bulk-copy stages and mbarriers, no CTA barrier per tile)
 #endif
 constexpr int kWarpsCta = PC_TPB / 32;
+#ifndef PC_KSPLIT_TILES
+#define PC_KSPLIT_TILES 8 // chunks of at least this many key tiles: the CTA pairs of a cluster split them (SPLIT = 2)
+#endif
 constexpr uint32_t kWT = kQTile / kWarpsCta; // per-warp tile: edge key words per stage (8 per lane)
 static_assert(!PC_WARPKEYS || kWT == 256u, "per-warp tiles of 8 key words per lane");
 constexpr int kListCap = PC_LISTCAP; // candidate edge indices; a tile can add kQTile, so flush above kListCap - kQTile
@@ -101,6 +104,7 @@ struct SingleShared {
     EdgeRec brec[kBatch];        // gathered exact records
     unsigned long long full[PC_WARPKEYS ? kStages * kWarpsCta : kStages];
     uint32_t ncand;
+    uint32_t scan_from;          // SPLIT = 2: this round's first tile (min over warps)
     uint32_t valid_end;          // per-warp phase 1: end of the reservations that fit the list
     uint32_t any_ovf;            // per-warp phase 1: some warp stopped on a full list
     uint32_t cta_lo, cta_hi;     // key range of the CTA's active points
@@ -145,6 +149,38 @@ __device__ __forceinline__ void issue_tile(SingleShared& sh, int s, const uint32
         : "memory");
 }
 
+// Thread-block-cluster helpers (SPLIT = 2).
+__device__ __forceinline__ unsigned cluster_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned dsmem_addr(const void* p, unsigned rank) { // p in this CTA -> rank's copy
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ uint32_t dsmem_ld(unsigned a) {
+    uint32_t v;
+    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void dsmem_st(unsigned a, uint32_t v) {
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t dsmem_add(unsigned a, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.shared::cluster.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ void dsmem_max(unsigned a, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.shared::cluster.max.u32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ double2 load_pt(const double2* p) {
     unsigned long long pol;
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -163,6 +199,33 @@ __device__ __forceinline__ double2 load_pt(const double2* p) {
 __device__ __forceinline__ uint32_t key_pair(uint32_t a, uint32_t b, uint32_t ka, uint32_t kb) {
     return __viaddmax_u16x2(a, ka, b + kb);
 }
+
+constexpr uint32_t kAllEPT = (1u << kEPT) - 1u;
+// Phase-1 candidate mask of one thread's kEPT key words against the key-range
+// constants (ka, kb) of key_pair: bit i set iff edge i of the words may meet a
+// point of that range; the common all-clear case costs the pair tests + folds.
+__device__ __forceinline__ uint32_t key_mask(const uint32_t (&d)[kEPT], uint32_t ka, uint32_t kb) {
+    uint32_t t[kEPT / 2];
+#pragma unroll
+    for (int g = 0; g < kEPT / 8; ++g)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) t[4 * g + i] = key_pair(d[8 * g + i], d[8 * g + 4 + i], ka, kb);
+    uint32_t mn = __vimin3_u16x2(t[0], t[1], t[2]);
+#pragma unroll
+    for (int i = 3; i < kEPT / 2; i += 2) mn = __vimin3_u16x2(mn, t[i], t[min(i + 1, kEPT / 2 - 1)]);
+    if ((mn & 0x80008000u) == 0x80008000u) return 0u;
+    uint32_t m = 0;
+#pragma unroll
+    for (int g = 0; g < kEPT / 8; ++g)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint32_t nt = ~t[4 * g + i];
+            m |= ((nt >> 15) & 1u) << (8 * g + 2 * i);
+            m |= (nt >> 31) << (8 * g + 2 * i + 1);
+        }
+    return m;
+}
+
 
 // A lane's binary64 points for the exact fallbacks: point k of the lane is g[k * 32].
 struct PtRef {
@@ -412,7 +475,7 @@ __device__ __forceinline__ void slow_robust(const float2* my_l, const PtRef& my_
     }
 }
 
-template <int MODE>
+template <int MODE, int SPLIT>
 __global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 : PC_MINB))
     pip_tile_kernel(const double2* __restrict__ pts, uint64_t n, const uint32_t* __restrict__ qk,
                     const uint2* __restrict__ filt, const EdgeRec* __restrict__ rec, uint32_t n_edges,
@@ -424,13 +487,15 @@ __global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 :
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (n_dev) n = min(n, (uint64_t)*n_dev); // bucketed input: only the in-box prefix is live
     const uint64_t cta_base = (uint64_t)blockIdx.x * (kTPB * kK);
-    if (cta_base >= n) return;
+    // SPLIT = 2: both CTAs of a pair take part in the key scan, also one without
+    // points (the grid is rounded up to whole pairs)
+    if (SPLIT == 1 && cta_base >= n) return;
     const uint32_t e_begin = blockIdx.y * edges_per_chunk;
     const uint32_t e_end = min(n_edges, e_begin + edges_per_chunk);
     if (e_begin >= e_end) return;
     const uint64_t wbase = cta_base + (uint64_t)warp * 32 * kK; // this warp's first point (global)
 
-    const uint32_t cta_n = (uint32_t)min((uint64_t)(kTPB * kK), n - cta_base);
+    const uint32_t cta_n = cta_base >= n ? 0u : (uint32_t)min((uint64_t)(kTPB * kK), n - cta_base);
     if (tid == 0) {
         for (int k = 0; k < (PC_WARPKEYS ? kStages * kWarpsCta : kStages); ++k) mbar_init(&sh.full[k], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -535,7 +600,7 @@ __global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 :
         sh.live = 1;
     }
     __syncthreads(); // points staged, CTA key range complete
-    if (!sh.live) return; // no active point: nothing to classify (uniform)
+    if (SPLIT == 1 && !sh.live) return; // no active point: nothing to classify (uniform)
     // C1/C2 per-point keys on the CTA's own y range (y-bucketed CTAs span a thin
     // slab, so the 15-bit keys resolve ~2^27 levels over the polygon and key ties
     // -- which take the binary64 path -- stay rare even for edges far shorter
@@ -598,7 +663,8 @@ __global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 :
     };
     while (seq_issued < (uint32_t)kStages && j_issue < n_wt) issue_w();
 #else
-    if (tid == 0) {
+    // (SPLIT = 2: the key tiles of a pair are issued round by round in phase 1)
+    if (SPLIT == 1 && tid == 0) {
         for (uint32_t q = 0; q < (uint32_t)kStages && q < n_tiles; ++q)
             issue_tile(sh, (int)q, qk, t_begin + q * kQTile, tile_words(q));
     }
@@ -771,11 +837,128 @@ __global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 :
         }
     }
 #else
+    if constexpr (SPLIT > 1) {
+        // The CTA pair of a cluster (adjacent y slabs, the same edge chunk) splits
+        // the chunk's key tiles: CTA r scans tiles q = r, r + 2, ... and tests each
+        // edge against both CTAs' key ranges, listing candidates in its own list
+        // and -- through distributed shared memory -- in the partner's.  Each CTA
+        // reads half the key bytes and waits on half the tile barriers.  Lists
+        // never flush mid-scan: a warp whose reservation does not fit stops
+        // listing for that target and records the tile (lo_*); after a round both
+        // CTAs classify their lists, and a new round rescans from the earliest
+        // unlisted tile, listing each target only from its own lo on.
+        const unsigned crank = cluster_rank(), peer = crank ^ 1u;
+        cluster_sync_all(); // the partner's prologue (key range, live flag) is complete
+        const uint32_t p_lo = dsmem_ld(dsmem_addr(&sh.cta_lo, peer)), p_hi = dsmem_ld(dsmem_addr(&sh.cta_hi, peer));
+        const bool own_live = sh.live != 0u, peer_live = dsmem_ld(dsmem_addr(&sh.live, peer)) != 0u;
+        const uint32_t pka = (0x7fffu - p_hi) * 0x10001u, pkb = p_lo * 0x10001u;
+        const unsigned r_ncand = dsmem_addr(&sh.ncand, peer), r_valid = dsmem_addr(&sh.valid_end, peer);
+        const unsigned r_list = dsmem_addr(&sh.list[0], peer), r_again = dsmem_addr(&sh.any_ovf, peer);
+        unsigned qk_s = smem_u32(&sh.qk[0][(kEPT / 4) * tid]);
+        asm volatile("" : "+r"(qk_s));
+        const unsigned bar0 = smem_u32(&sh.full[0]);
+        constexpr uint32_t kDone = 0xffffffffu;
+        uint32_t lo_own = crank, lo_peer = crank; // per warp: first tile not yet listed for that target
+        uint32_t seq = 0;                         // copies issued (= consumed at round ends); uniform
+        // warp-aggregated reservation of m's candidates (edges e0 + bit) in a list:
+        // all of them or none; returns false when they do not fit
+        auto list_warp = [&](uint32_t m, uint32_t e0, bool remote) {
+            const uint32_t c = (uint32_t)__popc(m);
+            uint32_t incl = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+            if (total == 0u) return true;
+            uint32_t base = 0;
+            if (lane == 0) base = remote ? dsmem_add(r_ncand, total) : atomicAdd(&sh.ncand, total);
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (base + total > (uint32_t)kListCap) return false;
+            uint32_t pos = base + incl - c;
+            while (m) {
+                const uint32_t e = e0 + (__ffs(m) - 1);
+                if (remote) dsmem_st(r_list + 4u * pos, e);
+                else sh.list[pos] = e;
+                ++pos;
+                m &= m - 1;
+            }
+            if (lane == 0) {
+                if (remote) dsmem_max(r_valid, base + total);
+                else atomicMax(&sh.valid_end, base + total);
+            }
+            return true;
+        };
+        for (;;) { // rounds (cluster-uniform)
+            if (tid == 0) sh.scan_from = kDone;
+            __syncthreads();
+            if (lane == 0) atomicMin(&sh.scan_from, min(lo_own, lo_peer));
+            __syncthreads();
+            const uint32_t from = sh.scan_from;
+            bool fail_own = false, fail_peer = false;
+            uint32_t q_issue = from;
+            if (tid == 0) {
+                for (uint32_t k = 0; k < (uint32_t)kStages && q_issue < n_tiles; ++k, q_issue += 2)
+                    issue_tile(sh, (int)((seq + k) % kStages), qk, t_begin + q_issue * kQTile, tile_words(q_issue));
+            } else {
+                for (uint32_t k = 0; k < (uint32_t)kStages && q_issue < n_tiles; ++k) q_issue += 2;
+            }
+            for (uint32_t q = from; q < n_tiles; q += 2) {
+                const unsigned st = seq % kStages;
+                mbar_wait_at(bar0 + 8u * st, (seq / kStages) & 1u);
+                uint32_t d[kEPT];
+                {
+                    const unsigned a = qk_s + st * (kQTile * 4u);
+#pragma unroll
+                    for (int j = 0; j < kEPT / 4; ++j)
+                        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                     : "=r"(d[4 * j]), "=r"(d[4 * j + 1]), "=r"(d[4 * j + 2]), "=r"(d[4 * j + 3])
+                                     : "r"(a + 16u * j));
+                }
+                const uint32_t e0 = t_begin + q * kQTile + (uint32_t)kEPT * (uint32_t)tid;
+                const uint32_t emask = e0 + kEPT <= e_end ? kAllEPT : (e0 >= e_end ? 0u : (1u << (e_end - e0)) - 1u);
+                // own range
+                const bool want_own = own_live && !fail_own && q >= lo_own, want_peer = peer_live && !fail_peer && q >= lo_peer;
+                uint32_t m_own = 0, m_peer = 0;
+                if (want_own) m_own = key_mask(d, ka, kb) & emask;
+                if (want_peer) m_peer = key_mask(d, pka, pkb) & emask;
+                if (__any_sync(0xffffffffu, m_own != 0u) && !list_warp(m_own, e0, false)) {
+                    fail_own = true;
+                    lo_own = q;
+                }
+                if (__any_sync(0xffffffffu, m_peer != 0u) && !list_warp(m_peer, e0, true)) {
+                    fail_peer = true;
+                    lo_peer = q;
+                }
+                ++seq;
+                __syncthreads(); // stage st consumed by every warp
+                if (q_issue < n_tiles) {
+                    if (tid == 0) issue_tile(sh, (int)((seq + kStages - 1) % kStages), qk, t_begin + q_issue * kQTile, tile_words(q_issue));
+                    q_issue += 2;
+                }
+            }
+            if (!fail_own) lo_own = kDone;
+            if (!fail_peer) lo_peer = kDone;
+            const int more = __syncthreads_or(lo_own != kDone || lo_peer != kDone);
+            if (more && tid == 0) {
+                sh.any_ovf = 1u;
+                dsmem_st(r_again, 1u);
+            }
+            cluster_sync_all(); // every listing (local and remote) and flag is visible
+            const uint32_t nc = sh.valid_end;
+            const bool again = sh.any_ovf != 0u;
+            __syncthreads(); // read by everyone before flush resets them
+            flush(nc);
+            cluster_sync_all(); // no listing into a list that is being classified / reset
+            if (!again) break;
+        }
+    } else {
     uint32_t pending = 0; // list size (uniform)
     // this thread's kEPT key words in stage 0 (a shared address kept in a register)
     unsigned qk_s = smem_u32(&sh.qk[0][(kEPT / 4) * tid]);
     asm volatile("" : "+r"(qk_s));
-    const unsigned bar0 = smem_u32(&sh.full[0]); // stage s's mbarrier: bar0 + 8 s
+    unsigned bar0 = smem_u32(&sh.full[0]); // stage s's mbarrier: bar0 + 8 s
     asm volatile("" : "+r"(bar0));
     for (uint32_t q = 0; q < n_tiles; ++q) {
         const int s = (int)(q % kStages);
@@ -836,6 +1019,7 @@ __global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 :
             pending = 0;
         }
     }
+    }
 #endif
 
     // ---- flags ----
@@ -882,11 +1066,12 @@ cudaError_t launch_t(const SingleArgs& a, cudaStream_t st, int dev, uint64_t* la
     const size_t smem = sizeof(SingleShared);
     static bool attr[64] = {};
     if (dev < 64 && !attr[dev]) {
-        cudaFuncSetAttribute(pip_tile_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(pip_tile_kernel<MODE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(pip_tile_kernel<MODE, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr[dev] = true;
     }
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pip_tile_kernel<MODE>, kTPB, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pip_tile_kernel<MODE, 1>, kTPB, smem);
     per_sm = std::max(per_sm, 1);
     const uint64_t pts_per_cta = (uint64_t)kTPB * kK;
     const uint64_t n_ptiles = (a.n + pts_per_cta - 1) / pts_per_cta;
@@ -900,11 +1085,37 @@ cudaError_t launch_t(const SingleArgs& a, cudaStream_t st, int dev, uint64_t* la
     chunks = std::min<uint64_t>(std::min<uint64_t>(chunks, (ne + 63) / 64), 65535);
     const uint32_t per_chunk = (uint32_t)(((ne + chunks - 1) / chunks + 63) / 64 * 64);
     chunks = (ne + per_chunk - 1) / per_chunk;
+    // Long chunks: CTA pairs (clusters of 2, adjacent y slabs) split the key
+    // tiles and list candidates for each other (SPLIT = 2), halving each CTA's
+    // key bytes and tile barriers; short chunks keep one CTA per point tile.
+    const bool split = PC_KSPLIT_TILES > 0 && (per_chunk + kQTile - 1) / kQTile >= (uint32_t)PC_KSPLIT_TILES &&
+                       n_ptiles >= 2;
+    if (split) {
+        dim3 grid((unsigned)((n_ptiles + 1) / 2 * 2), (unsigned)chunks); // whole pairs
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(kTPB);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, pip_tile_kernel<MODE, 2>, reinterpret_cast<const double2*>(a.pts),
+                                                 a.n, a.qk, a.filt, reinterpret_cast<const EdgeRec*>(a.rec), a.n_edges,
+                                                 per_chunk, a.bbox_keys, a.prefilter, a.tol, a.tol2, a.inside_bits,
+                                                 a.aux_bits, a.n_dev, a.orig);
+        ++*launches;
+        return e != cudaSuccess ? e : cudaGetLastError();
+    }
     dim3 grid((unsigned)n_ptiles, (unsigned)chunks);
-    pip_tile_kernel<MODE><<<grid, kTPB, smem, st>>>(reinterpret_cast<const double2*>(a.pts), a.n, a.qk, a.filt,
-                                                   reinterpret_cast<const EdgeRec*>(a.rec), a.n_edges, per_chunk,
-                                                   a.bbox_keys, a.prefilter, a.tol, a.tol2, a.inside_bits,
-                                                   a.aux_bits, a.n_dev, a.orig);
+    pip_tile_kernel<MODE, 1><<<grid, kTPB, smem, st>>>(reinterpret_cast<const double2*>(a.pts), a.n, a.qk, a.filt,
+                                                      reinterpret_cast<const EdgeRec*>(a.rec), a.n_edges, per_chunk,
+                                                      a.bbox_keys, a.prefilter, a.tol, a.tol2, a.inside_bits,
+                                                      a.aux_bits, a.n_dev, a.orig);
     ++*launches;
     return cudaGetLastError();
 }
