@@ -82,8 +82,12 @@ constexpr int kStages = PC_QSTAGES; // key-scan stages in flight
 #endif
 constexpr int kWarpsCta = PC_TPB / 32;
 #ifndef PC_KSPLIT_TILES
-#define PC_KSPLIT_TILES 8 // chunks of at least this many key tiles: the CTA pairs of a cluster split them (SPLIT = 2)
+#define PC_KSPLIT_TILES 8 // chunks of at least this many key tiles: the CTAs of a cluster split them
 #endif
+#ifndef PC_KSPLIT_G
+#define PC_KSPLIT_G 2 // CTAs per cluster that split the key tiles (2 or 4)
+#endif
+static_assert(PC_KSPLIT_G == 2 || PC_KSPLIT_G == 4, "key split over 2 or 4 CTAs");
 constexpr uint32_t kWT = kQTile / kWarpsCta; // per-warp tile: edge key words per stage (8 per lane)
 static_assert(!PC_WARPKEYS || kWT == 256u, "per-warp tiles of 8 key words per lane");
 constexpr int kListCap = PC_LISTCAP; // candidate edge indices; a tile can add kQTile, so flush above kListCap - kQTile
@@ -838,31 +842,35 @@ __global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 :
     }
 #else
     if constexpr (SPLIT > 1) {
-        // The CTA pair of a cluster (adjacent y slabs, the same edge chunk) splits
-        // the chunk's key tiles: CTA r scans tiles q = r, r + 2, ... and tests each
-        // edge against both CTAs' key ranges, listing candidates in its own list
-        // and -- through distributed shared memory -- in the partner's.  Each CTA
-        // reads half the key bytes and waits on half the tile barriers.  Lists
-        // never flush mid-scan: a warp whose reservation does not fit stops
-        // listing for that target and records the tile (lo_*); after a round both
-        // CTAs classify their lists, and a new round rescans from the earliest
-        // unlisted tile, listing each target only from its own lo on.
-        const unsigned crank = cluster_rank(), peer = crank ^ 1u;
-        cluster_sync_all(); // the partner's prologue (key range, live flag) is complete
-        const uint32_t p_lo = dsmem_ld(dsmem_addr(&sh.cta_lo, peer)), p_hi = dsmem_ld(dsmem_addr(&sh.cta_hi, peer));
-        const bool own_live = sh.live != 0u, peer_live = dsmem_ld(dsmem_addr(&sh.live, peer)) != 0u;
-        const uint32_t pka = (0x7fffu - p_hi) * 0x10001u, pkb = p_lo * 0x10001u;
-        const unsigned r_ncand = dsmem_addr(&sh.ncand, peer), r_valid = dsmem_addr(&sh.valid_end, peer);
-        const unsigned r_list = dsmem_addr(&sh.list[0], peer), r_again = dsmem_addr(&sh.any_ovf, peer);
+        // The SPLIT CTAs of a cluster (adjacent y slabs, the same edge chunk)
+        // split the chunk's key tiles: CTA r scans tiles q = r, r + SPLIT, ... and
+        // tests each edge against every member's key range, listing candidates in
+        // its own list and -- through distributed shared memory -- in the others'.
+        // Each CTA reads 1/SPLIT of the key bytes and waits on 1/SPLIT of the tile
+        // barriers.  Lists never flush mid-scan: a warp whose reservation does not
+        // fit stops listing for that member and records the tile (lo[]); after a
+        // round every CTA classifies its list, and a new round rescans from the
+        // earliest unlisted tile, listing each member only from its own lo on.
+        const unsigned crank = cluster_rank();
+        cluster_sync_all(); // every member's prologue (key range, live flag) is complete
+        uint32_t mka[SPLIT], mkb[SPLIT], lo[SPLIT];
+        uint32_t live_m = 0u; // bit r: member r has active points
+#pragma unroll
+        for (int r = 0; r < SPLIT; ++r) {
+            const uint32_t l = dsmem_ld(dsmem_addr(&sh.cta_lo, (unsigned)r)), h = dsmem_ld(dsmem_addr(&sh.cta_hi, (unsigned)r));
+            live_m |= (uint32_t)(dsmem_ld(dsmem_addr(&sh.live, (unsigned)r)) != 0u) << r;
+            mka[r] = (0x7fffu - h) * 0x10001u; // key_pair constants of member r
+            mkb[r] = l * 0x10001u;
+            lo[r] = crank; // per warp: first of this CTA's tiles not yet listed for member r
+        }
         unsigned qk_s = smem_u32(&sh.qk[0][(kEPT / 4) * tid]);
         asm volatile("" : "+r"(qk_s));
         const unsigned bar0 = smem_u32(&sh.full[0]);
         constexpr uint32_t kDone = 0xffffffffu;
-        uint32_t lo_own = crank, lo_peer = crank; // per warp: first tile not yet listed for that target
-        uint32_t seq = 0;                         // copies issued (= consumed at round ends); uniform
-        // warp-aggregated reservation of m's candidates (edges e0 + bit) in a list:
-        // all of them or none; returns false when they do not fit
-        auto list_warp = [&](uint32_t m, uint32_t e0, bool remote) {
+        uint32_t seq = 0; // copies issued (= consumed at round ends); uniform
+        // warp-aggregated reservation of m's candidates (edges e0 + bit) in member
+        // r's list: all of them or none; returns false when they do not fit
+        auto list_warp = [&](uint32_t m, uint32_t e0, unsigned r) {
             const uint32_t c = (uint32_t)__popc(m);
             uint32_t incl = c;
 #pragma unroll
@@ -873,38 +881,33 @@ __global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 :
             const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
             if (total == 0u) return true;
             uint32_t base = 0;
-            if (lane == 0) base = remote ? dsmem_add(r_ncand, total) : atomicAdd(&sh.ncand, total);
+            if (lane == 0) base = dsmem_add(dsmem_addr(&sh.ncand, r), total);
             base = __shfl_sync(0xffffffffu, base, 0);
             if (base + total > (uint32_t)kListCap) return false;
+            const unsigned rl = dsmem_addr(&sh.list[0], r);
             uint32_t pos = base + incl - c;
             while (m) {
-                const uint32_t e = e0 + (__ffs(m) - 1);
-                if (remote) dsmem_st(r_list + 4u * pos, e);
-                else sh.list[pos] = e;
+                dsmem_st(rl + 4u * pos, e0 + (__ffs(m) - 1));
                 ++pos;
                 m &= m - 1;
             }
-            if (lane == 0) {
-                if (remote) dsmem_max(r_valid, base + total);
-                else atomicMax(&sh.valid_end, base + total);
-            }
+            if (lane == 0) dsmem_max(dsmem_addr(&sh.valid_end, r), base + total);
             return true;
         };
         for (;;) { // rounds (cluster-uniform)
+            uint32_t lmin = kDone;
+#pragma unroll
+            for (int r = 0; r < SPLIT; ++r) lmin = min(lmin, lo[r]);
             if (tid == 0) sh.scan_from = kDone;
             __syncthreads();
-            if (lane == 0) atomicMin(&sh.scan_from, min(lo_own, lo_peer));
+            if (lane == 0) atomicMin(&sh.scan_from, lmin);
             __syncthreads();
             const uint32_t from = sh.scan_from;
-            bool fail_own = false, fail_peer = false;
+            uint32_t fail = 0u; // bit r: listing for member r stopped this round (warp-uniform)
             uint32_t q_issue = from;
-            if (tid == 0) {
-                for (uint32_t k = 0; k < (uint32_t)kStages && q_issue < n_tiles; ++k, q_issue += 2)
-                    issue_tile(sh, (int)((seq + k) % kStages), qk, t_begin + q_issue * kQTile, tile_words(q_issue));
-            } else {
-                for (uint32_t k = 0; k < (uint32_t)kStages && q_issue < n_tiles; ++k) q_issue += 2;
-            }
-            for (uint32_t q = from; q < n_tiles; q += 2) {
+            for (uint32_t k = 0; k < (uint32_t)kStages && q_issue < n_tiles; ++k, q_issue += SPLIT)
+                if (tid == 0) issue_tile(sh, (int)((seq + k) % kStages), qk, t_begin + q_issue * kQTile, tile_words(q_issue));
+            for (uint32_t q = from; q < n_tiles; q += SPLIT) {
                 const unsigned st = seq % kStages;
                 mbar_wait_at(bar0 + 8u * st, (seq / kStages) & 1u);
                 uint32_t d[kEPT];
@@ -918,32 +921,31 @@ __global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 :
                 }
                 const uint32_t e0 = t_begin + q * kQTile + (uint32_t)kEPT * (uint32_t)tid;
                 const uint32_t emask = e0 + kEPT <= e_end ? kAllEPT : (e0 >= e_end ? 0u : (1u << (e_end - e0)) - 1u);
-                // own range
-                const bool want_own = own_live && !fail_own && q >= lo_own, want_peer = peer_live && !fail_peer && q >= lo_peer;
-                uint32_t m_own = 0, m_peer = 0;
-                if (want_own) m_own = key_mask(d, ka, kb) & emask;
-                if (want_peer) m_peer = key_mask(d, pka, pkb) & emask;
-                if (__any_sync(0xffffffffu, m_own != 0u) && !list_warp(m_own, e0, false)) {
-                    fail_own = true;
-                    lo_own = q;
-                }
-                if (__any_sync(0xffffffffu, m_peer != 0u) && !list_warp(m_peer, e0, true)) {
-                    fail_peer = true;
-                    lo_peer = q;
+#pragma unroll
+                for (int r = 0; r < SPLIT; ++r) {
+                    const bool want = (live_m >> r & 1u) && !(fail >> r & 1u) && q >= lo[r]; // warp-uniform
+                    const uint32_t m = want ? key_mask(d, mka[r], mkb[r]) & emask : 0u;
+                    if (__any_sync(0xffffffffu, m != 0u) && !list_warp(m, e0, (unsigned)r)) {
+                        fail |= 1u << r;
+                        lo[r] = q;
+                    }
                 }
                 ++seq;
                 __syncthreads(); // stage st consumed by every warp
                 if (q_issue < n_tiles) {
                     if (tid == 0) issue_tile(sh, (int)((seq + kStages - 1) % kStages), qk, t_begin + q_issue * kQTile, tile_words(q_issue));
-                    q_issue += 2;
+                    q_issue += SPLIT;
                 }
             }
-            if (!fail_own) lo_own = kDone;
-            if (!fail_peer) lo_peer = kDone;
-            const int more = __syncthreads_or(lo_own != kDone || lo_peer != kDone);
-            if (more && tid == 0) {
-                sh.any_ovf = 1u;
-                dsmem_st(r_again, 1u);
+            bool more = false;
+#pragma unroll
+            for (int r = 0; r < SPLIT; ++r) {
+                if (!(fail >> r & 1u)) lo[r] = kDone;
+                more = more || lo[r] != kDone;
+            }
+            if (__syncthreads_or(more) && tid == 0) {
+#pragma unroll
+                for (int r = 0; r < SPLIT; ++r) dsmem_st(dsmem_addr(&sh.any_ovf, (unsigned)r), 1u);
             }
             cluster_sync_all(); // every listing (local and remote) and flag is visible
             const uint32_t nc = sh.valid_end;
@@ -1067,7 +1069,7 @@ cudaError_t launch_t(const SingleArgs& a, cudaStream_t st, int dev, uint64_t* la
     static bool attr[64] = {};
     if (dev < 64 && !attr[dev]) {
         cudaFuncSetAttribute(pip_tile_kernel<MODE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(pip_tile_kernel<MODE, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(pip_tile_kernel<MODE, PC_KSPLIT_G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr[dev] = true;
     }
     int per_sm = 0;
@@ -1085,13 +1087,14 @@ cudaError_t launch_t(const SingleArgs& a, cudaStream_t st, int dev, uint64_t* la
     chunks = std::min<uint64_t>(std::min<uint64_t>(chunks, (ne + 63) / 64), 65535);
     const uint32_t per_chunk = (uint32_t)(((ne + chunks - 1) / chunks + 63) / 64 * 64);
     chunks = (ne + per_chunk - 1) / per_chunk;
-    // Long chunks: CTA pairs (clusters of 2, adjacent y slabs) split the key
-    // tiles and list candidates for each other (SPLIT = 2), halving each CTA's
-    // key bytes and tile barriers; short chunks keep one CTA per point tile.
+    // Long chunks: the CTAs of a cluster (PC_KSPLIT_G of them, adjacent y slabs)
+    // split the key tiles and list candidates for each other, dividing each
+    // CTA's key bytes and tile barriers; short chunks keep one CTA per point tile.
+    constexpr int G = PC_KSPLIT_G;
     const bool split = PC_KSPLIT_TILES > 0 && (per_chunk + kQTile - 1) / kQTile >= (uint32_t)PC_KSPLIT_TILES &&
                        n_ptiles >= 2;
     if (split) {
-        dim3 grid((unsigned)((n_ptiles + 1) / 2 * 2), (unsigned)chunks); // whole pairs
+        dim3 grid((unsigned)((n_ptiles + G - 1) / G * G), (unsigned)chunks); // whole clusters
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = grid;
         cfg.blockDim = dim3(kTPB);
@@ -1099,12 +1102,12 @@ cudaError_t launch_t(const SingleArgs& a, cudaStream_t st, int dev, uint64_t* la
         cfg.stream = st;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.x = G;
         at[0].val.clusterDim.y = 1;
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        const cudaError_t e = cudaLaunchKernelEx(&cfg, pip_tile_kernel<MODE, 2>, reinterpret_cast<const double2*>(a.pts),
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, pip_tile_kernel<MODE, G>, reinterpret_cast<const double2*>(a.pts),
                                                  a.n, a.qk, a.filt, reinterpret_cast<const EdgeRec*>(a.rec), a.n_edges,
                                                  per_chunk, a.bbox_keys, a.prefilter, a.tol, a.tol2, a.inside_bits,
                                                  a.aux_bits, a.n_dev, a.orig);
