@@ -887,6 +887,7 @@ __global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 :
             const unsigned rl = dsmem_addr(&sh.list[0], r);
             uint32_t pos = base + incl - c;
             while (m) {
+                PC_DCHECK(pos < (uint32_t)kListCap && e0 + (__ffs(m) - 1) < e_end && r < (unsigned)SPLIT);
                 dsmem_st(rl + 4u * pos, e0 + (__ffs(m) - 1));
                 ++pos;
                 m &= m - 1;
@@ -908,6 +909,7 @@ __global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 :
             for (uint32_t k = 0; k < (uint32_t)kStages && q_issue < n_tiles; ++k, q_issue += SPLIT)
                 if (tid == 0) issue_tile(sh, (int)((seq + k) % kStages), qk, t_begin + q_issue * kQTile, tile_words(q_issue));
             for (uint32_t q = from; q < n_tiles; q += SPLIT) {
+                PC_DCHECK(q % SPLIT == crank);
                 const unsigned st = seq % kStages;
                 mbar_wait_at(bar0 + 8u * st, (seq / kStages) & 1u);
                 uint32_t d[kEPT];
@@ -950,6 +952,7 @@ __global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 :
             cluster_sync_all(); // every listing (local and remote) and flag is visible
             const uint32_t nc = sh.valid_end;
             const bool again = sh.any_ovf != 0u;
+            PC_DCHECK(nc <= (uint32_t)kListCap && (sh.live != 0u || nc == 0u)); // an idle CTA is never listed for
             __syncthreads(); // read by everyone before flush resets them
             flush(nc);
             cluster_sync_all(); // no listing into a list that is being classified / reset

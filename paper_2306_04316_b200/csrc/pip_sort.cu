@@ -38,9 +38,15 @@ namespace pcd {
 
 namespace {
 
-constexpr int kRkThreads = 512;
+#ifndef PC_RK_THREADS
+#define PC_RK_THREADS 512
+#endif
+#ifndef PC_RK_MINB
+#define PC_RK_MINB 2
+#endif
+constexpr int kRkThreads = PC_RK_THREADS;
 constexpr int kRkItems = 8;                        // per thread
-constexpr int kRkTile = kRkThreads * kRkItems;     // 4096 elements per tile
+constexpr int kRkTile = kRkThreads * kRkItems;     // 4096 elements per tile (default)
 constexpr int kRkWarps = kRkThreads / 32;
 constexpr uint32_t kRkLevels = 65280;              // in-box keys 0 .. 65279 (high byte < 0xff)
 constexpr uint16_t kRkReject = 0xffff;
@@ -224,7 +230,7 @@ struct RkShared {
 // once counted, 2 << 30 | inclusive prefix once known); CTAs start in tile
 // order, so a tile only ever waits on tiles already running.
 template <int PASS, bool IMPLICIT = PASS == 0, bool LOOKBACK = false>
-__global__ void __launch_bounds__(kRkThreads, 2) rk_scatter_kernel(uint64_t n, const uint16_t* __restrict__ keys_in,
+__global__ void __launch_bounds__(kRkThreads, PC_RK_MINB) rk_scatter_kernel(uint64_t n, const uint16_t* __restrict__ keys_in,
                                                                 const double2* __restrict__ pts_in,
                                                                 double2* __restrict__ pts_out,
                                                                 const uint32_t* __restrict__ idx_in,
