@@ -955,8 +955,11 @@ __global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 :
             PC_DCHECK(nc <= (uint32_t)kListCap && (sh.live != 0u || nc == 0u)); // an idle CTA is never listed for
             __syncthreads(); // read by everyone before flush resets them
             flush(nc);
-            cluster_sync_all(); // no listing into a list that is being classified / reset
+            // the last round: nobody touches another CTA's shared memory after the
+            // barrier above, so a CTA may leave without waiting for its partner's
+            // classification; otherwise wait until every list is classified / reset
             if (!again) break;
+            cluster_sync_all();
         }
     } else {
     uint32_t pending = 0; // list size (uniform)
