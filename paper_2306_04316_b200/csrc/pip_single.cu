@@ -895,7 +895,12 @@ __global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 :
             if (lane == 0) dsmem_max(dsmem_addr(&sh.valid_end, r), base + total);
             return true;
         };
-        for (;;) { // rounds (cluster-uniform)
+        // a cluster without any active point (e.g. past the in-box prefix of a
+        // bucketed batch) has nothing to scan (live_m is the same in every
+        // member); it still waits until every member has read the others' ranges
+        // above, so no CTA leaves while a partner may read its shared memory
+        if (live_m == 0u) cluster_sync_all();
+        for (; live_m != 0u;) { // rounds (cluster-uniform)
             uint32_t lmin = kDone;
 #pragma unroll
             for (int r = 0; r < SPLIT; ++r) lmin = min(lmin, lo[r]);
