@@ -44,6 +44,12 @@ namespace {
 #ifndef PC_RK_MINB
 #define PC_RK_MINB 2
 #endif
+#ifndef PC_RK_PF
+#define PC_RK_PF 1
+#endif
+#ifndef PC_RK_PF_DIST
+#define PC_RK_PF_DIST 64
+#endif
 constexpr int kRkThreads = PC_RK_THREADS;
 constexpr int kRkItems = 8;                        // per thread
 constexpr int kRkTile = kRkThreads * kRkItems;     // 4096 elements per tile (default)
@@ -247,6 +253,19 @@ __global__ void __launch_bounds__(kRkThreads, PC_RK_MINB) rk_scatter_kernel(uint
     const int shift = 8 * PASS;
     const uint64_t t0 = (uint64_t)blockIdx.x * kRkTile;
     const uint32_t tn = (uint32_t)min((uint64_t)kRkTile, n - t0);
+#if PC_RK_PF
+    // L2 prefetch of a later CTA's whole tile (keys, points, indices), as in the
+    // scan kernel: that CTA's up-front requests then hit L2
+    if (tid == 0) {
+        const uint64_t nb = t0 + (uint64_t)PC_RK_PF_DIST * kRkTile;
+        if (nb + kRkTile <= n) {
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pts_in + nb), "r"(kRkTile * 16u) : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(keys_in + nb), "r"(kRkTile * 2u) : "memory");
+            if constexpr (!IMPLICIT)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(idx_in + nb), "r"(kRkTile * 4u) : "memory");
+        }
+    }
+#endif
     // this thread's elements e = j * kRkThreads + tid: keys, indices and points
     // are all requested before the ranking, so their latency overlaps it
     uint32_t key[kRkItems], idx[IMPLICIT ? 1 : kRkItems];
