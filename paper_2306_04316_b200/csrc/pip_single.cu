@@ -922,6 +922,10 @@ __global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 :
         // bucketed batch) has nothing to scan (live_m is the same in every
         // member); it still waits until every member has read the others' ranges
         // above, so no CTA leaves while a partner may read its shared memory
+        // (live_m made opaque to the optimiser: with the idle test visible, ptxas
+        // schedules the C2 instantiation's phase 2 worse -- c4 C2 kernel 4.86 vs
+        // 4.65 ms, C1 / Robust unchanged; profiles/r2c_experiments.txt)
+        asm volatile("" : "+r"(live_m));
         if (live_m == 0u) cluster_sync_all();
         for (; live_m != 0u;) { // rounds (cluster-uniform)
             uint32_t lmin = kDone;
