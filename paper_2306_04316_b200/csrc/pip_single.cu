@@ -37,6 +37,9 @@
 
 #include "pip_device.cuh"
 
+#ifndef PC_EMPTYBAR
+#define PC_EMPTYBAR 0
+#endif
 #ifndef PC_PF
 #define PC_PF 1
 #endif
@@ -114,6 +117,7 @@ struct SingleShared {
     uint2 bfilt[kBatch];         // gathered per-point filter words
     EdgeRec brec[kBatch];        // gathered exact records
     unsigned long long full[PC_WARPKEYS ? kStages * kWarpsCta : kStages];
+    unsigned long long empty[kStages]; // key split: stage consumed by all kWarpsCta warps (PC_EMPTYBAR)
     uint32_t ncand;
     uint32_t scan_from;          // SPLIT = 2: this round's first tile (min over warps)
     uint32_t valid_end;          // per-warp phase 1: end of the reservations that fit the list
@@ -525,6 +529,7 @@ __global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 :
     const uint32_t cta_n = cta_base >= n ? 0u : (uint32_t)min((uint64_t)(kTPB * kK), n - cta_base);
     if (tid == 0) {
         for (int k = 0; k < (PC_WARPKEYS ? kStages * kWarpsCta : kStages); ++k) mbar_init(&sh.full[k], 1);
+        for (int k = 0; k < kStages; ++k) mbar_init(&sh.empty[k], kWarpsCta);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         sh.ncand = 0;
         sh.valid_end = 0;
@@ -889,6 +894,8 @@ __global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 :
         unsigned qk_s = smem_u32(&sh.qk[0][(kEPT / 4) * tid]);
         asm volatile("" : "+r"(qk_s));
         const unsigned bar0 = smem_u32(&sh.full[0]);
+        const unsigned ebar0 = smem_u32(&sh.empty[0]);
+        (void)ebar0;
         constexpr uint32_t kDone = 0xffffffffu;
         uint32_t seq = 0; // copies issued (= consumed at round ends); uniform
         // warp-aggregated reservation of m's candidates (edges e0 + bit) in member
@@ -965,11 +972,28 @@ __global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 :
                     }
                 }
                 ++seq;
+#if PC_EMPTYBAR
+                // stage st consumed: every warp arrives on the stage's "empty"
+                // mbarrier (release: after its reads of the stage) and only the
+                // issuing thread waits for all kWarpsCta arrivals before the next
+                // bulk copy overwrites the stage -- no CTA-wide barrier per tile
+                __syncwarp();
+                if (lane == 0)
+                    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(ebar0 + 8u * st) : "memory");
+                if (q_issue < n_tiles) {
+                    if (tid == 0) {
+                        mbar_wait_at(ebar0 + 8u * st, ((seq - 1u) / kStages) & 1u);
+                        issue_tile(sh, (int)st, qk, t_begin + q_issue * kQTile, tile_words(q_issue));
+                    }
+                    q_issue += SPLIT;
+                }
+#else
                 __syncthreads(); // stage st consumed by every warp
                 if (q_issue < n_tiles) {
                     if (tid == 0) issue_tile(sh, (int)((seq + kStages - 1) % kStages), qk, t_begin + q_issue * kQTile, tile_words(q_issue));
                     q_issue += SPLIT;
                 }
+#endif
             }
             bool more = false;
 #pragma unroll
