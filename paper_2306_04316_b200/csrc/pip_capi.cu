@@ -245,8 +245,10 @@ void enqueue_single(pc_ctx* c, DevState& d, cudaStream_t st, const double* d_pts
     pa.n_zero_words = nwords;
     check(c, pcd::launch_prep(pa, st, d.dev, &d.launches), "prep kernel");
     const bool tree = (mode == 0 || mode == 1) /* C1, C2 */ && c->tree_mode == 1 && pcd::tree_eligible(n_verts, n, true);
+    // y-ordering pays from ~24 edges on (measured break-even, tools/time_bucket_threshold.py:
+    // 1e6 points: 24 edges 59 vs 59 us, 63 edges 63 vs 106 us; 1e5 points: 16-20 edges)
     const bool bucket = !tree && n < 0xffffffffull &&
-                        (c->bucket_mode == 1 || (c->bucket_mode < 0 && n_edges >= 64 && n >= 4096));
+                        (c->bucket_mode == 1 || (c->bucket_mode < 0 && n_edges >= 24 && n >= 4096));
     pcd::SingleArgs sa{};
     sa.mode = mode;
     sa.pts = d_pts;
