@@ -72,6 +72,15 @@ constexpr uint32_t kAllK = kK >= 32 ? 0xffffffffu : (1u << kK) - 1u; // a mask o
 #ifndef PC_MINB
 #define PC_MINB 3
 #endif
+#ifndef PC_MINB_C2
+#define PC_MINB_C2 2 // C2: 2 CTAs/SM at 128 registers, no spills (c4 kernel 4.65 -> 3.79 ms, c1 0.093 -> 0.079)
+#endif
+#ifndef PC_MINB_SMALL
+#define PC_MINB_SMALL 2 // C1, one CTA per point tile and <= PC_SMALL_EDGES edges (c1 kernel 0.091 -> 0.081 ms)
+#endif
+#ifndef PC_SMALL_EDGES
+#define PC_SMALL_EDGES 2048 // (n = 1e4 edges is 8% slower at 2 CTAs/SM, n = 1e3 10% faster)
+#endif
 constexpr int kQTile = PC_QTILE; // edge key words per shared-memory stage (8 KB; 8 per thread)
 static_assert(kKeyTile % kQTile == 0 || kQTile % kKeyTile == 0, "tiles and the key array's padding");
 #ifndef PC_EPI
@@ -490,8 +499,8 @@ __device__ __forceinline__ void slow_robust(const float2* my_l, const PtRef& my_
     }
 }
 
-template <int MODE, int SPLIT>
-__global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 : PC_MINB))
+template <int MODE, int SPLIT, bool SMALL = false>
+__global__ void __launch_bounds__(kTPB, kTPB >= 512 ? 2 : (MODE == kRobust ? 2 : (MODE == kC2 ? PC_MINB_C2 : (SMALL ? PC_MINB_SMALL : PC_MINB))))
     pip_tile_kernel(const double2* __restrict__ pts, uint64_t n, const uint32_t* __restrict__ qk,
                     const uint2* __restrict__ filt, const EdgeRec* __restrict__ rec, uint32_t n_edges,
                     uint32_t edges_per_chunk, const unsigned long long* __restrict__ bbox_keys, int prefilter,
@@ -1132,10 +1141,17 @@ cudaError_t launch_t(const SingleArgs& a, cudaStream_t st, int dev, uint64_t* la
     if (dev < 64 && !attr[dev]) {
         cudaFuncSetAttribute(pip_tile_kernel<MODE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(pip_tile_kernel<MODE, PC_KSPLIT_G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if constexpr (MODE == kC1)
+            cudaFuncSetAttribute(pip_tile_kernel<MODE, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr[dev] = true;
     }
+    // C1 on small polygons: the instantiation with more registers per thread (PC_MINB_SMALL)
+    const bool small = MODE == kC1 && a.n_edges <= (uint32_t)PC_SMALL_EDGES;
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pip_tile_kernel<MODE, 1>, kTPB, smem);
+    if constexpr (MODE == kC1) {
+        if (small) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pip_tile_kernel<MODE, 1, true>, kTPB, smem);
+    }
+    if (per_sm == 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pip_tile_kernel<MODE, 1>, kTPB, smem);
     per_sm = std::max(per_sm, 1);
     const uint64_t pts_per_cta = (uint64_t)kTPB * kK;
     const uint64_t n_ptiles = (a.n + pts_per_cta - 1) / pts_per_cta;
@@ -1177,6 +1193,15 @@ cudaError_t launch_t(const SingleArgs& a, cudaStream_t st, int dev, uint64_t* la
         return e != cudaSuccess ? e : cudaGetLastError();
     }
     dim3 grid((unsigned)n_ptiles, (unsigned)chunks);
+    if constexpr (MODE == kC1) {
+        if (small) {
+            pip_tile_kernel<MODE, 1, true><<<grid, kTPB, smem, st>>>(
+                reinterpret_cast<const double2*>(a.pts), a.n, a.qk, a.filt, reinterpret_cast<const EdgeRec*>(a.rec),
+                a.n_edges, per_chunk, a.bbox_keys, a.prefilter, a.tol, a.tol2, a.inside_bits, a.aux_bits, a.n_dev, a.orig);
+            ++*launches;
+            return cudaGetLastError();
+        }
+    }
     pip_tile_kernel<MODE, 1><<<grid, kTPB, smem, st>>>(reinterpret_cast<const double2*>(a.pts), a.n, a.qk, a.filt,
                                                       reinterpret_cast<const EdgeRec*>(a.rec), a.n_edges, per_chunk,
                                                       a.bbox_keys, a.prefilter, a.tol, a.tol2, a.inside_bits,
